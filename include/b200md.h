@@ -1,0 +1,223 @@
+/*
+ * b200md.h — C ABI of the B200-native force/energy/partner-search/step path.
+ *
+ * This is the drop-in boundary for the hot path of the reference `tmd` library
+ * (ms2 2.0 restatement, /root/reference/proj).  Every entry point below replaces
+ * one reference interface; the reference declaration it stands in for is cited
+ * as include/tmd/<file>:<line> or src/<file>:<line>.
+ *
+ * Conventions
+ *  - Plain C: POD structs, raw pointers and sizes, no torch / CUDA types.
+ *  - Every call returns an `int` status (B2MD_OK == 0).  On failure the
+ *    message is available from b2md_last_error() (thread-local).  The status
+ *    codes mirror the reference exception hierarchy (include/tmd/error.hpp:8-30):
+ *    ModelError, ConfigError, IoError, NumericalError.  A C++ shim rethrows them
+ *    (see INTEGRATION.md).
+ *  - Host arrays use the reference's AoS layouts: Vec3 = 3 doubles (x,y,z)
+ *    (include/tmd/geom.hpp:9-11), Quat = 4 doubles (w,x,y,z)
+ *    (include/tmd/geom.hpp:37-38).  On the device the state is SoA.
+ *  - Molecules are ordered by species (include/tmd/model.hpp:66-68).
+ *  - There is no CPU fallback: a context needs a CUDA device; creating one
+ *    without a device fails with B2MD_CUDA_ERROR.  Pure host helpers
+ *    (species building, tuning, shard plans) work without a GPU.
+ */
+#ifndef B200MD_H
+#define B200MD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2MD_ABI_VERSION 1
+#define B2MD_MAX_SITES 16
+
+/* status codes (include/tmd/error.hpp:8-30) */
+enum {
+  B2MD_OK = 0,
+  B2MD_MODEL_ERROR = 1,      /* tmd::ModelError */
+  B2MD_CONFIG_ERROR = 2,     /* tmd::ConfigError */
+  B2MD_IO_ERROR = 3,         /* tmd::IoError */
+  B2MD_NUMERICAL_ERROR = 4,  /* tmd::NumericalError */
+  B2MD_CUDA_ERROR = 5,       /* device / driver failure (no reference analogue) */
+  B2MD_INVALID_ARGUMENT = 6  /* bad pointer / size at the C boundary */
+};
+
+/* tmd::SiteKind (include/tmd/model.hpp:16) */
+enum { B2MD_SITE_LJ = 0, B2MD_SITE_CHARGE = 1, B2MD_SITE_DUMMY = 2 };
+
+/* tmd::ElectrostaticsMethod (include/tmd/model.hpp:52) */
+enum { B2MD_METHOD_NONE = 0, B2MD_METHOD_REACTION_FIELD = 1, B2MD_METHOD_EWALD = 2 };
+
+/* tmd::Site (include/tmd/model.hpp:18-25) */
+typedef struct {
+  int32_t kind;
+  int32_t pad_;
+  double body_pos[3];
+  double sigma;
+  double epsilon;
+  double q;
+  double mass;
+} b2md_site;
+
+/* tmd::MoleculeSpecies after build_species (include/tmd/model.hpp:29-40) */
+typedef struct {
+  int32_t n_sites;
+  int32_t rotational_dof;
+  b2md_site sites[B2MD_MAX_SITES];
+  double total_mass;
+  double inertia_principal[3];
+  double net_charge;
+  double max_extent;
+} b2md_species;
+
+/* tmd::SystemComposition (include/tmd/model.hpp:54-72) */
+typedef struct {
+  int32_t n_species;
+  int32_t pad_;
+  const b2md_species* species; /* n_species entries, already built */
+  const int32_t* counts;       /* n_species entries */
+  double box_length;
+  double temperature;
+} b2md_composition;
+
+/* tmd::ForceFieldOptions (include/tmd/parallel.hpp:45-52) + tmd::EwaldParams
+ * (include/tmd/ewald.hpp:15-18).  `workers` is accepted for interface parity;
+ * the reference's ewald+workers!=1 rejection (src/parallel.cpp:65-66) is kept. */
+typedef struct {
+  double cutoff;
+  int32_t method;
+  int32_t has_ewald;
+  double eps_rf;         /* +inf = conducting boundary */
+  double ewald_alpha;
+  int32_t ewald_kmax;
+  int32_t workers;
+  int32_t volume_derivatives; /* 1 = accumulate s1/s2 (forced 0 for ewald) */
+  int32_t pad_;
+} b2md_ff_options;
+
+/* tmd::EnergyBreakdown (include/tmd/energy.hpp:9-25) */
+typedef struct {
+  double lj;
+  double elec_real;
+  double elec_recip;
+  double elec_self;
+  double rf;
+  double lrc;
+  double du_dv_explicit;
+  double du_dv_lrc;
+  double d2u_dv2_explicit;
+  double d2u_dv2_lrc;
+} b2md_energy;
+
+/* per-evaluation scalar outputs beyond EnergyBreakdown: the molecular virial
+ * (include/tmd/model.hpp:86) and the raw volume-derivative sums s1, s2
+ * (include/tmd/potentials.hpp:54-58). */
+typedef struct {
+  double virial;
+  double s1;
+  double s2;
+  int64_t com_pairs;     /* molecule pairs passing the COM partner search */
+} b2md_eval_stats;
+
+typedef struct b2md_ctx b2md_ctx;
+
+/* ---------------------------------------------------------------- host-only */
+
+const char* b2md_last_error(void);
+int b2md_abi_version(void);
+
+/* tmd::build_species (src/model.cpp:68-129): re-centre on the COM, rotate into
+ * the principal frame (Jacobi, src/model.cpp:12-60), zero tiny moments. */
+int b2md_build_species(const b2md_site* sites, int n_sites, b2md_species* out);
+
+/* tmd::ewald_tune (src/ewald.cpp:8-28) */
+int b2md_ewald_tune(double delta, double cutoff, double box_length, double* alpha, int* kmax);
+
+/* number of Ewald k-vectors of the reference's half-space rule
+ * (src/ewald.cpp:77-104) */
+int b2md_ewald_kvector_count(int kmax, int* count);
+
+/* Row-block shard plan for `world` ranks: the i<j tile triangle (32-molecule
+ * tiles) is cut into contiguous tile rows with balanced candidate-pair counts,
+ * the GPU analogue of the reference's static split of the flat pair index
+ * (src/parallel.cpp:84-91).  Outputs the tile-row range [row_begin,row_end)
+ * and the k-vector range [k_begin,k_end) owned by `rank`. */
+int b2md_shard_plan(int n_molecules, int n_kvectors, int world, int rank, int* row_begin,
+                    int* row_end, int* k_begin, int* k_end, int64_t* candidate_pairs);
+
+/* ------------------------------------------------------------- device paths */
+
+/* tmd::ForceField::ForceField (src/parallel.cpp:55-72).  Validates exactly as
+ * the reference (PairTable ctor src/potentials.cpp:35-51, comp.validate
+ * src/model.cpp:244-268, Ewald ctor src/ewald.cpp:30-35).  `n_replicas`
+ * independent systems of the same composition are held and stepped together
+ * (1 for a plain ForceField).  `dt` > 0 makes the context an Engine
+ * (src/engine.cpp:63-66); dt <= 0 gives a force-field-only context. */
+int b2md_create(int device, const b2md_composition* comp, const b2md_ff_options* opts, double dt,
+                int n_replicas, b2md_ctx** out);
+void b2md_destroy(b2md_ctx* ctx);
+
+/* non-empty when Ewald parameters look too coarse (src/ewald.cpp:41-44) */
+const char* b2md_warning(const b2md_ctx* ctx);
+
+/* tmd::ForceField::evaluate(SystemState&) (src/parallel.cpp:79-122) with host
+ * buffers: positions (n*3, NOT wrapped — exactly like the reference) and
+ * orientations (n*4) in, forces/torques (n*3), energy and stats out.  For
+ * n_replicas > 1 all arrays are replica-major and energy/stats hold one entry
+ * per replica.  Any output pointer may be NULL. */
+int b2md_evaluate(b2md_ctx* ctx, const double* pos, const double* orient, double* force,
+                  double* torque, b2md_energy* energy, b2md_eval_stats* stats);
+
+/* tmd::Engine::set_state (src/engine.cpp:91-98): upload, wrap, compute forces. */
+int b2md_set_state(b2md_ctx* ctx, const double* pos, const double* orient, const double* vel,
+                   const double* ang_vel);
+
+/* tmd::Engine::step (src/engine.cpp:102-143), `nsteps` times, device
+ * resident.  Returns B2MD_NUMERICAL_ERROR like check_finite
+ * (src/model.cpp:288-302); the state then holds the end of the failing step. */
+int b2md_step(b2md_ctx* ctx, int64_t nsteps);
+
+/* tmd::Engine::state() (include/tmd/engine.hpp:60): download.  NULL skips. */
+int b2md_get_state(b2md_ctx* ctx, double* pos, double* orient, double* vel, double* ang_vel,
+                   double* force, double* torque, b2md_energy* energy, b2md_eval_stats* stats);
+
+/* COM partner search of the current device state (src/potentials.cpp:156-158
+ * single-site, src/potentials.cpp:209-213 multi-site): the i<j molecule pairs
+ * passing the test, as (i,j) int32 pairs sorted by i then j.  With
+ * pairs == NULL only the count is returned.  `replica` selects the system. */
+int b2md_pair_list(b2md_ctx* ctx, int replica, int32_t* pairs, int64_t capacity,
+                   int64_t* n_pairs);
+
+/* Multi-GPU row sharding (one process per GPU).  b2md_nccl_unique_id fills a
+ * 128-byte ncclUniqueId on the root; every rank then calls b2md_attach_nccl
+ * with the broadcast id.  After attaching, each rank evaluates only its shard
+ * of the tile triangle and k-vectors and one packed ncclAllReduce(sum, f64)
+ * over NVLink combines forces, torques and energy sums every evaluation. */
+int b2md_nccl_unique_id(char id[128]);
+int b2md_attach_nccl(b2md_ctx* ctx, const char id[128], int rank, int world);
+
+/* Opaque cudaStream_t of the context (for event timing by the caller). */
+void* b2md_stream(b2md_ctx* ctx);
+
+/* Per-kernel CUDA-event timing of the device step (bench instrumentation).
+ * enable != 0 records an event pair around every launch of each kernel
+ * family; b2md_kernel_times returns {name, total_ms, launches} rows. */
+int b2md_profile_enable(b2md_ctx* ctx, int enable);
+int b2md_kernel_times(b2md_ctx* ctx, int max_rows, char (*names)[32], double* total_ms,
+                      int64_t* launches, int* n_rows);
+
+/* Use a CUDA graph for the device step loop (default on). */
+int b2md_set_graphs(b2md_ctx* ctx, int enable);
+
+/* Measured FP64 (DFMA) peak of the device, GFLOP/s, from a short
+ * microbenchmark (roofline denominator). */
+int b2md_measure_fp64_peak(int device, double* gflops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* B200MD_H */

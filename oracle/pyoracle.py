@@ -1,0 +1,247 @@
+"""Python bindings of the CPU checkers.  TEST INFRASTRUCTURE ONLY — imported
+by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference leg, never by the product package.
+
+  OracleFF      oracle/liboracle.so      C restatement (tmd_oracle.c)
+  RefFF/RefEngine oracle/_ref/libtmdref.so the unmodified reference tmd_core
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+from paper_1507_07548_b200 import _abi
+from paper_1507_07548_b200.model import EnergyBreakdown, SystemComposition
+
+HERE = Path(__file__).resolve().parent
+ORACLE_LIB = HERE / "liboracle.so"
+REF_LIB = HERE / "_ref" / "libtmdref.so"
+
+_D = C.POINTER(C.c_double)
+_oracle = None
+_ref = None
+
+
+def _d(a):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_D)
+
+
+def oracle_lib():
+    global _oracle
+    if _oracle is None:
+        if not ORACLE_LIB.exists():
+            raise RuntimeError(f"{ORACLE_LIB} missing: run `make -C oracle`")
+        L = C.CDLL(str(ORACLE_LIB))
+        L.oracle_last_error.restype = C.c_char_p
+        L.oracle_build_species.argtypes = [C.POINTER(_abi.b2md_site), C.c_int, C.POINTER(_abi.b2md_species)]
+        L.oracle_ewald_tune.argtypes = [C.c_double, C.c_double, C.c_double, _D, C.POINTER(C.c_int)]
+        L.oracle_ff_create.argtypes = [C.POINTER(_abi.b2md_composition), C.POINTER(_abi.b2md_ff_options), C.POINTER(C.c_void_p)]
+        L.oracle_ff_destroy.argtypes = [C.c_void_p]
+        L.oracle_ff_warning.argtypes = [C.c_void_p]
+        L.oracle_ff_warning.restype = C.c_char_p
+        L.oracle_ff_kvector_count.argtypes = [C.c_void_p]
+        L.oracle_evaluate.argtypes = [C.c_void_p, _D, _D, _D, _D, C.POINTER(_abi.b2md_energy), C.POINTER(_abi.b2md_eval_stats)]
+        L.oracle_evaluate_shard.argtypes = [C.c_void_p, _D, _D, C.c_int, C.c_int, C.c_int, C.c_int, _D, _D, _D]
+        L.oracle_pair_list.argtypes = [C.c_void_p, _D, C.POINTER(C.c_int32), C.c_int64]
+        L.oracle_pair_list.restype = C.c_int64
+        L.oracle_wrap.argtypes = [C.c_int, C.c_double, _D]
+        L.oracle_step.argtypes = [C.c_void_p, C.c_double, C.c_int64, _D, _D, _D, _D, _D, _D,
+                                  C.POINTER(_abi.b2md_energy), C.POINTER(_abi.b2md_eval_stats)]
+        _oracle = L
+    return _oracle
+
+
+def ref_available() -> bool:
+    return REF_LIB.exists()
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        if not REF_LIB.exists():
+            raise RuntimeError(f"{REF_LIB} missing: run `make -C oracle` where /root/reference exists")
+        L = C.CDLL(str(REF_LIB))
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_build_species.argtypes = [C.POINTER(_abi.b2md_site), C.c_int, C.POINTER(_abi.b2md_species)]
+        L.ref_ewald_tune.argtypes = [C.c_double, C.c_double, C.c_double, _D, C.POINTER(C.c_int)]
+        L.ref_ff_create.argtypes = [C.POINTER(_abi.b2md_composition), C.POINTER(_abi.b2md_ff_options), C.POINTER(C.c_void_p)]
+        L.ref_ff_destroy.argtypes = [C.c_void_p]
+        L.ref_ff_warning.argtypes = [C.c_void_p]
+        L.ref_ff_warning.restype = C.c_char_p
+        L.ref_evaluate.argtypes = [C.c_void_p, _D, _D, _D, _D, C.POINTER(_abi.b2md_energy), _D]
+        L.ref_pair_list.argtypes = [C.c_void_p, _D, C.POINTER(C.c_int32), C.c_int64]
+        L.ref_pair_list.restype = C.c_int64
+        L.ref_engine_create.argtypes = [C.POINTER(_abi.b2md_composition), C.POINTER(_abi.b2md_ff_options), C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]
+        L.ref_engine_destroy.argtypes = [C.c_void_p]
+        L.ref_engine_set_state.argtypes = [C.c_void_p, _D, _D, _D, _D]
+        L.ref_engine_step.argtypes = [C.c_void_p, C.c_int64]
+        L.ref_engine_get_state.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, _D, C.POINTER(_abi.b2md_energy), _D]
+        _ref = L
+    return _ref
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+def _check(lib, prefix, rc):
+    if rc:
+        raise OracleError(rc, getattr(lib, prefix + "_last_error")().decode())
+
+
+def build_species_c(sites, which="oracle") -> _abi.b2md_species:
+    lib = oracle_lib() if which == "oracle" else ref_lib()
+    arr = (_abi.b2md_site * max(len(sites), 1))(*[s.to_c() for s in sites])
+    out = _abi.b2md_species()
+    fn = lib.oracle_build_species if which == "oracle" else lib.ref_build_species
+    _check(lib, which if which == "oracle" else "ref", fn(arr, len(sites), C.byref(out)))
+    return out
+
+
+def ewald_tune(delta, cutoff, box, which="oracle"):
+    lib = oracle_lib() if which == "oracle" else ref_lib()
+    a, k = C.c_double(), C.c_int()
+    fn = lib.oracle_ewald_tune if which == "oracle" else lib.ref_ewald_tune
+    _check(lib, "oracle" if which == "oracle" else "ref", fn(delta, cutoff, box, C.byref(a), C.byref(k)))
+    return a.value, k.value
+
+
+class _FF:
+    prefix = "oracle"
+
+    def __init__(self, comp: SystemComposition, opts):
+        self.lib = oracle_lib() if self.prefix == "oracle" else ref_lib()
+        self.comp = comp
+        self.n = comp.molecule_count()
+        cc, self._keep = comp.to_c()
+        oc = opts.to_c()
+        h = C.c_void_p()
+        _check(self.lib, self.prefix, getattr(self.lib, self.prefix + "_ff_create")(C.byref(cc), C.byref(oc), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            getattr(self.lib, self.prefix + "_ff_destroy")(self.h)
+            self.h = None
+
+    @property
+    def warning(self) -> str:
+        return getattr(self.lib, self.prefix + "_ff_warning")(self.h).decode()
+
+    def pair_list(self, pos) -> np.ndarray:
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        fn = getattr(self.lib, self.prefix + "_pair_list")
+        n = fn(self.h, _d(pos), None, 0)
+        out = np.zeros((n, 2), dtype=np.int32)
+        if n:
+            fn(self.h, _d(pos), out.ctypes.data_as(C.POINTER(C.c_int32)), n)
+        return out
+
+
+class OracleFF(_FF):
+    """C restatement (serial ForceField::evaluate + Engine::step)."""
+
+    prefix = "oracle"
+
+    def evaluate(self, pos, orient):
+        n = self.n
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(n, 3)
+        orient = np.ascontiguousarray(orient, dtype=np.float64).reshape(n, 4)
+        f = np.zeros((n, 3))
+        t = np.zeros((n, 3))
+        e = _abi.b2md_energy()
+        s = _abi.b2md_eval_stats()
+        _check(self.lib, "oracle", self.lib.oracle_evaluate(self.h, _d(pos), _d(orient), _d(f), _d(t), C.byref(e), C.byref(s)))
+        return {"force": f, "torque": t, "energy": EnergyBreakdown.from_c(e), "virial": s.virial,
+                "s1": s.s1, "s2": s.s2, "com_pairs": s.com_pairs}
+
+    def evaluate_shard(self, pos, orient, row_begin, row_end, k_begin, k_end):
+        n = self.n
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        orient = np.ascontiguousarray(orient, dtype=np.float64)
+        f = np.zeros((n, 3))
+        t = np.zeros((n, 3))
+        sums = np.zeros(8)
+        _check(self.lib, "oracle", self.lib.oracle_evaluate_shard(self.h, _d(pos), _d(orient), row_begin, row_end, k_begin, k_end, _d(f), _d(t), _d(sums)))
+        return f, t, sums
+
+    def run(self, dt, nsteps, pos, orient, vel, ang_vel):
+        """set_state (wrap + forces) then Engine::step x nsteps; returns the state."""
+        n = self.n
+        pos = np.array(pos, dtype=np.float64).reshape(n, 3)
+        orient = np.array(orient, dtype=np.float64).reshape(n, 4)
+        vel = np.array(vel, dtype=np.float64).reshape(n, 3)
+        ang = np.array(ang_vel, dtype=np.float64).reshape(n, 3)
+        self.lib.oracle_wrap(n, self.comp.box_length, _d(pos))
+        r = self.evaluate(pos, orient)
+        f, t = r["force"], r["torque"]
+        e = _abi.b2md_energy()
+        s = _abi.b2md_eval_stats()
+        if nsteps > 0:
+            _check(self.lib, "oracle", self.lib.oracle_step(self.h, dt, nsteps, _d(pos), _d(orient), _d(vel), _d(ang), _d(f), _d(t), C.byref(e), C.byref(s)))
+            energy, virial = EnergyBreakdown.from_c(e), s.virial
+        else:
+            energy, virial = r["energy"], r["virial"]
+        return {"pos": pos, "orient": orient, "vel": vel, "ang_vel": ang, "force": f, "torque": t,
+                "energy": energy, "virial": virial}
+
+
+class RefFF(_FF):
+    """The unmodified reference tmd::ForceField (workers from opts)."""
+
+    prefix = "ref"
+
+    def evaluate(self, pos, orient):
+        n = self.n
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(n, 3)
+        orient = np.ascontiguousarray(orient, dtype=np.float64).reshape(n, 4)
+        f = np.zeros((n, 3))
+        t = np.zeros((n, 3))
+        e = _abi.b2md_energy()
+        v = np.zeros(1)
+        _check(self.lib, "ref", self.lib.ref_evaluate(self.h, _d(pos), _d(orient), _d(f), _d(t), C.byref(e), _d(v)))
+        return {"force": f, "torque": t, "energy": EnergyBreakdown.from_c(e), "virial": float(v[0])}
+
+
+class RefEngine:
+    """The unmodified reference tmd::Engine (thermostat off, NVE steps)."""
+
+    def __init__(self, comp: SystemComposition, opts, dt: float, seed: int = 1):
+        self.lib = ref_lib()
+        self.comp = comp
+        self.n = comp.molecule_count()
+        cc, self._keep = comp.to_c()
+        oc = opts.to_c()
+        h = C.c_void_p()
+        _check(self.lib, "ref", self.lib.ref_engine_create(C.byref(cc), C.byref(oc), dt, seed, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.ref_engine_destroy(self.h)
+            self.h = None
+
+    def set_state(self, pos, orient, vel, ang_vel):
+        arr = [np.ascontiguousarray(a, dtype=np.float64) for a in (pos, orient, vel, ang_vel)]
+        _check(self.lib, "ref", self.lib.ref_engine_set_state(self.h, *[_d(a) for a in arr]))
+
+    def step(self, n=1):
+        _check(self.lib, "ref", self.lib.ref_engine_step(self.h, n))
+
+    def state(self):
+        n = self.n
+        out = {k: np.zeros((n, w)) for k, w in (("pos", 3), ("orient", 4), ("vel", 3), ("ang_vel", 3), ("force", 3), ("torque", 3))}
+        e = _abi.b2md_energy()
+        v = np.zeros(1)
+        self.lib.ref_engine_get_state(self.h, *[_d(out[k]) for k in ("pos", "orient", "vel", "ang_vel", "force", "torque")], C.byref(e), _d(v))
+        out["energy"] = EnergyBreakdown.from_c(e)
+        out["virial"] = float(v[0])
+        return out

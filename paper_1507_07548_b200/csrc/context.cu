@@ -1,0 +1,919 @@
+// b200md context: device memory, launch sequences, CUDA graphs, NCCL and
+// the C ABI declared in include/b200md.h.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+
+#include <string>
+#include <vector>
+
+#include "../../include/b200md.h"
+#include "kernels.cuh"
+#include "model.hpp"
+#include "search_geometry.hpp"
+
+using namespace b2md;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(B2MD_CUDA_ERROR, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                          " at " #expr);                                  \
+  } while (0)
+
+#define NC(expr)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (expr);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      return set_err(B2MD_CUDA_ERROR, std::string("NCCL error: ") + ncclGetErrorString(r_) + \
+                                          " at " #expr);                                \
+  } while (0)
+
+#define TRY(expr)          \
+  do {                     \
+    int rc_ = (expr);      \
+    if (rc_) return rc_;   \
+  } while (0)
+
+int hi32(double x) {
+  int64_t b;
+  std::memcpy(&b, &x, 8);
+  return int(b >> 32);
+}
+
+template <typename T>
+int dalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  CU(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
+  CU(cudaMemset(*p, 0, count * sizeof(T)));
+  return B2MD_OK;
+}
+
+// AoS <-> SoA staging kernels (host layout Vec3 / Quat of include/tmd/geom.hpp)
+__global__ void k_aos_to_soa(const double* aos, int count, int width, double* d0, double* d1,
+                             double* d2, double* d3) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  d0[i] = aos[size_t(i) * width];
+  d1[i] = aos[size_t(i) * width + 1];
+  d2[i] = aos[size_t(i) * width + 2];
+  if (width == 4) d3[i] = aos[size_t(i) * width + 3];
+}
+__global__ void k_soa_to_aos(double* aos, int count, int width, const double* d0, const double* d1,
+                             const double* d2, const double* d3) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  aos[size_t(i) * width] = d0[i];
+  aos[size_t(i) * width + 1] = d1[i];
+  aos[size_t(i) * width + 2] = d2[i];
+  if (width == 4) aos[size_t(i) * width + 3] = d3[i];
+}
+
+enum Family { F_OFFSETS, F_SEARCH, F_FORCE, F_EWALD_TAB, F_EWALD_SK, F_EWALD_F, F_REDUCE,
+              F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_COUNT };
+const char* kFamilyName[F_COUNT] = {"offsets",  "search", "force",   "ewald_tables", "ewald_sk",
+                                    "ewald_force", "reduce", "kick_drift", "kick", "allreduce"};
+
+}  // namespace
+
+struct b2md_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ModelTables t;
+  SearchGeometry g;
+  int R = 1;
+  double dt = 0.0;
+  bool engine = false;
+  bool state_valid = false;
+  // device tables
+  DevTables* d_tab = nullptr;
+  int* d_species_of = nullptr;
+  int* d_site_begin = nullptr;
+  // state
+  double* d_state = nullptr;  // px..wz (13 arrays of R*n)
+  double* d_fbuf = nullptr;   // fx fy fz tx ty tz (6*R*n) + sums (R*kNumSums): allreduce unit
+  double* d_off = nullptr;    // 3 * R * total_sites
+  double* d_stage = nullptr;  // AoS staging, 4*R*n
+  uint32_t* d_mask = nullptr;
+  double* d_row_scal = nullptr;
+  uint32_t* d_super = nullptr;
+  int n_super_tiles = 0;
+  int* d_error = nullptr;
+  StateDev st{};
+  SysDev sys{};
+  // ewald
+  int nq = 0;
+  int* d_q_mol = nullptr;
+  int* d_q_site = nullptr;
+  double* d_q_val = nullptr;
+  int* d_mol_qbegin = nullptr;
+  DevKVec* d_kv = nullptr;
+  double2* d_etab = nullptr;
+  double2* d_S = nullptr;
+  double* d_uk = nullptr;
+  // sharding
+  int rank = 0, world = 1;
+  int row_begin = 0, row_end = 0, k_begin = 0, k_end = 0;
+  ncclComm_t comm = nullptr;
+  // graphs
+  bool use_graphs = true;
+  cudaGraphExec_t step_graph = nullptr;
+  // profiling
+  bool profile = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  size_t ev_used = 0;
+  std::vector<int> ev_family;
+  double prof_ms[F_COUNT] = {};
+  int64_t prof_n[F_COUNT] = {};
+  // host scratch
+  std::vector<double> h_sums;
+  std::string warning;
+};
+
+namespace {
+
+int n_total(const b2md_ctx* c) { return c->t.n * c->R; }
+
+int prof_begin(b2md_ctx* c, int fam) {
+  if (!c->profile) return B2MD_OK;
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    c->ev_pool.push_back({a, b});
+    c->ev_family.push_back(fam);
+  }
+  c->ev_family[c->ev_used] = fam;
+  CU(cudaEventRecord(c->ev_pool[c->ev_used].first, c->stream));
+  return B2MD_OK;
+}
+
+int prof_end(b2md_ctx* c) {
+  if (!c->profile) return B2MD_OK;
+  CU(cudaEventRecord(c->ev_pool[c->ev_used].second, c->stream));
+  ++c->ev_used;
+  return B2MD_OK;
+}
+
+int prof_harvest(b2md_ctx* c) {
+  if (c->ev_used == 0) return B2MD_OK;
+  CU(cudaStreamSynchronize(c->stream));
+  for (size_t k = 0; k < c->ev_used; ++k) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, c->ev_pool[k].first, c->ev_pool[k].second));
+    c->prof_ms[c->ev_family[k]] += ms;
+    c->prof_n[c->ev_family[k]] += 1;
+  }
+  c->ev_used = 0;
+  return B2MD_OK;
+}
+
+#define PROF(ctx, fam, launch)      \
+  do {                              \
+    TRY(prof_begin(ctx, fam));      \
+    launch;                         \
+    CU(cudaGetLastError());         \
+    TRY(prof_end(ctx));             \
+  } while (0)
+
+int launch_offsets(b2md_ctx* c) {
+  if (!c->t.any_offsets) return B2MD_OK;
+  const int nt = n_total(c);
+  PROF(c, F_OFFSETS, (k_offsets<<<(nt + 255) / 256, 256, 0, c->stream>>>(c->sys, c->st)));
+  return B2MD_OK;
+}
+
+int launch_search(b2md_ctx* c) {
+  if (c->n_super_tiles == 0) return B2MD_OK;
+  SearchArgs a;
+  a.s = c->sys;
+  a.px = c->st.px;
+  a.py = c->st.py;
+  a.pz = c->st.pz;
+  a.mask = c->d_mask;
+  a.super_tiles = c->d_super;
+  a.rc2 = c->t.single_site_path ? c->t.rc2 : c->t.rmax2[0];
+  const bool multi = c->t.ns > 1;
+  dim3 grid(c->n_super_tiles, c->R);
+  const int st = c->g.st;
+#define SEARCH_CASE(ST)                                                                  \
+  case ST:                                                                               \
+    if (multi)                                                                           \
+      PROF(c, F_SEARCH, (k_search<ST, true><<<grid, ST * 32, 0, c->stream>>>(a)));       \
+    else                                                                                 \
+      PROF(c, F_SEARCH, (k_search<ST, false><<<grid, ST * 32, 0, c->stream>>>(a)));      \
+    break;
+  switch (st) {
+    SEARCH_CASE(1)
+    SEARCH_CASE(2)
+    SEARCH_CASE(4)
+    SEARCH_CASE(8)
+    default:
+      return set_err(B2MD_INVALID_ARGUMENT, "bad super-tile size");
+  }
+#undef SEARCH_CASE
+  return B2MD_OK;
+}
+
+ForceArgs force_args(b2md_ctx* c) {
+  ForceArgs a;
+  a.s = c->sys;
+  a.st = c->st;
+  a.mask = c->d_mask;
+  a.row_scal = c->d_row_scal;
+  a.c12 = 0.0;
+  a.c6 = 0.0;
+  if (!c->t.lj.empty() && !c->t.lj[0].empty()) {
+    a.c12 = c->t.lj[0][0].c12;
+    a.c6 = c->t.lj[0][0].c6;
+  }
+  a.rc2 = c->t.rc2;
+  a.alpha = c->t.alpha;
+  a.two_alpha_over_sqrt_pi = 2.0 * c->t.alpha / std::sqrt(3.14159265358979323846);
+  a.rf_r3inv = c->t.rf_r3inv;
+  a.rf_shift = c->t.rf_shift;
+  a.vderiv = c->t.vderiv ? 1 : 0;
+  a.row_begin = 0;
+  a.row_end = c->t.n;
+  return a;
+}
+
+int launch_force(b2md_ctx* c) {
+  ForceArgs a = force_args(c);
+  dim3 grid((c->t.n + 7) / 8, c->R);
+  if (c->t.single_site_path) {
+    if (c->t.ns > 1)
+      PROF(c, F_FORCE, (k_force_single<true><<<grid, 256, 0, c->stream>>>(a)));
+    else
+      PROF(c, F_FORCE, (k_force_single<false><<<grid, 256, 0, c->stream>>>(a)));
+  } else if (c->t.method == B2MD_METHOD_EWALD) {
+    PROF(c, F_FORCE, (k_force_multi<2><<<grid, 256, 0, c->stream>>>(a)));
+  } else if (c->t.method == B2MD_METHOD_REACTION_FIELD) {
+    PROF(c, F_FORCE, (k_force_multi<1><<<grid, 256, 0, c->stream>>>(a)));
+  } else {
+    PROF(c, F_FORCE, (k_force_multi<0><<<grid, 256, 0, c->stream>>>(a)));
+  }
+  return B2MD_OK;
+}
+
+EwaldArgs ewald_args(b2md_ctx* c) {
+  EwaldArgs a;
+  a.s = c->sys;
+  a.st = c->st;
+  a.nq = c->nq;
+  a.kmax = c->t.kmax;
+  a.nk = c->k_end - c->k_begin;
+  a.k_begin = c->k_begin;
+  a.q_mol = c->d_q_mol;
+  a.q_site = c->d_q_site;
+  a.q_val = c->d_q_val;
+  a.mol_qbegin = c->d_mol_qbegin;
+  a.kv = c->d_kv;
+  a.tab = c->d_etab;
+  a.S = c->d_S;
+  a.uk = c->d_uk;
+  a.nk_total = int(c->t.kv.size());
+  a.two_pi_over_L = 2.0 * 3.14159265358979323846 / c->t.box;
+  return a;
+}
+
+int launch_ewald(b2md_ctx* c) {
+  if (!c->t.ewald || c->nq == 0) return B2MD_OK;
+  EwaldArgs a = ewald_args(c);
+  const int nt = c->nq * c->R;
+  PROF(c, F_EWALD_TAB, (k_ewald_tables<<<(nt + 127) / 128, 128, 0, c->stream>>>(a)));
+  if (a.nk > 0) {
+    PROF(c, F_EWALD_SK, (k_ewald_sk<<<dim3(a.nk, c->R), 256, 0, c->stream>>>(a)));
+    PROF(c, F_EWALD_F, (k_ewald_force<<<dim3((c->t.n + 7) / 8, c->R), 256, 0, c->stream>>>(a)));
+  }
+  return B2MD_OK;
+}
+
+int launch_reduce(b2md_ctx* c) {
+  double* sums = c->d_fbuf + size_t(6) * n_total(c);
+  const bool ew = c->t.ewald && c->nq > 0;
+  PROF(c, F_REDUCE,
+       (k_reduce_sums<<<dim3(kNumSums, c->R), 256, 0, c->stream>>>(
+           c->d_row_scal, ew ? c->d_uk : nullptr, c->t.n, c->g.n_pad, int(c->t.kv.size()),
+           c->k_begin, c->k_end, sums)));
+  return B2MD_OK;
+}
+
+int launch_allreduce(b2md_ctx* c) {
+  if (c->world <= 1 || !c->comm) return B2MD_OK;
+  const size_t count = size_t(6) * n_total(c) + size_t(kNumSums) * c->R;
+  TRY(prof_begin(c, F_ALLREDUCE));
+  NC(ncclAllReduce(c->d_fbuf, c->d_fbuf, count, ncclDouble, ncclSum, c->comm, c->stream));
+  TRY(prof_end(c));
+  return B2MD_OK;
+}
+
+// ForceField::evaluate (src/parallel.cpp:79-122) on the device state.
+int enqueue_forces(b2md_ctx* c, bool offsets) {
+  if (offsets) TRY(launch_offsets(c));
+  TRY(launch_search(c));
+  TRY(launch_force(c));
+  TRY(launch_ewald(c));
+  TRY(launch_reduce(c));
+  TRY(launch_allreduce(c));
+  return B2MD_OK;
+}
+
+StepArgs step_args(b2md_ctx* c) {
+  StepArgs a;
+  a.s = c->sys;
+  a.st = c->st;
+  a.dt = c->dt;
+  a.error_mol = c->d_error;
+  a.write_offsets = c->t.any_offsets ? 1 : 0;
+  return a;
+}
+
+// Engine::step (src/engine.cpp:102-143)
+int enqueue_step(b2md_ctx* c) {
+  StepArgs a = step_args(c);
+  const int nt = n_total(c);
+  PROF(c, F_KICK_DRIFT, (k_kick_drift<<<(nt + 255) / 256, 256, 0, c->stream>>>(a)));
+  TRY(enqueue_forces(c, false));
+  PROF(c, F_KICK, (k_kick<<<(nt + 255) / 256, 256, 0, c->stream>>>(a)));
+  return B2MD_OK;
+}
+
+int build_step_graph(b2md_ctx* c) {
+  if (c->step_graph) return B2MD_OK;
+  cudaGraph_t graph;
+  const bool prof = c->profile;
+  c->profile = false;
+  CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_step(c);
+  cudaGraph_t g2;
+  cudaError_t e = cudaStreamEndCapture(c->stream, &g2);
+  c->profile = prof;
+  if (rc) return rc;
+  CU(e);
+  graph = g2;
+  CU(cudaGraphInstantiate(&c->step_graph, graph, 0));
+  CU(cudaGraphDestroy(graph));
+  return B2MD_OK;
+}
+
+int upload_aos(b2md_ctx* c, const double* host, int width, double* d0, double* d1, double* d2,
+               double* d3) {
+  const int nt = n_total(c);
+  CU(cudaMemcpyAsync(c->d_stage, host, sizeof(double) * width * nt, cudaMemcpyHostToDevice, c->stream));
+  k_aos_to_soa<<<(nt + 255) / 256, 256, 0, c->stream>>>(c->d_stage, nt, width, d0, d1, d2, d3);
+  CU(cudaGetLastError());
+  return B2MD_OK;
+}
+
+int download_aos(b2md_ctx* c, double* host, int width, const double* d0, const double* d1,
+                 const double* d2, const double* d3) {
+  const int nt = n_total(c);
+  k_soa_to_aos<<<(nt + 255) / 256, 256, 0, c->stream>>>(c->d_stage, nt, width, d0, d1, d2, d3);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(host, c->d_stage, sizeof(double) * width * nt, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return B2MD_OK;
+}
+
+// EnergyBreakdown assembly (src/parallel.cpp:101-120)
+void assemble(const b2md_ctx* c, const double* sums, b2md_energy* e, b2md_eval_stats* st) {
+  const ModelTables& t = c->t;
+  if (e) {
+    std::memset(e, 0, sizeof *e);
+    e->lj = sums[0];
+    e->elec_real = sums[1];
+    e->rf = sums[2];
+    const double volume = t.box * t.box * t.box;
+    e->lrc = t.lrc_k / volume;
+    if (t.vderiv) {
+      e->du_dv_explicit = sums[3] / (3.0 * volume);
+      e->d2u_dv2_explicit = (sums[4] - 2.0 * sums[3]) / (9.0 * volume * volume);
+      e->du_dv_lrc = -t.lrc_k / (volume * volume);
+      e->d2u_dv2_lrc = 2.0 * t.lrc_k / (volume * volume * volume);
+    }
+    if (t.ewald) {
+      e->elec_recip = sums[7];
+      e->elec_self = t.self_plus_intra;
+    }
+  }
+  if (st) {
+    st->virial = sums[5];
+    st->s1 = sums[3];
+    st->s2 = sums[4];
+    st->com_pairs = int64_t(sums[6]);
+  }
+}
+
+int download_scalars(b2md_ctx* c, b2md_energy* e, b2md_eval_stats* st) {
+  if (!e && !st) return B2MD_OK;
+  c->h_sums.resize(size_t(kNumSums) * c->R);
+  CU(cudaMemcpyAsync(c->h_sums.data(), c->d_fbuf + size_t(6) * n_total(c),
+                     sizeof(double) * kNumSums * c->R, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (int r = 0; r < c->R; ++r)
+    assemble(c, c->h_sums.data() + size_t(r) * kNumSums, e ? e + r : nullptr, st ? st + r : nullptr);
+  return B2MD_OK;
+}
+
+int setup_shard(b2md_ctx* c) {
+  int64_t cand = 0;
+  shard_plan(c->t.n, int(c->t.kv.size()), c->world, c->rank, c->row_begin, c->row_end, c->k_begin,
+             c->k_end, cand);
+  // super tiles (SI, SJ), SI in this rank's super-tile rows, SI <= SJ
+  std::vector<uint32_t> list;
+  const int s0 = c->row_begin / c->g.st, s1 = (c->row_end + c->g.st - 1) / c->g.st;
+  for (int si = s0; si < s1; ++si)
+    for (int sj = si; sj < c->g.n_super; ++sj) list.push_back((uint32_t(si) << 16) | uint32_t(sj));
+  if (c->d_super) cudaFree(c->d_super);
+  c->d_super = nullptr;
+  TRY(dalloc(&c->d_super, list.size()));
+  if (!list.empty())
+    CU(cudaMemcpy(c->d_super, list.data(), sizeof(uint32_t) * list.size(), cudaMemcpyHostToDevice));
+  c->n_super_tiles = int(list.size());
+  // a fresh bit matrix: only this rank's tiles are ever written afterwards
+  CU(cudaMemset(c->d_mask, 0, sizeof(uint32_t) * size_t(c->R) * c->g.n_pad * c->g.words));
+  if (c->step_graph) {
+    cudaGraphExecDestroy(c->step_graph);
+    c->step_graph = nullptr;
+  }
+  return B2MD_OK;
+}
+
+int create_impl(int device, const b2md_composition* comp, const b2md_ff_options* opts, double dt,
+                int R, b2md_ctx* c) {
+  std::string err;
+  if (int rc = build_tables(*comp, *opts, c->t, err)) return set_err(rc, err);
+  const ModelTables& t = c->t;
+  if (t.ns > kMaxSpecies) return set_err(B2MD_CONFIG_ERROR, "b200md: at most 8 species");
+  size_t nlj = 0, nqq = 0;
+  for (const auto& v : t.lj) nlj += v.size();
+  for (const auto& v : t.qq) nqq += v.size();
+  if (nlj > size_t(kMaxLjTerms) || nqq > size_t(kMaxQqTerms))
+    return set_err(B2MD_CONFIG_ERROR, "b200md: too many site-site terms");
+  if (R < 1) return set_err(B2MD_INVALID_ARGUMENT, "n_replicas must be >= 1");
+  if (dt > 0.0) {
+    c->engine = true;
+    c->dt = dt;
+  }
+  c->R = R;
+  c->device = device;
+  c->warning = t.warning;
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return set_err(B2MD_CUDA_ERROR, "b200md: no such CUDA device");
+  CU(cudaSetDevice(device));
+  CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->g = search_geometry(t.n);
+  if (size_t(t.n) * size_t(t.n) > (size_t(1) << 32))
+    return set_err(B2MD_CONFIG_ERROR, "b200md: too many molecules");
+
+  // tables
+  DevTables* h = new DevTables();
+  std::memset(h, 0, sizeof(DevTables));
+  h->ns = t.ns;
+  for (int s = 0; s < t.ns; ++s) {
+    const b2md_species& sp = t.species[s];
+    DevSpecies& d = h->species[s];
+    d.n_sites = sp.n_sites;
+    d.rotational_dof = sp.rotational_dof;
+    const double n2 = sp.sites[0].body_pos[0] * sp.sites[0].body_pos[0] +
+                      sp.sites[0].body_pos[1] * sp.sites[0].body_pos[1] +
+                      sp.sites[0].body_pos[2] * sp.sites[0].body_pos[2];
+    d.centred = (sp.n_sites == 1 && n2 == 0.0) ? 1 : 0;
+    d.total_mass = sp.total_mass;
+    for (int k = 0; k < 3; ++k) d.inertia[k] = sp.inertia_principal[k];
+    for (int k = 0; k < sp.n_sites; ++k)
+      for (int x = 0; x < 3; ++x) d.body[k][x] = sp.sites[k].body_pos[x];
+  }
+  int lj_at = 0, qq_at = 0;
+  for (int p = 0; p < t.ns * t.ns; ++p) {
+    DevPairInfo& pi = h->pair[p];
+    pi.lj_begin = lj_at;
+    pi.lj_count = int(t.lj[p].size());
+    for (const auto& term : t.lj[p]) h->lj[lj_at++] = {term.a, term.b, term.c12, term.c6};
+    pi.qq_begin = qq_at;
+    pi.qq_count = int(t.qq[p].size());
+    for (const auto& term : t.qq[p]) h->qq[qq_at++] = {term.a, term.b, term.qq};
+    pi.rmax2 = t.single_site_path ? t.rc2 : t.rmax2[p];
+  }
+  int rc = dalloc(&c->d_tab, 1);
+  if (!rc) rc = cudaMemcpy(c->d_tab, h, sizeof(DevTables), cudaMemcpyHostToDevice) ? B2MD_CUDA_ERROR : 0;
+  delete h;
+  if (rc) return set_err(B2MD_CUDA_ERROR, "b200md: table upload failed");
+  TRY(dalloc(&c->d_species_of, t.n));
+  TRY(dalloc(&c->d_site_begin, t.n + 1));
+  CU(cudaMemcpy(c->d_species_of, t.species_of.data(), sizeof(int) * t.n, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(c->d_site_begin, t.site_begin.data(), sizeof(int) * (t.n + 1), cudaMemcpyHostToDevice));
+
+  const size_t nt = size_t(t.n) * R;
+  TRY(dalloc(&c->d_state, 13 * nt));
+  TRY(dalloc(&c->d_fbuf, 6 * nt + size_t(kNumSums) * R));
+  TRY(dalloc(&c->d_off, 3 * size_t(t.total_sites) * R));
+  TRY(dalloc(&c->d_stage, 4 * nt));
+  TRY(dalloc(&c->d_mask, size_t(R) * c->g.n_pad * c->g.words));
+  TRY(dalloc(&c->d_row_scal, size_t(R) * kNumRowScalars * c->g.n_pad));
+  TRY(dalloc(&c->d_error, 1));
+  const int big = INT_MAX;
+  CU(cudaMemcpy(c->d_error, &big, sizeof(int), cudaMemcpyHostToDevice));
+  double* s = c->d_state;
+  c->st.px = s + 0 * nt;
+  c->st.py = s + 1 * nt;
+  c->st.pz = s + 2 * nt;
+  c->st.qw = s + 3 * nt;
+  c->st.qx = s + 4 * nt;
+  c->st.qy = s + 5 * nt;
+  c->st.qz = s + 6 * nt;
+  c->st.vx = s + 7 * nt;
+  c->st.vy = s + 8 * nt;
+  c->st.vz = s + 9 * nt;
+  c->st.wx = s + 10 * nt;
+  c->st.wy = s + 11 * nt;
+  c->st.wz = s + 12 * nt;
+  c->st.fx = c->d_fbuf + 0 * nt;
+  c->st.fy = c->d_fbuf + 1 * nt;
+  c->st.fz = c->d_fbuf + 2 * nt;
+  c->st.tx = c->d_fbuf + 3 * nt;
+  c->st.ty = c->d_fbuf + 4 * nt;
+  c->st.tz = c->d_fbuf + 5 * nt;
+  const size_t ns3 = size_t(t.total_sites) * R;
+  c->st.ox = c->d_off;
+  c->st.oy = c->d_off + ns3;
+  c->st.oz = c->d_off + 2 * ns3;
+
+  c->sys.n = t.n;
+  c->sys.R = R;
+  c->sys.total_sites = t.total_sites;
+  c->sys.n_pad = c->g.n_pad;
+  c->sys.words = c->g.words;
+  c->sys.ns = t.ns;
+  c->sys.species_of = c->d_species_of;
+  c->sys.site_begin = c->d_site_begin;
+  c->sys.tab = c->d_tab;
+  MinImage& mi = c->sys.mi;
+  mi.L = t.box;
+  mi.negL = -t.box;
+  mi.hi_lo = hi32(0.5 * t.box);
+  mi.hi_hi = mi.hi_lo + 1;
+  mi.hi_max = hi32(1.5 * t.box) - 1;
+
+  // Ewald
+  if (t.ewald) {
+    c->nq = int(t.charged.size());
+    std::vector<int> qm, qs, qb(t.n + 1, 0);
+    std::vector<double> qv;
+    for (const auto& ch : t.charged) {
+      qm.push_back(ch.mol);
+      qs.push_back(ch.site);
+      qv.push_back(ch.q);
+      qb[ch.mol + 1]++;
+    }
+    for (int m = 0; m < t.n; ++m) qb[m + 1] += qb[m];
+    TRY(dalloc(&c->d_q_mol, c->nq));
+    TRY(dalloc(&c->d_q_site, c->nq));
+    TRY(dalloc(&c->d_q_val, c->nq));
+    TRY(dalloc(&c->d_mol_qbegin, t.n + 1));
+    if (c->nq) {
+      CU(cudaMemcpy(c->d_q_mol, qm.data(), sizeof(int) * c->nq, cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(c->d_q_site, qs.data(), sizeof(int) * c->nq, cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(c->d_q_val, qv.data(), sizeof(double) * c->nq, cudaMemcpyHostToDevice));
+    }
+    CU(cudaMemcpy(c->d_mol_qbegin, qb.data(), sizeof(int) * (t.n + 1), cudaMemcpyHostToDevice));
+    std::vector<DevKVec> kv;
+    for (const auto& k : t.kv) kv.push_back({k.kx, k.ky, k.kz, k.coeff, k.nx, k.ny, k.nz, 0});
+    TRY(dalloc(&c->d_kv, kv.size()));
+    if (!kv.empty())
+      CU(cudaMemcpy(c->d_kv, kv.data(), sizeof(DevKVec) * kv.size(), cudaMemcpyHostToDevice));
+    TRY(dalloc(&c->d_etab, size_t(R) * 3 * (t.kmax + 1) * std::max(c->nq, 1)));
+    TRY(dalloc(&c->d_S, size_t(R) * std::max<size_t>(kv.size(), 1)));
+    TRY(dalloc(&c->d_uk, size_t(R) * std::max<size_t>(kv.size(), 1)));
+  }
+  c->rank = 0;
+  c->world = 1;
+  TRY(setup_shard(c));
+  CU(cudaDeviceSynchronize());
+  return B2MD_OK;
+}
+
+void free_ctx(b2md_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
+  for (auto& e : c->ev_pool) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  if (c->comm) ncclCommDestroy(c->comm);
+  void* ptrs[] = {c->d_tab,   c->d_species_of, c->d_site_begin, c->d_state, c->d_fbuf, c->d_off,
+                  c->d_stage, c->d_mask,       c->d_row_scal,   c->d_super, c->d_error, c->d_q_mol,
+                  c->d_q_site, c->d_q_val,     c->d_mol_qbegin, c->d_kv,    c->d_etab,  c->d_S,
+                  c->d_uk};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int check_error_flag(b2md_ctx* c) {
+  int flag = INT_MAX;
+  CU(cudaMemcpyAsync(&flag, c->d_error, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (flag == INT_MAX) return B2MD_OK;
+  const int r = flag / c->t.n, i = flag % c->t.n;
+  double v[6];
+  const size_t nt = n_total(c);
+  const double* srcs[6] = {c->st.px + flag, c->st.py + flag, c->st.pz + flag,
+                           c->st.vx + flag, c->st.vy + flag, c->st.vz + flag};
+  for (int k = 0; k < 6; ++k) CU(cudaMemcpy(&v[k], srcs[k], sizeof(double), cudaMemcpyDeviceToHost));
+  (void)nt;
+  char buf[512];
+  std::snprintf(buf, sizeof buf,
+                "engine step: non-finite state for molecule %d (pos %g %g %g, vel %g %g %g)%s", i,
+                v[0], v[1], v[2], v[3], v[4], v[5], c->R > 1 ? " in replica" : "");
+  std::string msg = buf;
+  if (c->R > 1) msg += " " + std::to_string(r);
+  return set_err(B2MD_NUMERICAL_ERROR, msg);
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+extern "C" {
+
+const char* b2md_last_error(void) { return g_err.c_str(); }
+int b2md_abi_version(void) { return B2MD_ABI_VERSION; }
+
+int b2md_build_species(const b2md_site* sites, int n_sites, b2md_species* out) {
+  if (!sites || !out) return set_err(B2MD_INVALID_ARGUMENT, "build_species: null pointer");
+  std::string err;
+  if (int rc = build_species(sites, n_sites, *out, err)) return set_err(rc, err);
+  return B2MD_OK;
+}
+
+int b2md_ewald_tune(double delta, double cutoff, double box_length, double* alpha, int* kmax) {
+  if (!alpha || !kmax) return set_err(B2MD_INVALID_ARGUMENT, "ewald_tune: null pointer");
+  std::string err;
+  if (int rc = ewald_tune(delta, cutoff, box_length, *alpha, *kmax, err)) return set_err(rc, err);
+  return B2MD_OK;
+}
+
+int b2md_ewald_kvector_count(int kmax, int* count) {
+  if (!count || kmax < 0) return set_err(B2MD_INVALID_ARGUMENT, "kvector_count: bad argument");
+  *count = count_kvectors(kmax);
+  return B2MD_OK;
+}
+
+int b2md_shard_plan(int n_molecules, int n_kvectors, int world, int rank, int* row_begin,
+                    int* row_end, int* k_begin, int* k_end, int64_t* candidate_pairs) {
+  if (n_molecules < 1 || world < 1 || rank < 0 || rank >= world || !row_begin || !row_end ||
+      !k_begin || !k_end || !candidate_pairs)
+    return set_err(B2MD_INVALID_ARGUMENT, "shard_plan: bad argument");
+  shard_plan(n_molecules, n_kvectors, world, rank, *row_begin, *row_end, *k_begin, *k_end,
+             *candidate_pairs);
+  return B2MD_OK;
+}
+
+int b2md_create(int device, const b2md_composition* comp, const b2md_ff_options* opts, double dt,
+                int n_replicas, b2md_ctx** out) {
+  if (!comp || !opts || !out) return set_err(B2MD_INVALID_ARGUMENT, "create: null pointer");
+  *out = nullptr;
+  b2md_ctx* c = new b2md_ctx();
+  int rc = create_impl(device, comp, opts, dt, n_replicas, c);
+  if (rc) {
+    const std::string keep = g_err;
+    free_ctx(c);
+    g_err = keep;
+    return rc;
+  }
+  *out = c;
+  return B2MD_OK;
+}
+
+void b2md_destroy(b2md_ctx* ctx) { free_ctx(ctx); }
+
+const char* b2md_warning(const b2md_ctx* ctx) { return ctx ? ctx->warning.c_str() : ""; }
+
+int b2md_evaluate(b2md_ctx* c, const double* pos, const double* orient, double* force,
+                  double* torque, b2md_energy* energy, b2md_eval_stats* stats) {
+  if (!c || !pos) return set_err(B2MD_INVALID_ARGUMENT, "evaluate: null pointer");
+  CU(cudaSetDevice(c->device));
+  TRY(upload_aos(c, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
+  if (orient) {
+    TRY(upload_aos(c, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
+  } else if (c->t.any_offsets) {
+    return set_err(B2MD_INVALID_ARGUMENT, "evaluate: orientations required for multi-site species");
+  }
+  TRY(enqueue_forces(c, true));
+  if (force) TRY(download_aos(c, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
+  if (torque) TRY(download_aos(c, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
+  TRY(download_scalars(c, energy, stats));
+  CU(cudaStreamSynchronize(c->stream));
+  c->state_valid = false;  // velocities not set: not an engine state
+  return B2MD_OK;
+}
+
+int b2md_set_state(b2md_ctx* c, const double* pos, const double* orient, const double* vel,
+                   const double* ang_vel) {
+  if (!c || !pos || !orient || !vel || !ang_vel)
+    return set_err(B2MD_INVALID_ARGUMENT, "set_state: null pointer");
+  CU(cudaSetDevice(c->device));
+  TRY(upload_aos(c, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
+  TRY(upload_aos(c, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
+  TRY(upload_aos(c, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
+  TRY(upload_aos(c, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
+  const int nt = n_total(c);
+  // state_.wrap() (engine.cpp:96): px, py, pz are contiguous
+  k_wrap<<<(3 * nt + 255) / 256, 256, 0, c->stream>>>(c->st.px, 3 * nt, c->t.box);
+  CU(cudaGetLastError());
+  const int big = INT_MAX;
+  CU(cudaMemcpyAsync(c->d_error, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  TRY(enqueue_forces(c, true));
+  CU(cudaStreamSynchronize(c->stream));
+  c->state_valid = true;
+  return B2MD_OK;
+}
+
+int b2md_step(b2md_ctx* c, int64_t nsteps) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "step: null context");
+  if (!c->engine) return set_err(B2MD_CONFIG_ERROR, "engine: time step must be positive");
+  if (!c->state_valid) return set_err(B2MD_CONFIG_ERROR, "engine: set_state must precede step");
+  if (nsteps <= 0) return B2MD_OK;
+  CU(cudaSetDevice(c->device));
+  if (c->use_graphs && !c->profile) {
+    TRY(build_step_graph(c));
+    for (int64_t k = 0; k < nsteps; ++k) CU(cudaGraphLaunch(c->step_graph, c->stream));
+  } else {
+    for (int64_t k = 0; k < nsteps; ++k) TRY(enqueue_step(c));
+  }
+  return check_error_flag(c);
+}
+
+int b2md_get_state(b2md_ctx* c, double* pos, double* orient, double* vel, double* ang_vel,
+                   double* force, double* torque, b2md_energy* energy, b2md_eval_stats* stats) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "get_state: null context");
+  CU(cudaSetDevice(c->device));
+  if (pos) TRY(download_aos(c, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
+  if (orient) TRY(download_aos(c, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
+  if (vel) TRY(download_aos(c, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
+  if (ang_vel) TRY(download_aos(c, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
+  if (force) TRY(download_aos(c, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
+  if (torque) TRY(download_aos(c, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
+  TRY(download_scalars(c, energy, stats));
+  return B2MD_OK;
+}
+
+int b2md_pair_list(b2md_ctx* c, int replica, int32_t* pairs, int64_t capacity, int64_t* n_pairs) {
+  if (!c || !n_pairs) return set_err(B2MD_INVALID_ARGUMENT, "pair_list: null pointer");
+  if (replica < 0 || replica >= c->R) return set_err(B2MD_INVALID_ARGUMENT, "pair_list: bad replica");
+  CU(cudaSetDevice(c->device));
+  const int n = c->t.n;
+  const uint32_t* mask = c->d_mask + size_t(replica) * c->g.n_pad * c->g.words;
+  int64_t* d_cnt = nullptr;
+  CU(cudaMalloc(&d_cnt, sizeof(int64_t) * (n + 1)));
+  k_pair_count<<<(n + 255) / 256, 256, 0, c->stream>>>(mask, n, c->g.n_pad, c->g.words, d_cnt);
+  std::vector<int64_t> cnt(n + 1, 0);
+  cudaError_t e = cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    cudaFree(d_cnt);
+    return set_err(B2MD_CUDA_ERROR, cudaGetErrorString(e));
+  }
+  // exclusive scan of the per-row counts
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    const int64_t v = cnt[i];
+    cnt[i] = total;
+    total += v;
+  }
+  *n_pairs = total;
+  if (pairs && total > 0) {
+    if (capacity < total) {
+      cudaFree(d_cnt);
+      return set_err(B2MD_INVALID_ARGUMENT, "pair_list: capacity too small");
+    }
+    int32_t* d_pairs = nullptr;
+    e = cudaMalloc(&d_pairs, sizeof(int32_t) * 2 * total);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_cnt, cnt.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) {
+      k_pair_fill<<<(n + 255) / 256, 256, 0, c->stream>>>(mask, n, c->g.words, d_cnt, d_pairs);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(pairs, d_pairs, sizeof(int32_t) * 2 * total, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(d_pairs);
+    if (e != cudaSuccess) {
+      cudaFree(d_cnt);
+      return set_err(B2MD_CUDA_ERROR, cudaGetErrorString(e));
+    }
+  }
+  cudaFree(d_cnt);
+  return B2MD_OK;
+}
+
+int b2md_nccl_unique_id(char id[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId u;
+  NC(ncclGetUniqueId(&u));
+  std::memcpy(id, &u, 128);
+  return B2MD_OK;
+}
+
+int b2md_attach_nccl(b2md_ctx* c, const char id[128], int rank, int world) {
+  if (!c || !id || world < 1 || rank < 0 || rank >= world)
+    return set_err(B2MD_INVALID_ARGUMENT, "attach_nccl: bad argument");
+  CU(cudaSetDevice(c->device));
+  if (c->comm) {
+    ncclCommDestroy(c->comm);
+    c->comm = nullptr;
+  }
+  if (world > 1) {
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    NC(ncclCommInitRank(&c->comm, world, u, rank));
+  }
+  c->rank = rank;
+  c->world = world;
+  TRY(setup_shard(c));
+  return B2MD_OK;
+}
+
+void* b2md_stream(b2md_ctx* c) { return c ? reinterpret_cast<void*>(c->stream) : nullptr; }
+
+int b2md_profile_enable(b2md_ctx* c, int enable) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "profile_enable: null context");
+  TRY(prof_harvest(c));
+  c->profile = enable != 0;
+  if (c->profile)
+    for (int f = 0; f < F_COUNT; ++f) {
+      c->prof_ms[f] = 0.0;
+      c->prof_n[f] = 0;
+    }
+  return B2MD_OK;
+}
+
+int b2md_kernel_times(b2md_ctx* c, int max_rows, char (*names)[32], double* total_ms,
+                      int64_t* launches, int* n_rows) {
+  if (!c || !n_rows) return set_err(B2MD_INVALID_ARGUMENT, "kernel_times: null pointer");
+  TRY(prof_harvest(c));
+  int k = 0;
+  for (int f = 0; f < F_COUNT && k < max_rows; ++f) {
+    if (c->prof_n[f] == 0) continue;
+    if (names) std::snprintf(names[k], 32, "%s", kFamilyName[f]);
+    if (total_ms) total_ms[k] = c->prof_ms[f];
+    if (launches) launches[k] = c->prof_n[f];
+    ++k;
+  }
+  *n_rows = k;
+  return B2MD_OK;
+}
+
+int b2md_set_graphs(b2md_ctx* c, int enable) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "set_graphs: null context");
+  c->use_graphs = enable != 0;
+  return B2MD_OK;
+}
+
+int b2md_measure_fp64_peak(int device, double* gflops) {
+  if (!gflops) return set_err(B2MD_INVALID_ARGUMENT, "measure_fp64_peak: null pointer");
+  CU(cudaSetDevice(device));
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const int blocks = sms * 8, threads = 256, iters = 20000;
+  double* out = nullptr;
+  CU(cudaMalloc(&out, sizeof(double) * blocks * threads));
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  k_dfma_peak<<<blocks, threads>>>(out, 200, 1.0000001, 1e-7);
+  CU(cudaEventRecord(e0));
+  for (int r = 0; r < 5; ++r) k_dfma_peak<<<blocks, threads>>>(out, iters, 1.0000001, 1e-7);
+  CU(cudaEventRecord(e1));
+  CU(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, e0, e1));
+  *gflops = 5.0 * blocks * threads * double(iters) * 8 * 2 / (double(ms) * 1e6);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return B2MD_OK;
+}
+
+}  // extern "C"

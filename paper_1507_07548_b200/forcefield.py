@@ -1,0 +1,308 @@
+"""ForceField / Engine mirrors of include/tmd/parallel.hpp:45-80 and
+include/tmd/engine.hpp:52-112 over the b200md C ABI (include/b200md.h).
+
+Same names, argument meaning and error behaviour as the reference: a
+ForceField is built from a SystemComposition and ForceFieldOptions and its
+evaluate(state) overwrites state.force / torque / virial / energy
+(src/parallel.cpp:79-122).  Everything runs on the GPU; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from .errors import check
+from .model import (
+    ElectrostaticsMethod,
+    EnergyBreakdown,
+    SystemComposition,
+    SystemState,
+)
+
+
+@dataclass
+class EwaldParams:  # ewald.hpp:15-18
+    alpha: float = 0.0
+    kmax: int = 0
+
+
+def ewald_tune(delta: float, cutoff: float, box_length: float) -> EwaldParams:
+    """tmd::ewald_tune (src/ewald.cpp:8-28)."""
+    a = C.c_double()
+    k = C.c_int()
+    check(_abi.lib().b2md_ewald_tune(delta, cutoff, box_length, C.byref(a), C.byref(k)))
+    return EwaldParams(a.value, k.value)
+
+
+def kvector_count(kmax: int) -> int:
+    c = C.c_int()
+    check(_abi.lib().b2md_ewald_kvector_count(kmax, C.byref(c)))
+    return c.value
+
+
+@dataclass
+class ForceFieldOptions:  # parallel.hpp:45-52
+    cutoff: float = 0.0
+    method: ElectrostaticsMethod = ElectrostaticsMethod.none
+    eps_rf: float = math.inf
+    ewald: EwaldParams | None = None
+    workers: int = 1
+    volume_derivatives: bool = True
+
+    def to_c(self) -> _abi.b2md_ff_options:
+        o = _abi.b2md_ff_options()
+        o.cutoff = float(self.cutoff)
+        o.method = int(self.method)
+        o.eps_rf = float(self.eps_rf)
+        o.has_ewald = 1 if self.ewald is not None else 0
+        if self.ewald is not None:
+            o.ewald_alpha = float(self.ewald.alpha)
+            o.ewald_kmax = int(self.ewald.kmax)
+        o.workers = int(self.workers)
+        o.volume_derivatives = 1 if self.volume_derivatives else 0
+        return o
+
+
+@dataclass
+class EvalStats:
+    virial: float = 0.0
+    s1: float = 0.0
+    s2: float = 0.0
+    com_pairs: int = 0
+
+
+def _f64(a, shape) -> np.ndarray:
+    out = np.ascontiguousarray(a, dtype=np.float64)
+    if out.shape != shape:
+        out = out.reshape(shape)
+    return out
+
+
+class _Context:
+    """Owns one b2md_ctx (device memory + stream)."""
+
+    def __init__(self, comp: SystemComposition, opts: ForceFieldOptions, dt: float, replicas: int,
+                 device: int):
+        self.comp = comp
+        self.opts = opts
+        self.n = comp.molecule_count()
+        self.replicas = int(replicas)
+        self.device = int(device)
+        cc, self._keep = comp.to_c()
+        oc = opts.to_c()
+        ctx = C.c_void_p()
+        check(_abi.lib().b2md_create(self.device, C.byref(cc), C.byref(oc), float(dt),
+                                     self.replicas, C.byref(ctx)))
+        self.ctx = ctx
+
+    def close(self) -> None:
+        if getattr(self, "ctx", None) is not None and self.ctx.value:
+            _abi.lib().b2md_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def warning(self) -> str:
+        return _abi.lib().b2md_warning(self.ctx).decode()
+
+    def energies(self, e_arr, s_arr):
+        es = [EnergyBreakdown.from_c(e_arr[r]) for r in range(self.replicas)]
+        ss = [EvalStats(s_arr[r].virial, s_arr[r].s1, s_arr[r].s2, s_arr[r].com_pairs)
+              for r in range(self.replicas)]
+        return es, ss
+
+    def pair_list(self, replica: int = 0) -> np.ndarray:
+        """(n_pairs, 2) int32 i<j molecule pairs passing the COM partner
+        search of the last evaluation, sorted by i then j."""
+        n = C.c_int64()
+        check(_abi.lib().b2md_pair_list(self.ctx, replica, None, 0, C.byref(n)))
+        out = np.zeros((n.value, 2), dtype=np.int32)
+        if n.value:
+            check(_abi.lib().b2md_pair_list(
+                self.ctx, replica, out.ctypes.data_as(C.POINTER(C.c_int32)), n.value, C.byref(n)))
+        return out
+
+
+class ForceField:
+    """tmd::ForceField (parallel.hpp:56-80) on a B200."""
+
+    def __init__(self, comp: SystemComposition, opts: ForceFieldOptions, device: int = 0):
+        self._c = _Context(comp, opts, 0.0, 1, device)
+        self.last_stats = EvalStats()
+
+    def composition(self) -> SystemComposition:
+        return self._c.comp
+
+    @property
+    def warning(self) -> str:
+        return self._c.warning
+
+    def evaluate(self, state: SystemState) -> None:
+        """ForceField::evaluate (src/parallel.cpp:79-122): fills state.force,
+        torque, virial and energy.  Positions are used as given (not wrapped)."""
+        n = self._c.n
+        pos = _f64(state.pos, (n, 3))
+        orient = _f64(state.orient, (n, 4))
+        force = np.empty((n, 3))
+        torque = np.empty((n, 3))
+        e = (_abi.b2md_energy * 1)()
+        s = (_abi.b2md_eval_stats * 1)()
+        check(_abi.lib().b2md_evaluate(self._c.ctx, _abi.dptr(pos), _abi.dptr(orient),
+                                       _abi.dptr(force), _abi.dptr(torque), e, s))
+        es, ss = self._c.energies(e, s)
+        state.force = force
+        state.torque = torque
+        state.energy = es[0]
+        state.virial = ss[0].virial
+        self.last_stats = ss[0]
+
+    def pair_list(self) -> np.ndarray:
+        return self._c.pair_list(0)
+
+    def close(self) -> None:
+        self._c.close()
+
+
+class Engine:
+    """The NVE hot path of tmd::Engine (engine.hpp:52-112): set_state,
+    compute_forces, step — device resident.  `replicas` independent systems
+    of the same composition are stepped together (one launch each kernel)."""
+
+    def __init__(self, comp: SystemComposition, ff_opts: ForceFieldOptions, dt: float,
+                 device: int = 0, replicas: int = 1):
+        if dt <= 0.0:
+            from .errors import ConfigError
+            raise ConfigError("engine: time step must be positive")
+        self._c = _Context(comp, ff_opts, dt, replicas, device)
+        self.dt = float(dt)
+        self.replicas = int(replicas)
+
+    @property
+    def ctx(self):
+        return self._c.ctx
+
+    @property
+    def n(self) -> int:
+        return self._c.n
+
+    def composition(self) -> SystemComposition:
+        return self._c.comp
+
+    def set_state(self, states) -> None:
+        """Engine::set_state (src/engine.cpp:91-98): upload, wrap, forces."""
+        if isinstance(states, SystemState):
+            states = [states]
+        if len(states) != self.replicas:
+            raise ValueError("one state per replica required")
+        n = self._c.n
+        for s in states:
+            if s.molecule_count() != n:
+                from .errors import ConfigError
+                raise ConfigError("engine: state does not match composition")
+        cat = lambda k, w: np.ascontiguousarray(
+            np.concatenate([_f64(getattr(s, k), (n, w)) for s in states]), dtype=np.float64)
+        check(_abi.lib().b2md_set_state(self._c.ctx, _abi.dptr(cat("pos", 3)),
+                                        _abi.dptr(cat("orient", 4)), _abi.dptr(cat("vel", 3)),
+                                        _abi.dptr(cat("ang_vel", 3))))
+
+    def set_state_raw(self, pos, orient, vel, ang_vel) -> None:
+        """set_state from replica-major contiguous float64 host buffers."""
+        check(_abi.lib().b2md_set_state(self._c.ctx, _abi.dptr(pos), _abi.dptr(orient),
+                                        _abi.dptr(vel), _abi.dptr(ang_vel)))
+
+    def step(self, nsteps: int = 1) -> None:
+        """Engine::step (src/engine.cpp:102-143) x nsteps."""
+        check(_abi.lib().b2md_step(self._c.ctx, int(nsteps)))
+
+    def states(self) -> list[SystemState]:
+        n, R = self._c.n, self.replicas
+        pos = np.empty((R * n, 3))
+        orient = np.empty((R * n, 4))
+        vel = np.empty((R * n, 3))
+        ang = np.empty((R * n, 3))
+        force = np.empty((R * n, 3))
+        torque = np.empty((R * n, 3))
+        e = (_abi.b2md_energy * R)()
+        s = (_abi.b2md_eval_stats * R)()
+        check(_abi.lib().b2md_get_state(self._c.ctx, *(map(_abi.dptr, (pos, orient, vel, ang, force, torque))), e, s))
+        es, ss = self._c.energies(e, s)
+        out = []
+        for r in range(R):
+            st = SystemState(0, self._c.comp.box_length)
+            sl = slice(r * n, (r + 1) * n)
+            st.pos, st.orient, st.vel, st.ang_vel = pos[sl], orient[sl], vel[sl], ang[sl]
+            st.force, st.torque = force[sl], torque[sl]
+            st.energy, st.virial = es[r], ss[r].virial
+            out.append(st)
+        self.last_stats = ss
+        return out
+
+    def state(self) -> SystemState:
+        return self.states()[0]
+
+    def energies(self):
+        """Per-replica (EnergyBreakdown, EvalStats) without downloading arrays."""
+        R = self.replicas
+        e = (_abi.b2md_energy * R)()
+        s = (_abi.b2md_eval_stats * R)()
+        check(_abi.lib().b2md_get_state(self._c.ctx, None, None, None, None, None, None, e, s))
+        return self._c.energies(e, s)
+
+    def pair_list(self, replica: int = 0) -> np.ndarray:
+        return self._c.pair_list(replica)
+
+    def attach_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
+        check(_abi.lib().b2md_attach_nccl(self._c.ctx, unique_id, rank, world))
+
+    def set_graphs(self, enable: bool) -> None:
+        check(_abi.lib().b2md_set_graphs(self._c.ctx, 1 if enable else 0))
+
+    def profile(self, enable: bool) -> None:
+        check(_abi.lib().b2md_profile_enable(self._c.ctx, 1 if enable else 0))
+
+    def kernel_times(self) -> dict:
+        rows = 16
+        names = (C.c_char * 32 * rows)()
+        ms = (C.c_double * rows)()
+        cnt = (C.c_int64 * rows)()
+        nr = C.c_int()
+        check(_abi.lib().b2md_kernel_times(self._c.ctx, rows, names, ms, cnt, C.byref(nr)))
+        return {names[k].value.decode(): (ms[k], cnt[k]) for k in range(nr.value)}
+
+    def stream(self) -> int:
+        return _abi.lib().b2md_stream(self._c.ctx)
+
+    def close(self) -> None:
+        self._c.close()
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(_abi.lib().b2md_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_plan(n_molecules: int, n_kvectors: int, world: int, rank: int) -> dict:
+    """b2md_shard_plan: tile-row and k-vector ranges of `rank`."""
+    vals = [C.c_int() for _ in range(4)]
+    cand = C.c_int64()
+    check(_abi.lib().b2md_shard_plan(n_molecules, n_kvectors, world, rank,
+                                     *[C.byref(v) for v in vals], C.byref(cand)))
+    rb, re, kb, ke = (v.value for v in vals)
+    return {"row_begin": rb, "row_end": re, "k_begin": kb, "k_end": ke,
+            "candidate_pairs": cand.value}
+
+
+def measure_fp64_peak(device: int = 0) -> float:
+    g = C.c_double()
+    check(_abi.lib().b2md_measure_fp64_peak(device, C.byref(g)))
+    return g.value
