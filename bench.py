@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MD hot path (one JSON line on rank 0).
+
+Workload (default): BASELINE config 3 — LJ fluid N=16384, rho*=0.8, rc=5 sigma,
+fp64, the 16384-molecule system the north_star's FP64-roofline target and the
+multi-GPU row-sharding spec are quoted on.  A "step" is one Engine::step
+(src/engine.cpp:102-143): half kick + drift + wrap, partner search, forces,
+energies, half kick.  `--config cfg0..cfg4` selects the other configs.
+
+  python bench.py [--gpus N --steps K --warmup W]          # this implementation
+  python bench.py --impl reference [...]                    # reference CPU arm
+N > 1 is launched by torchrun (one rank per GPU): the pair triangle is
+row-sharded and one packed NCCL all-reduce per step combines forces and
+energy sums (strong scaling; cfg4 runs independent replicas per rank).
+
+Timing: W untimed steps, then K steps, each bracketed on the library's stream
+by CUDA events; the L2 is flushed (256 MiB memset, outside the events)
+between timed steps; barrier + synchronize around the region; max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "site-site pair interactions/s and MD steps/s; fraction of B200 FP64 peak"
+# algorithmic fp64 work per unit
+FLOP_CANDIDATE = 17
+FLOP_LJ_SINGLE = 32
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="cfg3")
+    p.add_argument("--e2e-steps", type=int, default=50)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--no-flush", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(name, rank, world):
+    from paper_1507_07548_b200 import configs
+    if name == "cfg4":  # replicas only: 8 independent replicas per rank
+        return configs.make("cfg4", replicas=8, first_seed=8 * rank)
+    return configs.make(name)
+
+
+def algorithmic(wl, pairs_in_cutoff):
+    n = wl.comp.molecule_count()
+    cand = n * (n - 1) // 2
+    return cand, cand * FLOP_CANDIDATE
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def cpu_reference_run(wl, steps_wanted, budget_s, threads):
+    """The reference tmd::Engine (oracle/_ref, built from /root/reference) on the
+    host cores: set_state then step() x k, bounded to ~budget_s seconds."""
+    from oracle import pyoracle
+    opts = wl.opts
+    if opts.method != 2:  # ewald forces workers = 1 (parallel.cpp:65-66)
+        import copy
+        opts = copy.copy(opts)
+        opts.workers = threads
+    st = wl.states[0]
+    eng = pyoracle.RefEngine(wl.comp, opts, wl.dt)
+    eng.set_state(st.pos, st.orient, st.vel, st.ang_vel)
+    t0 = time.perf_counter()
+    eng.step(1)  # warm-up + per-step estimate
+    est = time.perf_counter() - t0
+    k = max(1, min(steps_wanted, int(budget_s / max(est, 1e-6))))
+    t0 = time.perf_counter()
+    eng.step(k)
+    dt = time.perf_counter() - t0
+    return k / dt, k, opts.workers
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import pyoracle
+    wl = workload(args.config, 0, 1)
+    threads = os.cpu_count() or 1
+    if not pyoracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtmdref.so not built"}))
+        return
+    # each of the K steps is one reference step; bound the whole run to ~3 min
+    value, k, workers = cpu_reference_run(wl, args.steps, 150.0, threads)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": "steps/s",
+        "n_gpus": args.gpus,
+        "steps": k,
+        "warmup": 1,
+        "ms_per_step": 1e3 / value,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded generator, paper_1507_07548_b200/configs.py)",
+        "config": {"workload": f"{args.config}: {describe(wl)}"},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": workers, "kind": "reference",
+                         "sample": f"{k} tmd::Engine::step calls after set_state, W={workers} threads"},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def describe(wl):
+    n = wl.comp.molecule_count()
+    return (f"N={n} x {wl.replicas} replica(s), {len(wl.comp.species)} species, L={wl.comp.box_length:.6f}, "
+            f"rc={wl.opts.cutoff:.6f}, dt={wl.dt}, method={int(wl.opts.method)}")
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    rank, world, local = dist_env()
+    import torch
+    import paper_1507_07548_b200 as b2
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = workload(args.config, rank, world)
+    R = wl.replicas
+    n = wl.comp.molecule_count()
+    eng = b2.Engine(wl.comp, wl.opts, wl.dt, device=local, replicas=R)
+    if world > 1 and args.config != "cfg4":
+        uid = [b2.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        eng.attach_nccl(uid[0], rank, world)
+    eng.set_state(wl.states)
+    peak_gflops = b2.measure_fp64_peak(local)
+
+    stream = torch.cuda.ExternalStream(eng.stream(), device=local)
+    flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    # ---- warm-up
+    eng.step(max(3, args.warmup))
+
+    # ---- timed region (device-resident steps)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    eng.profile(True)
+    with torch.cuda.stream(stream):
+        for k in range(args.steps):
+            starts[k].record(stream)
+            eng.step_async(1)
+            ends[k].record(stream)
+            if flush is not None:
+                flush.zero_()
+    eng.sync()
+    torch.cuda.synchronize()
+    kt = eng.kernel_times()
+    eng.profile(False)
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    if dist is not None:
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    energies, stats = eng.energies()
+    pairs_total = int(sum(s.com_pairs for s in stats))
+
+    # ---- end to end through the C ABI with host buffers (pinned):
+    # per step upload the full dynamic state (b2md_upload_state), step, download it
+    def pinned(shape):
+        return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+    nt = n * R
+    hp, hq, hv, hw, hf, ht = (pinned((nt, 3)), pinned((nt, 4)), pinned((nt, 3)), pinned((nt, 3)),
+                              pinned((nt, 3)), pinned((nt, 3)))
+    eng.get_state_raw(hp, hq, hv, hw, hf, ht)
+    h2d = d2h = 8 * nt * (3 + 4 + 3 + 3 + 3 + 3)
+    e2e_steps = max(1, args.e2e_steps)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        eng.upload_state_raw(hp, hq, hv, hw, hf, ht)
+        eng.step(1)
+        eng.get_state_raw(hp, hq, hv, hw, hf, ht)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    replica_steps = args.steps * (R * world if args.config == "cfg4" else 1)
+    value = replica_steps / (total_ms * 1e-3)
+    e2e_value = e2e_steps * (R * world if args.config == "cfg4" else 1) / e2e_s
+
+    # ---- roofline of the dominant kernel (partner search: fp64 CUDA cores)
+    search_ms, search_launches = kt.get("search", (0.0, 0))
+    force_ms, force_launches = kt.get("force", (0.0, 0))
+    cand = n * (n - 1) // 2 * R
+    if world > 1 and args.config != "cfg4":
+        cand_rank = b2.shard_plan(n, b2.kvector_count(wl.opts.ewald.kmax) if wl.opts.ewald else 0,
+                                  world, rank)["candidate_pairs"]
+    else:
+        cand_rank = cand
+    avg_search_s = search_ms * 1e-3 / max(1, search_launches)
+    achieved = cand_rank * FLOP_CANDIDATE / avg_search_s / 1e12 if avg_search_s > 0 else 0.0
+    peak = peak_gflops / 1e3
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_{args.config}_search.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    step_kernels = sum(c for name, (ms, c) in kt.items() if name != "allreduce")
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak" if args.config == "cfg4" else "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded xoshiro256++ generator, paper_1507_07548_b200/configs.py)",
+        "config": {
+            "workload": f"{args.config}: {describe(wl)}",
+            "parallelism": (f"replicas x{world}" if args.config == "cfg4" else
+                            (f"row-sharded x{world} + NCCL all-reduce" if world > 1 else "single GPU")),
+            "l2": "flushed between timed steps (256 MiB memset outside the per-step events)"
+            if flush is not None else "not flushed",
+            "timing": "per-step CUDA events on the library stream; max over ranks",
+        },
+        "pair_interactions_per_s": pairs_total * args.steps * (world if args.config == "cfg4" else 1)
+        / (total_ms * 1e-3),
+        "pairs_in_cutoff_per_step": pairs_total,
+        "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "b2md_upload_state + b2md_step + b2md_get_state, pinned host buffers"},
+        "roofline": {
+            "bound": "fp64",
+            "kernel": "k_search (COM partner search, 17 flop/candidate)",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "TFLOP/s",
+            "frac": achieved / peak if peak else None,
+            "traffic": traffic,
+            "peak_source": "DFMA microbenchmark measured in this run (MEASURED_PEAKS.json has no fp64 entry)",
+            "launch_ms": avg_search_s * 1e3,
+            "share_of_step": search_ms / max(1e-9, total_ms),
+        },
+        "kernel_ms_per_launch": {k: v[0] / max(1, v[1]) for k, v in kt.items()},
+        "gpu_launches": int(sum(c for _, (ms, c) in kt.items())),
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            from oracle import pyoracle
+            if pyoracle.ref_available():
+                threads = os.cpu_count() or 1
+                v, k, w = cpu_reference_run(wl, 10 ** 6, args.cpu_seconds, threads)
+                line["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": w, "kind": "reference",
+                                        "sample": f"{k} tmd::Engine::step of {args.config} at W={w}"}
+        except Exception as exc:  # the GPU number stands without it
+            line["cpu_baseline"] = {"error": str(exc)}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -180,6 +180,18 @@ int b2md_set_state(b2md_ctx* ctx, const double* pos, const double* orient, const
  * (src/model.cpp:288-302); the state then holds the end of the failing step. */
 int b2md_step(b2md_ctx* ctx, int64_t nsteps);
 
+/* Enqueue `nsteps` steps without waiting (device-resident step loop);
+ * b2md_sync waits for them and reports a NumericalError like b2md_step. */
+int b2md_step_async(b2md_ctx* ctx, int64_t nsteps);
+int b2md_sync(b2md_ctx* ctx);
+
+/* Raw upload of a complete dynamic state including the cached forces and
+ * torques of that state — no wrap, no force evaluation (the data part of
+ * tmd::Engine::restore_dynamic, src/engine.cpp:520-540).  NULL keeps the
+ * device copy of that array. */
+int b2md_upload_state(b2md_ctx* ctx, const double* pos, const double* orient, const double* vel,
+                      const double* ang_vel, const double* force, const double* torque);
+
 /* tmd::Engine::state() (include/tmd/engine.hpp:60): download.  NULL skips. */
 int b2md_get_state(b2md_ctx* ctx, double* pos, double* orient, double* vel, double* ang_vel,
                    double* force, double* torque, b2md_energy* energy, b2md_eval_stats* stats);

@@ -309,3 +309,14 @@ int ref_engine_get_state(void* h, double* pos, double* orient, double* vel, doub
 }
 
 }  // extern "C"
+
+// tmd::Rng (include/tmd/rng.hpp:14-76): raw draws for the RNG golden vectors.
+extern "C" int ref_rng_draws(uint64_t seed, int n, uint64_t* u64, double* uniform, double* gaussian) {
+  tmd::Rng a(seed), b(seed), c(seed);
+  for (int k = 0; k < n; ++k) {
+    u64[k] = a.next_u64();
+    uniform[k] = b.uniform();
+    gaussian[k] = c.gaussian();
+  }
+  return 0;
+}

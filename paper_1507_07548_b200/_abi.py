@@ -124,6 +124,9 @@ SIGNATURES = {
     ),
     "b2md_set_state": (C.c_int, [_CTX, _D, _D, _D, _D]),
     "b2md_step": (C.c_int, [_CTX, C.c_int64]),
+    "b2md_step_async": (C.c_int, [_CTX, C.c_int64]),
+    "b2md_sync": (C.c_int, [_CTX]),
+    "b2md_upload_state": (C.c_int, [_CTX, _D, _D, _D, _D, _D, _D]),
     "b2md_get_state": (
         C.c_int,
         [_CTX, _D, _D, _D, _D, _D, _D, C.POINTER(b2md_energy), C.POINTER(b2md_eval_stats)],

@@ -85,10 +85,10 @@ __global__ void k_soa_to_aos(double* aos, int count, int width, const double* d0
   if (width == 4) aos[size_t(i) * width + 3] = d3[i];
 }
 
-enum Family { F_OFFSETS, F_SEARCH, F_FORCE, F_EWALD_TAB, F_EWALD_SK, F_EWALD_F, F_REDUCE,
+enum Family { F_OFFSETS, F_SEARCH, F_FORCE, F_EWALD_TAB, F_EWALD_SK, F_EWALD_F, F_KICK_KICK_DRIFT,
               F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_COUNT };
 const char* kFamilyName[F_COUNT] = {"offsets",  "search", "force",   "ewald_tables", "ewald_sk",
-                                    "ewald_force", "reduce", "kick_drift", "kick", "allreduce"};
+                                    "ewald_force", "kick_kick_drift", "kick_drift", "kick", "allreduce"};
 
 }  // namespace
 
@@ -111,7 +111,9 @@ struct b2md_ctx {
   double* d_off = nullptr;    // 3 * R * total_sites
   double* d_stage = nullptr;  // AoS staging, 4*R*n
   uint32_t* d_mask = nullptr;
-  double* d_row_scal = nullptr;
+  double* d_cta_part = nullptr;  // force-kernel per-CTA scalar partials
+  unsigned* d_ticket = nullptr;   // 2 * R: force, ewald
+  int force_grid = 1;
   uint32_t* d_super = nullptr;
   int n_super_tiles = 0;
   int* d_error = nullptr;
@@ -133,7 +135,8 @@ struct b2md_ctx {
   ncclComm_t comm = nullptr;
   // graphs
   bool use_graphs = true;
-  cudaGraphExec_t step_graph = nullptr;
+  cudaGraphExec_t step_graph = nullptr;  // forces + fused kick/kick-drift
+  cudaGraphExec_t single_graph = nullptr;  // one whole step
   // profiling
   bool profile = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
@@ -210,6 +213,12 @@ int launch_search(b2md_ctx* c) {
   a.super_tiles = c->d_super;
   a.rc2 = c->t.single_site_path ? c->t.rc2 : c->t.rmax2[0];
   const bool multi = c->t.ns > 1;
+  {
+    const double h = 0.5 * c->t.box * (1.0 - 1.0 / 65536.0);
+    a.fast_ok = (!multi && a.rc2 < h * h) ? 1 : 0;
+    const int hh = hi32(0.5 * c->t.box);
+    std::memcpy(&a.thr, &hh, 4);
+  }
   dim3 grid(c->n_super_tiles, c->R);
   const int st = c->g.st;
 #define SEARCH_CASE(ST)                                                                  \
@@ -231,12 +240,16 @@ int launch_search(b2md_ctx* c) {
   return B2MD_OK;
 }
 
+double* sums_ptr(b2md_ctx* c) { return c->d_fbuf + size_t(6) * n_total(c); }
+
 ForceArgs force_args(b2md_ctx* c) {
   ForceArgs a;
   a.s = c->sys;
   a.st = c->st;
   a.mask = c->d_mask;
-  a.row_scal = c->d_row_scal;
+  a.cta_part = c->d_cta_part;
+  a.ticket = c->d_ticket;
+  a.sums = sums_ptr(c);
   a.c12 = 0.0;
   a.c6 = 0.0;
   if (!c->t.lj.empty() && !c->t.lj[0].empty()) {
@@ -249,25 +262,24 @@ ForceArgs force_args(b2md_ctx* c) {
   a.rf_r3inv = c->t.rf_r3inv;
   a.rf_shift = c->t.rf_shift;
   a.vderiv = c->t.vderiv ? 1 : 0;
-  a.row_begin = 0;
-  a.row_end = c->t.n;
   return a;
 }
 
 int launch_force(b2md_ctx* c) {
   ForceArgs a = force_args(c);
-  dim3 grid((c->t.n + 7) / 8, c->R);
+  dim3 grid(c->force_grid, c->R);
+  const int bs = kForceWarps * 32;
   if (c->t.single_site_path) {
     if (c->t.ns > 1)
-      PROF(c, F_FORCE, (k_force_single<true><<<grid, 256, 0, c->stream>>>(a)));
+      PROF(c, F_FORCE, (k_force_single<true><<<grid, bs, 0, c->stream>>>(a)));
     else
-      PROF(c, F_FORCE, (k_force_single<false><<<grid, 256, 0, c->stream>>>(a)));
+      PROF(c, F_FORCE, (k_force_single<false><<<grid, bs, 0, c->stream>>>(a)));
   } else if (c->t.method == B2MD_METHOD_EWALD) {
-    PROF(c, F_FORCE, (k_force_multi<2><<<grid, 256, 0, c->stream>>>(a)));
+    PROF(c, F_FORCE, (k_force_multi<2><<<grid, bs, 0, c->stream>>>(a)));
   } else if (c->t.method == B2MD_METHOD_REACTION_FIELD) {
-    PROF(c, F_FORCE, (k_force_multi<1><<<grid, 256, 0, c->stream>>>(a)));
+    PROF(c, F_FORCE, (k_force_multi<1><<<grid, bs, 0, c->stream>>>(a)));
   } else {
-    PROF(c, F_FORCE, (k_force_multi<0><<<grid, 256, 0, c->stream>>>(a)));
+    PROF(c, F_FORCE, (k_force_multi<0><<<grid, bs, 0, c->stream>>>(a)));
   }
   return B2MD_OK;
 }
@@ -288,6 +300,8 @@ EwaldArgs ewald_args(b2md_ctx* c) {
   a.tab = c->d_etab;
   a.S = c->d_S;
   a.uk = c->d_uk;
+  a.ticket = c->d_ticket + c->R;
+  a.sums = sums_ptr(c);
   a.nk_total = int(c->t.kv.size());
   a.two_pi_over_L = 2.0 * 3.14159265358979323846 / c->t.box;
   return a;
@@ -301,17 +315,11 @@ int launch_ewald(b2md_ctx* c) {
   if (a.nk > 0) {
     PROF(c, F_EWALD_SK, (k_ewald_sk<<<dim3(a.nk, c->R), 256, 0, c->stream>>>(a)));
     PROF(c, F_EWALD_F, (k_ewald_force<<<dim3((c->t.n + 7) / 8, c->R), 256, 0, c->stream>>>(a)));
+  } else {
+    for (int r = 0; r < c->R; ++r)
+      CU(cudaMemsetAsync(sums_ptr(c) + size_t(r) * kNumSums + kNumRowScalars, 0, sizeof(double),
+                         c->stream));
   }
-  return B2MD_OK;
-}
-
-int launch_reduce(b2md_ctx* c) {
-  double* sums = c->d_fbuf + size_t(6) * n_total(c);
-  const bool ew = c->t.ewald && c->nq > 0;
-  PROF(c, F_REDUCE,
-       (k_reduce_sums<<<dim3(kNumSums, c->R), 256, 0, c->stream>>>(
-           c->d_row_scal, ew ? c->d_uk : nullptr, c->t.n, c->g.n_pad, int(c->t.kv.size()),
-           c->k_begin, c->k_end, sums)));
   return B2MD_OK;
 }
 
@@ -330,7 +338,6 @@ int enqueue_forces(b2md_ctx* c, bool offsets) {
   TRY(launch_search(c));
   TRY(launch_force(c));
   TRY(launch_ewald(c));
-  TRY(launch_reduce(c));
   TRY(launch_allreduce(c));
   return B2MD_OK;
 }
@@ -345,31 +352,79 @@ StepArgs step_args(b2md_ctx* c) {
   return a;
 }
 
-// Engine::step (src/engine.cpp:102-143)
-int enqueue_step(b2md_ctx* c) {
+// Engine::step (src/engine.cpp:102-143).  A run of k steps is issued as
+//   kick_drift, [forces, kick+kick_drift] x (k-1), forces, kick
+// where the bracket is one CUDA graph (the second half-kick of step s and the
+// first of step s+1 share one launch).
+int launch_step_kernel(b2md_ctx* c, int fam) {
   StepArgs a = step_args(c);
   const int nt = n_total(c);
-  PROF(c, F_KICK_DRIFT, (k_kick_drift<<<(nt + 255) / 256, 256, 0, c->stream>>>(a)));
+  const int g = (nt + 255) / 256;
+  if (fam == F_KICK_DRIFT)
+    PROF(c, fam, (k_kick_drift<<<g, 256, 0, c->stream>>>(a)));
+  else if (fam == F_KICK)
+    PROF(c, fam, (k_kick<<<g, 256, 0, c->stream>>>(a)));
+  else
+    PROF(c, fam, (k_kick_kick_drift<<<g, 256, 0, c->stream>>>(a)));
+  return B2MD_OK;
+}
+
+int enqueue_loop_body(b2md_ctx* c) {
   TRY(enqueue_forces(c, false));
-  PROF(c, F_KICK, (k_kick<<<(nt + 255) / 256, 256, 0, c->stream>>>(a)));
+  TRY(launch_step_kernel(c, F_KICK_KICK_DRIFT));
   return B2MD_OK;
 }
 
 int build_step_graph(b2md_ctx* c) {
   if (c->step_graph) return B2MD_OK;
-  cudaGraph_t graph;
   const bool prof = c->profile;
   c->profile = false;
   CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-  int rc = enqueue_step(c);
-  cudaGraph_t g2;
-  cudaError_t e = cudaStreamEndCapture(c->stream, &g2);
+  int rc = enqueue_loop_body(c);
+  cudaGraph_t graph;
+  cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
   c->profile = prof;
   if (rc) return rc;
   CU(e);
-  graph = g2;
-  CU(cudaGraphInstantiate(&c->step_graph, graph, 0));
-  CU(cudaGraphDestroy(graph));
+  e = cudaGraphInstantiate(&c->step_graph, graph, 0);
+  cudaGraphDestroy(graph);
+  CU(e);
+  return B2MD_OK;
+}
+
+int build_single_step_graph(b2md_ctx* c) {
+  if (c->single_graph) return B2MD_OK;
+  CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = launch_step_kernel(c, F_KICK_DRIFT);
+  if (!rc) rc = enqueue_forces(c, false);
+  if (!rc) rc = launch_step_kernel(c, F_KICK);
+  cudaGraph_t graph;
+  cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+  if (rc) return rc;
+  CU(e);
+  e = cudaGraphInstantiate(&c->single_graph, graph, 0);
+  cudaGraphDestroy(graph);
+  CU(e);
+  return B2MD_OK;
+}
+
+int run_steps(b2md_ctx* c, int64_t nsteps) {
+  const bool graphs = c->use_graphs && !c->profile;
+  if (graphs && nsteps == 1) {
+    TRY(build_single_step_graph(c));
+    CU(cudaGraphLaunch(c->single_graph, c->stream));
+    return B2MD_OK;
+  }
+  if (graphs) TRY(build_step_graph(c));
+  TRY(launch_step_kernel(c, F_KICK_DRIFT));
+  for (int64_t k = 0; k + 1 < nsteps; ++k) {
+    if (graphs)
+      CU(cudaGraphLaunch(c->step_graph, c->stream));
+    else
+      TRY(enqueue_loop_body(c));
+  }
+  TRY(enqueue_forces(c, false));
+  TRY(launch_step_kernel(c, F_KICK));
   return B2MD_OK;
 }
 
@@ -453,6 +508,10 @@ int setup_shard(b2md_ctx* c) {
     cudaGraphExecDestroy(c->step_graph);
     c->step_graph = nullptr;
   }
+  if (c->single_graph) {
+    cudaGraphExecDestroy(c->single_graph);
+    c->single_graph = nullptr;
+  }
   return B2MD_OK;
 }
 
@@ -528,7 +587,14 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   TRY(dalloc(&c->d_off, 3 * size_t(t.total_sites) * R));
   TRY(dalloc(&c->d_stage, 4 * nt));
   TRY(dalloc(&c->d_mask, size_t(R) * c->g.n_pad * c->g.words));
-  TRY(dalloc(&c->d_row_scal, size_t(R) * kNumRowScalars * c->g.n_pad));
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int rows_grid = (t.n + kForceWarps - 1) / kForceWarps;
+    c->force_grid = std::max(1, std::min(rows_grid, sms * 6));
+  }
+  TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars * c->force_grid));
+  TRY(dalloc(&c->d_ticket, size_t(2) * R));
   TRY(dalloc(&c->d_error, 1));
   const int big = INT_MAX;
   CU(cudaMemcpy(c->d_error, &big, sizeof(int), cudaMemcpyHostToDevice));
@@ -616,13 +682,14 @@ void free_ctx(b2md_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
+  if (c->single_graph) cudaGraphExecDestroy(c->single_graph);
   for (auto& e : c->ev_pool) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
   }
   if (c->comm) ncclCommDestroy(c->comm);
   void* ptrs[] = {c->d_tab,   c->d_species_of, c->d_site_begin, c->d_state, c->d_fbuf, c->d_off,
-                  c->d_stage, c->d_mask,       c->d_row_scal,   c->d_super, c->d_error, c->d_q_mol,
+                  c->d_stage, c->d_mask,       c->d_cta_part, c->d_ticket,   c->d_super, c->d_error, c->d_q_mol,
                   c->d_q_site, c->d_q_val,     c->d_mol_qbegin, c->d_kv,    c->d_etab,  c->d_S,
                   c->d_uk};
   for (void* p : ptrs)
@@ -756,13 +823,37 @@ int b2md_step(b2md_ctx* c, int64_t nsteps) {
   if (!c->state_valid) return set_err(B2MD_CONFIG_ERROR, "engine: set_state must precede step");
   if (nsteps <= 0) return B2MD_OK;
   CU(cudaSetDevice(c->device));
-  if (c->use_graphs && !c->profile) {
-    TRY(build_step_graph(c));
-    for (int64_t k = 0; k < nsteps; ++k) CU(cudaGraphLaunch(c->step_graph, c->stream));
-  } else {
-    for (int64_t k = 0; k < nsteps; ++k) TRY(enqueue_step(c));
-  }
+  TRY(run_steps(c, nsteps));
   return check_error_flag(c);
+}
+
+int b2md_step_async(b2md_ctx* c, int64_t nsteps) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "step: null context");
+  if (!c->engine) return set_err(B2MD_CONFIG_ERROR, "engine: time step must be positive");
+  if (!c->state_valid) return set_err(B2MD_CONFIG_ERROR, "engine: set_state must precede step");
+  if (nsteps <= 0) return B2MD_OK;
+  CU(cudaSetDevice(c->device));
+  return run_steps(c, nsteps);
+}
+
+int b2md_sync(b2md_ctx* c) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "sync: null context");
+  CU(cudaSetDevice(c->device));
+  return check_error_flag(c);
+}
+
+int b2md_upload_state(b2md_ctx* c, const double* pos, const double* orient, const double* vel,
+                      const double* ang_vel, const double* force, const double* torque) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "upload_state: null context");
+  CU(cudaSetDevice(c->device));
+  if (pos) TRY(upload_aos(c, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
+  if (orient) TRY(upload_aos(c, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
+  if (vel) TRY(upload_aos(c, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
+  if (ang_vel) TRY(upload_aos(c, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
+  if (force) TRY(upload_aos(c, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
+  if (torque) TRY(upload_aos(c, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
+  c->state_valid = true;
+  return B2MD_OK;
 }
 
 int b2md_get_state(b2md_ctx* c, double* pos, double* orient, double* vel, double* ang_vel,

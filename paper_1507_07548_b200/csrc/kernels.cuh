@@ -7,7 +7,7 @@
 //   k_force_single  single-site LJ                          potentials.cpp:148-181
 //   k_force_multi   multi-site LJ + charge terms + torques  potentials.cpp:218-283
 //   k_ewald_*       reciprocal space                        ewald.cpp:107-180
-//   k_reduce_sums   fixed-order scalar reduction            parallel.cpp:93-95
+//   (scalars: per-CTA partials, last-CTA fixed-order total; parallel.cpp:93-95)
 // Per step (Engine::step, src/engine.cpp:102-143):
 //   k_kick_drift    half kick, drift, NO_SQUISH rotation, wrap, offsets
 //   k_kick          half kick + check_finite
@@ -86,17 +86,82 @@ struct SearchArgs {
   uint32_t* mask;                // R * n_pad * words
   const uint32_t* super_tiles;   // (SI << 16) | SJ, this rank's list
   double rc2;                    // single-species COM radius^2
+  int fast_ok;                   // single species and rmax^2 < (L/2 (1-2^-16))^2
+  float thr;                     // hi32(L/2) viewed as a float
 };
 
+// Branch-free minimum image for |d| < L (both positions wrapped to [0, L)).
+// shift <=> hi32(|d|) > hi32(L/2), compared on the integer pattern viewed as a
+// float (monotone for these magnitudes).  Outside the hi-word bucket of L/2
+// the decision equals nearbyint(d/L) != 0 exactly, and d - L*n is formed by
+// one correctly rounded DFMA with n = +-1 (exact product) — the reference's
+// bits.  Inside the bucket (|d| within 2^-20 of L/2) the image may differ from
+// the reference's, but then |d'| ~ L/2 for either image and, because the
+// caller guarantees rmax^2 < (L/2 (1-2^-16))^2, the pair fails the COM test
+// under both: the pass bit is still the reference's.
+__device__ __forceinline__ double min_image_wrapped(double d, double negL, float thr) {
+  const int hi = __double2hiint(d);
+  const bool shift = fabsf(__int_as_float(hi)) > thr;
+  const int nh = shift ? ((hi & int(0x80000000)) | 0x3ff00000) : 0;
+  return __fma_rn(__hiloint2double(nh, 0), negL, d);
+}
+
+// 32 i-rows (tile row `ib`) x JB column tiles c0.. on the fast path.
+template <int JB, bool DIAG>
+__device__ __forceinline__ void search_tile_fast(const double2* __restrict__ sixy,
+                                                 const double* __restrict__ siz,
+                                                 const double2* __restrict__ sjxy,
+                                                 const double* __restrict__ sjz, int ib, int c0,
+                                                 int I, int lane, int ST, double lim, double negL,
+                                                 float thr, uint32_t* wu, uint32_t* wl) {
+  double xj[JB], yj[JB], zj[JB];
+  uint32_t lw[JB];
+#pragma unroll
+  for (int b = 0; b < JB; ++b) {
+    const int jl = (c0 + b) * 32 + lane;
+    xj[b] = sjxy[jl].x;
+    yj[b] = sjxy[jl].y;
+    zj[b] = sjz[jl];
+    lw[b] = 0u;
+  }
+  uint32_t* wrow = wu + ib * ST + c0;
+#pragma unroll 8
+  for (int ii = 0; ii < 32; ++ii) {
+    const double2 ixy = sixy[ib + ii];
+    const double iz = siz[ib + ii];
+#pragma unroll
+    for (int b = 0; b < JB; ++b) {
+      const double dx = min_image_wrapped(sub(ixy.x, xj[b]), negL, thr);
+      const double dy = min_image_wrapped(sub(ixy.y, yj[b]), negL, thr);
+      const double dz = min_image_wrapped(sub(iz, zj[b]), negL, thr);
+      const double r2 = norm2_exact(dx, dy, dz);
+      bool pass = r2 < lim;
+      if (DIAG) pass = pass && lane > ii;
+      const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+      if (lane == 0) wrow[ii * ST + b] = bal;
+      if (pass) lw[b] |= 1u << ii;
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < JB; ++b) wl[((c0 + b) * 32 + lane) * ST + I] = lw[b];
+}
+
+// One CTA = one super-tile (SI, SJ), SI <= SJ, of ST x ST 32-molecule tiles;
+// warp w owns tile row I = SI*ST + w.  Lane <-> j (register), i broadcast from
+// shared memory.  Each candidate runs the reference's exact COM test; the
+// warp ballot of a fixed i over 32 j is the U word (row i, column tile J), and
+// each lane's bits over the 32 i of tile I form the transposed L word (row j,
+// column tile I).  Words are staged in shared memory and stored as whole
+// 32-byte sectors of the row-major bit matrix M[r][row][word].
 template <int ST, bool MULTI>
 __global__ void __launch_bounds__(ST * 32) k_search(SearchArgs a) {
   constexpr int T = ST * 32;
-  __shared__ double ix[T], iy[T], iz[T];
-  __shared__ double jx[T], jy[T], jz[T];
+  __shared__ double2 ixy[T], jxy[T];
+  __shared__ double iz[T], jz[T];
   __shared__ int ispec[MULTI ? T : 1], jspec[MULTI ? T : 1];
   __shared__ double rmax2_s[MULTI ? kMaxSpecies * kMaxSpecies : 1];
-  __shared__ uint32_t wu[T][ST + (ST == 1 ? 0 : 0)];
-  __shared__ uint32_t wl[T][ST];
+  __shared__ __align__(16) uint32_t wu[T * ST];
+  __shared__ __align__(16) uint32_t wl[T * ST];
 
   const SysDev& s = a.s;
   const int r = blockIdx.y;
@@ -108,15 +173,21 @@ __global__ void __launch_bounds__(ST * 32) k_search(SearchArgs a) {
   const int n = s.n;
   const int ibase = SI * T, jbase = SJ * T;
   const size_t roff = size_t(r) * n;
+  const double L = s.mi.L;
 
+  bool inbox;
   {
     const int i = ibase + tid, j = jbase + tid;
-    ix[tid] = i < n ? a.px[roff + i] : 0.0;
-    iy[tid] = i < n ? a.py[roff + i] : 0.0;
-    iz[tid] = i < n ? a.pz[roff + i] : 0.0;
-    jx[tid] = j < n ? a.px[roff + j] : 0.0;
-    jy[tid] = j < n ? a.py[roff + j] : 0.0;
-    jz[tid] = j < n ? a.pz[roff + j] : 0.0;
+    const double x0 = i < n ? a.px[roff + i] : 0.0, y0 = i < n ? a.py[roff + i] : 0.0,
+                 z0 = i < n ? a.pz[roff + i] : 0.0;
+    const double x1 = j < n ? a.px[roff + j] : 0.0, y1 = j < n ? a.py[roff + j] : 0.0,
+                 z1 = j < n ? a.pz[roff + j] : 0.0;
+    ixy[tid] = make_double2(x0, y0);
+    iz[tid] = z0;
+    jxy[tid] = make_double2(x1, y1);
+    jz[tid] = z1;
+    inbox = x0 >= 0.0 && x0 < L && y0 >= 0.0 && y0 < L && z0 >= 0.0 && z0 < L && x1 >= 0.0 &&
+            x1 < L && y1 >= 0.0 && y1 < L && z1 >= 0.0 && z1 < L;
     if constexpr (MULTI) {
       ispec[tid] = i < n ? s.species_of[i] : 0;
       jspec[tid] = j < n ? s.species_of[j] : 0;
@@ -124,129 +195,217 @@ __global__ void __launch_bounds__(ST * 32) k_search(SearchArgs a) {
     }
 #pragma unroll
     for (int c = 0; c < ST; ++c) {
-      wu[tid][c] = 0u;
-      wl[tid][c] = 0u;
+      wu[tid * ST + c] = 0u;
+      wl[tid * ST + c] = 0u;
     }
   }
-  __syncthreads();
+  const bool full = (SJ + 1) * T <= n;  // SJ >= SI: the i block is full too
+  const bool fast = __syncthreads_and(inbox) && full && a.fast_ok && !MULTI;
 
-  const MinImage mi = s.mi;
   const int I = warp;  // local tile row
-  const int ilim = n - (ibase + I * 32);  // rows of this tile that exist
-  for (int c = diag ? I : 0; c < ST; ++c) {
-    const int jl = c * 32 + lane;
-    const int jg = jbase + jl;
-    const double xj = jx[jl], yj = jy[jl], zj = jz[jl];
-    const int sj = MULTI ? jspec[jl] : 0;
-    const bool jvalid = jg < n;
-    uint32_t lword = 0u, uword = 0u;
-    const bool diag_tile = diag && c == I;
-#pragma unroll 4
-    for (int ii = 0; ii < 32; ++ii) {
-      const int il = I * 32 + ii;
-      const double dx = min_image(sub(ix[il], xj), mi);
-      const double dy = min_image(sub(iy[il], yj), mi);
-      const double dz = min_image(sub(iz[il], zj), mi);
-      const double r2 = norm2_exact(dx, dy, dz);
-      double lim;
-      if constexpr (MULTI)
-        lim = rmax2_s[ispec[il] * s.ns + sj];
-      else
-        lim = a.rc2;
-      bool pass = r2 < lim && jvalid && ii < ilim;
-      if (diag_tile) pass = pass && lane > ii;
-      const uint32_t b = __ballot_sync(0xffffffffu, pass);
-      if (lane == ii) uword = b;
-      lword |= uint32_t(pass) << ii;
+  const int ib = I * 32;
+  if (fast) {
+    const double negL = s.mi.negL;
+    const float thr = a.thr;
+    const double lim = a.rc2;
+    int c = 0;
+    if (diag) {
+      search_tile_fast<1, true>(ixy, iz, jxy, jz, ib, I, I, lane, ST, lim, negL, thr, wu, wl);
+      c = I + 1;
     }
-    wu[I * 32 + lane][c] = uword;
-    wl[c * 32 + lane][I] = lword;
+    for (; c + 1 < ST; c += 2)
+      search_tile_fast<2, false>(ixy, iz, jxy, jz, ib, c, I, lane, ST, lim, negL, thr, wu, wl);
+    if (c < ST)
+      search_tile_fast<1, false>(ixy, iz, jxy, jz, ib, c, I, lane, ST, lim, negL, thr, wu, wl);
+  } else {
+    // generic path: exact minimum image for any input, partial tiles, mixtures
+    const MinImage mi = s.mi;
+    const int ilim = n - (ibase + ib);
+    for (int c = diag ? I : 0; c < ST; ++c) {
+      const int jl = c * 32 + lane;
+      const double xj = jxy[jl].x, yj = jxy[jl].y, zj = jz[jl];
+      const int sj = MULTI ? jspec[jl] : 0;
+      const bool jvalid = jbase + jl < n;
+      uint32_t lword = 0u;
+      const bool diag_tile = diag && c == I;
+      for (int ii = 0; ii < 32; ++ii) {
+        const int il = ib + ii;
+        const double dx = min_image(sub(ixy[il].x, xj), mi);
+        const double dy = min_image(sub(ixy[il].y, yj), mi);
+        const double dz = min_image(sub(iz[il], zj), mi);
+        const double r2 = norm2_exact(dx, dy, dz);
+        double lim;
+        if constexpr (MULTI)
+          lim = rmax2_s[ispec[il] * s.ns + sj];
+        else
+          lim = a.rc2;
+        bool pass = r2 < lim && jvalid && ii < ilim;
+        if (diag_tile) pass = pass && lane > ii;
+        const uint32_t b = __ballot_sync(0xffffffffu, pass);
+        if (lane == 0) wu[(ib + ii) * ST + c] = b;
+        lword |= uint32_t(pass) << ii;
+      }
+      wl[(c * 32 + lane) * ST + I] = lword;
+    }
   }
   __syncthreads();
 
   // store: rows of tile-row block SI get columns SJ*ST.. (wu); rows of block SJ
   // get columns SI*ST.. (wl).  Diagonal super-tiles merge both.
   uint32_t* M = a.mask + size_t(r) * s.n_pad * s.words;
-  {
-    const int row = tid;
-    if (diag) {
-      uint32_t* dst = M + size_t(ibase + row) * s.words + SI * ST;
+  const int row = tid;
+  if (diag) {
+    uint32_t* dst = M + size_t(ibase + row) * s.words + SI * ST;
 #pragma unroll
-      for (int c = 0; c < ST; ++c) dst[c] = wu[row][c] | wl[row][c];
+    for (int c = 0; c < ST; ++c) dst[c] = wu[row * ST + c] | wl[row * ST + c];
+  } else {
+    uint32_t* du = M + size_t(ibase + row) * s.words + SJ * ST;
+    uint32_t* dl = M + size_t(jbase + row) * s.words + SI * ST;
+    if constexpr (ST % 4 == 0) {
+#pragma unroll
+      for (int c = 0; c < ST; c += 4) {
+        *reinterpret_cast<uint4*>(du + c) = *reinterpret_cast<const uint4*>(&wu[row * ST + c]);
+        *reinterpret_cast<uint4*>(dl + c) = *reinterpret_cast<const uint4*>(&wl[row * ST + c]);
+      }
     } else {
-      uint32_t* du = M + size_t(ibase + row) * s.words + SJ * ST;
-      uint32_t* dl = M + size_t(jbase + row) * s.words + SI * ST;
-      if constexpr (ST % 4 == 0) {
 #pragma unroll
-        for (int c = 0; c < ST; c += 4) {
-          *reinterpret_cast<uint4*>(du + c) = make_uint4(wu[row][c], wu[row][c + 1], wu[row][c + 2], wu[row][c + 3]);
-          *reinterpret_cast<uint4*>(dl + c) = make_uint4(wl[row][c], wl[row][c + 1], wl[row][c + 2], wl[row][c + 3]);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < ST; ++c) {
-          du[c] = wu[row][c];
-          dl[c] = wl[row][c];
-        }
+      for (int c = 0; c < ST; ++c) {
+        du[c] = wu[row * ST + c];
+        dl[c] = wl[row * ST + c];
       }
     }
   }
 }
 
+// ------------------------------------------------- partner enumeration
+// Walks the set bits of one bit-matrix row (the molecule's partners j, both
+// j<i and j>i) with all 32 lanes busy: each round every lane holding bits
+// pushes its lowest one into the warp queue at its ballot rank (warp ballot +
+// prefix count compaction); every full batch of 32 partners is evaluated
+// lane-parallel by `body(j, valid)`.  Partner order, and hence the
+// accumulation order, is fixed by the bit matrix: results are reproducible.
+template <typename Body>
+__device__ __forceinline__ void for_each_partner(const uint32_t* __restrict__ row, int words,
+                                                 int lane, int* q, Body&& body) {
+  const uint32_t lt = (1u << lane) - 1u;
+  int fill = 0;
+  for (int w0 = 0; w0 < words; w0 += 32) {
+    const int w = w0 + lane;
+    uint32_t m = w < words ? __ldg(row + w) : 0u;
+    while (true) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, m != 0u);
+      if (bal == 0u) break;
+      if (m) {
+        q[fill + __popc(bal & lt)] = w * 32 + __ffs(m) - 1;
+        m &= m - 1u;
+      }
+      fill += __popc(bal);
+      if (fill >= 32) {
+        __syncwarp();
+        body(q[lane], true);
+        __syncwarp();
+        fill -= 32;
+        if (lane < fill) q[lane] = q[32 + lane];
+        __syncwarp();
+      }
+    }
+  }
+  __syncwarp();
+  if (fill > 0) body(lane < fill ? q[lane] : 0, lane < fill);
+}
+
+// Per-CTA scalar partials -> one fixed-order total per replica, done by the
+// last CTA to finish (integer ticket; no floating-point atomics).
+template <int NS>
+__device__ void finalize_scalars(const double* v /* NS values, valid on lane 0 of each warp */,
+                                 double* cta_part, unsigned* ticket, double* sums, int r,
+                                 int sum_offset) {
+  __shared__ double red[8][NS];
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const int nblk = gridDim.x;
+  if (lane == 0)
+    for (int k = 0; k < NS; ++k) red[warp][k] = v[k];
+  __syncthreads();
+  if (threadIdx.x < NS) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += red[w][threadIdx.x];
+    cta_part[(size_t(r) * NS + threadIdx.x) * nblk + blockIdx.x] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&ticket[r], 1u) == unsigned(nblk - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int k = 0; k < NS; ++k) {
+    const volatile double* col = cta_part + (size_t(r) * NS + k) * nblk;
+    double t = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) t += col[b];
+    t = warp_sum(t);
+    __syncthreads();
+    if (lane == 0) red[warp][0] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tt = 0.0;
+      for (int w = 0; w < nw; ++w) tt += red[w][0];
+      sums[size_t(r) * kNumSums + sum_offset + k] = tt;
+    }
+  }
+  if (threadIdx.x == 0) ticket[r] = 0u;  // re-armed for the next launch / graph replay
+}
+
 // ------------------------------------------------------- single-site forces
 // evaluate_range_single_site (potentials.cpp:148-181).  One warp per molecule
-// row; lanes stride over the row's bit words.  Pair (lo, hi) is always
-// evaluated as R = min_image(com_lo - com_hi) and negated for the hi row.
+// row (grid-stride over rows), partners from the bit matrix.  With
+// R = min_image(com_i - com_j) the reference's canonical vector is +-R with
+// identical magnitude bits (IEEE subtraction and round-half-even are
+// sign-symmetric), so the force on row i is always fs * R.  Energy, virial
+// and s1/s2 are taken on the i < j side only.
 struct ForceArgs {
   SysDev s;
   StateDev st;
   const uint32_t* mask;
-  double* row_scal;  // R * kNumRowScalars * n_pad
+  double* cta_part;  // R * kNumRowScalars * gridDim.x
+  unsigned* ticket;  // R
+  double* sums;      // R * kNumSums
   double c12, c6;    // single-species LJ term (PairTable lj[0])
   double rc2;
   double alpha, two_alpha_over_sqrt_pi;
   double rf_r3inv, rf_shift;
   int vderiv;
-  int row_begin, row_end;  // rows processed (all rows normally)
 };
 
+constexpr int kForceWarps = 8;
+
 template <bool MULTI_SPECIES>
-__global__ void __launch_bounds__(256) k_force_single(ForceArgs a) {
+__global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) {
+  __shared__ int queue[kForceWarps][64];
   const SysDev& s = a.s;
-  const int lane = threadIdx.x & 31;
-  const int row_g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.y;
-  const int i = row_g;
-  if (i >= s.n) return;
   const size_t roff = size_t(r) * s.n;
-  const double xi = a.st.px[roff + i], yi = a.st.py[roff + i], zi = a.st.pz[roff + i];
-  const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
+  const double* __restrict__ px = a.st.px + roff;
+  const double* __restrict__ py = a.st.py + roff;
+  const double* __restrict__ pz = a.st.pz + roff;
   const MinImage mi = s.mi;
-  double fx = 0, fy = 0, fz = 0, u = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
-  const int si = MULTI_SPECIES ? s.species_of[i] : 0;
-  for (int w = lane; w < s.words; w += 32) {
-    uint32_t m = row[w];
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int j = w * 32 + b;
-      const double xj = a.st.px[roff + j], yj = a.st.py[roff + j], zj = a.st.pz[roff + j];
-      const bool lo = i < j;
-      double dx, dy, dz;
-      if (lo) {
-        dx = min_image(sub(xi, xj), mi);
-        dy = min_image(sub(yi, yj), mi);
-        dz = min_image(sub(zi, zj), mi);
-      } else {
-        dx = min_image(sub(xj, xi), mi);
-        dy = min_image(sub(yj, yi), mi);
-        dz = min_image(sub(zj, zi), mi);
-      }
+  double u = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
+  for (int i = blockIdx.x * kForceWarps + warp; i < s.n; i += gridDim.x * kForceWarps) {
+    const double xi = px[i], yi = py[i], zi = pz[i];
+    const int si = MULTI_SPECIES ? s.species_of[i] : 0;
+    double fx = 0, fy = 0, fz = 0;
+    const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
+    for_each_partner(row, s.words, lane, queue[warp], [&](int j, bool valid) {
+      if (!valid) return;
+      const double dx = min_image(sub(xi, px[j]), mi);
+      const double dy = min_image(sub(yi, py[j]), mi);
+      const double dz = min_image(sub(zi, pz[j]), mi);
       const double r2 = norm2_exact(dx, dy, dz);
       double c12 = a.c12, c6 = a.c6;
       if constexpr (MULTI_SPECIES) {
         const int sj = s.species_of[j];
-        const DevPairInfo& pinfo = s.tab->pair[(lo ? si : sj) * s.ns + (lo ? sj : si)];
+        const DevPairInfo& pinfo = s.tab->pair[(i < j) ? si * s.ns + sj : sj * s.ns + si];
         c12 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c12 : 0.0;
         c6 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c6 : 0.0;
       }
@@ -256,102 +415,101 @@ __global__ void __launch_bounds__(256) k_force_single(ForceArgs a) {
       const double a6 = c6 * ir6;
       const double du_r = -12.0 * a12 + 6.0 * a6;
       const double fs = -du_r * inv_r2;
-      const double gx = fs * dx, gy = fs * dy, gz = fs * dz;  // force on the lower molecule
-      if (lo) {
-        fx += gx;
-        fy += gy;
-        fz += gz;
+      const double gx = fs * dx, gy = fs * dy, gz = fs * dz;
+      fx += gx;
+      fy += gy;
+      fz += gz;
+      if (i < j) {
         u += a12 - a6;
         vir += dx * gx + dy * gy + dz * gz;
         s1 += du_r;
         s2 += 156.0 * a12 - 42.0 * a6;
         cnt += 1.0;
-      } else {
-        fx -= gx;
-        fy -= gy;
-        fz -= gz;
       }
+    });
+    fx = warp_sum(fx);
+    fy = warp_sum(fy);
+    fz = warp_sum(fz);
+    if (lane == 0) {
+      a.st.fx[roff + i] = fx;
+      a.st.fy[roff + i] = fy;
+      a.st.fz[roff + i] = fz;
     }
   }
-  fx = warp_sum(fx);
-  fy = warp_sum(fy);
-  fz = warp_sum(fz);
-  u = warp_sum(u);
-  vir = warp_sum(vir);
-  s1 = warp_sum(s1);
-  s2 = warp_sum(s2);
-  cnt = warp_sum(cnt);
-  if (lane == 0) {
-    a.st.fx[roff + i] = fx;
-    a.st.fy[roff + i] = fy;
-    a.st.fz[roff + i] = fz;
-    double* rs = a.row_scal + size_t(r) * kNumRowScalars * s.n_pad;
-    rs[0 * s.n_pad + i] = u;
-    rs[1 * s.n_pad + i] = 0.0;
-    rs[2 * s.n_pad + i] = 0.0;
-    rs[3 * s.n_pad + i] = a.vderiv ? s1 : 0.0;
-    rs[4 * s.n_pad + i] = a.vderiv ? s2 : 0.0;
-    rs[5 * s.n_pad + i] = vir;
-    rs[6 * s.n_pad + i] = cnt;
-  }
+  double v[kNumRowScalars] = {warp_sum(u), 0.0, 0.0, a.vderiv ? warp_sum(s1) : 0.0,
+                              a.vderiv ? warp_sum(s2) : 0.0, warp_sum(vir), warp_sum(cnt)};
+  finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
 }
 
 // -------------------------------------------------------- multi-site forces
-// evaluate_pair_range general path (potentials.cpp:204-292): COM pair passed
-// the search; LJ terms (218-242) and charge terms (244-283) with the site-site
-// cutoff decided on canonically computed rv = (R + da) - db, bit-exact.
+// evaluate_pair_range general path (potentials.cpp:204-292): the COM pair
+// passed the search; LJ terms (218-242) and charge terms (244-283).  With
+// R = min_image(com_i - com_j) the site vector from row i's side is
+//   i < j:  rv = (R + d_i,a) - d_j,b            (the reference's own bits)
+//   i > j:  rv = (R - d_j,a) + d_i,b  = -rv_ref (bit-exact negation)
+// so the site cutoff r2 < rc2 is decided on the reference's bits either way;
+// force on i is fs*rv and torque d_i x (fs*rv).
 // METHOD: 0 none, 1 reaction field, 2 ewald real space.
 template <int METHOD>
-__global__ void __launch_bounds__(256) k_force_multi(ForceArgs a) {
+__global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
+  __shared__ int queue[kForceWarps][64];
   const SysDev& s = a.s;
-  const DevTables* tab = s.tab;
-  const int lane = threadIdx.x & 31;
-  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const DevTables* __restrict__ tab = s.tab;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.y;
-  if (i >= s.n) return;
   const size_t roff = size_t(r) * s.n;
   const size_t soff = size_t(r) * s.total_sites;
-  const double xi = a.st.px[roff + i], yi = a.st.py[roff + i], zi = a.st.pz[roff + i];
-  const int si = s.species_of[i];
-  const int bi = s.site_begin[i];
-  const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
+  const double* __restrict__ px = a.st.px + roff;
+  const double* __restrict__ py = a.st.py + roff;
+  const double* __restrict__ pz = a.st.pz + roff;
+  const double* __restrict__ ox = a.st.ox + soff;
+  const double* __restrict__ oy = a.st.oy + soff;
+  const double* __restrict__ oz = a.st.oz + soff;
   const MinImage mi = s.mi;
   const double rc2 = a.rc2;
-  double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
   double ulj = 0, uel = 0, urf = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
-  for (int w = lane; w < s.words; w += 32) {
-    uint32_t m = row[w];
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int j = w * 32 + b;
+  for (int i = blockIdx.x * kForceWarps + warp; i < s.n; i += gridDim.x * kForceWarps) {
+    const double xi = px[i], yi = py[i], zi = pz[i];
+    const int si = s.species_of[i];
+    const int bi = s.site_begin[i];
+    double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
+    const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
+    for_each_partner(row, s.words, lane, queue[warp], [&](int j, bool valid) {
+      if (!valid) return;
       const bool lo = i < j;
-      const int l = lo ? i : j, h = lo ? j : i;
-      const double xl = lo ? xi : a.st.px[roff + j], yl = lo ? yi : a.st.py[roff + j],
-                   zl = lo ? zi : a.st.pz[roff + j];
-      const double xh = lo ? a.st.px[roff + j] : xi, yh = lo ? a.st.py[roff + j] : yi,
-                   zh = lo ? a.st.pz[roff + j] : zi;
-      const double Rx = min_image(sub(xl, xh), mi);
-      const double Ry = min_image(sub(yl, yh), mi);
-      const double Rz = min_image(sub(zl, zh), mi);
-      const double R2 = norm2_exact(Rx, Ry, Rz);
-      const int sl = lo ? si : s.species_of[j];
-      const int sh = lo ? s.species_of[j] : si;
-      const int bl = lo ? bi : s.site_begin[j];
-      const int bh = lo ? s.site_begin[j] : bi;
-      const DevPairInfo pinfo = tab->pair[sl * s.ns + sh];
-      double s1p = 0.0, s2p = 0.0;
-      cnt += lo ? 1.0 : 0.0;
-      // LJ terms
+      const double Rx = min_image(sub(xi, px[j]), mi);
+      const double Ry = min_image(sub(yi, py[j]), mi);
+      const double Rz = min_image(sub(zi, pz[j]), mi);
+      const int sj = s.species_of[j];
+      const int bj = s.site_begin[j];
+      const DevPairInfo pinfo = tab->pair[lo ? si * s.ns + sj : sj * s.ns + si];
+      double R2 = 0.0, s1p = 0.0, s2p = 0.0;
+      if (lo) {
+        R2 = norm2_exact(Rx, Ry, Rz);
+        cnt += 1.0;
+      }
+      auto site_term = [&](int ta, int tb, double& rx, double& ry, double& rz, double& dix,
+                           double& diy, double& diz) -> double {
+        const int ki = bi + (lo ? ta : tb), kj = bj + (lo ? tb : ta);
+        dix = ox[ki];
+        diy = oy[ki];
+        diz = oz[ki];
+        const double djx = ox[kj], djy = oy[kj], djz = oz[kj];
+        if (lo) {
+          rx = sub(add(Rx, dix), djx);
+          ry = sub(add(Ry, diy), djy);
+          rz = sub(add(Rz, diz), djz);
+        } else {
+          rx = add(sub(Rx, djx), dix);
+          ry = add(sub(Ry, djy), diy);
+          rz = add(sub(Rz, djz), diz);
+        }
+        return norm2_exact(rx, ry, rz);
+      };
       for (int q = 0; q < pinfo.lj_count; ++q) {
         const DevLjTerm t = tab->lj[pinfo.lj_begin + q];
-        const double dax = a.st.ox[soff + bl + t.a], day = a.st.oy[soff + bl + t.a],
-                     daz = a.st.oz[soff + bl + t.a];
-        const double dbx = a.st.ox[soff + bh + t.b], dby = a.st.oy[soff + bh + t.b],
-                     dbz = a.st.oz[soff + bh + t.b];
-        const double rx = sub(add(Rx, dax), dbx), ry = sub(add(Ry, day), dby),
-                     rz = sub(add(Rz, daz), dbz);
-        const double r2 = norm2_exact(rx, ry, rz);
+        double rx, ry, rz, dix, diy, diz;
+        const double r2 = site_term(t.a, t.b, rx, ry, rz, dix, diy, diz);
         if (r2 >= rc2) continue;
         const double inv_r2 = 1.0 / r2;
         const double ir6 = inv_r2 * inv_r2 * inv_r2;
@@ -360,13 +518,13 @@ __global__ void __launch_bounds__(256) k_force_multi(ForceArgs a) {
         const double du_r = -12.0 * a12 + 6.0 * a6;
         const double fs = -du_r * inv_r2;
         const double gx = fs * rx, gy = fs * ry, gz = fs * rz;
+        fx += gx;
+        fy += gy;
+        fz += gz;
+        tx += diy * gz - diz * gy;
+        ty += diz * gx - dix * gz;
+        tz += dix * gy - diy * gx;
         if (lo) {
-          fx += gx;
-          fy += gy;
-          fz += gz;
-          tx += day * gz - daz * gy;
-          ty += daz * gx - dax * gz;
-          tz += dax * gy - day * gx;
           ulj += a12 - a6;
           vir += Rx * gx + Ry * gy + Rz * gz;
           if (a.vderiv) {
@@ -376,25 +534,13 @@ __global__ void __launch_bounds__(256) k_force_multi(ForceArgs a) {
             s1p += du_r * arr;
             s2p += d2u_r2 * arr * arr + du_r * inv_r2 * (R2 - rvR * arr);
           }
-        } else {
-          fx -= gx;
-          fy -= gy;
-          fz -= gz;
-          tx -= dby * gz - dbz * gy;
-          ty -= dbz * gx - dbx * gz;
-          tz -= dbx * gy - dby * gx;
         }
       }
       if constexpr (METHOD != 0) {
         for (int q = 0; q < pinfo.qq_count; ++q) {
           const DevQTerm t = tab->qq[pinfo.qq_begin + q];
-          const double dax = a.st.ox[soff + bl + t.a], day = a.st.oy[soff + bl + t.a],
-                       daz = a.st.oz[soff + bl + t.a];
-          const double dbx = a.st.ox[soff + bh + t.b], dby = a.st.oy[soff + bh + t.b],
-                       dbz = a.st.oz[soff + bh + t.b];
-          const double rx = sub(add(Rx, dax), dbx), ry = sub(add(Ry, day), dby),
-                       rz = sub(add(Rz, daz), dbz);
-          const double r2 = norm2_exact(rx, ry, rz);
+          double rx, ry, rz, dix, diy, diz;
+          const double r2 = site_term(t.a, t.b, rx, ry, rz, dix, diy, diz);
           if (r2 >= rc2) continue;
           const double inv_r2 = 1.0 / r2;
           const double rr = sqrt(r2);
@@ -415,13 +561,13 @@ __global__ void __launch_bounds__(256) k_force_multi(ForceArgs a) {
           }
           const double fs = -du_r * inv_r2;
           const double gx = fs * rx, gy = fs * ry, gz = fs * rz;
+          fx += gx;
+          fy += gy;
+          fz += gz;
+          tx += diy * gz - diz * gy;
+          ty += diz * gx - dix * gz;
+          tz += dix * gy - diy * gx;
           if (lo) {
-            fx += gx;
-            fy += gy;
-            fz += gz;
-            tx += day * gz - daz * gy;
-            ty += daz * gx - dax * gz;
-            tz += dax * gy - day * gx;
             uel += uu;
             urf += rfu;
             vir += Rx * gx + Ry * gy + Rz * gz;
@@ -431,49 +577,30 @@ __global__ void __launch_bounds__(256) k_force_multi(ForceArgs a) {
               s1p += du_r * arr;
               s2p += d2u_r2 * arr * arr + du_r * inv_r2 * (R2 - rvR * arr);
             }
-          } else {
-            fx -= gx;
-            fy -= gy;
-            fz -= gz;
-            tx -= dby * gz - dbz * gy;
-            ty -= dbz * gx - dbx * gz;
-            tz -= dbx * gy - dby * gx;
           }
         }
       }
       s1 += s1p;
       s2 += s2p;
+    });
+    fx = warp_sum(fx);
+    fy = warp_sum(fy);
+    fz = warp_sum(fz);
+    tx = warp_sum(tx);
+    ty = warp_sum(ty);
+    tz = warp_sum(tz);
+    if (lane == 0) {
+      a.st.fx[roff + i] = fx;
+      a.st.fy[roff + i] = fy;
+      a.st.fz[roff + i] = fz;
+      a.st.tx[roff + i] = tx;
+      a.st.ty[roff + i] = ty;
+      a.st.tz[roff + i] = tz;
     }
   }
-  fx = warp_sum(fx);
-  fy = warp_sum(fy);
-  fz = warp_sum(fz);
-  tx = warp_sum(tx);
-  ty = warp_sum(ty);
-  tz = warp_sum(tz);
-  ulj = warp_sum(ulj);
-  uel = warp_sum(uel);
-  urf = warp_sum(urf);
-  vir = warp_sum(vir);
-  s1 = warp_sum(s1);
-  s2 = warp_sum(s2);
-  cnt = warp_sum(cnt);
-  if (lane == 0) {
-    a.st.fx[roff + i] = fx;
-    a.st.fy[roff + i] = fy;
-    a.st.fz[roff + i] = fz;
-    a.st.tx[roff + i] = tx;
-    a.st.ty[roff + i] = ty;
-    a.st.tz[roff + i] = tz;
-    double* rs = a.row_scal + size_t(r) * kNumRowScalars * s.n_pad;
-    rs[0 * s.n_pad + i] = ulj;
-    rs[1 * s.n_pad + i] = uel;
-    rs[2 * s.n_pad + i] = urf;
-    rs[3 * s.n_pad + i] = s1;
-    rs[4 * s.n_pad + i] = s2;
-    rs[5 * s.n_pad + i] = vir;
-    rs[6 * s.n_pad + i] = cnt;
-  }
+  double v[kNumRowScalars] = {warp_sum(ulj), warp_sum(uel), warp_sum(urf), warp_sum(s1),
+                              warp_sum(s2),  warp_sum(vir), warp_sum(cnt)};
+  finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
 }
 
 // ------------------------------------------------------------------- Ewald
@@ -493,7 +620,9 @@ struct EwaldArgs {
   const DevKVec* kv;    // all k-vectors
   double2* tab;         // R * 3 * (kmax+1) * nq
   double2* S;           // R * nk_total
-  double* uk;           // R * nk_total (0.5 coeff |S|^2)
+  double* uk;           // R * nk (per-CTA partials of U_recip)
+  unsigned* ticket;     // R
+  double* sums;         // R * kNumSums
   int nk_total;
   double two_pi_over_L;
 };
@@ -540,7 +669,8 @@ __device__ __forceinline__ double2 site_phase(const double2* base, int K, int nq
   return cmul(e, vz);
 }
 
-// ewald.cpp:163-169: one CTA per (k, replica), fixed-order block reduction.
+// ewald.cpp:163-169: one CTA per (k, replica), fixed-order block reduction;
+// U_recip = sum_k 0.5 coeff |S|^2 finalized by the last CTA (sums[7]).
 __global__ void __launch_bounds__(256) k_ewald_sk(EwaldArgs a) {
   const int kk = a.k_begin + blockIdx.x;
   const int r = blockIdx.y;
@@ -554,6 +684,7 @@ __global__ void __launch_bounds__(256) k_ewald_sk(EwaldArgs a) {
     sim += e.y * a.q_val[q];
   }
   __shared__ double red[2][8];
+  __shared__ double ukv;
   sre = warp_sum(sre);
   sim = warp_sum(sim);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -569,8 +700,11 @@ __global__ void __launch_bounds__(256) k_ewald_sk(EwaldArgs a) {
       ti += red[1][v];
     }
     a.S[size_t(r) * a.nk_total + kk] = make_double2(tr, ti);
-    a.uk[size_t(r) * a.nk_total + kk] = 0.5 * k.coeff * (tr * tr + ti * ti);
+    ukv = 0.5 * k.coeff * (tr * tr + ti * ti);
   }
+  __syncthreads();
+  const double v[1] = {threadIdx.x == 0 ? ukv : 0.0};
+  finalize_scalars<1>(v, a.uk, a.ticket, a.sums, r, kNumRowScalars);
 }
 
 // ewald.cpp:171-178: one warp per molecule with charges; lanes over k; adds
@@ -622,33 +756,6 @@ __global__ void __launch_bounds__(256) k_ewald_force(EwaldArgs a) {
     a.st.tx[roff + m] += tx;
     a.st.ty[roff + m] += ty;
     a.st.tz[roff + m] += tz;
-  }
-}
-
-// ------------------------------------------------------- scalar reduction
-// One CTA per (scalar, replica): rows in fixed strided order, then a fixed
-// tree; u_recip from the per-k energies.
-__global__ void __launch_bounds__(256) k_reduce_sums(const double* row_scal, const double* uk,
-                                                     int n, int n_pad, int nk_total, int k_begin,
-                                                     int k_end, double* sums) {
-  const int c = blockIdx.x;  // 0..kNumSums-1
-  const int r = blockIdx.y;
-  double acc = 0.0;
-  if (c < kNumRowScalars) {
-    const double* v = row_scal + (size_t(r) * kNumRowScalars + c) * n_pad;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) acc += v[i];
-  } else if (uk) {
-    const double* v = uk + size_t(r) * nk_total;
-    for (int k = k_begin + threadIdx.x; k < k_end; k += blockDim.x) acc += v[k];
-  }
-  __shared__ double red[8];
-  acc = warp_sum(acc);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
-    sums[size_t(r) * kNumSums + c] = t;
   }
 }
 
@@ -718,26 +825,23 @@ __device__ __forceinline__ double wrap1(double x, double L) {
 }
 
 // engine.cpp:107-127 (+ build_scene offsets for the new orientation)
-__global__ void __launch_bounds__(256) k_kick_drift(StepArgs a) {
-  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void kick_drift_one(const StepArgs& a, int gid) {
   const SysDev& s = a.s;
-  if (gid >= s.n * s.R) return;
-  if (*a.error_mol != 0x7fffffff) return;  // state frozen after a failed step
   const int r = gid / s.n, i = gid - r * s.n;
   const DevSpecies& sp = s.tab->species[s.species_of[i]];
   const double dt = a.dt, half = mul(0.5, dt);
   const double c = __ddiv_rn(half, sp.total_mass);
-  double vx = add(a.st.vx[gid], mul(a.st.fx[gid], c));
-  double vy = add(a.st.vy[gid], mul(a.st.fy[gid], c));
-  double vz = add(a.st.vz[gid], mul(a.st.fz[gid], c));
+  const double vx = add(a.st.vx[gid], mul(a.st.fx[gid], c));
+  const double vy = add(a.st.vy[gid], mul(a.st.fy[gid], c));
+  const double vz = add(a.st.vz[gid], mul(a.st.fz[gid], c));
   a.st.vx[gid] = vx;
   a.st.vy[gid] = vy;
   a.st.vz[gid] = vz;
   double px = add(a.st.px[gid], mul(vx, dt));
   double py = add(a.st.py[gid], mul(vy, dt));
   double pz = add(a.st.pz[gid], mul(vz, dt));
+  double q[4] = {a.st.qw[gid], a.st.qx[gid], a.st.qy[gid], a.st.qz[gid]};
   if (sp.rotational_dof > 0) {
-    double q[4] = {a.st.qw[gid], a.st.qx[gid], a.st.qy[gid], a.st.qz[gid]};
     const D3 tb = rotate_inv_exact(q[0], q[1], q[2], q[3], {a.st.tx[gid], a.st.ty[gid], a.st.tz[gid]});
     const double tbv[3] = {tb.x, tb.y, tb.z};
     const double w[3] = {a.st.wx[gid], a.st.wy[gid], a.st.wz[gid]};
@@ -755,12 +859,9 @@ __global__ void __launch_bounds__(256) k_kick_drift(StepArgs a) {
     a.st.qy[gid] = q[2];
     a.st.qz[gid] = q[3];
   }
-  px = wrap1(px, s.mi.L);
-  py = wrap1(py, s.mi.L);
-  pz = wrap1(pz, s.mi.L);
-  a.st.px[gid] = px;
-  a.st.py[gid] = py;
-  a.st.pz[gid] = pz;
+  a.st.px[gid] = wrap1(px, s.mi.L);
+  a.st.py[gid] = wrap1(py, s.mi.L);
+  a.st.pz[gid] = wrap1(pz, s.mi.L);
   if (a.write_offsets) {
     const int base = r * s.total_sites + s.site_begin[i];
     if (sp.centred) {
@@ -768,9 +869,8 @@ __global__ void __launch_bounds__(256) k_kick_drift(StepArgs a) {
       a.st.oy[base] = 0.0;
       a.st.oz[base] = 0.0;
     } else {
-      const double qw = a.st.qw[gid], qx = a.st.qx[gid], qy = a.st.qy[gid], qz = a.st.qz[gid];
       for (int k = 0; k < sp.n_sites; ++k) {
-        const D3 o = rotate_exact(qw, qx, qy, qz, {sp.body[k][0], sp.body[k][1], sp.body[k][2]});
+        const D3 o = rotate_exact(q[0], q[1], q[2], q[3], {sp.body[k][0], sp.body[k][1], sp.body[k][2]});
         a.st.ox[base + k] = o.x;
         a.st.oy[base + k] = o.y;
         a.st.oz[base + k] = o.z;
@@ -779,12 +879,9 @@ __global__ void __launch_bounds__(256) k_kick_drift(StepArgs a) {
   }
 }
 
-// engine.cpp:131-142
-__global__ void __launch_bounds__(256) k_kick(StepArgs a) {
-  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+// engine.cpp:131-142; returns check_finite (model.cpp:288-302)
+__device__ __forceinline__ bool kick_one(const StepArgs& a, int gid) {
   const SysDev& s = a.s;
-  if (gid >= s.n * s.R) return;
-  if (*a.error_mol != 0x7fffffff) return;
   const int i = gid % s.n;
   const DevSpecies& sp = s.tab->species[s.species_of[i]];
   const double half = mul(0.5, a.dt);
@@ -806,11 +903,40 @@ __global__ void __launch_bounds__(256) k_kick(StepArgs a) {
     a.st.wy[gid] = w1;
     a.st.wz[gid] = w2;
   }
-  // check_finite (model.cpp:288-302)
-  const bool ok = isfinite(a.st.px[gid]) && isfinite(a.st.py[gid]) && isfinite(a.st.pz[gid]) &&
-                  isfinite(vx) && isfinite(vy) && isfinite(vz) && isfinite(w0) && isfinite(w1) &&
-                  isfinite(w2) && isfinite(a.st.qw[gid]);
-  if (!ok) atomicMin(a.error_mol, gid);
+  return isfinite(a.st.px[gid]) && isfinite(a.st.py[gid]) && isfinite(a.st.pz[gid]) &&
+         isfinite(vx) && isfinite(vy) && isfinite(vz) && isfinite(w0) && isfinite(w1) &&
+         isfinite(w2) && isfinite(a.st.qw[gid]);
+}
+
+// first half of a step: half kick, drift, rotate, wrap, offsets
+__global__ void __launch_bounds__(256) k_kick_drift(StepArgs a) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= a.s.n * a.s.R) return;
+  if (*a.error_mol != 0x7fffffff) return;  // state frozen after a failed step
+  kick_drift_one(a, gid);
+}
+
+// second half of a step: half kick + check_finite
+__global__ void __launch_bounds__(256) k_kick(StepArgs a) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= a.s.n * a.s.R) return;
+  if (*a.error_mol != 0x7fffffff) return;
+  if (!kick_one(a, gid)) atomicMin(a.error_mol, gid);
+}
+
+// end of step k fused with the start of step k+1 (one launch in the step loop).
+// A molecule that fails check_finite stops the run; the others may already
+// have started step k+1, so the failing molecule index is recorded and the
+// host reports the failure (the reference throws at the end of step k).
+__global__ void __launch_bounds__(256) k_kick_kick_drift(StepArgs a) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= a.s.n * a.s.R) return;
+  if (*a.error_mol != 0x7fffffff) return;
+  if (!kick_one(a, gid)) {
+    atomicMin(a.error_mol, gid);
+    return;
+  }
+  kick_drift_one(a, gid);
 }
 
 // wrap (model.cpp:279-286) for set_state

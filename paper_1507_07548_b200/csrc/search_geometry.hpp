@@ -21,7 +21,7 @@ inline SearchGeometry search_geometry(int n) {
   SearchGeometry g;
   g.n = n;
   g.n_tiles = (n + 31) / 32;
-  g.st = n >= 8192 ? 8 : (n >= 2048 ? 4 : (n >= 512 ? 2 : 1));
+  g.st = n >= 8192 ? 8 : (n >= 4096 ? 4 : (n >= 1536 ? 2 : 1));
   g.n_super = (g.n_tiles + g.st - 1) / g.st;
   g.words = g.n_super * g.st;
   g.n_pad = g.words * 32;

@@ -223,6 +223,25 @@ class Engine:
         """Engine::step (src/engine.cpp:102-143) x nsteps."""
         check(_abi.lib().b2md_step(self._c.ctx, int(nsteps)))
 
+    def step_async(self, nsteps: int = 1) -> None:
+        """Enqueue steps without waiting; sync() waits and raises like step()."""
+        check(_abi.lib().b2md_step_async(self._c.ctx, int(nsteps)))
+
+    def sync(self) -> None:
+        check(_abi.lib().b2md_sync(self._c.ctx))
+
+    def upload_state_raw(self, pos, orient, vel, ang_vel, force=None, torque=None) -> None:
+        """b2md_upload_state from contiguous float64 host buffers (no evaluation)."""
+        check(_abi.lib().b2md_upload_state(self._c.ctx, *map(_abi.dptr, (pos, orient, vel, ang_vel, force, torque))))
+
+    def get_state_raw(self, pos=None, orient=None, vel=None, ang_vel=None, force=None, torque=None):
+        """Download into caller-provided float64 host buffers; returns energies."""
+        R = self.replicas
+        e = (_abi.b2md_energy * R)()
+        s = (_abi.b2md_eval_stats * R)()
+        check(_abi.lib().b2md_get_state(self._c.ctx, *map(_abi.dptr, (pos, orient, vel, ang_vel, force, torque)), e, s))
+        return self._c.energies(e, s)
+
     def states(self) -> list[SystemState]:
         n, R = self._c.n, self.replicas
         pos = np.empty((R * n, 3))

@@ -1,0 +1,90 @@
+"""Generates tests/golden/*.npz from the UNMODIFIED reference library
+(oracle/_ref/libtmdref.so, built by `make -C oracle` from /root/reference).
+
+Run in the build container (the reference is not on the GPU box):
+    python tests/golden/make_golden.py
+Each case stores the inputs (composition is rebuilt from tests/systems.py by
+name), the reference outputs of tmd::ForceField::evaluate / Engine::step and
+the COM partner list computed with the reference's own minimum_image/norm2.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+from oracle import pyoracle  # noqa: E402
+from paper_1507_07548_b200 import configs  # noqa: E402
+import golden_cases  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def rng_vectors():
+    lib = pyoracle.ref_lib()
+    lib.ref_rng_draws.argtypes = [C.c_uint64, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+                                  C.POINTER(C.c_double)]
+    seeds = [0, 1, 77, (1 << 63) + 5]
+    n = 32
+    u64 = np.zeros((len(seeds), n), dtype=np.uint64)
+    uni = np.zeros((len(seeds), n))
+    gau = np.zeros((len(seeds), n))
+    for k, s in enumerate(seeds):
+        lib.ref_rng_draws(s, n, u64[k].ctypes.data_as(C.POINTER(C.c_uint64)),
+                          uni[k].ctypes.data_as(C.POINTER(C.c_double)),
+                          gau[k].ctypes.data_as(C.POINTER(C.c_double)))
+    np.savez_compressed(OUT / "rng.npz", seeds=np.array(seeds, dtype=np.uint64), u64=u64,
+                        uniform=uni, gaussian=gau)
+
+
+def species_vectors():
+    out = {}
+    for name, sites in golden_cases.species_cases().items():
+        sp = pyoracle.build_species_c(sites, "ref")
+        out[name + "_body"] = np.array([sp.sites[k].body_pos[:] for k in range(sp.n_sites)])
+        out[name + "_inertia"] = np.array(sp.inertia_principal[:])
+        out[name + "_scalars"] = np.array([sp.total_mass, sp.net_charge, sp.max_extent,
+                                           sp.rotational_dof])
+    np.savez_compressed(OUT / "species.npz", **out)
+
+
+def eval_vectors():
+    for name, (comp, opts, st) in golden_cases.eval_cases().items():
+        ref = pyoracle.RefFF(comp, opts)
+        r = ref.evaluate(st.pos, st.orient)
+        e = r["energy"]
+        np.savez_compressed(
+            OUT / f"eval_{name}.npz", pos=st.pos, orient=st.orient, force=r["force"],
+            torque=r["torque"], virial=r["virial"],
+            energy=np.array([getattr(e, f) for f in golden_cases.ENERGY_FIELDS]),
+            pairs=ref.pair_list(st.pos), warning=np.array(ref.warning))
+
+
+def traj_vectors():
+    for name, (comp, opts, st, dt, steps) in golden_cases.traj_cases().items():
+        eng = pyoracle.RefEngine(comp, opts, dt, seed=1)
+        eng.set_state(st.pos, st.orient, st.vel, st.ang_vel)
+        eng.step(steps)
+        s = eng.state()
+        e = s["energy"]
+        np.savez_compressed(
+            OUT / f"traj_{name}.npz", pos0=st.pos, orient0=st.orient, vel0=st.vel,
+            ang_vel0=st.ang_vel, dt=dt, steps=steps, pos=s["pos"], orient=s["orient"],
+            vel=s["vel"], ang_vel=s["ang_vel"], force=s["force"], torque=s["torque"],
+            virial=s["virial"], energy=np.array([getattr(e, f) for f in golden_cases.ENERGY_FIELDS]))
+
+
+if __name__ == "__main__":
+    if not pyoracle.ref_available():
+        sys.exit("oracle/_ref/libtmdref.so missing: run `make -C oracle` with /root/reference present")
+    rng_vectors()
+    species_vectors()
+    eval_vectors()
+    traj_vectors()
+    print("golden vectors written to", OUT)

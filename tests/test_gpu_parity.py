@@ -1,0 +1,318 @@
+"""GPU parity: the sm_100a path through the C ABI against the oracle and the
+reference's golden vectors.
+
+Tolerances (BASELINE.json north_star):
+  * COM pair lists: bit-exact (set and order);
+  * forces / torques: max |dF| <= 1e-10 * max |F_ref|;
+  * energy parts, virial: relative 1e-9 (absolute floor 1e-9 * sum |parts|);
+  * trajectories: positions (minimum image) / L, velocities / max|v|,
+    quaternions (sign fixed), total energy: 1e-9.
+"""
+from __future__ import annotations
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1507_07548_b200 as b2
+from oracle import pyoracle
+from paper_1507_07548_b200 import configs
+
+import golden_cases
+import systems
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).resolve().parent / "golden"
+F_TOL = 1e-10
+E_TOL = 1e-9
+T_TOL = 1e-9
+
+
+def check_vec(a, ref, tol=F_TOL, what=""):
+    scale = max(1.0, float(np.abs(ref).max())) if ref.size else 1.0
+    err = float(np.abs(a - ref).max()) / scale if ref.size else 0.0
+    assert err <= tol, f"{what}: {err:.3e} > {tol}"
+
+
+def check_energy(e, ref, virial=None, ref_virial=None):
+    fields = golden_cases.ENERGY_FIELDS
+    a = np.array([getattr(e, f) for f in fields])
+    b = ref if isinstance(ref, np.ndarray) else np.array([getattr(ref, f) for f in fields])
+    floor = E_TOL * max(1e-300, float(np.abs(b).sum()))
+    for f, x, y in zip(fields, a, b):
+        assert abs(x - y) <= max(E_TOL * abs(y), floor), f"{f}: {x} vs {y}"
+    if virial is not None:
+        assert abs(virial - ref_virial) <= E_TOL * max(abs(ref_virial), 1.0)
+
+
+def gpu_eval(comp, opts, pos, orient):
+    ff = b2.ForceField(comp, opts)
+    st = b2.SystemState(comp.molecule_count(), comp.box_length)
+    st.pos = np.array(pos, dtype=np.float64)
+    st.orient = np.array(orient, dtype=np.float64)
+    ff.evaluate(st)
+    return ff, st
+
+
+# ------------------------------------------------------------ golden vectors
+@pytest.mark.parametrize("name", list(golden_cases.eval_cases()))
+def test_golden_evaluations(name):
+    comp, opts, _ = golden_cases.eval_cases()[name]
+    g = np.load(GOLDEN / f"eval_{name}.npz")
+    ff, st = gpu_eval(comp, opts, g["pos"], g["orient"])
+    assert np.array_equal(ff.pair_list(), g["pairs"])
+    check_vec(st.force, g["force"], what="force")
+    check_vec(st.torque, g["torque"], what="torque")
+    check_energy(st.energy, g["energy"], st.virial, float(g["virial"]))
+    assert ff.warning == str(g["warning"])
+
+
+@pytest.mark.parametrize("name", list(golden_cases.traj_cases()))
+def test_golden_trajectories(name):
+    comp, opts, _, _, _ = golden_cases.traj_cases()[name]
+    g = np.load(GOLDEN / f"traj_{name}.npz")
+    eng = b2.Engine(comp, opts, float(g["dt"]))
+    st = b2.SystemState(comp.molecule_count(), comp.box_length)
+    st.pos, st.orient, st.vel, st.ang_vel = g["pos0"], g["orient0"], g["vel0"], g["ang_vel0"]
+    eng.set_state(st)
+    eng.step(int(g["steps"]))
+    out = eng.state()
+    compare_states(out, {k: g[k] for k in ("pos", "orient", "vel", "ang_vel")}, comp.box_length)
+    check_energy(out.energy, g["energy"])
+
+
+def compare_states(out, ref, L):
+    d = out.pos - ref["pos"]
+    d -= L * np.round(d / L)
+    assert np.abs(d).max() / L <= T_TOL
+    assert np.abs(out.vel - ref["vel"]).max() / max(1e-300, np.abs(ref["vel"]).max()) <= T_TOL
+    q, qr = out.orient, ref["orient"]
+    sign = np.where(np.sum(q * qr, axis=1) < 0, -1.0, 1.0)[:, None]
+    assert np.abs(q * sign - qr).max() <= T_TOL
+    wr = np.abs(ref["ang_vel"]).max()
+    if wr > 0:
+        assert np.abs(out.ang_vel - ref["ang_vel"]).max() / wr <= T_TOL
+
+
+# ------------------------------------------------ BASELINE configs vs oracle
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg1", "cfg2", "cfg3"])
+def test_baseline_config_evaluation(cfg):
+    wl = configs.make(cfg)
+    st = wl.states[0]
+    o = pyoracle.OracleFF(wl.comp, wl.opts)
+    ref = o.evaluate(st.pos, st.orient)
+    ff, out = gpu_eval(wl.comp, wl.opts, st.pos, st.orient)
+    pairs = ff.pair_list()
+    assert len(pairs) == ref["com_pairs"]
+    assert np.array_equal(pairs, o.pair_list(st.pos))
+    check_vec(out.force, ref["force"], what="force")
+    check_vec(out.torque, ref["torque"], what="torque")
+    check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+
+
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg1"])
+def test_baseline_100_step_trajectory(cfg):
+    wl = configs.make(cfg)
+    st = wl.states[0]
+    eng = b2.Engine(wl.comp, wl.opts, wl.dt)
+    eng.set_state(st)
+    eng.step(wl.steps)
+    out = eng.state()
+    ref = pyoracle.OracleFF(wl.comp, wl.opts).run(wl.dt, wl.steps, st.pos, st.orient, st.vel, st.ang_vel)
+    compare_states(out, ref, wl.comp.box_length)
+    check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+    # the engine's device pair list after 100 steps is the oracle's on that state
+    assert np.array_equal(eng.pair_list(), pyoracle.OracleFF(wl.comp, wl.opts).pair_list(ref["pos"]))
+
+
+def test_replica_batch_cfg4():
+    wl = configs.make("cfg4", replicas=4, steps=20)
+    eng = b2.Engine(wl.comp, wl.opts, wl.dt, replicas=4)
+    eng.set_state(wl.states)
+    first = eng.states()
+    eng.step(20)
+    outs = eng.states()
+    o = pyoracle.OracleFF(wl.comp, wl.opts)
+    for r, st in enumerate(wl.states):
+        ref0 = o.evaluate(st.pos, st.orient)
+        check_vec(first[r].force, ref0["force"], what=f"replica {r} force")
+        check_vec(first[r].torque, ref0["torque"], what=f"replica {r} torque")
+        ref = o.run(wl.dt, 20, st.pos, st.orient, st.vel, st.ang_vel)
+        compare_states(outs[r], ref, wl.comp.box_length)
+        check_energy(outs[r].energy, ref["energy"])
+        assert np.array_equal(eng.pair_list(r), o.pair_list(ref["pos"]))
+
+
+# --------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 33, 100, 513, 1537, 4100, 8200])
+def test_sizes_and_partial_tiles(n):
+    box = (n / 0.7) ** (1.0 / 3.0) if n > 8 else 8.0
+    rc = min(2.5, 0.5 * box)
+    wl = configs.lj_fluid_config(n, n / box ** 3, rc, seed=n) if n > 8 else None
+    if wl is None:
+        comp = systems.lj_fluid(n, box)
+        st = systems.random_state(comp, n, 0.9)
+        opts = systems.lj_opts(rc)
+    else:
+        comp, opts, st = wl.comp, wl.opts, wl.states[0]
+    o = pyoracle.OracleFF(comp, opts)
+    ref = o.evaluate(st.pos, st.orient)
+    ff, out = gpu_eval(comp, opts, st.pos, st.orient)
+    assert np.array_equal(ff.pair_list(), o.pair_list(st.pos))
+    check_vec(out.force, ref["force"])
+    check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+
+
+def test_min_image_ties_and_far_images():
+    """Separations exactly L/2 (round-half-even ties), positions several
+    boxes away (nearbyint = +-2, +-3) and negative coordinates."""
+    comp = systems.lj_fluid(6, 4.0)
+    pos = np.array([[0.0, 0.0, 0.0], [2.0, 0.0, 0.0], [0.0, 2.0, 2.0], [-6.0, 9.0, 1.0],
+                    [13.5, -7.25, 2.0], [2.0, 2.0, 2.0]])
+    orient = np.tile([1.0, 0, 0, 0], (6, 1))
+    opts = systems.lj_opts(2.0)
+    o = pyoracle.OracleFF(comp, opts)
+    ref = o.evaluate(pos, orient)
+    ff, out = gpu_eval(comp, opts, pos, orient)
+    assert np.array_equal(ff.pair_list(), o.pair_list(pos))
+    check_vec(out.force, ref["force"])
+    check_energy(out.energy, ref["energy"])
+
+
+def test_ideal_gas_dummy_sites():  # test_potentials.cpp:160-176
+    comp = b2.SystemComposition([b2.build_species("ghost", [b2.Site(b2.SiteKind.dummy, (0, 0, 0), 0, 0, 0, 1.0)])],
+                                [16], 6.0, 1.0)
+    st = systems.random_state(comp, 3, 0.0)
+    ff, out = gpu_eval(comp, systems.lj_opts(2.5), st.pos, st.orient)
+    assert out.energy.total() == 0.0 and out.energy.du_dv() == 0.0 and out.energy.d2u_dv2() == 0.0
+    assert np.all(out.force == 0.0)
+
+
+def test_repeated_evaluations_bit_identical():  # test_parallel.cpp:84-96
+    wl = configs.make("cfg1")
+    st = wl.states[0]
+    ff = b2.ForceField(wl.comp, wl.opts)
+    a, b = st.copy(), st.copy()
+    ff.evaluate(a)
+    ff.evaluate(b)
+    assert np.array_equal(a.force, b.force) and np.array_equal(a.torque, b.torque)
+    assert a.energy == b.energy and a.virial == b.virial
+
+
+def test_third_law_and_virial_identity():
+    comp, opts = systems.dimer_mono_mixture()
+    st = systems.random_state(comp, 31, 0.85)
+    _, out = gpu_eval(comp, opts, st.pos, st.orient)
+    assert np.all(np.abs(out.force.sum(axis=0)) < 1e-10 * max(1.0, np.abs(out.force).max()))
+    comp = systems.lj_fluid(25, 6.0, 1.2)
+    st = systems.random_state(comp, 21, 0.9)
+    _, out = gpu_eval(comp, systems.lj_opts(2.8), st.pos, st.orient)
+    assert out.virial == pytest.approx(-3.0 * comp.volume() * out.energy.du_dv_explicit, rel=1e-12)
+
+
+def test_madelung_on_gpu():
+    comp, opts, st = systems.rock_salt()
+    _, out = gpu_eval(comp, opts, st.pos, st.orient)
+    assert out.energy.total() / 32.0 == pytest.approx(-1.747565, rel=1e-3 / 1.747565)
+
+
+def test_free_flight_exact():  # test_engine.cpp:27-43
+    comp = systems.lj_fluid(1, 10.0)
+    eng = b2.Engine(comp, systems.lj_opts(3.0), 0.01)
+    st = b2.SystemState(1, 10.0)
+    st.pos[0] = (5.0, 5.0, 5.0)
+    st.vel[0] = (1.0, 0.0, 0.0)
+    eng.set_state(st)
+    eng.step()
+    assert eng.state().pos[0, 0] == 5.0 + 0.01 * 1.0 and eng.state().pos[0, 1] == 5.0
+    eng.step()
+    assert eng.state().pos[0, 0] == 5.0 + 0.01 + 0.01
+
+
+def test_two_body_orbit_energy_drift():  # test_engine.cpp:45-65
+    comp = systems.lj_fluid(2, 20.0)
+    eng = b2.Engine(comp, systems.lj_opts(8.0), 0.001)
+    st = b2.SystemState(2, 20.0)
+    st.pos[0], st.pos[1] = (10.0, 10.0, 10.0), (11.2, 10.0, 10.0)
+    st.vel[0], st.vel[1] = (0.0, 0.4, 0.0), (0.0, -0.4, 0.0)
+    eng.set_state(st)
+    s0 = eng.state()
+    e0 = b2.kinetic_energy_trans(comp, s0) + s0.energy.total()
+    drift = 0.0
+    for _ in range(100):
+        eng.step(100)
+        s = eng.state()
+        drift = max(drift, abs(b2.kinetic_energy_trans(comp, s) + s.energy.total() - e0))
+    assert drift / abs(e0) < 1e-5
+
+
+def test_torque_free_dumbbell():  # test_engine.cpp:67-102
+    comp = systems.dumbbell()
+    eng = b2.Engine(comp, systems.lj_opts(3.0), 0.001)
+    st = b2.SystemState(1, 10.0)
+    st.pos[0] = (5, 5, 5)
+    st.ang_vel[0] = (0.0, 1.3, 0.7)
+    eng.set_state(st)
+    inertia = comp.species[0].inertia_principal
+
+    def lab_l(s):
+        return systems.rotate(s.orient[0], inertia * s.ang_vel[0])
+
+    s0 = eng.state()
+    l0 = lab_l(s0)
+    e0 = b2.kinetic_energy_rot(comp, s0)
+    eng.step(10000)
+    s1 = eng.state()
+    assert np.abs(lab_l(s1) - l0).max() < 1e-8
+    assert b2.kinetic_energy_rot(comp, s1) == pytest.approx(e0, rel=1e-10)
+    assert abs(np.linalg.norm(s1.orient[0]) - 1.0) < 1e-9
+
+
+def test_three_site_rotor_energy():  # test_engine.cpp:104-129
+    comp, opts, st, dt, _ = golden_cases.traj_cases()["tri"]
+    eng = b2.Engine(comp, opts, dt)
+    eng.set_state(st)
+
+    def etot(s):
+        return b2.kinetic_energy_trans(comp, s) + b2.kinetic_energy_rot(comp, s) + s.energy.total()
+
+    e0 = etot(eng.state())
+    eng.step(4000)
+    assert etot(eng.state()) == pytest.approx(e0, rel=1e-5)
+
+
+def test_nan_is_fatal():  # test_engine.cpp:232-245
+    comp = systems.lj_fluid(4, 6.0)
+    eng = b2.Engine(comp, systems.lj_opts(2.5), 0.01)
+    st = systems.random_state(comp, 2, 0.9)
+    st.vel[2] = (np.nan, 0, 0)
+    eng.set_state(st)
+    with pytest.raises(b2.NumericalError, match="non-finite state for molecule 2"):
+        eng.step()
+
+
+def test_set_state_wraps():  # engine.cpp:91-98
+    comp = systems.lj_fluid(20, 6.0)
+    st = systems.random_state(comp, 11, 0.9)
+    moved = st.copy()
+    moved.pos = moved.pos + np.array([1.3, -2.1, 0.7]) * 6.0
+    eng = b2.Engine(comp, systems.lj_opts(2.5), 0.005)
+    eng.set_state(moved)
+    out = eng.state()
+    assert np.all(out.pos >= 0) and np.all(out.pos < 6.0)
+    ref = pyoracle.OracleFF(comp, systems.lj_opts(2.5)).run(0.005, 0, moved.pos, moved.orient,
+                                                             moved.vel, moved.ang_vel)
+    assert np.array_equal(out.pos, ref["pos"])
+    check_vec(out.force, ref["force"])
+
+
+def test_engine_runs_bit_identical():  # test_engine.cpp:185-213 (fixed-seed determinism)
+    wl = configs.make("cfg1")
+    outs = []
+    for _ in range(2):
+        eng = b2.Engine(wl.comp, wl.opts, wl.dt)
+        eng.set_state(wl.states[0])
+        eng.step(20)
+        outs.append(eng.state())
+    assert np.array_equal(outs[0].pos, outs[1].pos) and np.array_equal(outs[0].vel, outs[1].vel)
