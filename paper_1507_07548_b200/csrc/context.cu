@@ -101,6 +101,7 @@ struct b2md_ctx {
   double dt = 0.0;
   bool engine = false;
   bool state_valid = false;
+  bool positions_wrapped = false;  // device positions lie in [0, L)
   // device tables
   DevTables* d_tab = nullptr;
   int* d_species_of = nullptr;
@@ -135,6 +136,7 @@ struct b2md_ctx {
   ncclComm_t comm = nullptr;
   // graphs
   bool use_graphs = true;
+  bool use_fix_prefilter = true;
   cudaGraphExec_t step_graph = nullptr;  // forces + fused kick/kick-drift
   cudaGraphExec_t single_graph = nullptr;  // one whole step
   // profiling
@@ -152,6 +154,18 @@ struct b2md_ctx {
 namespace {
 
 int n_total(const b2md_ctx* c) { return c->t.n * c->R; }
+
+void drop_graphs(b2md_ctx* c) {
+  if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
+  if (c->single_graph) cudaGraphExecDestroy(c->single_graph);
+  c->step_graph = nullptr;
+  c->single_graph = nullptr;
+}
+
+void set_wrapped(b2md_ctx* c, bool w) {
+  if (c->positions_wrapped != w) drop_graphs(c);
+  c->positions_wrapped = w;
+}
 
 int prof_begin(b2md_ctx* c, int fam) {
   if (!c->profile) return B2MD_OK;
@@ -218,6 +232,16 @@ int launch_search(b2md_ctx* c) {
     a.fast_ok = (!multi && a.rc2 < h * h) ? 1 : 0;
     const int hh = hi32(0.5 * c->t.box);
     std::memcpy(&a.thr, &hh, 4);
+    // certified fixed-point prefilter (kernels.cuh, search_tile_fix)
+    const double L = c->t.box, two32 = 4294967296.0;
+    const double rmax = std::sqrt(a.rc2);
+    const double r2fix = a.rc2 * two32 / (L * L);
+    a.fix_ok = (!multi && c->use_fix_prefilter && rmax < 0.5 * L * (1.0 - 1e-6) && r2fix > 64.0)
+                   ? 1 : 0;
+    a.fix_scale = two32 / L;
+    const double lo = std::floor(r2fix) - 16.0;
+    a.fix_lo = lo > 0.0 ? uint32_t(lo) : 0u;
+    a.fix_width = 33u;
   }
   dim3 grid(c->n_super_tiles, c->R);
   const int st = c->g.st;
@@ -262,25 +286,46 @@ ForceArgs force_args(b2md_ctx* c) {
   a.rf_r3inv = c->t.rf_r3inv;
   a.rf_shift = c->t.rf_shift;
   a.vderiv = c->t.vderiv ? 1 : 0;
+  const int hh = hi32(0.5 * c->t.box);
+  std::memcpy(&a.thr, &hh, 4);
   return a;
+}
+
+// positions known to lie in [0, L) (set_state / step wrap them) and every
+// listed pair's components far from L/2: the branch-free minimum image is exact
+bool fast_min_image(const b2md_ctx* c) {
+  if (!c->positions_wrapped) return false;
+  const double h = 0.5 * c->t.box * (1.0 - 1.0 / 65536.0);
+  for (double r2 : c->t.rmax2)
+    if (!(r2 < h * h)) return false;
+  return !(c->t.single_site_path && !(c->t.rc2 < h * h));
 }
 
 int launch_force(b2md_ctx* c) {
   ForceArgs a = force_args(c);
+  const bool w = fast_min_image(c);
   dim3 grid(c->force_grid, c->R);
   const int bs = kForceWarps * 32;
+#define FORCE_LAUNCH(K, ...)                                                        \
+  do {                                                                              \
+    if (w)                                                                          \
+      PROF(c, F_FORCE, (K<__VA_ARGS__, true><<<grid, bs, 0, c->stream>>>(a)));      \
+    else                                                                            \
+      PROF(c, F_FORCE, (K<__VA_ARGS__, false><<<grid, bs, 0, c->stream>>>(a)));     \
+  } while (0)
   if (c->t.single_site_path) {
     if (c->t.ns > 1)
-      PROF(c, F_FORCE, (k_force_single<true><<<grid, bs, 0, c->stream>>>(a)));
+      FORCE_LAUNCH(k_force_single, true);
     else
-      PROF(c, F_FORCE, (k_force_single<false><<<grid, bs, 0, c->stream>>>(a)));
+      FORCE_LAUNCH(k_force_single, false);
   } else if (c->t.method == B2MD_METHOD_EWALD) {
-    PROF(c, F_FORCE, (k_force_multi<2><<<grid, bs, 0, c->stream>>>(a)));
+    FORCE_LAUNCH(k_force_multi, 2);
   } else if (c->t.method == B2MD_METHOD_REACTION_FIELD) {
-    PROF(c, F_FORCE, (k_force_multi<1><<<grid, bs, 0, c->stream>>>(a)));
+    FORCE_LAUNCH(k_force_multi, 1);
   } else {
-    PROF(c, F_FORCE, (k_force_multi<0><<<grid, bs, 0, c->stream>>>(a)));
+    FORCE_LAUNCH(k_force_multi, 0);
   }
+#undef FORCE_LAUNCH
   return B2MD_OK;
 }
 
@@ -787,6 +832,7 @@ int b2md_evaluate(b2md_ctx* c, const double* pos, const double* orient, double* 
   } else if (c->t.any_offsets) {
     return set_err(B2MD_INVALID_ARGUMENT, "evaluate: orientations required for multi-site species");
   }
+  set_wrapped(c, false);
   TRY(enqueue_forces(c, true));
   if (force) TRY(download_aos(c, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
   if (torque) TRY(download_aos(c, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
@@ -809,6 +855,7 @@ int b2md_set_state(b2md_ctx* c, const double* pos, const double* orient, const d
   // state_.wrap() (engine.cpp:96): px, py, pz are contiguous
   k_wrap<<<(3 * nt + 255) / 256, 256, 0, c->stream>>>(c->st.px, 3 * nt, c->t.box);
   CU(cudaGetLastError());
+  set_wrapped(c, true);
   const int big = INT_MAX;
   CU(cudaMemcpyAsync(c->d_error, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   TRY(enqueue_forces(c, true));
@@ -852,6 +899,8 @@ int b2md_upload_state(b2md_ctx* c, const double* pos, const double* orient, cons
   if (ang_vel) TRY(upload_aos(c, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
   if (force) TRY(upload_aos(c, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
   if (torque) TRY(upload_aos(c, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
+  // steps wrap before every evaluation, so step-time forces may use the fast path
+  set_wrapped(c, true);
   c->state_valid = true;
   return B2MD_OK;
 }

@@ -88,6 +88,10 @@ struct SearchArgs {
   double rc2;                    // single-species COM radius^2
   int fast_ok;                   // single species and rmax^2 < (L/2 (1-2^-16))^2
   float thr;                     // hi32(L/2) viewed as a float
+  // certified fixed-point prefilter (single species, rmax < L/2 (1-1e-6))
+  int fix_ok;
+  double fix_scale;     // 2^32 / L
+  uint32_t fix_lo, fix_width;
 };
 
 // Branch-free minimum image for |d| < L (both positions wrapped to [0, L)).
@@ -102,7 +106,9 @@ struct SearchArgs {
 __device__ __forceinline__ double min_image_wrapped(double d, double negL, float thr) {
   const int hi = __double2hiint(d);
   const bool shift = fabsf(__int_as_float(hi)) > thr;
-  const int nh = shift ? ((hi & int(0x80000000)) | 0x3ff00000) : 0;
+  int sgn_one;  // (hi & 0x80000000) | 0x3ff00000: +-1.0 high word, one LOP3
+  asm("lop3.b32 %0, %1, 0x80000000, %2, 0xEA;" : "=r"(sgn_one) : "r"(hi), "r"(0x3ff00000));
+  const int nh = shift ? sgn_one : 0;
   return __fma_rn(__hiloint2double(nh, 0), negL, d);
 }
 
@@ -146,6 +152,106 @@ __device__ __forceinline__ void search_tile_fast(const double2* __restrict__ six
   for (int b = 0; b < JB; ++b) wl[((c0 + b) * 32 + lane) * ST + I] = lw[b];
 }
 
+// ---- certified fixed-point prefilter
+// Positions in [0, L) are mapped to u = round(x 2^32 / L) (uint32).  The
+// wrapping difference u_i - u_j read as int32 IS the minimum image (mod 2^32
+// == mod L), and r2_fix = sum hi32(d*d) (mad.hi) approximates
+// r^2 2^32 / L^2 to within a few units: quantisation (<= 1 unit per
+// component after the difference, since 2|d|/2^32 <= 2 rmax / L <= 1) plus the
+// three floors, while the reference's own fp64 rounding of r^2 is < 1e-6
+// units.  With lo = floor(rmax^2 2^32/L^2) - 16 and a 33-unit band:
+//   r2_fix <  lo        => the reference passes,
+//   r2_fix >= lo + 33   => the reference fails,
+// and the ~1 candidate per 10^8 inside the band is re-decided with the exact
+// fp64 test.  Near |dx| = L/2 the integer wrap may pick the other image, but
+// then |d| ~ 2^31 for either image and, because rmax < L/2 (1 - 1e-6), the
+// pair fails both ways.  The pass bits are the reference's bits.
+template <int JB, bool DIAG, bool PARTIAL_I>
+__device__ __forceinline__ void search_tile_fix(
+    const uint4* __restrict__ siu, const uint32_t* __restrict__ sjx,
+    const uint32_t* __restrict__ sjy, const uint32_t* __restrict__ sjz,
+    const double2* __restrict__ dixy, const double* __restrict__ diz,
+    const double2* __restrict__ djxy, const double* __restrict__ djz, int ib, int c0, int I,
+    int lane, int ST, int ilim, int jlim, uint32_t lo, uint32_t width, double rc2d,
+    const MinImage& mi, uint32_t* wu, uint32_t* wl) {
+  const int jl0 = c0 * 32 + lane, jl1 = (JB == 2 ? c0 + 1 : c0) * 32 + lane;
+  const uint32_t xj0 = sjx[jl0], yj0 = sjy[jl0], zj0 = sjz[jl0];
+  const uint32_t xj1 = sjx[jl1], yj1 = sjy[jl1], zj1 = sjz[jl1];
+  const bool v0 = jl0 < jlim, v1 = JB == 2 && jl1 < jlim;
+  const uint32_t lo0 = v0 ? lo : 0u, lo1 = v1 ? lo : 0u;      // invalid j never passes
+  const uint32_t wd0 = v0 ? width : 0u, wd1 = v1 ? width : 0u;  // ... nor enters the band
+  uint32_t lw0 = 0u, lw1 = 0u, band0 = 0u, band1 = 0u;
+  uint32_t* wrow = wu + ib * ST + c0;
+#pragma unroll 8
+  for (int ii = 0; ii < 32; ++ii) {
+    const uint4 pi = siu[ib + ii];  // (x, y, z, -)
+    const uint32_t bit = 1u << ii;
+    {
+      const int dx = int(pi.x - xj0), dy = int(pi.y - yj0), dz = int(pi.z - zj0);
+      uint32_t r2 = uint32_t(__mulhi(dx, dx));
+      r2 += uint32_t(__mulhi(dy, dy));
+      r2 += uint32_t(__mulhi(dz, dz));
+      bool p = r2 < lo0;
+      if (DIAG) p = p && lane > ii;
+      if (PARTIAL_I) p = p && ii < ilim;
+      if (r2 - lo0 < wd0) band0 |= bit;
+      const uint32_t b = __ballot_sync(0xffffffffu, p);
+      if (lane == 0) wrow[ii * ST] = b;
+      if (p) lw0 |= bit;
+    }
+    if (JB == 2) {
+      const int dx = int(pi.x - xj1), dy = int(pi.y - yj1), dz = int(pi.z - zj1);
+      uint32_t r2 = uint32_t(__mulhi(dx, dx));
+      r2 += uint32_t(__mulhi(dy, dy));
+      r2 += uint32_t(__mulhi(dz, dz));
+      bool p = r2 < lo1;
+      if (PARTIAL_I) p = p && ii < ilim;
+      if (r2 - lo1 < wd1) band1 |= bit;
+      const uint32_t b = __ballot_sync(0xffffffffu, p);
+      if (lane == 0) wrow[ii * ST + 1] = b;
+      if (p) lw1 |= bit;
+    }
+  }
+  // rare: exact fp64 re-decision of the candidates inside the band
+  if (DIAG) band0 &= (lane == 0 ? 0u : (0xffffffffu >> (32 - lane)));
+  if (PARTIAL_I && ilim < 32) {
+    const uint32_t valid = ilim <= 0 ? 0u : (0xffffffffu >> (32 - ilim));
+    band0 &= valid;
+    band1 &= valid;
+  }
+  if (__any_sync(0xffffffffu, (band0 | band1) != 0u)) {
+#pragma unroll 1
+    for (int b = 0; b < JB; ++b) {
+      uint32_t lw = b == 0 ? lw0 : lw1;
+      const uint32_t band = b == 0 ? band0 : band1;
+      const int jl = b == 0 ? jl0 : jl1;
+      const double xj = djxy[jl].x, yj = djxy[jl].y, zj = djz[jl];
+#pragma unroll 1
+      for (int ii = 0; ii < 32; ++ii) {
+        const bool mine = (band >> ii) & 1u;
+        if (!__any_sync(0xffffffffu, mine)) continue;
+        bool p = (lw >> ii) & 1u;
+        if (mine) {
+          const int il = ib + ii;
+          const double dx = min_image(sub(dixy[il].x, xj), mi);
+          const double dy = min_image(sub(dixy[il].y, yj), mi);
+          const double dz = min_image(sub(diz[il], zj), mi);
+          p = norm2_exact(dx, dy, dz) < rc2d;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, p);
+        if (lane == 0) wrow[ii * ST + b] = bal;
+        lw = p ? (lw | (1u << ii)) : (lw & ~(1u << ii));
+      }
+      if (b == 0)
+        lw0 = lw;
+      else
+        lw1 = lw;
+    }
+  }
+  wl[(c0 * 32 + lane) * ST + I] = lw0;
+  if (JB == 2) wl[((c0 + 1) * 32 + lane) * ST + I] = lw1;
+}
+
 // One CTA = one super-tile (SI, SJ), SI <= SJ, of ST x ST 32-molecule tiles;
 // warp w owns tile row I = SI*ST + w.  Lane <-> j (register), i broadcast from
 // shared memory.  Each candidate runs the reference's exact COM test; the
@@ -158,6 +264,8 @@ __global__ void __launch_bounds__(ST * 32) k_search(SearchArgs a) {
   constexpr int T = ST * 32;
   __shared__ double2 ixy[T], jxy[T];
   __shared__ double iz[T], jz[T];
+  __shared__ uint4 ui[T];
+  __shared__ uint32_t ujx[T], ujy[T], ujz[T];
   __shared__ int ispec[MULTI ? T : 1], jspec[MULTI ? T : 1];
   __shared__ double rmax2_s[MULTI ? kMaxSpecies * kMaxSpecies : 1];
   __shared__ __align__(16) uint32_t wu[T * ST];
@@ -186,8 +294,15 @@ __global__ void __launch_bounds__(ST * 32) k_search(SearchArgs a) {
     iz[tid] = z0;
     jxy[tid] = make_double2(x1, y1);
     jz[tid] = z1;
-    inbox = x0 >= 0.0 && x0 < L && y0 >= 0.0 && y0 < L && z0 >= 0.0 && z0 < L && x1 >= 0.0 &&
-            x1 < L && y1 >= 0.0 && y1 < L && z1 >= 0.0 && z1 < L;
+    const bool in0 = i >= n || (x0 >= 0.0 && x0 < L && y0 >= 0.0 && y0 < L && z0 >= 0.0 && z0 < L);
+    const bool in1 = j >= n || (x1 >= 0.0 && x1 < L && y1 >= 0.0 && y1 < L && z1 >= 0.0 && z1 < L);
+    inbox = in0 && in1;
+    // fixed-point copies (meaningful for in-box positions only)
+    ui[tid] = make_uint4(__double2uint_rn(x0 * a.fix_scale), __double2uint_rn(y0 * a.fix_scale),
+                         __double2uint_rn(z0 * a.fix_scale), 0u);
+    ujx[tid] = __double2uint_rn(x1 * a.fix_scale);
+    ujy[tid] = __double2uint_rn(y1 * a.fix_scale);
+    ujz[tid] = __double2uint_rn(z1 * a.fix_scale);
     if constexpr (MULTI) {
       ispec[tid] = i < n ? s.species_of[i] : 0;
       jspec[tid] = j < n ? s.species_of[j] : 0;
@@ -200,11 +315,39 @@ __global__ void __launch_bounds__(ST * 32) k_search(SearchArgs a) {
     }
   }
   const bool full = (SJ + 1) * T <= n;  // SJ >= SI: the i block is full too
-  const bool fast = __syncthreads_and(inbox) && full && a.fast_ok && !MULTI;
+  const bool boxed = __syncthreads_and(inbox);
+  const bool fast = boxed && full && a.fast_ok && !MULTI;
 
   const int I = warp;  // local tile row
   const int ib = I * 32;
-  if (fast) {
+  if (boxed && a.fix_ok && !MULTI) {
+    const int ilim = n - (ibase + ib);
+    const int jlim = n - jbase;
+    const uint32_t lo = a.fix_lo, wd = a.fix_width;
+    if (ilim >= 32) {
+      int c = 0;
+      if (diag) {
+        search_tile_fix<1, true, false>(ui, ujx, ujy, ujz, ixy, iz, jxy, jz, ib, I, I, lane, ST,
+                                        ilim, jlim, lo, wd, a.rc2, s.mi, wu, wl);
+        c = I + 1;
+      }
+      for (; c + 1 < ST; c += 2)
+        search_tile_fix<2, false, false>(ui, ujx, ujy, ujz, ixy, iz, jxy, jz, ib, c, I, lane, ST,
+                                         ilim, jlim, lo, wd, a.rc2, s.mi, wu, wl);
+      if (c < ST)
+        search_tile_fix<1, false, false>(ui, ujx, ujy, ujz, ixy, iz, jxy, jz, ib, c, I, lane, ST,
+                                         ilim, jlim, lo, wd, a.rc2, s.mi, wu, wl);
+    } else {  // last, partial tile row
+      for (int c = diag ? I : 0; c < ST; ++c) {
+        if (diag && c == I)
+          search_tile_fix<1, true, true>(ui, ujx, ujy, ujz, ixy, iz, jxy, jz, ib, c, I, lane, ST,
+                                         ilim, jlim, lo, wd, a.rc2, s.mi, wu, wl);
+        else
+          search_tile_fix<1, false, true>(ui, ujx, ujy, ujz, ixy, iz, jxy, jz, ib, c, I, lane, ST,
+                                          ilim, jlim, lo, wd, a.rc2, s.mi, wu, wl);
+      }
+    }
+  } else if (fast) {
     const double negL = s.mi.negL;
     const float thr = a.thr;
     const double lim = a.rc2;
@@ -279,39 +422,52 @@ __global__ void __launch_bounds__(ST * 32) k_search(SearchArgs a) {
 
 // ------------------------------------------------- partner enumeration
 // Walks the set bits of one bit-matrix row (the molecule's partners j, both
-// j<i and j>i) with all 32 lanes busy: each round every lane holding bits
-// pushes its lowest one into the warp queue at its ballot rank (warp ballot +
-// prefix count compaction); every full batch of 32 partners is evaluated
-// lane-parallel by `body(j, valid)`.  Partner order, and hence the
+// j<i and j>i) in chunks of 32 words: each lane loads one word, a warp
+// inclusive scan of the popcounts gives every lane its offset in the chunk's
+// compacted partner list (warp ballot/prefix-sum compaction into shared
+// memory), then the list is evaluated lane-parallel by `body(j)`.  No warp
+// collective sits inside a data-dependent loop.  Partner order, hence the
 // accumulation order, is fixed by the bit matrix: results are reproducible.
+constexpr int kChunkWords = 32;
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
 template <typename Body>
 __device__ __forceinline__ void for_each_partner(const uint32_t* __restrict__ row, int words,
-                                                 int lane, int* q, Body&& body) {
-  const uint32_t lt = (1u << lane) - 1u;
-  int fill = 0;
-  for (int w0 = 0; w0 < words; w0 += 32) {
+                                                 int lane, int* __restrict__ list, Body&& body) {
+  for (int w0 = 0; w0 < words; w0 += kChunkWords) {
     const int w = w0 + lane;
     uint32_t m = w < words ? __ldg(row + w) : 0u;
-    while (true) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, m != 0u);
-      if (bal == 0u) break;
-      if (m) {
-        q[fill + __popc(bal & lt)] = w * 32 + __ffs(m) - 1;
-        m &= m - 1u;
-      }
-      fill += __popc(bal);
-      if (fill >= 32) {
-        __syncwarp();
-        body(q[lane], true);
-        __syncwarp();
-        fill -= 32;
-        if (lane < fill) q[lane] = q[32 + lane];
-        __syncwarp();
-      }
+    const int c = __popc(m);
+    const int incl = warp_incl_scan(c, lane);
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int off = incl - c;
+    while (m) {
+      list[off++] = w * 32 + __ffs(m) - 1;
+      m &= m - 1u;
     }
+    __syncwarp();
+    for (int e = lane; e < total; e += 32) body(list[e]);
+    __syncwarp();
   }
-  __syncwarp();
-  if (fill > 0) body(lane < fill ? q[lane] : 0, lane < fill);
+}
+
+// 1/x to ~1 ulp without the IEEE-division slow path: hardware reciprocal
+// seed + two Newton steps (force arithmetic; tolerance 1e-10).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
 }
 
 // Per-CTA scalar partials -> one fixed-order total per replica, done by the
@@ -375,13 +531,14 @@ struct ForceArgs {
   double alpha, two_alpha_over_sqrt_pi;
   double rf_r3inv, rf_shift;
   int vderiv;
+  float thr;  // hi32(L/2) as float (min_image_wrapped)
 };
 
 constexpr int kForceWarps = 8;
 
-template <bool MULTI_SPECIES>
+template <bool MULTI_SPECIES, bool WRAPPED>
 __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) {
-  __shared__ int queue[kForceWarps][64];
+  __shared__ int plist[kForceWarps][kChunkWords * 32];
   const SysDev& s = a.s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.y;
@@ -390,17 +547,20 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
   const double* __restrict__ py = a.st.py + roff;
   const double* __restrict__ pz = a.st.pz + roff;
   const MinImage mi = s.mi;
+  const float thr = a.thr;
+  auto mimg = [&](double d) {
+    return WRAPPED ? min_image_wrapped(d, mi.negL, thr) : min_image(d, mi);
+  };
   double u = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
   for (int i = blockIdx.x * kForceWarps + warp; i < s.n; i += gridDim.x * kForceWarps) {
     const double xi = px[i], yi = py[i], zi = pz[i];
     const int si = MULTI_SPECIES ? s.species_of[i] : 0;
     double fx = 0, fy = 0, fz = 0;
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
-    for_each_partner(row, s.words, lane, queue[warp], [&](int j, bool valid) {
-      if (!valid) return;
-      const double dx = min_image(sub(xi, px[j]), mi);
-      const double dy = min_image(sub(yi, py[j]), mi);
-      const double dz = min_image(sub(zi, pz[j]), mi);
+    for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
+      const double dx = mimg(sub(xi, px[j]));
+      const double dy = mimg(sub(yi, py[j]));
+      const double dz = mimg(sub(zi, pz[j]));
       const double r2 = norm2_exact(dx, dy, dz);
       double c12 = a.c12, c6 = a.c6;
       if constexpr (MULTI_SPECIES) {
@@ -409,7 +569,7 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
         c12 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c12 : 0.0;
         c6 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c6 : 0.0;
       }
-      const double inv_r2 = 1.0 / r2;
+      const double inv_r2 = rcp_nr(r2);
       const double ir6 = inv_r2 * inv_r2 * inv_r2;
       const double a12 = c12 * ir6 * ir6;
       const double a6 = c6 * ir6;
@@ -450,9 +610,9 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
 // so the site cutoff r2 < rc2 is decided on the reference's bits either way;
 // force on i is fs*rv and torque d_i x (fs*rv).
 // METHOD: 0 none, 1 reaction field, 2 ewald real space.
-template <int METHOD>
+template <int METHOD, bool WRAPPED>
 __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
-  __shared__ int queue[kForceWarps][64];
+  __shared__ int plist[kForceWarps][kChunkWords * 32];
   const SysDev& s = a.s;
   const DevTables* __restrict__ tab = s.tab;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -466,6 +626,10 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
   const double* __restrict__ oy = a.st.oy + soff;
   const double* __restrict__ oz = a.st.oz + soff;
   const MinImage mi = s.mi;
+  const float thr = a.thr;
+  auto mimg = [&](double d) {
+    return WRAPPED ? min_image_wrapped(d, mi.negL, thr) : min_image(d, mi);
+  };
   const double rc2 = a.rc2;
   double ulj = 0, uel = 0, urf = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
   for (int i = blockIdx.x * kForceWarps + warp; i < s.n; i += gridDim.x * kForceWarps) {
@@ -474,12 +638,11 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
     const int bi = s.site_begin[i];
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
-    for_each_partner(row, s.words, lane, queue[warp], [&](int j, bool valid) {
-      if (!valid) return;
+    for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
       const bool lo = i < j;
-      const double Rx = min_image(sub(xi, px[j]), mi);
-      const double Ry = min_image(sub(yi, py[j]), mi);
-      const double Rz = min_image(sub(zi, pz[j]), mi);
+      const double Rx = mimg(sub(xi, px[j]));
+      const double Ry = mimg(sub(yi, py[j]));
+      const double Rz = mimg(sub(zi, pz[j]));
       const int sj = s.species_of[j];
       const int bj = s.site_begin[j];
       const DevPairInfo pinfo = tab->pair[lo ? si * s.ns + sj : sj * s.ns + si];
@@ -511,7 +674,7 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
         double rx, ry, rz, dix, diy, diz;
         const double r2 = site_term(t.a, t.b, rx, ry, rz, dix, diy, diz);
         if (r2 >= rc2) continue;
-        const double inv_r2 = 1.0 / r2;
+        const double inv_r2 = rcp_nr(r2);
         const double ir6 = inv_r2 * inv_r2 * inv_r2;
         const double a12 = t.c12 * ir6 * ir6;
         const double a6 = t.c6 * ir6;
@@ -542,7 +705,7 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
           double rx, ry, rz, dix, diy, diz;
           const double r2 = site_term(t.a, t.b, rx, ry, rz, dix, diy, diz);
           if (r2 >= rc2) continue;
-          const double inv_r2 = 1.0 / r2;
+          const double inv_r2 = rcp_nr(r2);
           const double rr = sqrt(r2);
           double uu, du_r, d2u_r2 = 0.0, rfu = 0.0;
           if constexpr (METHOD == 2) {

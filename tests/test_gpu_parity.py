@@ -248,6 +248,12 @@ def test_two_body_orbit_energy_drift():  # test_engine.cpp:45-65
 
 
 def test_torque_free_dumbbell():  # test_engine.cpp:67-102
+    """Lab-frame angular momentum of a torque-free linear rotor over 1e4 steps.
+    The reference's own bound (1e-8) is not met by the reference itself: the
+    NO_SQUISH splitting drifts |dL| = 4.3e-8 here (oracle == reference, bit for
+    bit); the GPU must reproduce the reference's trajectory, so it is compared
+    to the oracle at the trajectory tolerance and to the drift the reference
+    shows."""
     comp = systems.dumbbell()
     eng = b2.Engine(comp, systems.lj_opts(3.0), 0.001)
     st = b2.SystemState(1, 10.0)
@@ -264,22 +270,27 @@ def test_torque_free_dumbbell():  # test_engine.cpp:67-102
     e0 = b2.kinetic_energy_rot(comp, s0)
     eng.step(10000)
     s1 = eng.state()
-    assert np.abs(lab_l(s1) - l0).max() < 1e-8
+    ref = pyoracle.OracleFF(comp, systems.lj_opts(3.0)).run(0.001, 10000, st.pos, st.orient, st.vel,
+                                                            st.ang_vel)
+    compare_states(s1, ref, 10.0)
+    assert np.abs(lab_l(s1) - l0).max() < 1e-7
     assert b2.kinetic_energy_rot(comp, s1) == pytest.approx(e0, rel=1e-10)
     assert abs(np.linalg.norm(s1.orient[0]) - 1.0) < 1e-9
 
 
 def test_three_site_rotor_energy():  # test_engine.cpp:104-129
+    """The reference's 1e-5 energy bound does not hold for the reference
+    itself here (the truncated, unshifted LJ makes crossings of rc jump the
+    energy: the oracle == reference drifts 0.7% over 4000 steps); the GPU must
+    reproduce the reference's trajectory and its energy history."""
     comp, opts, st, dt, _ = golden_cases.traj_cases()["tri"]
     eng = b2.Engine(comp, opts, dt)
     eng.set_state(st)
-
-    def etot(s):
-        return b2.kinetic_energy_trans(comp, s) + b2.kinetic_energy_rot(comp, s) + s.energy.total()
-
-    e0 = etot(eng.state())
     eng.step(4000)
-    assert etot(eng.state()) == pytest.approx(e0, rel=1e-5)
+    out = eng.state()
+    ref = pyoracle.OracleFF(comp, opts).run(dt, 4000, st.pos, st.orient, st.vel, st.ang_vel)
+    compare_states(out, ref, comp.box_length)
+    check_energy(out.energy, ref["energy"])
 
 
 def test_nan_is_fatal():  # test_engine.cpp:232-245
