@@ -112,6 +112,7 @@ struct b2md_ctx {
   double* d_off = nullptr;    // 3 * R * total_sites
   double* d_stage = nullptr;  // AoS staging, 4*R*n
   uint32_t* d_mask = nullptr;
+  uint4* d_fixpos = nullptr;  // fixed-point positions (search prefilter)
   double* d_cta_part = nullptr;  // force-kernel per-CTA scalar partials
   unsigned* d_ticket = nullptr;   // 2 * R: force, ewald
   int force_grid = 1;
@@ -225,23 +226,27 @@ int launch_search(b2md_ctx* c) {
   a.pz = c->st.pz;
   a.mask = c->d_mask;
   a.super_tiles = c->d_super;
+  a.fixpos = c->d_fixpos;
   a.rc2 = c->t.single_site_path ? c->t.rc2 : c->t.rmax2[0];
   const bool multi = c->t.ns > 1;
   {
-    const double h = 0.5 * c->t.box * (1.0 - 1.0 / 65536.0);
-    a.fast_ok = (!multi && a.rc2 < h * h) ? 1 : 0;
-    const int hh = hi32(0.5 * c->t.box);
-    std::memcpy(&a.thr, &hh, 4);
     // certified fixed-point prefilter (kernels.cuh, search_tile_fix)
     const double L = c->t.box, two32 = 4294967296.0;
     const double rmax = std::sqrt(a.rc2);
-    const double r2fix = a.rc2 * two32 / (L * L);
-    a.fix_ok = (!multi && c->use_fix_prefilter && rmax < 0.5 * L * (1.0 - 1e-6) && r2fix > 64.0)
-                   ? 1 : 0;
+    const double r2fix = a.rc2 * 1073741824.0 / (L * L);  // rmax^2 in (L/32768)^2 units
+    const double dmax = std::ceil(rmax * 32768.0 / L) + 2.0;
+    const double K = 3.0 * (2.0 * dmax + 1.0) + 64.0;   // |r2_fix - r2 (65536/L)^2| bound
+    const double lo = std::floor(r2fix) - K;
+    a.fix_ok = (!multi && c->use_fix_prefilter && rmax < 0.5 * L * (1.0 - 1e-3) && lo > 0.0 &&
+                r2fix + K < 1.0e9) ? 1 : 0;
     a.fix_scale = two32 / L;
-    const double lo = std::floor(r2fix) - 16.0;
     a.fix_lo = lo > 0.0 ? uint32_t(lo) : 0u;
-    a.fix_width = 33u;
+    a.fix_width = uint32_t(2.0 * K + 2.0);
+    const double r2_32 = a.rc2 * two32 / (L * L);
+    const double lo32 = std::floor(r2_32) - 8.0;
+    a.fix_lo32 = lo32 > 0.0 ? uint32_t(lo32) : 0u;
+    a.fix_w32 = 17u;
+    if (!(r2_32 + 64.0 < two32) || lo32 <= 0.0) a.fix_ok = 0;
   }
   dim3 grid(c->n_super_tiles, c->R);
   const int st = c->g.st;
@@ -379,7 +384,14 @@ int launch_allreduce(b2md_ctx* c) {
 
 // ForceField::evaluate (src/parallel.cpp:79-122) on the device state.
 int enqueue_forces(b2md_ctx* c, bool offsets) {
-  if (offsets) TRY(launch_offsets(c));
+  if (offsets) {  // evaluate / set_state path: the integrator did not refresh these
+    TRY(launch_offsets(c));
+    const int nt = n_total(c);
+    k_fix_positions<<<(nt + 255) / 256, 256, 0, c->stream>>>(c->st.px, c->st.py, c->st.pz, nt,
+                                                            c->t.box, 4294967296.0 / c->t.box,
+                                                            c->d_fixpos);
+    CU(cudaGetLastError());
+  }
   TRY(launch_search(c));
   TRY(launch_force(c));
   TRY(launch_ewald(c));
@@ -394,6 +406,8 @@ StepArgs step_args(b2md_ctx* c) {
   a.dt = c->dt;
   a.error_mol = c->d_error;
   a.write_offsets = c->t.any_offsets ? 1 : 0;
+  a.fixpos = c->d_fixpos;
+  a.fix_scale = 4294967296.0 / c->t.box;
   return a;
 }
 
@@ -632,6 +646,7 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   TRY(dalloc(&c->d_off, 3 * size_t(t.total_sites) * R));
   TRY(dalloc(&c->d_stage, 4 * nt));
   TRY(dalloc(&c->d_mask, size_t(R) * c->g.n_pad * c->g.words));
+  TRY(dalloc(&c->d_fixpos, nt));
   {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -734,7 +749,7 @@ void free_ctx(b2md_ctx* c) {
   }
   if (c->comm) ncclCommDestroy(c->comm);
   void* ptrs[] = {c->d_tab,   c->d_species_of, c->d_site_begin, c->d_state, c->d_fbuf, c->d_off,
-                  c->d_stage, c->d_mask,       c->d_cta_part, c->d_ticket,   c->d_super, c->d_error, c->d_q_mol,
+                  c->d_stage, c->d_mask,       c->d_cta_part, c->d_ticket, c->d_fixpos,   c->d_super, c->d_error, c->d_q_mol,
                   c->d_q_site, c->d_q_val,     c->d_mol_qbegin, c->d_kv,    c->d_etab,  c->d_S,
                   c->d_uk};
   for (void* p : ptrs)

@@ -73,36 +73,28 @@ __global__ void k_offsets(SysDev s, StateDev st) {
 }
 
 // ----------------------------------------------------------- partner search
-// One CTA = one super-tile (SI, SJ), SI <= SJ, of ST x ST 32-molecule tiles;
-// warp w owns tile row I = SI*ST + w.  Lane <-> j (register), i broadcast from
-// shared memory.  Each candidate runs the reference's exact COM test; the
-// warp ballot of a fixed i over 32 j is the U word (row i, column tile J), and
-// each lane's bits over the 32 i of tile I form the transposed L word (row j,
-// column tile I).  Words are staged in shared memory and stored as whole
-// 32-byte sectors of the row-major bit matrix M[r][row][word].
 struct SearchArgs {
   SysDev s;
   const double *px, *py, *pz;
-  uint32_t* mask;                // R * n_pad * words
-  const uint32_t* super_tiles;   // (SI << 16) | SJ, this rank's list
-  double rc2;                    // single-species COM radius^2
-  int fast_ok;                   // single species and rmax^2 < (L/2 (1-2^-16))^2
-  float thr;                     // hi32(L/2) viewed as a float
+  uint32_t* mask;               // R * n_pad * words
+  const uint32_t* super_tiles;  // (SI << 16) | SJ, this rank's list
+  const uint4* fixpos;          // R * n: (round(x 2^32/L), .., .., in-box flag)
+  double rc2;                   // single-species COM radius^2
   // certified fixed-point prefilter (single species, rmax < L/2 (1-1e-6))
   int fix_ok;
-  double fix_scale;     // 2^32 / L
-  uint32_t fix_lo, fix_width;
+  double fix_scale;  // 2^32 / L
+  uint32_t fix_lo, fix_width;  // 15-bit test (units (L/32768)^2)
+  uint32_t fix_lo32, fix_w32;  // 32-bit refinement (units L^2/2^32)
 };
 
-// Branch-free minimum image for |d| < L (both positions wrapped to [0, L)).
+// Branch-free minimum image for |d| < L (both positions wrapped to [0, L)),
+// used by the force kernels on pairs the search already accepted.
 // shift <=> hi32(|d|) > hi32(L/2), compared on the integer pattern viewed as a
 // float (monotone for these magnitudes).  Outside the hi-word bucket of L/2
 // the decision equals nearbyint(d/L) != 0 exactly, and d - L*n is formed by
 // one correctly rounded DFMA with n = +-1 (exact product) — the reference's
-// bits.  Inside the bucket (|d| within 2^-20 of L/2) the image may differ from
-// the reference's, but then |d'| ~ L/2 for either image and, because the
-// caller guarantees rmax^2 < (L/2 (1-2^-16))^2, the pair fails the COM test
-// under both: the pass bit is still the reference's.
+// bits.  Accepted pairs have every component below rmax < L/2 (1-2^-16), so
+// they never reach the bucket.
 __device__ __forceinline__ double min_image_wrapped(double d, double negL, float thr) {
   const int hi = __double2hiint(d);
   const bool shift = fabsf(__int_as_float(hi)) > thr;
@@ -112,160 +104,141 @@ __device__ __forceinline__ double min_image_wrapped(double d, double negL, float
   return __fma_rn(__hiloint2double(nh, 0), negL, d);
 }
 
-// 32 i-rows (tile row `ib`) x JB column tiles c0.. on the fast path.
-template <int JB, bool DIAG>
-__device__ __forceinline__ void search_tile_fast(const double2* __restrict__ sixy,
-                                                 const double* __restrict__ siz,
-                                                 const double2* __restrict__ sjxy,
-                                                 const double* __restrict__ sjz, int ib, int c0,
-                                                 int I, int lane, int ST, double lim, double negL,
-                                                 float thr, uint32_t* wu, uint32_t* wl) {
-  double xj[JB], yj[JB], zj[JB];
-  uint32_t lw[JB];
-#pragma unroll
-  for (int b = 0; b < JB; ++b) {
-    const int jl = (c0 + b) * 32 + lane;
-    xj[b] = sjxy[jl].x;
-    yj[b] = sjxy[jl].y;
-    zj[b] = sjz[jl];
-    lw[b] = 0u;
-  }
-  uint32_t* wrow = wu + ib * ST + c0;
-#pragma unroll 8
-  for (int ii = 0; ii < 32; ++ii) {
-    const double2 ixy = sixy[ib + ii];
-    const double iz = siz[ib + ii];
-#pragma unroll
-    for (int b = 0; b < JB; ++b) {
-      const double dx = min_image_wrapped(sub(ixy.x, xj[b]), negL, thr);
-      const double dy = min_image_wrapped(sub(ixy.y, yj[b]), negL, thr);
-      const double dz = min_image_wrapped(sub(iz, zj[b]), negL, thr);
-      const double r2 = norm2_exact(dx, dy, dz);
-      bool pass = r2 < lim;
-      if (DIAG) pass = pass && lane > ii;
-      const uint32_t bal = __ballot_sync(0xffffffffu, pass);
-      if (lane == 0) wrow[ii * ST + b] = bal;
-      if (pass) lw[b] |= 1u << ii;
-    }
-  }
-#pragma unroll
-  for (int b = 0; b < JB; ++b) wl[((c0 + b) * 32 + lane) * ST + I] = lw[b];
-}
-
 // ---- certified fixed-point prefilter
 // Positions in [0, L) are mapped to u = round(x 2^32 / L) (uint32).  The
 // wrapping difference u_i - u_j read as int32 IS the minimum image (mod 2^32
-// == mod L), and r2_fix = sum hi32(d*d) (mad.hi) approximates
-// r^2 2^32 / L^2 to within a few units: quantisation (<= 1 unit per
-// component after the difference, since 2|d|/2^32 <= 2 rmax / L <= 1) plus the
-// three floors, while the reference's own fp64 rounding of r^2 is < 1e-6
-// units.  With lo = floor(rmax^2 2^32/L^2) - 16 and a 33-unit band:
-//   r2_fix <  lo        => the reference passes,
-//   r2_fix >= lo + 33   => the reference fails,
-// and the ~1 candidate per 10^8 inside the band is re-decided with the exact
-// fp64 test.  Near |dx| = L/2 the integer wrap may pick the other image, but
-// then |d| ~ 2^31 for either image and, because rmax < L/2 (1 - 1e-6), the
-// pair fails both ways.  The pass bits are the reference's bits.
+// == mod L); its top 15 bits d = (u_i - u_j) >> 17 (arithmetic) are squared
+// with full-rate 32-bit IMADs: r2_fix = dx^2 + dy^2 + dz^2 approximates
+// r^2 (32768/L)^2 with |error| <= sum (2|d| + 1) (floor of each component),
+// bounded on the host by K from rmax; the reference's own fp64 rounding of r^2
+// is < 1e-3 units.  With t = r2_fix - (floor(rmax^2 (65536/L)^2) - K):
+//   t <  0           => the reference passes,
+//   t >= W = 2K + 2  => the reference fails,
+// and the candidates with 0 <= t < W (~2e-4 of all) are re-decided with the
+// exact fp64 test.  Near |dx| = L/2 the integer wrap may pick the other image,
+// but then |d| ~ 2^14 for either image and, because rmax < L/2 (1 - 1e-3),
+// the pair fails both ways.  The pass bits are the reference's bits.
+//
+// Each lane accumulates its own pass bits over the 32 i rows (the L word of
+// its j); the U words (row i over 32 j) are one warp bit-transpose per tile.
+
+// 32x32 bit transpose across a warp: lane k holds row k on entry and column k
+// on exit (block-recursive swap of off-diagonal halves, 5 shuffle stages).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+  uint32_t m = 0x0000ffffu;
+#pragma unroll
+  for (int j = 16; j != 0; j >>= 1, m ^= (m << j)) {
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
+
+// t = r2_fix - lo (signed; 15-bit components: r2_fix <= 3 * 2^28 < 2^31, no overflow)
+__device__ __forceinline__ int fix_t(uint4 pi, uint32_t xj, uint32_t yj, uint32_t zj, int neglo) {
+  const int dx = int(pi.x - xj) >> 17, dy = int(pi.y - yj) >> 17, dz = int(pi.z - zj) >> 17;
+  return dx * dx + dy * dy + dz * dz + neglo;
+}
+
+// 32 i-rows (local tile row at `ib`) x JB column tiles c0.. : U words (row
+// ib+ii, columns c0..) to wu, L words to wl.
+// Exact decision of one band candidate: the 32-bit fixed-point distance
+// (sum hi32(d^2), |error| <= 6 units of L^2/2^32) settles all but ~1e-7 of
+// them; the rest take the reference's fp64 test.
+struct FixRefine {
+  uint32_t lo32, w32;  // pass if r2_32 < lo32, fail if r2_32 >= lo32 + w32
+  double rc2;
+};
+
+__device__ __noinline__ bool refine_pair(uint4 pi, uint4 pj, int ig, int jg,
+                                         const double* __restrict__ gx,
+                                         const double* __restrict__ gy,
+                                         const double* __restrict__ gz, const FixRefine& f,
+                                         const MinImage& mi) {
+  const int dx = int(pi.x - pj.x), dy = int(pi.y - pj.y), dz = int(pi.z - pj.z);
+  const uint32_t r2 =
+      uint32_t(__mulhi(dx, dx)) + uint32_t(__mulhi(dy, dy)) + uint32_t(__mulhi(dz, dz));
+  if (r2 < f.lo32) return true;
+  if (r2 - f.lo32 >= f.w32) return false;
+  const double ex = min_image(sub(gx[ig], gx[jg]), mi);
+  const double ey = min_image(sub(gy[ig], gy[jg]), mi);
+  const double ez = min_image(sub(gz[ig], gz[jg]), mi);
+  return norm2_exact(ex, ey, ez) < f.rc2;
+}
+
+// 32 i-rows (local tile row at `ib`) x JB column tiles c0.. : U words (row
+// ib+ii, columns c0..) to wu, L words to wl.
 template <int JB, bool DIAG, bool PARTIAL_I>
 __device__ __forceinline__ void search_tile_fix(
-    const uint4* __restrict__ siu, const uint32_t* __restrict__ sjx,
-    const uint32_t* __restrict__ sjy, const uint32_t* __restrict__ sjz,
-    const double2* __restrict__ dixy, const double* __restrict__ diz,
-    const double2* __restrict__ djxy, const double* __restrict__ djz, int ib, int c0, int I,
-    int lane, int ST, int ilim, int jlim, uint32_t lo, uint32_t width, double rc2d,
-    const MinImage& mi, uint32_t* wu, uint32_t* wl) {
-  const int jl0 = c0 * 32 + lane, jl1 = (JB == 2 ? c0 + 1 : c0) * 32 + lane;
-  const uint32_t xj0 = sjx[jl0], yj0 = sjy[jl0], zj0 = sjz[jl0];
-  const uint32_t xj1 = sjx[jl1], yj1 = sjy[jl1], zj1 = sjz[jl1];
-  const bool v0 = jl0 < jlim, v1 = JB == 2 && jl1 < jlim;
-  const uint32_t lo0 = v0 ? lo : 0u, lo1 = v1 ? lo : 0u;      // invalid j never passes
-  const uint32_t wd0 = v0 ? width : 0u, wd1 = v1 ? width : 0u;  // ... nor enters the band
-  uint32_t lw0 = 0u, lw1 = 0u, band0 = 0u, band1 = 0u;
-  uint32_t* wrow = wu + ib * ST + c0;
+    const uint4* __restrict__ siu, const uint4* __restrict__ sju,
+    const double* __restrict__ gx, const double* __restrict__ gy, const double* __restrict__ gz,
+    int ig0, int jg0, int ib, int c0, int I, int lane, int ST, int ilim, int jlim, int neglo,
+    int width, const FixRefine& f, const MinImage& mi, uint32_t* wu, uint32_t* wl) {
+  uint32_t xj[JB], yj[JB], zj[JB], lw[JB], bw[JB];
+  int nl[JB];
+#pragma unroll
+  for (int b = 0; b < JB; ++b) {
+    const int jl = (c0 + b) * 32 + lane;
+    const uint4 pj = sju[jl];
+    xj[b] = pj.x;
+    yj[b] = pj.y;
+    zj[b] = pj.z;
+    nl[b] = jl < jlim ? neglo : (1 << 30);  // invalid j: t > W always
+    lw[b] = 0u;
+    bw[b] = 0u;
+  }
+  // rows are visited from ii = 31 down to 0 and bits are shifted in at the
+  // bottom, so bit ii ends up at position ii: lw = [t < 0] (pass), bw =
+  // [t < W] (pass or band).  Diagonal / partial-tile masks are applied after.
 #pragma unroll 8
-  for (int ii = 0; ii < 32; ++ii) {
-    const uint4 pi = siu[ib + ii];  // (x, y, z, -)
-    const uint32_t bit = 1u << ii;
-    {
-      const int dx = int(pi.x - xj0), dy = int(pi.y - yj0), dz = int(pi.z - zj0);
-      uint32_t r2 = uint32_t(__mulhi(dx, dx));
-      r2 += uint32_t(__mulhi(dy, dy));
-      r2 += uint32_t(__mulhi(dz, dz));
-      bool p = r2 < lo0;
-      if (DIAG) p = p && lane > ii;
-      if (PARTIAL_I) p = p && ii < ilim;
-      if (r2 - lo0 < wd0) band0 |= bit;
-      const uint32_t b = __ballot_sync(0xffffffffu, p);
-      if (lane == 0) wrow[ii * ST] = b;
-      if (p) lw0 |= bit;
-    }
-    if (JB == 2) {
-      const int dx = int(pi.x - xj1), dy = int(pi.y - yj1), dz = int(pi.z - zj1);
-      uint32_t r2 = uint32_t(__mulhi(dx, dx));
-      r2 += uint32_t(__mulhi(dy, dy));
-      r2 += uint32_t(__mulhi(dz, dz));
-      bool p = r2 < lo1;
-      if (PARTIAL_I) p = p && ii < ilim;
-      if (r2 - lo1 < wd1) band1 |= bit;
-      const uint32_t b = __ballot_sync(0xffffffffu, p);
-      if (lane == 0) wrow[ii * ST + 1] = b;
-      if (p) lw1 |= bit;
-    }
-  }
-  // rare: exact fp64 re-decision of the candidates inside the band
-  if (DIAG) band0 &= (lane == 0 ? 0u : (0xffffffffu >> (32 - lane)));
-  if (PARTIAL_I && ilim < 32) {
-    const uint32_t valid = ilim <= 0 ? 0u : (0xffffffffu >> (32 - ilim));
-    band0 &= valid;
-    band1 &= valid;
-  }
-  if (__any_sync(0xffffffffu, (band0 | band1) != 0u)) {
-#pragma unroll 1
+  for (int k = 0; k < 32; ++k) {
+    const uint4 pi = siu[ib + 31 - k];  // (x, y, z, -)
+#pragma unroll
     for (int b = 0; b < JB; ++b) {
-      uint32_t lw = b == 0 ? lw0 : lw1;
-      const uint32_t band = b == 0 ? band0 : band1;
-      const int jl = b == 0 ? jl0 : jl1;
-      const double xj = djxy[jl].x, yj = djxy[jl].y, zj = djz[jl];
-#pragma unroll 1
-      for (int ii = 0; ii < 32; ++ii) {
-        const bool mine = (band >> ii) & 1u;
-        if (!__any_sync(0xffffffffu, mine)) continue;
-        bool p = (lw >> ii) & 1u;
-        if (mine) {
-          const int il = ib + ii;
-          const double dx = min_image(sub(dixy[il].x, xj), mi);
-          const double dy = min_image(sub(dixy[il].y, yj), mi);
-          const double dz = min_image(sub(diz[il], zj), mi);
-          p = norm2_exact(dx, dy, dz) < rc2d;
-        }
-        const uint32_t bal = __ballot_sync(0xffffffffu, p);
-        if (lane == 0) wrow[ii * ST + b] = bal;
-        lw = p ? (lw | (1u << ii)) : (lw & ~(1u << ii));
-      }
-      if (b == 0)
-        lw0 = lw;
-      else
-        lw1 = lw;
+      const int t = fix_t(pi, xj[b], yj[b], zj[b], nl[b]);
+      lw[b] = lw[b] + lw[b] + (uint32_t(t) >> 31);
+      bw[b] = bw[b] + bw[b] + (uint32_t(t - width) >> 31);
     }
   }
-  wl[(c0 * 32 + lane) * ST + I] = lw0;
-  if (JB == 2) wl[((c0 + 1) * 32 + lane) * ST + I] = lw1;
+  uint32_t valid = 0xffffffffu;
+  if (PARTIAL_I) valid = ilim <= 0 ? 0u : (ilim >= 32 ? 0xffffffffu : ((1u << ilim) - 1u));
+#pragma unroll
+  for (int b = 0; b < JB; ++b) {
+    uint32_t m = valid;
+    if (DIAG && b == 0) m &= (1u << lane) - 1u;  // j = lane > i = ii only
+    lw[b] &= m;
+    // rare: band members are decided exactly, lane by lane (no collectives)
+    uint32_t band = bw[b] & ~lw[b] & m;
+    if (band) {
+      const int jl = (c0 + b) * 32 + lane;
+      const uint4 pj = sju[jl];
+      while (band) {
+        const int ii = __ffs(band) - 1;
+        band &= band - 1u;
+        if (refine_pair(siu[ib + ii], pj, ig0 + ib + ii, jg0 + jl, gx, gy, gz, f, mi))
+          lw[b] |= 1u << ii;
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < JB; ++b) {
+    wl[((c0 + b) * 32 + lane) * ST + I] = lw[b];
+    wu[(ib + lane) * ST + c0 + b] = warp_transpose32(lw[b], lane);
+  }
 }
 
 // One CTA = one super-tile (SI, SJ), SI <= SJ, of ST x ST 32-molecule tiles;
 // warp w owns tile row I = SI*ST + w.  Lane <-> j (register), i broadcast from
-// shared memory.  Each candidate runs the reference's exact COM test; the
-// warp ballot of a fixed i over 32 j is the U word (row i, column tile J), and
-// each lane's bits over the 32 i of tile I form the transposed L word (row j,
-// column tile I).  Words are staged in shared memory and stored as whole
-// 32-byte sectors of the row-major bit matrix M[r][row][word].
+// shared memory.  The warp ballot of a fixed i over 32 j is the U word (row
+// i, column tile J); the warp transpose of a tile's 32 U words gives the L
+// words (row j, column tile I).  Words are staged in shared memory and stored
+// as whole 32-byte sectors of the row-major bit matrix M[r][row][word].
+// Certified fixed-point path for single-species, in-box tiles; the exact
+// generic fp64 path (any position, mixtures, rmax >= L/2) otherwise.
 template <int ST, bool MULTI>
-__global__ void __launch_bounds__(ST * 32) k_search(SearchArgs a) {
+__global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArgs a) {
   constexpr int T = ST * 32;
-  __shared__ double2 ixy[T], jxy[T];
-  __shared__ double iz[T], jz[T];
-  __shared__ uint4 ui[T];
-  __shared__ uint32_t ujx[T], ujy[T], ujz[T];
+  __shared__ uint4 ui[T], uj[T];
   __shared__ int ispec[MULTI ? T : 1], jspec[MULTI ? T : 1];
   __shared__ double rmax2_s[MULTI ? kMaxSpecies * kMaxSpecies : 1];
   __shared__ __align__(16) uint32_t wu[T * ST];
@@ -281,101 +254,90 @@ __global__ void __launch_bounds__(ST * 32) k_search(SearchArgs a) {
   const int n = s.n;
   const int ibase = SI * T, jbase = SJ * T;
   const size_t roff = size_t(r) * n;
-  const double L = s.mi.L;
+  const double* __restrict__ gx = a.px + roff;
+  const double* __restrict__ gy = a.py + roff;
+  const double* __restrict__ gz = a.pz + roff;
 
   bool inbox;
   {
     const int i = ibase + tid, j = jbase + tid;
-    const double x0 = i < n ? a.px[roff + i] : 0.0, y0 = i < n ? a.py[roff + i] : 0.0,
-                 z0 = i < n ? a.pz[roff + i] : 0.0;
-    const double x1 = j < n ? a.px[roff + j] : 0.0, y1 = j < n ? a.py[roff + j] : 0.0,
-                 z1 = j < n ? a.pz[roff + j] : 0.0;
-    ixy[tid] = make_double2(x0, y0);
-    iz[tid] = z0;
-    jxy[tid] = make_double2(x1, y1);
-    jz[tid] = z1;
-    const bool in0 = i >= n || (x0 >= 0.0 && x0 < L && y0 >= 0.0 && y0 < L && z0 >= 0.0 && z0 < L);
-    const bool in1 = j >= n || (x1 >= 0.0 && x1 < L && y1 >= 0.0 && y1 < L && z1 >= 0.0 && z1 < L);
-    inbox = in0 && in1;
-    // fixed-point copies (meaningful for in-box positions only)
-    ui[tid] = make_uint4(__double2uint_rn(x0 * a.fix_scale), __double2uint_rn(y0 * a.fix_scale),
-                         __double2uint_rn(z0 * a.fix_scale), 0u);
-    ujx[tid] = __double2uint_rn(x1 * a.fix_scale);
-    ujy[tid] = __double2uint_rn(y1 * a.fix_scale);
-    ujz[tid] = __double2uint_rn(z1 * a.fix_scale);
+    // fixed-point positions + in-box flag, written by the integrator
+    // (k_kick_drift) or k_fix_positions
+    const uint4 fi = i < n ? a.fixpos[roff + i] : make_uint4(0u, 0u, 0u, 1u);
+    const uint4 fj = j < n ? a.fixpos[roff + j] : make_uint4(0u, 0u, 0u, 1u);
+    ui[tid] = fi;
+    uj[tid] = fj;
+    inbox = fi.w != 0u && fj.w != 0u;
     if constexpr (MULTI) {
       ispec[tid] = i < n ? s.species_of[i] : 0;
       jspec[tid] = j < n ? s.species_of[j] : 0;
       for (int k = tid; k < s.ns * s.ns; k += T) rmax2_s[k] = s.tab->pair[k].rmax2;
     }
+    if (diag || !a.fix_ok || MULTI) {  // only partially written there: merge needs zeros
 #pragma unroll
-    for (int c = 0; c < ST; ++c) {
-      wu[tid * ST + c] = 0u;
-      wl[tid * ST + c] = 0u;
+      for (int c = 0; c < ST; ++c) {
+        wu[tid * ST + c] = 0u;
+        wl[tid * ST + c] = 0u;
+      }
     }
   }
-  const bool full = (SJ + 1) * T <= n;  // SJ >= SI: the i block is full too
   const bool boxed = __syncthreads_and(inbox);
-  const bool fast = boxed && full && a.fast_ok && !MULTI;
 
   const int I = warp;  // local tile row
   const int ib = I * 32;
+  const int ilim = n - (ibase + ib);
   if (boxed && a.fix_ok && !MULTI) {
-    const int ilim = n - (ibase + ib);
     const int jlim = n - jbase;
-    const uint32_t lo = a.fix_lo, wd = a.fix_width;
-    if (ilim >= 32) {
-      int c = 0;
-      if (diag) {
-        search_tile_fix<1, true, false>(ui, ujx, ujy, ujz, ixy, iz, jxy, jz, ib, I, I, lane, ST,
-                                        ilim, jlim, lo, wd, a.rc2, s.mi, wu, wl);
-        c = I + 1;
+    const int neglo = -int(a.fix_lo);
+    const int wd = int(a.fix_width);
+    FixRefine refine;
+    refine.lo32 = a.fix_lo32;
+    refine.w32 = a.fix_w32;
+    refine.rc2 = a.rc2;
+    if (!diag && ilim >= 32) {
+      // hot path: uniform, compile-time trip count (no divergence emulation
+      // around the ballots)
+#pragma unroll 1
+      for (int c = 0; c < ST; c += (ST >= 2 ? 2 : 1)) {
+        if constexpr (ST >= 2)
+          search_tile_fix<2, false, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, I,
+                                           lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
+        else
+          search_tile_fix<1, false, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, I,
+                                           lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
       }
-      for (; c + 1 < ST; c += 2)
-        search_tile_fix<2, false, false>(ui, ujx, ujy, ujz, ixy, iz, jxy, jz, ib, c, I, lane, ST,
-                                         ilim, jlim, lo, wd, a.rc2, s.mi, wu, wl);
-      if (c < ST)
-        search_tile_fix<1, false, false>(ui, ujx, ujy, ujz, ixy, iz, jxy, jz, ib, c, I, lane, ST,
-                                         ilim, jlim, lo, wd, a.rc2, s.mi, wu, wl);
+    } else if (ilim >= 32) {
+      search_tile_fix<1, true, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, I, I, lane,
+                                      ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
+      for (int c = I + 1; c < ST; ++c)
+        search_tile_fix<1, false, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, I,
+                                         lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
     } else {  // last, partial tile row
       for (int c = diag ? I : 0; c < ST; ++c) {
         if (diag && c == I)
-          search_tile_fix<1, true, true>(ui, ujx, ujy, ujz, ixy, iz, jxy, jz, ib, c, I, lane, ST,
-                                         ilim, jlim, lo, wd, a.rc2, s.mi, wu, wl);
+          search_tile_fix<1, true, true>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, I,
+                                         lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
         else
-          search_tile_fix<1, false, true>(ui, ujx, ujy, ujz, ixy, iz, jxy, jz, ib, c, I, lane, ST,
-                                          ilim, jlim, lo, wd, a.rc2, s.mi, wu, wl);
+          search_tile_fix<1, false, true>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, I,
+                                          lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
       }
     }
-  } else if (fast) {
-    const double negL = s.mi.negL;
-    const float thr = a.thr;
-    const double lim = a.rc2;
-    int c = 0;
-    if (diag) {
-      search_tile_fast<1, true>(ixy, iz, jxy, jz, ib, I, I, lane, ST, lim, negL, thr, wu, wl);
-      c = I + 1;
-    }
-    for (; c + 1 < ST; c += 2)
-      search_tile_fast<2, false>(ixy, iz, jxy, jz, ib, c, I, lane, ST, lim, negL, thr, wu, wl);
-    if (c < ST)
-      search_tile_fast<1, false>(ixy, iz, jxy, jz, ib, c, I, lane, ST, lim, negL, thr, wu, wl);
   } else {
     // generic path: exact minimum image for any input, partial tiles, mixtures
     const MinImage mi = s.mi;
-    const int ilim = n - (ibase + ib);
     for (int c = diag ? I : 0; c < ST; ++c) {
       const int jl = c * 32 + lane;
-      const double xj = jxy[jl].x, yj = jxy[jl].y, zj = jz[jl];
-      const int sj = MULTI ? jspec[jl] : 0;
       const bool jvalid = jbase + jl < n;
-      uint32_t lword = 0u;
+      const int jg = jvalid ? jbase + jl : 0;
+      const double xj = gx[jg], yj = gy[jg], zj = gz[jg];
+      const int sj = MULTI ? jspec[jl] : 0;
       const bool diag_tile = diag && c == I;
       for (int ii = 0; ii < 32; ++ii) {
         const int il = ib + ii;
-        const double dx = min_image(sub(ixy[il].x, xj), mi);
-        const double dy = min_image(sub(ixy[il].y, yj), mi);
-        const double dz = min_image(sub(iz[il], zj), mi);
+        const int ig = ii < ilim ? ibase + il : 0;
+        const double dx = min_image(sub(gx[ig], xj), mi);
+        const double dy = min_image(sub(gy[ig], yj), mi);
+        const double dz = min_image(sub(gz[ig], zj), mi);
         const double r2 = norm2_exact(dx, dy, dz);
         double lim;
         if constexpr (MULTI)
@@ -386,9 +348,9 @@ __global__ void __launch_bounds__(ST * 32) k_search(SearchArgs a) {
         if (diag_tile) pass = pass && lane > ii;
         const uint32_t b = __ballot_sync(0xffffffffu, pass);
         if (lane == 0) wu[(ib + ii) * ST + c] = b;
-        lword |= uint32_t(pass) << ii;
       }
-      wl[(c * 32 + lane) * ST + I] = lword;
+      __syncwarp();
+      wl[(c * 32 + lane) * ST + I] = warp_transpose32(wu[(ib + lane) * ST + c], lane);
     }
   }
   __syncthreads();
@@ -981,10 +943,26 @@ struct StepArgs {
   double dt;
   int* error_mol;  // first non-finite molecule (global index), INT_MAX if none
   int write_offsets;
+  uint4* fixpos;     // fixed-point positions for the search (may be null)
+  double fix_scale;  // 2^32 / L
 };
 
 __device__ __forceinline__ double wrap1(double x, double L) {
   return sub(x, mul(L, floor(__ddiv_rn(x, L))));  // model.cpp:282
+}
+
+// Fixed-point copy of the positions for the partner search's certified
+// prefilter: (round(x 2^32/L), .., .., [x, y, z all in [0, L)]).
+__device__ __forceinline__ uint4 fix_position(double x, double y, double z, double L, double scale) {
+  const bool in = x >= 0.0 && x < L && y >= 0.0 && y < L && z >= 0.0 && z < L;
+  return make_uint4(__double2uint_rn(x * scale), __double2uint_rn(y * scale),
+                    __double2uint_rn(z * scale), in ? 1u : 0u);
+}
+
+__global__ void k_fix_positions(const double* px, const double* py, const double* pz, int count,
+                                double L, double scale, uint4* fixpos) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid < count) fixpos[gid] = fix_position(px[gid], py[gid], pz[gid], L, scale);
 }
 
 // engine.cpp:107-127 (+ build_scene offsets for the new orientation)
@@ -1022,9 +1000,13 @@ __device__ __forceinline__ void kick_drift_one(const StepArgs& a, int gid) {
     a.st.qy[gid] = q[2];
     a.st.qz[gid] = q[3];
   }
-  a.st.px[gid] = wrap1(px, s.mi.L);
-  a.st.py[gid] = wrap1(py, s.mi.L);
-  a.st.pz[gid] = wrap1(pz, s.mi.L);
+  px = wrap1(px, s.mi.L);
+  py = wrap1(py, s.mi.L);
+  pz = wrap1(pz, s.mi.L);
+  a.st.px[gid] = px;
+  a.st.py[gid] = py;
+  a.st.pz[gid] = pz;
+  if (a.fixpos) a.fixpos[gid] = fix_position(px, py, pz, s.mi.L, a.fix_scale);
   if (a.write_offsets) {
     const int base = r * s.total_sites + s.site_begin[i];
     if (sp.centred) {
