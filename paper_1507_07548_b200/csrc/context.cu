@@ -109,7 +109,8 @@ struct b2md_ctx {
   // state
   double* d_state = nullptr;  // px..wz (13 arrays of R*n)
   double* d_fbuf = nullptr;   // fx fy fz tx ty tz (6*R*n) + sums (R*kNumSums): allreduce unit
-  double* d_off = nullptr;    // 3 * R * total_sites
+  double4* d_off = nullptr;   // R * total_sites site offsets
+  double4* d_pos4 = nullptr;  // R * n packed positions
   double* d_stage = nullptr;  // AoS staging, 4*R*n
   uint32_t* d_mask = nullptr;
   uint4* d_fixpos = nullptr;  // fixed-point positions (search prefilter)
@@ -387,9 +388,9 @@ int enqueue_forces(b2md_ctx* c, bool offsets) {
   if (offsets) {  // evaluate / set_state path: the integrator did not refresh these
     TRY(launch_offsets(c));
     const int nt = n_total(c);
-    k_fix_positions<<<(nt + 255) / 256, 256, 0, c->stream>>>(c->st.px, c->st.py, c->st.pz, nt,
-                                                            c->t.box, 4294967296.0 / c->t.box,
-                                                            c->d_fixpos);
+    k_stage_positions<<<(nt + 255) / 256, 256, 0, c->stream>>>(
+        c->st.px, c->st.py, c->st.pz, nt, c->t.box, 4294967296.0 / c->t.box, c->d_fixpos,
+        c->st.pos4);
     CU(cudaGetLastError());
   }
   TRY(launch_search(c));
@@ -643,7 +644,8 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   const size_t nt = size_t(t.n) * R;
   TRY(dalloc(&c->d_state, 13 * nt));
   TRY(dalloc(&c->d_fbuf, 6 * nt + size_t(kNumSums) * R));
-  TRY(dalloc(&c->d_off, 3 * size_t(t.total_sites) * R));
+  TRY(dalloc(&c->d_off, size_t(t.total_sites) * R));
+  TRY(dalloc(&c->d_pos4, nt));
   TRY(dalloc(&c->d_stage, 4 * nt));
   TRY(dalloc(&c->d_mask, size_t(R) * c->g.n_pad * c->g.words));
   TRY(dalloc(&c->d_fixpos, nt));
@@ -678,10 +680,8 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   c->st.tx = c->d_fbuf + 3 * nt;
   c->st.ty = c->d_fbuf + 4 * nt;
   c->st.tz = c->d_fbuf + 5 * nt;
-  const size_t ns3 = size_t(t.total_sites) * R;
-  c->st.ox = c->d_off;
-  c->st.oy = c->d_off + ns3;
-  c->st.oz = c->d_off + 2 * ns3;
+  c->st.off = c->d_off;
+  c->st.pos4 = c->d_pos4;
 
   c->sys.n = t.n;
   c->sys.R = R;
@@ -749,7 +749,7 @@ void free_ctx(b2md_ctx* c) {
   }
   if (c->comm) ncclCommDestroy(c->comm);
   void* ptrs[] = {c->d_tab,   c->d_species_of, c->d_site_begin, c->d_state, c->d_fbuf, c->d_off,
-                  c->d_stage, c->d_mask,       c->d_cta_part, c->d_ticket, c->d_fixpos,   c->d_super, c->d_error, c->d_q_mol,
+                  c->d_stage, c->d_mask,       c->d_cta_part, c->d_ticket, c->d_fixpos, c->d_pos4,   c->d_super, c->d_error, c->d_q_mol,
                   c->d_q_site, c->d_q_val,     c->d_mol_qbegin, c->d_kv,    c->d_etab,  c->d_S,
                   c->d_uk};
   for (void* p : ptrs)

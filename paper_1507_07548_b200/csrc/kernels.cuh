@@ -32,7 +32,8 @@ struct StateDev {
   double *wx, *wy, *wz;
   double *fx, *fy, *fz;
   double *tx, *ty, *tz;
-  double *ox, *oy, *oz;  // site offsets, R * total_sites
+  double4* off;   // site offsets (x, y, z, -), R * total_sites
+  double4* pos4;  // positions (x, y, z, -), R * n: one 32-byte gather per partner
 };
 
 struct SysDev {
@@ -58,17 +59,13 @@ __global__ void k_offsets(SysDev s, StateDev st) {
   const DevSpecies& sp = s.tab->species[s.species_of[i]];
   const int base = r * s.total_sites + s.site_begin[i];
   if (sp.centred) {
-    st.ox[base] = 0.0;
-    st.oy[base] = 0.0;
-    st.oz[base] = 0.0;
+    st.off[base] = make_double4(0.0, 0.0, 0.0, 0.0);
     return;
   }
   const double qw = st.qw[gid], qx = st.qx[gid], qy = st.qy[gid], qz = st.qz[gid];
   for (int k = 0; k < sp.n_sites; ++k) {
     const D3 o = rotate_exact(qw, qx, qy, qz, {sp.body[k][0], sp.body[k][1], sp.body[k][2]});
-    st.ox[base + k] = o.x;
-    st.oy[base + k] = o.y;
-    st.oz[base + k] = o.z;
+    st.off[base + k] = make_double4(o.x, o.y, o.z, 0.0);
   }
 }
 
@@ -150,7 +147,7 @@ struct FixRefine {
   double rc2;
 };
 
-__device__ __noinline__ bool refine_pair(uint4 pi, uint4 pj, int ig, int jg,
+__device__ __forceinline__ bool refine_pair(uint4 pi, uint4 pj, int ig, int jg,
                                          const double* __restrict__ gx,
                                          const double* __restrict__ gy,
                                          const double* __restrict__ gz, const FixRefine& f,
@@ -401,24 +398,47 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
+// Queue capacity per warp: a carried partial batch (< 32) + one chunk (<= 1024).
+constexpr int kQueue = kChunkWords * 32 + 32;
+
 template <typename Body>
 __device__ __forceinline__ void for_each_partner(const uint32_t* __restrict__ row, int words,
-                                                 int lane, int* __restrict__ list, Body&& body) {
+                                                 int lane, int* __restrict__ q, Body&& body) {
+  int fill = 0;  // warp-uniform queue length carried between chunks
+  // the next chunk's words are loaded before the current one is expanded
+  uint32_t next = lane < words ? __ldg(row + lane) : 0u;
   for (int w0 = 0; w0 < words; w0 += kChunkWords) {
     const int w = w0 + lane;
-    uint32_t m = w < words ? __ldg(row + w) : 0u;
+    uint32_t m = next;
+    next = w + kChunkWords < words ? __ldg(row + w + kChunkWords) : 0u;
     const int c = __popc(m);
     const int incl = warp_incl_scan(c, lane);
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    int off = incl - c;
+    int off = fill + incl - c;
     while (m) {
-      list[off++] = w * 32 + __ffs(m) - 1;
+      q[off++] = w * 32 + __ffs(m) - 1;
       m &= m - 1u;
     }
+    fill += total;
     __syncwarp();
-    for (int e = lane; e < total; e += 32) body(list[e]);
+    int e = 0;
+    for (; e + 64 <= fill; e += 64) {  // two full batches: both gathers in flight
+      const int j0 = q[e + lane], j1 = q[e + 32 + lane];
+      body(j0);
+      body(j1);
+    }
+    if (e + 32 <= fill) {
+      body(q[e + lane]);
+      e += 32;
+    }
+    const int rem = fill - e;  // carry the partial batch
+    const int v = lane < rem ? q[e + lane] : 0;
     __syncwarp();
+    if (lane < rem) q[lane] = v;
+    __syncwarp();
+    fill = rem;
   }
+  if (lane < fill) body(q[lane]);
 }
 
 // 1/x to ~1 ulp without the IEEE-division slow path: hardware reciprocal
@@ -500,14 +520,12 @@ constexpr int kForceWarps = 8;
 
 template <bool MULTI_SPECIES, bool WRAPPED>
 __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) {
-  __shared__ int plist[kForceWarps][kChunkWords * 32];
+  __shared__ int queue[kForceWarps][kQueue];
   const SysDev& s = a.s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.y;
   const size_t roff = size_t(r) * s.n;
-  const double* __restrict__ px = a.st.px + roff;
-  const double* __restrict__ py = a.st.py + roff;
-  const double* __restrict__ pz = a.st.pz + roff;
+  const double4* __restrict__ p4 = a.st.pos4 + roff;
   const MinImage mi = s.mi;
   const float thr = a.thr;
   auto mimg = [&](double d) {
@@ -515,14 +533,15 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
   };
   double u = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
   for (int i = blockIdx.x * kForceWarps + warp; i < s.n; i += gridDim.x * kForceWarps) {
-    const double xi = px[i], yi = py[i], zi = pz[i];
+    const double4 pi = p4[i];
     const int si = MULTI_SPECIES ? s.species_of[i] : 0;
     double fx = 0, fy = 0, fz = 0;
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
-    for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
-      const double dx = mimg(sub(xi, px[j]));
-      const double dy = mimg(sub(yi, py[j]));
-      const double dz = mimg(sub(zi, pz[j]));
+    for_each_partner(row, s.words, lane, queue[warp], [&](int j) {
+      const double4 pj = p4[j];
+      const double dx = mimg(sub(pi.x, pj.x));
+      const double dy = mimg(sub(pi.y, pj.y));
+      const double dz = mimg(sub(pi.z, pj.z));
       const double r2 = norm2_exact(dx, dy, dz);
       double c12 = a.c12, c6 = a.c6;
       if constexpr (MULTI_SPECIES) {
@@ -574,19 +593,15 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
 // METHOD: 0 none, 1 reaction field, 2 ewald real space.
 template <int METHOD, bool WRAPPED>
 __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
-  __shared__ int plist[kForceWarps][kChunkWords * 32];
+  __shared__ int plist[kForceWarps][kQueue];
   const SysDev& s = a.s;
   const DevTables* __restrict__ tab = s.tab;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.y;
   const size_t roff = size_t(r) * s.n;
   const size_t soff = size_t(r) * s.total_sites;
-  const double* __restrict__ px = a.st.px + roff;
-  const double* __restrict__ py = a.st.py + roff;
-  const double* __restrict__ pz = a.st.pz + roff;
-  const double* __restrict__ ox = a.st.ox + soff;
-  const double* __restrict__ oy = a.st.oy + soff;
-  const double* __restrict__ oz = a.st.oz + soff;
+  const double4* __restrict__ p4 = a.st.pos4 + roff;
+  const double4* __restrict__ o4 = a.st.off + soff;
   const MinImage mi = s.mi;
   const float thr = a.thr;
   auto mimg = [&](double d) {
@@ -595,16 +610,17 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
   const double rc2 = a.rc2;
   double ulj = 0, uel = 0, urf = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
   for (int i = blockIdx.x * kForceWarps + warp; i < s.n; i += gridDim.x * kForceWarps) {
-    const double xi = px[i], yi = py[i], zi = pz[i];
+    const double4 pi = p4[i];
     const int si = s.species_of[i];
     const int bi = s.site_begin[i];
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
     for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
       const bool lo = i < j;
-      const double Rx = mimg(sub(xi, px[j]));
-      const double Ry = mimg(sub(yi, py[j]));
-      const double Rz = mimg(sub(zi, pz[j]));
+      const double4 pj = p4[j];
+      const double Rx = mimg(sub(pi.x, pj.x));
+      const double Ry = mimg(sub(pi.y, pj.y));
+      const double Rz = mimg(sub(pi.z, pj.z));
       const int sj = s.species_of[j];
       const int bj = s.site_begin[j];
       const DevPairInfo pinfo = tab->pair[lo ? si * s.ns + sj : sj * s.ns + si];
@@ -616,10 +632,11 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
       auto site_term = [&](int ta, int tb, double& rx, double& ry, double& rz, double& dix,
                            double& diy, double& diz) -> double {
         const int ki = bi + (lo ? ta : tb), kj = bj + (lo ? tb : ta);
-        dix = ox[ki];
-        diy = oy[ki];
-        diz = oz[ki];
-        const double djx = ox[kj], djy = oy[kj], djz = oz[kj];
+        const double4 di = o4[ki], dj = o4[kj];
+        dix = di.x;
+        diy = di.y;
+        diz = di.z;
+        const double djx = dj.x, djy = dj.y, djz = dj.z;
         if (lo) {
           rx = sub(add(Rx, dix), djx);
           ry = sub(add(Ry, diy), djy);
@@ -759,8 +776,8 @@ __global__ void k_ewald_tables(EwaldArgs a) {
   const int m = a.q_mol[q];
   const size_t roff = size_t(r) * a.s.n;
   const size_t soff = size_t(r) * a.s.total_sites + a.q_site[q];
-  const double p[3] = {a.st.px[roff + m] + a.st.ox[soff], a.st.py[roff + m] + a.st.oy[soff],
-                       a.st.pz[roff + m] + a.st.oz[soff]};
+  const double4 o = a.st.off[soff];
+  const double p[3] = {a.st.px[roff + m] + o.x, a.st.py[roff + m] + o.y, a.st.pz[roff + m] + o.z};
   const int K = a.kmax + 1;
   double2* base = a.tab + size_t(r) * 3 * K * a.nq;
   for (int ax = 0; ax < 3; ++ax) {
@@ -847,7 +864,8 @@ __global__ void __launch_bounds__(256) k_ewald_force(EwaldArgs a) {
   double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
   for (int q = q0; q < q1; ++q) {
     const int site = a.q_site[q];
-    const double ox = a.st.ox[soff + site], oy = a.st.oy[soff + site], oz = a.st.oz[soff + site];
+    const double4 o4 = a.st.off[soff + site];
+    const double ox = o4.x, oy = o4.y, oz = o4.z;
     const double qv = a.q_val[q];
     double sfx = 0, sfy = 0, sfz = 0;
     for (int kk = a.k_begin + lane; kk < a.k_begin + a.nk; kk += 32) {
@@ -959,10 +977,15 @@ __device__ __forceinline__ uint4 fix_position(double x, double y, double z, doub
                     __double2uint_rn(z * scale), in ? 1u : 0u);
 }
 
-__global__ void k_fix_positions(const double* px, const double* py, const double* pz, int count,
-                                double L, double scale, uint4* fixpos) {
+// Positions as the search (fixed point) and the force kernels (packed) read
+// them; the integrator writes both itself.
+__global__ void k_stage_positions(const double* px, const double* py, const double* pz, int count,
+                                  double L, double scale, uint4* fixpos, double4* pos4) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid < count) fixpos[gid] = fix_position(px[gid], py[gid], pz[gid], L, scale);
+  if (gid >= count) return;
+  const double x = px[gid], y = py[gid], z = pz[gid];
+  fixpos[gid] = fix_position(x, y, z, L, scale);
+  pos4[gid] = make_double4(x, y, z, 0.0);
 }
 
 // engine.cpp:107-127 (+ build_scene offsets for the new orientation)
@@ -1006,19 +1029,16 @@ __device__ __forceinline__ void kick_drift_one(const StepArgs& a, int gid) {
   a.st.px[gid] = px;
   a.st.py[gid] = py;
   a.st.pz[gid] = pz;
+  a.st.pos4[gid] = make_double4(px, py, pz, 0.0);
   if (a.fixpos) a.fixpos[gid] = fix_position(px, py, pz, s.mi.L, a.fix_scale);
   if (a.write_offsets) {
     const int base = r * s.total_sites + s.site_begin[i];
     if (sp.centred) {
-      a.st.ox[base] = 0.0;
-      a.st.oy[base] = 0.0;
-      a.st.oz[base] = 0.0;
+      a.st.off[base] = make_double4(0.0, 0.0, 0.0, 0.0);
     } else {
       for (int k = 0; k < sp.n_sites; ++k) {
         const D3 o = rotate_exact(q[0], q[1], q[2], q[3], {sp.body[k][0], sp.body[k][1], sp.body[k][2]});
-        a.st.ox[base + k] = o.x;
-        a.st.oy[base + k] = o.y;
-        a.st.oz[base + k] = o.z;
+        a.st.off[base + k] = make_double4(o.x, o.y, o.z, 0.0);
       }
     }
   }
