@@ -1,0 +1,144 @@
+// dropin_test.cpp — the reference's own types, generators and CPU ForceField /
+// Engine next to the GPU drop-ins of tmd_gpu.hpp.  Built where the reference
+// headers exist (integration/Makefile); the binary runs on the GPU box.
+// Exit status 0 iff forces/torques agree to 1e-10 x max|F|, energies and
+// 50-step trajectories to 1e-9.
+#include <cmath>
+#include <cstdio>
+#include <numbers>
+
+#include "tmd_gpu.hpp"
+
+using namespace tmd;
+
+namespace {
+
+Site lj(double x, double y, double z, double s, double e, double m) {
+  Site t;
+  t.kind = SiteKind::lj;
+  t.body_pos = {x, y, z};
+  t.sigma = s;
+  t.epsilon = e;
+  t.mass = m;
+  return t;
+}
+
+Site charge(double x, double y, double z, double q, double m) {
+  Site t;
+  t.kind = SiteKind::charge;
+  t.body_pos = {x, y, z};
+  t.q = q;
+  t.mass = m;
+  return t;
+}
+
+double max_abs(const std::vector<Vec3>& a) {
+  double m = 0.0;
+  for (const auto& v : a) m = std::max({m, std::abs(v.x), std::abs(v.y), std::abs(v.z)});
+  return m;
+}
+
+double max_diff(const std::vector<Vec3>& a, const std::vector<Vec3>& b) {
+  double m = 0.0;
+  for (std::size_t i = 0; i < a.size(); ++i)
+    m = std::max({m, std::abs(a[i].x - b[i].x), std::abs(a[i].y - b[i].y), std::abs(a[i].z - b[i].z)});
+  return m;
+}
+
+int failures = 0;
+
+void expect(bool ok, const char* what, double v) {
+  std::printf("  %-44s %.3e %s\n", what, v, ok ? "ok" : "FAIL");
+  if (!ok) ++failures;
+}
+
+void compare_eval(const char* name, const SystemComposition& comp, const ForceFieldOptions& opts,
+                  const SystemState& st) {
+  std::printf("%s (N=%d)\n", name, comp.molecule_count());
+  ForceField cpu(comp, opts);
+  GpuForceField gpu(comp, opts);
+  SystemState a = st, b = st;
+  cpu.evaluate(a);
+  gpu.evaluate(b);
+  const double fs = std::max(1.0, max_abs(a.force)), ts = std::max(1.0, max_abs(a.torque));
+  expect(max_diff(a.force, b.force) <= 1e-10 * fs, "max |dF| / max |F|", max_diff(a.force, b.force) / fs);
+  expect(max_diff(a.torque, b.torque) <= 1e-10 * ts, "max |dtau| / max |tau|", max_diff(a.torque, b.torque) / ts);
+  const double de = std::abs(a.energy.total() - b.energy.total()) / std::abs(a.energy.total());
+  expect(de <= 1e-9, "|dU| / |U|", de);
+  const double dv = std::abs(a.virial - b.virial) / std::max(1.0, std::abs(a.virial));
+  expect(dv <= 1e-9, "|dW| / |W|", dv);
+}
+
+}  // namespace
+
+int main() {
+  // 2CLJ (BASELINE config 1 shape, smaller N), reference init_lattice
+  {
+    SystemComposition comp;
+    comp.species = {build_species("2clj", {lj(0.25, 0, 0, 1, 1, 0.5), lj(-0.25, 0, 0, 1, 1, 0.5)})};
+    comp.counts = {500};
+    comp.box_length = std::cbrt(500 / 0.3);
+    comp.temperature = 2.0;
+    ForceFieldOptions opts;
+    opts.cutoff = 0.45 * comp.box_length;
+    const SystemState st = init_lattice(comp, 7);
+    compare_eval("2CLJ", comp, opts, st);
+
+    SimulationPlan plan;
+    plan.dt = 0.002;
+    plan.thermostat_interval_equil = 0;
+    plan.thermostat_interval_prod = 0;
+    Engine ref(comp, opts, plan, 7);
+    GpuEngine gpu(comp, opts, 0.002);
+    ref.set_state(st);
+    gpu.set_state(st);
+    for (int k = 0; k < 50; ++k) ref.step();
+    gpu.step(50);
+    const SystemState a = ref.state(), b = gpu.state();
+    double dp = 0.0;
+    for (int i = 0; i < comp.molecule_count(); ++i)
+      for (int k = 0; k < 3; ++k) {
+        double d = a.pos[i][k] - b.pos[i][k];
+        d -= comp.box_length * std::nearbyint(d / comp.box_length);
+        dp = std::max(dp, std::abs(d));
+      }
+    std::printf("2CLJ engine, 50 steps\n");
+    expect(dp / comp.box_length <= 1e-9, "max |dpos| / L", dp / comp.box_length);
+    const double de = std::abs(a.energy.total() - b.energy.total()) / std::abs(a.energy.total());
+    expect(de <= 1e-9, "|dU| / |U|", de);
+  }
+  // charged rigid dimers + LJ with reaction field (test_potentials.cpp:214-258 shape)
+  {
+    SystemComposition comp;
+    comp.species = {build_species("pair", {charge(0.2, 0, 0, 0.5, 1), charge(-0.2, 0, 0, -0.5, 1),
+                                           lj(0, 0, 0, 1, 1, 1)})};
+    comp.counts = {256};
+    comp.box_length = std::cbrt(256 / 0.5);
+    comp.temperature = 1.0;
+    ForceFieldOptions opts;
+    opts.cutoff = 0.45 * comp.box_length;
+    opts.method = ElectrostaticsMethod::reaction_field;
+    opts.eps_rf = 65.0;
+    compare_eval("RF dimers", comp, opts, init_lattice(comp, 3));
+  }
+  // ions with Ewald (reference ewald_tune)
+  {
+    SystemComposition comp;
+    comp.species = {build_species("cat", {lj(0, 0, 0, 1.0, 0.5, 1.0)}),
+                    build_species("ani", {lj(0, 0, 0, 1.2, 0.5, 1.0)})};
+    comp.species[0].sites[0].q = 1.0;
+    comp.species[0].net_charge = 1.0;
+    comp.species[1].sites[0].q = -1.0;
+    comp.species[1].net_charge = -1.0;
+    comp.counts = {108, 108};
+    comp.box_length = std::cbrt(216 / 0.4);
+    comp.temperature = 1.0;
+    ForceFieldOptions opts;
+    opts.cutoff = 0.45 * comp.box_length;
+    opts.method = ElectrostaticsMethod::ewald;
+    opts.ewald = ewald_tune(1e-6, opts.cutoff, comp.box_length);
+    compare_eval("Ewald ions", comp, opts, init_lattice(comp, 5));
+  }
+  std::printf("%s\n", failures ? "FAILED" : "PASSED");
+  return failures ? 1 : 0;
+}

@@ -1,0 +1,184 @@
+// tmd_gpu.hpp — the binding a tmd maintainer adds to the reference to use the
+// B200 path: tmd::GpuForceField / tmd::GpuEngine over the C ABI of
+// include/b200md.h, with the reference's own types (include/tmd/*.hpp) and
+// exceptions (include/tmd/error.hpp).  Header-only; link libb200md.so.
+//
+//   tmd::ForceField::evaluate(SystemState&)  (src/parallel.cpp:79-122)
+//     -> tmd::GpuForceField::evaluate(SystemState&)     same contract
+//   tmd::Engine::set_state / step / state      (src/engine.cpp:91-143)
+//     -> tmd::GpuEngine::set_state / step / state        device-resident
+#pragma once
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "b200md.h"
+#include "tmd/engine.hpp"
+#include "tmd/parallel.hpp"
+
+namespace tmd {
+
+namespace b2md_detail {
+
+inline void check(int rc) {
+  if (rc == B2MD_OK) return;
+  const std::string msg = b2md_last_error();
+  switch (rc) {
+    case B2MD_MODEL_ERROR: throw ModelError(msg);
+    case B2MD_CONFIG_ERROR: throw ConfigError(msg);
+    case B2MD_IO_ERROR: throw IoError(msg);
+    case B2MD_NUMERICAL_ERROR: throw NumericalError(msg);
+    default: throw Error(msg);
+  }
+}
+
+// an already-built tmd::MoleculeSpecies -> b2md_species (no second build pass)
+inline b2md_species to_c(const MoleculeSpecies& sp) {
+  if (sp.site_count() > B2MD_MAX_SITES) throw ModelError("b200md: too many sites in species");
+  b2md_species o;
+  std::memset(&o, 0, sizeof o);
+  o.n_sites = sp.site_count();
+  o.rotational_dof = sp.rotational_dof;
+  for (int k = 0; k < sp.site_count(); ++k) {
+    const Site& s = sp.sites[k];
+    o.sites[k].kind = static_cast<int32_t>(s.kind);
+    o.sites[k].body_pos[0] = s.body_pos.x;
+    o.sites[k].body_pos[1] = s.body_pos.y;
+    o.sites[k].body_pos[2] = s.body_pos.z;
+    o.sites[k].sigma = s.sigma;
+    o.sites[k].epsilon = s.epsilon;
+    o.sites[k].q = s.q;
+    o.sites[k].mass = s.mass;
+  }
+  o.total_mass = sp.total_mass;
+  o.inertia_principal[0] = sp.inertia_principal.x;
+  o.inertia_principal[1] = sp.inertia_principal.y;
+  o.inertia_principal[2] = sp.inertia_principal.z;
+  o.net_charge = sp.net_charge;
+  o.max_extent = sp.max_extent;
+  return o;
+}
+
+inline b2md_ff_options to_c(const ForceFieldOptions& f) {
+  b2md_ff_options o;
+  std::memset(&o, 0, sizeof o);
+  o.cutoff = f.cutoff;
+  o.method = static_cast<int32_t>(f.method);
+  o.eps_rf = f.eps_rf;
+  o.has_ewald = f.ewald ? 1 : 0;
+  if (f.ewald) {
+    o.ewald_alpha = f.ewald->alpha;
+    o.ewald_kmax = f.ewald->kmax;
+  }
+  o.workers = f.workers;
+  o.volume_derivatives = f.volume_derivatives ? 1 : 0;
+  return o;
+}
+
+inline void from_c(const b2md_energy& e, EnergyBreakdown& o) {
+  o.lj = e.lj;
+  o.elec_real = e.elec_real;
+  o.elec_recip = e.elec_recip;
+  o.elec_self = e.elec_self;
+  o.rf = e.rf;
+  o.lrc = e.lrc;
+  o.du_dv_explicit = e.du_dv_explicit;
+  o.du_dv_lrc = e.du_dv_lrc;
+  o.d2u_dv2_explicit = e.d2u_dv2_explicit;
+  o.d2u_dv2_lrc = e.d2u_dv2_lrc;
+}
+
+// Vec3 / Quat are plain structs of doubles (geom.hpp:9-38): AoS as the ABI expects
+static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 layout");
+static_assert(sizeof(Quat) == 4 * sizeof(double), "Quat layout");
+
+class Context {
+ public:
+  Context(const SystemComposition& comp, const ForceFieldOptions& opts, double dt, int device) {
+    std::vector<b2md_species> sp;
+    for (const auto& s : comp.species) sp.push_back(to_c(s));
+    std::vector<int32_t> counts(comp.counts.begin(), comp.counts.end());
+    b2md_composition c;
+    std::memset(&c, 0, sizeof c);
+    c.n_species = comp.species_count();
+    c.species = sp.data();
+    c.counts = counts.data();
+    c.box_length = comp.box_length;
+    c.temperature = comp.temperature;
+    const b2md_ff_options o = to_c(opts);
+    check(b2md_create(device, &c, &o, dt, 1, &ctx_));
+  }
+  ~Context() { b2md_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  b2md_ctx* get() const { return ctx_; }
+
+ private:
+  b2md_ctx* ctx_ = nullptr;
+};
+
+}  // namespace b2md_detail
+
+// Drop-in for tmd::ForceField (parallel.hpp:56-80).
+class GpuForceField {
+ public:
+  GpuForceField(const SystemComposition& comp, const ForceFieldOptions& opts, int device = 0)
+      : comp_(comp), ctx_(comp, opts, 0.0, device) {}
+
+  void evaluate(SystemState& state) {
+    const int n = state.molecule_count();
+    state.force.resize(n);
+    state.torque.resize(n);
+    b2md_energy e;
+    b2md_eval_stats st;
+    b2md_detail::check(b2md_evaluate(ctx_.get(), &state.pos[0].x, &state.orient[0].w,
+                                     &state.force[0].x, &state.torque[0].x, &e, &st));
+    b2md_detail::from_c(e, state.energy);
+    state.virial = st.virial;
+  }
+
+  const char* warning() const { return b2md_warning(ctx_.get()); }
+
+ private:
+  const SystemComposition& comp_;
+  b2md_detail::Context ctx_;
+};
+
+// The step path of tmd::Engine (engine.hpp:52-112), device resident.
+class GpuEngine {
+ public:
+  GpuEngine(const SystemComposition& comp, const ForceFieldOptions& opts, double dt, int device = 0)
+      : comp_(comp), ctx_(comp, opts, dt, device) {
+    if (dt <= 0.0) throw ConfigError("engine: time step must be positive");
+  }
+
+  void set_state(const SystemState& s) {  // engine.cpp:91-98
+    if (s.molecule_count() != comp_.molecule_count())
+      throw ConfigError("engine: state does not match composition");
+    b2md_detail::check(b2md_set_state(ctx_.get(), &s.pos[0].x, &s.orient[0].w, &s.vel[0].x,
+                                      &s.ang_vel[0].x));
+  }
+
+  void step(long n = 1) { b2md_detail::check(b2md_step(ctx_.get(), n)); }  // engine.cpp:102-143
+
+  SystemState state() const {
+    SystemState s;
+    s.resize(comp_.molecule_count());
+    s.box_length = comp_.box_length;
+    b2md_energy e;
+    b2md_eval_stats st;
+    b2md_detail::check(b2md_get_state(ctx_.get(), &s.pos[0].x, &s.orient[0].w, &s.vel[0].x,
+                                      &s.ang_vel[0].x, &s.force[0].x, &s.torque[0].x, &e, &st));
+    b2md_detail::from_c(e, s.energy);
+    s.virial = st.virial;
+    return s;
+  }
+
+ private:
+  SystemComposition comp_;
+  b2md_detail::Context ctx_;
+};
+
+}  // namespace tmd

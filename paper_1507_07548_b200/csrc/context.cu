@@ -419,13 +419,14 @@ StepArgs step_args(b2md_ctx* c) {
 int launch_step_kernel(b2md_ctx* c, int fam) {
   StepArgs a = step_args(c);
   const int nt = n_total(c);
-  const int g = (nt + 255) / 256;
+  // small CTAs: 16k molecules must still spread over all 148 SMs
+  const int bs = 64, g = (nt + bs - 1) / bs;
   if (fam == F_KICK_DRIFT)
-    PROF(c, fam, (k_kick_drift<<<g, 256, 0, c->stream>>>(a)));
+    PROF(c, fam, (k_kick_drift<<<g, bs, 0, c->stream>>>(a)));
   else if (fam == F_KICK)
-    PROF(c, fam, (k_kick<<<g, 256, 0, c->stream>>>(a)));
+    PROF(c, fam, (k_kick<<<g, bs, 0, c->stream>>>(a)));
   else
-    PROF(c, fam, (k_kick_kick_drift<<<g, 256, 0, c->stream>>>(a)));
+    PROF(c, fam, (k_kick_kick_drift<<<g, bs, 0, c->stream>>>(a)));
   return B2MD_OK;
 }
 
