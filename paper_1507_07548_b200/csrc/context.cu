@@ -654,7 +654,7 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const int rows_grid = (t.n + kForceWarps - 1) / kForceWarps;
-    c->force_grid = std::max(1, std::min(rows_grid, sms * 6));
+    c->force_grid = std::max(1, std::min(rows_grid, sms * 4));
   }
   TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars * c->force_grid));
   TRY(dalloc(&c->d_ticket, size_t(2) * R));

@@ -381,12 +381,13 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
 
 // ------------------------------------------------- partner enumeration
 // Walks the set bits of one bit-matrix row (the molecule's partners j, both
-// j<i and j>i) in chunks of 32 words: each lane loads one word, a warp
-// inclusive scan of the popcounts gives every lane its offset in the chunk's
-// compacted partner list (warp ballot/prefix-sum compaction into shared
-// memory), then the list is evaluated lane-parallel by `body(j)`.  No warp
-// collective sits inside a data-dependent loop.  Partner order, hence the
-// accumulation order, is fixed by the bit matrix: results are reproducible.
+// j<i and j>i) in chunks of 32 words: each lane loads one word, a ballot
+// skips empty chunks, a warp bit-transpose + prefix sum of popcounts
+// compacts the chunk's partners into a shared-memory queue (ballot /
+// prefix-sum compaction), full batches of 32 partners are evaluated
+// lane-parallel by `body(j)` (no collectives inside) and the partial batch is
+// carried to the next chunk.  Partner order, hence the accumulation order, is
+// a fixed function of the bit matrix: results are reproducible.
 constexpr int kChunkWords = 32;
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -408,16 +409,32 @@ __device__ __forceinline__ void for_each_partner(const uint32_t* __restrict__ ro
   // the next chunk's words are loaded before the current one is expanded
   uint32_t next = lane < words ? __ldg(row + lane) : 0u;
   for (int w0 = 0; w0 < words; w0 += kChunkWords) {
-    const int w = w0 + lane;
-    uint32_t m = next;
-    next = w + kChunkWords < words ? __ldg(row + w + kChunkWords) : 0u;
-    const int c = __popc(m);
-    const int incl = warp_incl_scan(c, lane);
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    int off = fill + incl - c;
-    while (m) {
-      q[off++] = w * 32 + __ffs(m) - 1;
-      m &= m - 1u;
+    const uint32_t m = next;
+    next = w0 + kChunkWords + lane < words ? __ldg(row + w0 + kChunkWords + lane) : 0u;
+    const int c0 = __popc(m);
+    const int total = int(__reduce_add_sync(0xffffffffu, unsigned(c0)));
+    if (total == 0) continue;  // empty chunk
+    const int mx = int(__reduce_max_sync(0xffffffffu, unsigned(c0)));
+    if (mx * 32 > 2 * total + 128) {
+      // bits concentrated in a few words (clustered partner runs): a 32x32
+      // bit transpose gives lane b bit b of every word, i.e. partners
+      // j = (w0 + k) * 32 + b, which spreads each run across lanes
+      uint32_t t = warp_transpose32(m, lane);
+      const int c = __popc(t);
+      int off = fill + warp_incl_scan(c, lane) - c;
+      while (t) {
+        const int k = __ffs(t) - 1;
+        t &= t - 1u;
+        q[off++] = (w0 + k) * 32 + lane;
+      }
+    } else {
+      // balanced chunk: lane k expands word k (ascending j, gather-friendly)
+      uint32_t t = m;
+      int off = fill + warp_incl_scan(c0, lane) - c0;
+      while (t) {
+        q[off++] = (w0 + lane) * 32 + __ffs(t) - 1;
+        t &= t - 1u;
+      }
     }
     fill += total;
     __syncwarp();
@@ -477,10 +494,13 @@ __device__ void finalize_scalars(const double* v /* NS values, valid on lane 0 o
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // fixed-order totals; __ldcg (L2, not a possibly stale L1) lets the loads
+  // of a thread's column slice be in flight together
   for (int k = 0; k < NS; ++k) {
-    const volatile double* col = cta_part + (size_t(r) * NS + k) * nblk;
+    const double* col = cta_part + (size_t(r) * NS + k) * nblk;
     double t = 0.0;
-    for (int b = threadIdx.x; b < nblk; b += blockDim.x) t += col[b];
+#pragma unroll 4
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) t += __ldcg(col + b);
     t = warp_sum(t);
     __syncthreads();
     if (lane == 0) red[warp][0] = t;
