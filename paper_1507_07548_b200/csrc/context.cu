@@ -319,11 +319,24 @@ int launch_force(b2md_ctx* c) {
     else                                                                            \
       PROF(c, F_FORCE, (K<__VA_ARGS__, false><<<grid, bs, 0, c->stream>>>(a)));     \
   } while (0)
+  // single species, every site pair an LJ term in (ia, ib) order, no charges
+  int rigid_ns = 0;
+  if (!c->t.single_site_path && c->t.ns == 1 && c->t.qq[0].empty()) {
+    const int ns = c->t.species[0].n_sites;
+    bool full = int(c->t.lj[0].size()) == ns * ns;
+    for (int k = 0; full && k < ns * ns; ++k)
+      full = c->t.lj[0][k].a == k / ns && c->t.lj[0][k].b == k % ns;
+    if (full && (ns == 2 || ns == 3)) rigid_ns = ns;
+  }
   if (c->t.single_site_path) {
     if (c->t.ns > 1)
       FORCE_LAUNCH(k_force_single, true);
     else
       FORCE_LAUNCH(k_force_single, false);
+  } else if (rigid_ns == 2) {
+    FORCE_LAUNCH(k_force_rigid, 2);
+  } else if (rigid_ns == 3) {
+    FORCE_LAUNCH(k_force_rigid, 3);
   } else if (c->t.method == B2MD_METHOD_EWALD) {
     FORCE_LAUNCH(k_force_multi, 2);
   } else if (c->t.method == B2MD_METHOD_REACTION_FIELD) {

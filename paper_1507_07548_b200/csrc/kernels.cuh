@@ -402,7 +402,7 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 // Queue capacity per warp: a carried partial batch (< 32) + one chunk (<= 1024).
 constexpr int kQueue = kChunkWords * 32 + 32;
 
-template <typename Body>
+template <bool DUAL = true, typename Body>
 __device__ __forceinline__ void for_each_partner(const uint32_t* __restrict__ row, int words,
                                                  int lane, int* __restrict__ q, Body&& body) {
   int fill = 0;  // warp-uniform queue length carried between chunks
@@ -439,11 +439,14 @@ __device__ __forceinline__ void for_each_partner(const uint32_t* __restrict__ ro
     fill += total;
     __syncwarp();
     int e = 0;
-    for (; e + 64 <= fill; e += 64) {  // two full batches: both gathers in flight
-      const int j0 = q[e + lane], j1 = q[e + 32 + lane];
-      body(j0);
-      body(j1);
-    }
+    if (DUAL)
+      for (; e + 64 <= fill; e += 64) {  // two full batches: both gathers in flight
+        const int j0 = q[e + lane], j1 = q[e + 32 + lane];
+        body(j0);
+        body(j1);
+      }
+    else
+      for (; e + 64 <= fill; e += 32) body(q[e + lane]);
     if (e + 32 <= fill) {
       body(q[e + lane]);
       e += 32;
@@ -761,6 +764,128 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
     }
   }
   double v[kNumRowScalars] = {warp_sum(ulj), warp_sum(uel), warp_sum(urf), warp_sum(s1),
+                              warp_sum(s2),  warp_sum(vir), warp_sum(cnt)};
+  finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
+}
+
+// ------------------------------------ single-species all-LJ rigid molecules
+// The general path of potentials.cpp:204-242 specialised to one species whose
+// site pairs are all LJ terms in the PairTable's (ia, ib) order
+// (potentials.cpp:54-70) and no charges: 2CLJ (BASELINE cfg1, cfg4) and the
+// 3-site rotors of the reference tests.  Term parameters and the row's site
+// offsets sit in registers; each partner's site offsets are gathered once per
+// pair (not once per term).  Same arithmetic and orientation rules as
+// k_force_multi.
+template <int NS, bool WRAPPED>
+__global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a) {
+  __shared__ int plist[kForceWarps][kQueue];
+  const SysDev& s = a.s;
+  const DevTables* __restrict__ tab = s.tab;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.y;
+  const size_t roff = size_t(r) * s.n;
+  const size_t soff = size_t(r) * s.total_sites;
+  const double4* __restrict__ p4 = a.st.pos4 + roff;
+  const double4* __restrict__ o4 = a.st.off + soff;
+  const MinImage mi = s.mi;
+  const float thr = a.thr;
+  auto mimg = [&](double d) {
+    return WRAPPED ? min_image_wrapped(d, mi.negL, thr) : min_image(d, mi);
+  };
+  double c12[NS][NS], c6[NS][NS];
+#pragma unroll
+  for (int ta = 0; ta < NS; ++ta)
+#pragma unroll
+    for (int tb = 0; tb < NS; ++tb) {
+      c12[ta][tb] = tab->lj[ta * NS + tb].c12;
+      c6[ta][tb] = tab->lj[ta * NS + tb].c6;
+    }
+  const double rc2 = a.rc2;
+  double ulj = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
+  for (int i = blockIdx.x * kForceWarps + warp; i < s.n; i += gridDim.x * kForceWarps) {
+    const double4 pi = p4[i];
+    const int bi = i * NS;  // single species: site_begin[i] = i * NS
+    double4 di[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) di[k] = o4[bi + k];
+    double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
+    const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
+    for_each_partner<false>(row, s.words, lane, plist[warp], [&](int j) {
+      const bool lo = i < j;
+      const double4 pj = p4[j];
+      double4 dj[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) dj[k] = o4[j * NS + k];
+      const double Rx = mimg(sub(pi.x, pj.x));
+      const double Ry = mimg(sub(pi.y, pj.y));
+      const double Rz = mimg(sub(pi.z, pj.z));
+      const double R2 = lo ? norm2_exact(Rx, Ry, Rz) : 0.0;
+      cnt += lo ? 1.0 : 0.0;
+      double s1p = 0.0, s2p = 0.0;
+#pragma unroll
+      for (int ta = 0; ta < NS; ++ta)
+#pragma unroll
+        for (int tb = 0; tb < NS; ++tb) {
+          // reference term (ta on the lower molecule, tb on the upper one)
+          const double4 dI = lo ? di[ta] : di[tb];
+          const double4 dJ = lo ? dj[tb] : dj[ta];
+          double rx, ry, rz;
+          if (lo) {
+            rx = sub(add(Rx, dI.x), dJ.x);
+            ry = sub(add(Ry, dI.y), dJ.y);
+            rz = sub(add(Rz, dI.z), dJ.z);
+          } else {
+            rx = add(sub(Rx, dJ.x), dI.x);
+            ry = add(sub(Ry, dJ.y), dI.y);
+            rz = add(sub(Rz, dJ.z), dI.z);
+          }
+          const double r2 = norm2_exact(rx, ry, rz);
+          if (r2 < rc2) {
+            const double inv_r2 = rcp_nr(r2);
+            const double ir6 = inv_r2 * inv_r2 * inv_r2;
+            const double a12 = c12[ta][tb] * ir6 * ir6;
+            const double a6 = c6[ta][tb] * ir6;
+            const double du_r = -12.0 * a12 + 6.0 * a6;
+            const double fs = -du_r * inv_r2;
+            const double gx = fs * rx, gy = fs * ry, gz = fs * rz;
+            fx += gx;
+            fy += gy;
+            fz += gz;
+            tx += dI.y * gz - dI.z * gy;
+            ty += dI.z * gx - dI.x * gz;
+            tz += dI.x * gy - dI.y * gx;
+            if (lo) {
+              ulj += a12 - a6;
+              vir += Rx * gx + Ry * gy + Rz * gz;
+              if (a.vderiv) {
+                const double d2u_r2 = 156.0 * a12 - 42.0 * a6;
+                const double rvR = rx * Rx + ry * Ry + rz * Rz;
+                const double arr = rvR * inv_r2;
+                s1p += du_r * arr;
+                s2p += d2u_r2 * arr * arr + du_r * inv_r2 * (R2 - rvR * arr);
+              }
+            }
+          }
+        }
+      s1 += s1p;
+      s2 += s2p;
+    });
+    fx = warp_sum(fx);
+    fy = warp_sum(fy);
+    fz = warp_sum(fz);
+    tx = warp_sum(tx);
+    ty = warp_sum(ty);
+    tz = warp_sum(tz);
+    if (lane == 0) {
+      a.st.fx[roff + i] = fx;
+      a.st.fy[roff + i] = fy;
+      a.st.fz[roff + i] = fz;
+      a.st.tx[roff + i] = tx;
+      a.st.ty[roff + i] = ty;
+      a.st.tz[roff + i] = tz;
+    }
+  }
+  double v[kNumRowScalars] = {warp_sum(ulj), 0.0, 0.0, warp_sum(s1),
                               warp_sum(s2),  warp_sum(vir), warp_sum(cnt)};
   finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
 }
