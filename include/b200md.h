@@ -211,6 +211,12 @@ int b2md_pair_list(b2md_ctx* ctx, int replica, int32_t* pairs, int64_t capacity,
 int b2md_nccl_unique_id(char id[128]);
 int b2md_attach_nccl(b2md_ctx* ctx, const char id[128], int rank, int world);
 
+/* Restrict the context to rank `rank`'s shard of a `world`-way split
+ * WITHOUT a communicator: evaluations then return that rank's partial forces,
+ * torques and sums (what each rank holds before the all-reduce).  For tests
+ * of the decomposition on one device; b2md_attach_nccl is the production path. */
+int b2md_set_shard(b2md_ctx* ctx, int rank, int world);
+
 /* Opaque cudaStream_t of the context (for event timing by the caller). */
 void* b2md_stream(b2md_ctx* ctx);
 

@@ -137,6 +137,7 @@ SIGNATURES = {
     ),
     "b2md_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "b2md_attach_nccl": (C.c_int, [_CTX, C.c_char_p, C.c_int, C.c_int]),
+    "b2md_set_shard": (C.c_int, [_CTX, C.c_int, C.c_int]),
     "b2md_stream": (C.c_void_p, [_CTX]),
     "b2md_profile_enable": (C.c_int, [_CTX, C.c_int]),
     "b2md_kernel_times": (

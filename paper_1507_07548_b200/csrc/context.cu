@@ -111,7 +111,7 @@ struct b2md_ctx {
   double* d_fbuf = nullptr;   // fx fy fz tx ty tz (6*R*n) + sums (R*kNumSums): allreduce unit
   double4* d_off = nullptr;   // R * total_sites site offsets
   double4* d_pos4 = nullptr;  // R * n packed positions
-  double* d_stage = nullptr;  // AoS staging, 4*R*n
+  double* d_stage = nullptr;  // AoS staging: 6 slots of 4*R*n (one per array, no reuse waits)
   uint32_t* d_mask = nullptr;
   uint4* d_fixpos = nullptr;  // fixed-point positions (search prefilter)
   double* d_cta_part = nullptr;  // force-kernel per-CTA scalar partials
@@ -502,22 +502,26 @@ int run_steps(b2md_ctx* c, int64_t nsteps) {
   return B2MD_OK;
 }
 
-int upload_aos(b2md_ctx* c, const double* host, int width, double* d0, double* d1, double* d2,
-               double* d3) {
+// Host AoS <-> device SoA.  Every array has its own staging slot, so a
+// sequence of transfers is queued without host synchronisation; callers
+// synchronise once.
+int upload_aos(b2md_ctx* c, int slot, const double* host, int width, double* d0, double* d1,
+               double* d2, double* d3) {
   const int nt = n_total(c);
-  CU(cudaMemcpyAsync(c->d_stage, host, sizeof(double) * width * nt, cudaMemcpyHostToDevice, c->stream));
-  k_aos_to_soa<<<(nt + 255) / 256, 256, 0, c->stream>>>(c->d_stage, nt, width, d0, d1, d2, d3);
+  double* stage = c->d_stage + size_t(slot) * 4 * nt;
+  CU(cudaMemcpyAsync(stage, host, sizeof(double) * width * nt, cudaMemcpyHostToDevice, c->stream));
+  k_aos_to_soa<<<(nt + 255) / 256, 256, 0, c->stream>>>(stage, nt, width, d0, d1, d2, d3);
   CU(cudaGetLastError());
   return B2MD_OK;
 }
 
-int download_aos(b2md_ctx* c, double* host, int width, const double* d0, const double* d1,
-                 const double* d2, const double* d3) {
+int download_aos(b2md_ctx* c, int slot, double* host, int width, const double* d0,
+                 const double* d1, const double* d2, const double* d3) {
   const int nt = n_total(c);
-  k_soa_to_aos<<<(nt + 255) / 256, 256, 0, c->stream>>>(c->d_stage, nt, width, d0, d1, d2, d3);
+  double* stage = c->d_stage + size_t(slot) * 4 * nt;
+  k_soa_to_aos<<<(nt + 255) / 256, 256, 0, c->stream>>>(stage, nt, width, d0, d1, d2, d3);
   CU(cudaGetLastError());
-  CU(cudaMemcpyAsync(host, c->d_stage, sizeof(double) * width * nt, cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
+  CU(cudaMemcpyAsync(host, stage, sizeof(double) * width * nt, cudaMemcpyDeviceToHost, c->stream));
   return B2MD_OK;
 }
 
@@ -660,7 +664,7 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   TRY(dalloc(&c->d_fbuf, 6 * nt + size_t(kNumSums) * R));
   TRY(dalloc(&c->d_off, size_t(t.total_sites) * R));
   TRY(dalloc(&c->d_pos4, nt));
-  TRY(dalloc(&c->d_stage, 4 * nt));
+  TRY(dalloc(&c->d_stage, 6 * 4 * nt));
   TRY(dalloc(&c->d_mask, size_t(R) * c->g.n_pad * c->g.words));
   TRY(dalloc(&c->d_fixpos, nt));
   {
@@ -855,16 +859,16 @@ int b2md_evaluate(b2md_ctx* c, const double* pos, const double* orient, double* 
                   double* torque, b2md_energy* energy, b2md_eval_stats* stats) {
   if (!c || !pos) return set_err(B2MD_INVALID_ARGUMENT, "evaluate: null pointer");
   CU(cudaSetDevice(c->device));
-  TRY(upload_aos(c, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
+  TRY(upload_aos(c, 0, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
   if (orient) {
-    TRY(upload_aos(c, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
+    TRY(upload_aos(c, 1, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
   } else if (c->t.any_offsets) {
     return set_err(B2MD_INVALID_ARGUMENT, "evaluate: orientations required for multi-site species");
   }
   set_wrapped(c, false);
   TRY(enqueue_forces(c, true));
-  if (force) TRY(download_aos(c, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
-  if (torque) TRY(download_aos(c, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
+  if (force) TRY(download_aos(c, 4, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
+  if (torque) TRY(download_aos(c, 5, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
   TRY(download_scalars(c, energy, stats));
   CU(cudaStreamSynchronize(c->stream));
   c->state_valid = false;  // velocities not set: not an engine state
@@ -876,10 +880,10 @@ int b2md_set_state(b2md_ctx* c, const double* pos, const double* orient, const d
   if (!c || !pos || !orient || !vel || !ang_vel)
     return set_err(B2MD_INVALID_ARGUMENT, "set_state: null pointer");
   CU(cudaSetDevice(c->device));
-  TRY(upload_aos(c, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
-  TRY(upload_aos(c, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
-  TRY(upload_aos(c, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
-  TRY(upload_aos(c, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
+  TRY(upload_aos(c, 0, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
+  TRY(upload_aos(c, 1, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
+  TRY(upload_aos(c, 2, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
+  TRY(upload_aos(c, 3, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
   const int nt = n_total(c);
   // state_.wrap() (engine.cpp:96): px, py, pz are contiguous
   k_wrap<<<(3 * nt + 255) / 256, 256, 0, c->stream>>>(c->st.px, 3 * nt, c->t.box);
@@ -922,12 +926,12 @@ int b2md_upload_state(b2md_ctx* c, const double* pos, const double* orient, cons
                       const double* ang_vel, const double* force, const double* torque) {
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "upload_state: null context");
   CU(cudaSetDevice(c->device));
-  if (pos) TRY(upload_aos(c, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
-  if (orient) TRY(upload_aos(c, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
-  if (vel) TRY(upload_aos(c, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
-  if (ang_vel) TRY(upload_aos(c, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
-  if (force) TRY(upload_aos(c, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
-  if (torque) TRY(upload_aos(c, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
+  if (pos) TRY(upload_aos(c, 0, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
+  if (orient) TRY(upload_aos(c, 1, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
+  if (vel) TRY(upload_aos(c, 2, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
+  if (ang_vel) TRY(upload_aos(c, 3, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
+  if (force) TRY(upload_aos(c, 4, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
+  if (torque) TRY(upload_aos(c, 5, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
   // steps wrap before every evaluation, so step-time forces may use the fast path
   set_wrapped(c, true);
   c->state_valid = true;
@@ -938,13 +942,14 @@ int b2md_get_state(b2md_ctx* c, double* pos, double* orient, double* vel, double
                    double* force, double* torque, b2md_energy* energy, b2md_eval_stats* stats) {
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "get_state: null context");
   CU(cudaSetDevice(c->device));
-  if (pos) TRY(download_aos(c, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
-  if (orient) TRY(download_aos(c, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
-  if (vel) TRY(download_aos(c, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
-  if (ang_vel) TRY(download_aos(c, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
-  if (force) TRY(download_aos(c, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
-  if (torque) TRY(download_aos(c, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
+  if (pos) TRY(download_aos(c, 0, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
+  if (orient) TRY(download_aos(c, 1, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
+  if (vel) TRY(download_aos(c, 2, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
+  if (ang_vel) TRY(download_aos(c, 3, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
+  if (force) TRY(download_aos(c, 4, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
+  if (torque) TRY(download_aos(c, 5, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
   TRY(download_scalars(c, energy, stats));
+  CU(cudaStreamSynchronize(c->stream));
   return B2MD_OK;
 }
 
@@ -1017,6 +1022,20 @@ int b2md_attach_nccl(b2md_ctx* c, const char id[128], int rank, int world) {
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
     NC(ncclCommInitRank(&c->comm, world, u, rank));
+  }
+  c->rank = rank;
+  c->world = world;
+  TRY(setup_shard(c));
+  return B2MD_OK;
+}
+
+int b2md_set_shard(b2md_ctx* c, int rank, int world) {
+  if (!c || world < 1 || rank < 0 || rank >= world)
+    return set_err(B2MD_INVALID_ARGUMENT, "set_shard: bad argument");
+  CU(cudaSetDevice(c->device));
+  if (c->comm) {
+    ncclCommDestroy(c->comm);
+    c->comm = nullptr;
   }
   c->rank = rank;
   c->world = world;

@@ -168,6 +168,11 @@ class ForceField:
     def pair_list(self) -> np.ndarray:
         return self._c.pair_list(0)
 
+    def set_shard(self, rank: int, world: int) -> None:
+        """Evaluate only `rank`'s shard of a `world`-way decomposition (partial
+        results, no communicator) — b2md_set_shard."""
+        check(_abi.lib().b2md_set_shard(self._c.ctx, rank, world))
+
     def close(self) -> None:
         self._c.close()
 

@@ -327,3 +327,39 @@ def test_engine_runs_bit_identical():  # test_engine.cpp:185-213 (fixed-seed det
         eng.step(20)
         outs.append(eng.state())
     assert np.array_equal(outs[0].pos, outs[1].pos) and np.array_equal(outs[0].vel, outs[1].vel)
+
+
+# ------------------------------------------------ multi-GPU decomposition
+@pytest.mark.parametrize("case", ["lj", "two_clj", "water_ions"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_shards_sum_to_full_evaluation(case, world):
+    """Each rank's shard (tile rows + k-vector range, b2md_set_shard — what a
+    rank holds before the NCCL all-reduce) evaluated on this GPU; the sum over
+    ranks must equal the full evaluation (reduction-order rounding only)."""
+    if case == "lj":
+        wl = configs.lj_fluid_config(5000, 0.8, 3.0, seed=4)
+        comp, opts, st = wl.comp, wl.opts, wl.states[0]
+    elif case == "two_clj":
+        wl = configs.two_clj_config(2048, 0.3, 1, 2.0, 0.002, 1, "c1")
+        comp, opts, st = wl.comp, wl.opts, wl.states[0]
+    else:
+        comp, opts, st = golden_cases._water_ions_small(300, 10, 2)
+    _, full = gpu_eval(comp, opts, st.pos, st.orient)
+    f = np.zeros_like(full.force)
+    t = np.zeros_like(full.torque)
+    parts = np.zeros(5)
+    for rank in range(world):
+        ff = b2.ForceField(comp, opts)
+        ff.set_shard(rank, world)
+        s = st.copy()
+        ff.evaluate(s)
+        f += s.force
+        t += s.torque
+        e = s.energy
+        parts += [e.lj, e.elec_real, e.elec_recip, s.virial, ff.last_stats.com_pairs]
+    check_vec(f, full.force, 1e-12, "sharded force")
+    check_vec(t, full.torque, 1e-12, "sharded torque")
+    e = full.energy
+    ref = np.array([e.lj, e.elec_real, e.elec_recip, full.virial])
+    assert np.all(np.abs(parts[:4] - ref) <= 1e-11 * np.maximum(1.0, np.abs(ref)))
+    assert int(parts[4]) == len(pyoracle.OracleFF(comp, opts).pair_list(st.pos))
