@@ -221,8 +221,11 @@ int b2md_set_shard(b2md_ctx* ctx, int rank, int world);
 void* b2md_stream(b2md_ctx* ctx);
 
 /* Per-kernel CUDA-event timing of the device step (bench instrumentation).
- * enable != 0 records an event pair around every launch of each kernel
- * family; b2md_kernel_times returns {name, total_ms, launches} rows. */
+ * enable = 1 records an event pair around every launch of each kernel
+ * family, enable = 2 only around the partner search (the dominant kernel;
+ * least perturbation); 0 turns it off.  Single steps run as a CUDA graph whose
+ * event-record nodes are re-pointed at fresh events before every launch.
+ * b2md_kernel_times returns {name, total_ms, launches} rows. */
 int b2md_profile_enable(b2md_ctx* ctx, int enable);
 int b2md_kernel_times(b2md_ctx* ctx, int max_rows, char (*names)[32], double* total_ms,
                       int64_t* launches, int* n_rows);

@@ -141,8 +141,16 @@ struct b2md_ctx {
   bool use_fix_prefilter = true;
   cudaGraphExec_t step_graph = nullptr;  // forces + fused kick/kick-drift
   cudaGraphExec_t single_graph = nullptr;  // one whole step
+  cudaGraphExec_t prof_graph = nullptr;    // one whole step with event-record nodes
+  cudaGraph_t prof_template = nullptr;      // its template (owns the node handles)
+  bool capturing_prof = false;
+  std::vector<cudaEvent_t> cap_ev;          // placeholder events captured into prof_graph
+  std::vector<int> cap_fam;                 // kernel family of each captured event pair
+  std::vector<cudaGraphNode_t> cap_nodes;   // the event-record node of each placeholder
   // profiling
   bool profile = false;
+  int profile_level = 1;   // 1: every kernel family, 2: the partner search only
+  bool prof_open = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
   size_t ev_used = 0;
   std::vector<int> ev_family;
@@ -160,8 +168,16 @@ int n_total(const b2md_ctx* c) { return c->t.n * c->R; }
 void drop_graphs(b2md_ctx* c) {
   if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
   if (c->single_graph) cudaGraphExecDestroy(c->single_graph);
+  if (c->prof_graph) cudaGraphExecDestroy(c->prof_graph);
+  if (c->prof_template) cudaGraphDestroy(c->prof_template);
+  c->prof_template = nullptr;
+  for (cudaEvent_t e : c->cap_ev) cudaEventDestroy(e);
+  c->cap_ev.clear();
+  c->cap_fam.clear();
+  c->cap_nodes.clear();
   c->step_graph = nullptr;
   c->single_graph = nullptr;
+  c->prof_graph = nullptr;
 }
 
 void set_wrapped(b2md_ctx* c, bool w) {
@@ -169,8 +185,23 @@ void set_wrapped(b2md_ctx* c, bool w) {
   c->positions_wrapped = w;
 }
 
+bool prof_on(const b2md_ctx* c, int fam) {
+  return c->profile && (c->profile_level == 1 || fam == F_SEARCH);
+}
+
 int prof_begin(b2md_ctx* c, int fam) {
-  if (!c->profile) return B2MD_OK;
+  if (!prof_on(c, fam)) return B2MD_OK;
+  c->prof_open = true;
+  if (c->capturing_prof) {  // placeholder events; re-pointed before every launch
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    c->cap_ev.push_back(e);
+    c->cap_fam.push_back(fam);
+    // External: captured as an event-record node (plain records in a capture
+    // only express dependencies)
+    CU(cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal));
+    return B2MD_OK;
+  }
   if (c->ev_used == c->ev_pool.size()) {
     cudaEvent_t a, b;
     CU(cudaEventCreate(&a));
@@ -184,7 +215,15 @@ int prof_begin(b2md_ctx* c, int fam) {
 }
 
 int prof_end(b2md_ctx* c) {
-  if (!c->profile) return B2MD_OK;
+  if (!c->prof_open) return B2MD_OK;
+  c->prof_open = false;
+  if (c->capturing_prof) {
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    c->cap_ev.push_back(e);
+    CU(cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal));
+    return B2MD_OK;
+  }
   CU(cudaEventRecord(c->ev_pool[c->ev_used].second, c->stream));
   ++c->ev_used;
   return B2MD_OK;
@@ -482,7 +521,74 @@ int build_single_step_graph(b2md_ctx* c) {
   return B2MD_OK;
 }
 
+// One step as a graph with CUDA-event record nodes around every kernel
+// family: per-kernel timing at graph-launch speed.  Before each launch the
+// nodes are re-pointed at fresh events of the profiling pool.
+int build_prof_graph(b2md_ctx* c) {
+  if (c->prof_graph) return B2MD_OK;
+  CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  c->capturing_prof = true;
+  int rc = launch_step_kernel(c, F_KICK_DRIFT);
+  if (!rc) rc = enqueue_forces(c, false);
+  if (!rc) rc = launch_step_kernel(c, F_KICK);
+  c->capturing_prof = false;
+  cudaGraph_t graph;
+  cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+  if (rc) return rc;
+  CU(e);
+  size_t nn = 0;
+  CU(cudaGraphGetNodes(graph, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  CU(cudaGraphGetNodes(graph, nodes.data(), &nn));
+  c->cap_nodes.assign(c->cap_ev.size(), nullptr);
+  for (cudaGraphNode_t node : nodes) {
+    cudaGraphNodeType ty;
+    CU(cudaGraphNodeGetType(node, &ty));
+    if (ty != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t ev;
+    CU(cudaGraphEventRecordNodeGetEvent(node, &ev));
+    for (size_t k = 0; k < c->cap_ev.size(); ++k)
+      if (c->cap_ev[k] == ev) c->cap_nodes[k] = node;
+  }
+  for (cudaGraphNode_t node : c->cap_nodes)
+    if (!node) {
+      cudaGraphDestroy(graph);
+      return set_err(B2MD_CUDA_ERROR, "profiling graph: event node not found");
+    }
+  e = cudaGraphInstantiate(&c->prof_graph, graph, 0);
+  // instantiated nodes are addressed through the template graph's handles
+  if (e == cudaSuccess) {
+    c->prof_template = graph;
+  } else {
+    cudaGraphDestroy(graph);
+  }
+  CU(e);
+  return B2MD_OK;
+}
+
+int launch_prof_graph(b2md_ctx* c) {
+  TRY(build_prof_graph(c));
+  for (size_t p = 0; 2 * p + 1 < c->cap_nodes.size(); ++p) {
+    if (c->ev_used == c->ev_pool.size()) {
+      cudaEvent_t a, b;
+      CU(cudaEventCreate(&a));
+      CU(cudaEventCreate(&b));
+      c->ev_pool.push_back({a, b});
+      c->ev_family.push_back(0);
+    }
+    c->ev_family[c->ev_used] = c->cap_fam[p];
+    CU(cudaGraphExecEventRecordNodeSetEvent(c->prof_graph, c->cap_nodes[2 * p],
+                                            c->ev_pool[c->ev_used].first));
+    CU(cudaGraphExecEventRecordNodeSetEvent(c->prof_graph, c->cap_nodes[2 * p + 1],
+                                            c->ev_pool[c->ev_used].second));
+    ++c->ev_used;
+  }
+  CU(cudaGraphLaunch(c->prof_graph, c->stream));
+  return B2MD_OK;
+}
+
 int run_steps(b2md_ctx* c, int64_t nsteps) {
+  if (c->profile && c->use_graphs && nsteps == 1) return launch_prof_graph(c);
   const bool graphs = c->use_graphs && !c->profile;
   if (graphs && nsteps == 1) {
     TRY(build_single_step_graph(c));
@@ -582,14 +688,7 @@ int setup_shard(b2md_ctx* c) {
   c->n_super_tiles = int(list.size());
   // a fresh bit matrix: only this rank's tiles are ever written afterwards
   CU(cudaMemset(c->d_mask, 0, sizeof(uint32_t) * size_t(c->R) * c->g.n_pad * c->g.words));
-  if (c->step_graph) {
-    cudaGraphExecDestroy(c->step_graph);
-    c->step_graph = nullptr;
-  }
-  if (c->single_graph) {
-    cudaGraphExecDestroy(c->single_graph);
-    c->single_graph = nullptr;
-  }
+  drop_graphs(c);
   return B2MD_OK;
 }
 
@@ -759,8 +858,7 @@ void free_ctx(b2md_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
-  if (c->single_graph) cudaGraphExecDestroy(c->single_graph);
+  drop_graphs(c);
   for (auto& e : c->ev_pool) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -1048,7 +1146,9 @@ void* b2md_stream(b2md_ctx* c) { return c ? reinterpret_cast<void*>(c->stream) :
 int b2md_profile_enable(b2md_ctx* c, int enable) {
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "profile_enable: null context");
   TRY(prof_harvest(c));
+  if (enable != c->profile_level || (enable != 0) != c->profile) drop_graphs(c);
   c->profile = enable != 0;
+  if (enable) c->profile_level = enable;
   if (c->profile)
     for (int f = 0; f < F_COUNT; ++f) {
       c->prof_ms[f] = 0.0;

@@ -290,8 +290,9 @@ class Engine:
     def set_graphs(self, enable: bool) -> None:
         check(_abi.lib().b2md_set_graphs(self._c.ctx, 1 if enable else 0))
 
-    def profile(self, enable: bool) -> None:
-        check(_abi.lib().b2md_profile_enable(self._c.ctx, 1 if enable else 0))
+    def profile(self, enable, level: int = 1) -> None:
+        """Per-kernel CUDA-event timing: level 1 all kernels, 2 search only."""
+        check(_abi.lib().b2md_profile_enable(self._c.ctx, int(level) if enable else 0))
 
     def kernel_times(self) -> dict:
         rows = 16
