@@ -117,6 +117,7 @@ struct b2md_ctx {
   double* d_cta_part = nullptr;  // force-kernel per-CTA scalar partials
   unsigned* d_ticket = nullptr;   // 2 * R: force, ewald
   int force_grid = 1;
+  int force_warps = 8;
   uint32_t* d_super = nullptr;
   int n_super_tiles = 0;
   int* d_error = nullptr;
@@ -350,7 +351,7 @@ int launch_force(b2md_ctx* c) {
   ForceArgs a = force_args(c);
   const bool w = fast_min_image(c);
   dim3 grid(c->force_grid, c->R);
-  const int bs = kForceWarps * 32;
+  const int bs = c->force_warps * 32;
 #define FORCE_LAUNCH(K, ...)                                                        \
   do {                                                                              \
     if (w)                                                                          \

@@ -555,7 +555,8 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
     return WRAPPED ? min_image_wrapped(d, mi.negL, thr) : min_image(d, mi);
   };
   double u = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
-  for (int i = blockIdx.x * kForceWarps + warp; i < s.n; i += gridDim.x * kForceWarps) {
+  const int wpb = blockDim.x >> 5;  // warps per CTA (<= kForceWarps; fewer for small systems)
+  for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
     const double4 pi = p4[i];
     const int si = MULTI_SPECIES ? s.species_of[i] : 0;
     double fx = 0, fy = 0, fz = 0;
@@ -632,7 +633,8 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
   };
   const double rc2 = a.rc2;
   double ulj = 0, uel = 0, urf = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
-  for (int i = blockIdx.x * kForceWarps + warp; i < s.n; i += gridDim.x * kForceWarps) {
+  const int wpb = blockDim.x >> 5;  // warps per CTA (<= kForceWarps; fewer for small systems)
+  for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
     const double4 pi = p4[i];
     const int si = s.species_of[i];
     const int bi = s.site_begin[i];
@@ -802,7 +804,8 @@ __global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a
     }
   const double rc2 = a.rc2;
   double ulj = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
-  for (int i = blockIdx.x * kForceWarps + warp; i < s.n; i += gridDim.x * kForceWarps) {
+  const int wpb = blockDim.x >> 5;  // warps per CTA (<= kForceWarps; fewer for small systems)
+  for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
     const double4 pi = p4[i];
     const int bi = i * NS;  // single species: site_begin[i] = i * NS
     double4 di[NS];
