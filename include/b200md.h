@@ -203,6 +203,24 @@ int b2md_get_state(b2md_ctx* ctx, double* pos, double* orient, double* vel, doub
 int b2md_pair_list(b2md_ctx* ctx, int replica, int32_t* pairs, int64_t capacity,
                    int64_t* n_pairs);
 
+/* Green-Kubo heat flux J_q (tmd::heat_flux, include/tmd/greenkubo.hpp:93,
+ * src/greenkubo.cpp:182-266) of the context's current device state: the
+ * state set_state / step left (Engine::run samples it every n_ext steps,
+ * src/engine.cpp:235-238).  `enthalpy` holds one partial molar enthalpy per
+ * species; n_enthalpy != species count is B2MD_CONFIG_ERROR, as the
+ * reference throws ConfigError.  Writes jq[3 * n_replicas].  Charge terms are
+ * bare Coulomb (+ reaction field), the reference's choice, under every
+ * method.  Under NCCL sharding every rank calls it (collective) and gets the
+ * full sum. */
+int b2md_heat_flux(b2md_ctx* ctx, const double* enthalpy, int n_enthalpy, double* jq);
+
+/* Same, of a host state (the reference's free-function form: positions taken
+ * as given, no wrap).  Overwrites the device state; step needs a new
+ * set_state afterwards.  pos/orient/vel/ang_vel: AoS, n_replicas systems. */
+int b2md_heat_flux_state(b2md_ctx* ctx, const double* pos, const double* orient,
+                         const double* vel, const double* ang_vel, const double* enthalpy,
+                         int n_enthalpy, double* jq);
+
 /* Multi-GPU row sharding (one process per GPU).  b2md_nccl_unique_id fills a
  * 128-byte ncclUniqueId on the root; every rank then calls b2md_attach_nccl
  * with the broadcast id.  After attaching, each rank evaluates only its shard

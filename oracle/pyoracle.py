@@ -51,6 +51,7 @@ def oracle_lib():
         L.oracle_pair_list.argtypes = [C.c_void_p, _D, C.POINTER(C.c_int32), C.c_int64]
         L.oracle_pair_list.restype = C.c_int64
         L.oracle_wrap.argtypes = [C.c_int, C.c_double, _D]
+        L.oracle_heat_flux.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, C.c_int, _D]
         L.oracle_step.argtypes = [C.c_void_p, C.c_double, C.c_int64, _D, _D, _D, _D, _D, _D,
                                   C.POINTER(_abi.b2md_energy), C.POINTER(_abi.b2md_eval_stats)]
         _oracle = L
@@ -77,6 +78,7 @@ def ref_lib():
         L.ref_evaluate.argtypes = [C.c_void_p, _D, _D, _D, _D, C.POINTER(_abi.b2md_energy), _D]
         L.ref_pair_list.argtypes = [C.c_void_p, _D, C.POINTER(C.c_int32), C.c_int64]
         L.ref_pair_list.restype = C.c_int64
+        L.ref_heat_flux.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, C.c_int, _D]
         L.ref_engine_create.argtypes = [C.POINTER(_abi.b2md_composition), C.POINTER(_abi.b2md_ff_options), C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]
         L.ref_engine_destroy.argtypes = [C.c_void_p]
         L.ref_engine_set_state.argtypes = [C.c_void_p, _D, _D, _D, _D]
@@ -146,10 +148,24 @@ class _FF:
         return out
 
 
+def _heat_flux(ff, pos, orient, vel, ang_vel, enthalpy):
+    n = ff.n
+    arr = [np.ascontiguousarray(a, dtype=np.float64).reshape(n, w)
+           for a, w in ((pos, 3), (orient, 4), (vel, 3), (ang_vel, 3))]
+    h = np.ascontiguousarray(enthalpy, dtype=np.float64).reshape(-1)
+    out = np.zeros(3)
+    _check(ff.lib, ff.prefix, getattr(ff.lib, ff.prefix + "_heat_flux")(
+        ff.h, *[_d(a) for a in arr], _d(h) if h.size else None, int(h.size), _d(out)))
+    return out
+
+
 class OracleFF(_FF):
     """C restatement (serial ForceField::evaluate + Engine::step)."""
 
     prefix = "oracle"
+
+    def heat_flux(self, pos, orient, vel, ang_vel, enthalpy):
+        return _heat_flux(self, pos, orient, vel, ang_vel, enthalpy)
 
     def evaluate(self, pos, orient):
         n = self.n
@@ -198,6 +214,9 @@ class RefFF(_FF):
     """The unmodified reference tmd::ForceField (workers from opts)."""
 
     prefix = "ref"
+
+    def heat_flux(self, pos, orient, vel, ang_vel, enthalpy):
+        return _heat_flux(self, pos, orient, vel, ang_vel, enthalpy)
 
     def evaluate(self, pos, orient):
         n = self.n

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "tmd/engine.hpp"
+#include "tmd/greenkubo.hpp"
 #include "tmd/parallel.hpp"
 #include "../include/b200md.h"
 
@@ -319,4 +320,22 @@ extern "C" int ref_rng_draws(uint64_t seed, int n, uint64_t* u64, double* unifor
     gaussian[k] = c.gaussian();
   }
   return 0;
+}
+
+// tmd::heat_flux (include/tmd/greenkubo.hpp:93, src/greenkubo.cpp:182-266)
+extern "C" int ref_heat_flux(void* h, const double* pos, const double* orient, const double* vel,
+                             const double* ang_vel, const double* enthalpy, int n_enthalpy,
+                             double* jq) {
+  return guarded([&]() -> int {
+    auto* f = static_cast<RefFF*>(h);
+    tmd::SystemState st;
+    st.box_length = f->comp.box_length;
+    get_state(st, f->comp.molecule_count(), pos, orient, vel, ang_vel);
+    std::vector<double> hh(enthalpy, enthalpy + n_enthalpy);
+    const tmd::Vec3 j = tmd::heat_flux(f->comp, st, f->ff->table(), hh);
+    jq[0] = j.x;
+    jq[1] = j.y;
+    jq[2] = j.z;
+    return B2MD_OK;
+  });
 }

@@ -987,3 +987,89 @@ int oracle_step(oracle_ff* ff, double dt, int64_t nsteps, double* pos, double* o
   }
   return B2MD_OK;
 }
+
+/* greenkubo.cpp:182-266 */
+int oracle_heat_flux(oracle_ff* ff, const double* pos, const double* orient, const double* vel,
+                     const double* ang_vel, const double* enthalpy, int n_enthalpy, double* jq) {
+  if (!ff || !pos || !orient || !vel || !ang_vel || !jq || (n_enthalpy > 0 && !enthalpy))
+    return fail(B2MD_INVALID_ARGUMENT, "heat_flux: null pointer");
+  if (n_enthalpy != ff->ns) /* greenkubo.cpp:184-185 */
+    return fail(B2MD_CONFIG_ERROR, "heat flux: partial molar enthalpy required for every component");
+  const int n = ff->n;
+  build_offsets(ff, orient);
+  const double rc2 = ff->rc2;
+  const int method = ff->opts.method;
+  double* pair_u = (double*)calloc((size_t)n, sizeof(double));
+  vec3* w_lab = (vec3*)malloc(sizeof(vec3) * (size_t)n);
+  for (int i = 0; i < n; ++i) w_lab[i] = rotate(load4(orient, i), load3(ang_vel, i));
+  vec3 transport = v3(0, 0, 0);
+  for (int i = 0; i < n; ++i) {
+    for (int j = i + 1; j < n; ++j) {
+      const vec3 R = minimum_image(vsub(load3(pos, i), load3(pos, j)), ff->box);
+      const pair_terms* terms = &ff->terms[ff->species_of[i] * ff->ns + ff->species_of[j]];
+      const int bi = ff->site_begin[i], bj = ff->site_begin[j];
+      double u_pair = 0.0;
+      vec3 f_pair = v3(0, 0, 0), gamma_ij = v3(0, 0, 0), gamma_ji = v3(0, 0, 0);
+      for (int q = 0; q < terms->nlj; ++q) {
+        const lj_term* t = &terms->lj[q];
+        const vec3 da = load3(ff->off, bi + t->a), db = load3(ff->off, bj + t->b);
+        const vec3 rv = vsub(vadd(R, da), db);
+        const double r2 = vnorm2(rv);
+        if (r2 >= rc2) continue;
+        const double inv_r2 = 1.0 / r2;
+        const double ir6 = inv_r2 * inv_r2 * inv_r2;
+        const double a12 = t->c12 * ir6 * ir6;
+        const double a6 = t->c6 * ir6;
+        const double u = a12 - a6, du_dr_r = -12.0 * a12 + 6.0 * a6;
+        u_pair += u;
+        const vec3 f = vscale(-du_dr_r * inv_r2, rv);
+        f_pair = vadd(f_pair, f);
+        gamma_ij = vadd(gamma_ij, vcross(da, f));
+        gamma_ji = vsub(gamma_ji, vcross(db, f));
+      }
+      for (int q = 0; q < terms->nqq; ++q) {
+        const q_term* t = &terms->qq[q];
+        const vec3 da = load3(ff->off, bi + t->a), db = load3(ff->off, bj + t->b);
+        const vec3 rv = vsub(vadd(R, da), db);
+        const double r2 = vnorm2(rv);
+        if (r2 >= rc2) continue;
+        const double inv_r2 = 1.0 / r2;
+        const double r = sqrt(r2);
+        const double u_c = t->qq / r;
+        double u = u_c, du_r = -u_c;
+        if (method == B2MD_METHOD_REACTION_FIELD) {
+          const double rf = t->qq * ff->rf_r3inv * r2;
+          u += rf + t->qq * ff->rf_shift;
+          du_r += 2.0 * rf;
+        }
+        u_pair += u;
+        const vec3 f = vscale(-du_r * inv_r2, rv);
+        f_pair = vadd(f_pair, f);
+        gamma_ij = vadd(gamma_ij, vcross(da, f));
+        gamma_ji = vsub(gamma_ji, vcross(db, f));
+      }
+      if (u_pair == 0.0 && f_pair.x == 0.0 && f_pair.y == 0.0 && f_pair.z == 0.0) continue;
+      pair_u[i] += u_pair;
+      pair_u[j] += u_pair;
+      const vec3 vi = load3(vel, i), vj = load3(vel, j);
+      transport = vadd(transport, vscale(0.5 * (vdot(f_pair, vi) + vdot(gamma_ij, w_lab[i]) +
+                                                vdot(f_pair, vj) - vdot(gamma_ji, w_lab[j])),
+                                         R));
+    }
+  }
+  vec3 out = transport;
+  for (int i = 0; i < n; ++i) {
+    const b2md_species* sp = &ff->species[ff->species_of[i]];
+    const vec3 w = load3(ang_vel, i), v = load3(vel, i);
+    const double* I = sp->inertia_principal;
+    const double e_kin = 0.5 * sp->total_mass * vnorm2(v) +
+                         0.5 * (I[0] * w.x * w.x + I[1] * w.y * w.y + I[2] * w.z * w.z);
+    out = vadd(out, vscale(e_kin + 0.5 * pair_u[i] - enthalpy[ff->species_of[i]], v));
+  }
+  jq[0] = out.x;
+  jq[1] = out.y;
+  jq[2] = out.z;
+  free(pair_u);
+  free(w_lab);
+  return B2MD_OK;
+}

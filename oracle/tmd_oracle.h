@@ -64,6 +64,11 @@ int oracle_step(oracle_ff* ff, double dt, int64_t nsteps, double* pos, double* o
                 double* ang_vel, double* force, double* torque, b2md_energy* energy,
                 b2md_eval_stats* stats);
 
+/* heat_flux (src/greenkubo.cpp:182-266): J_q of the given state;
+ * `enthalpy` holds one partial molar enthalpy per species. */
+int oracle_heat_flux(oracle_ff* ff, const double* pos, const double* orient, const double* vel,
+                     const double* ang_vel, const double* enthalpy, int n_enthalpy, double* jq);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,7 @@ from .forcefield import (
     ForceField,
     ForceFieldOptions,
     ewald_tune,
+    heat_flux,
     kvector_count,
     measure_fp64_peak,
     nccl_unique_id,

@@ -86,9 +86,10 @@ __global__ void k_soa_to_aos(double* aos, int count, int width, const double* d0
 }
 
 enum Family { F_OFFSETS, F_SEARCH, F_FORCE, F_EWALD_TAB, F_EWALD_SK, F_EWALD_F, F_KICK_KICK_DRIFT,
-              F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_COUNT };
+              F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_HEAT_FLUX, F_COUNT };
 const char* kFamilyName[F_COUNT] = {"offsets",  "search", "force",   "ewald_tables", "ewald_sk",
-                                    "ewald_force", "kick_kick_drift", "kick_drift", "kick", "allreduce"};
+                                    "ewald_force", "kick_kick_drift", "kick_drift", "kick", "allreduce",
+                                    "heat_flux"};
 
 }  // namespace
 
@@ -133,6 +134,7 @@ struct b2md_ctx {
   double2* d_etab = nullptr;
   double2* d_S = nullptr;
   double* d_uk = nullptr;
+  double* d_flux = nullptr;  // R * kNumSums: heat flux totals
   // sharding
   int rank = 0, world = 1;
   int row_begin = 0, row_end = 0, k_begin = 0, k_end = 0;
@@ -433,6 +435,63 @@ int launch_allreduce(b2md_ctx* c) {
   TRY(prof_begin(c, F_ALLREDUCE));
   NC(ncclAllReduce(c->d_fbuf, c->d_fbuf, count, ncclDouble, ncclSum, c->comm, c->stream));
   TRY(prof_end(c));
+  return B2MD_OK;
+}
+
+// heat_flux (src/greenkubo.cpp:182-266) over the current mask, site offsets
+// and packed positions (valid after set_state / step / evaluate), then the
+// cross-rank sum of the per-replica 3-vectors.
+int launch_heat_flux(b2md_ctx* c, const double* enthalpy) {
+  FluxArgs a;
+  a.f = force_args(c);
+  for (int k = 0; k < kMaxSpecies; ++k) a.enthalpy[k] = k < c->t.ns ? enthalpy[k] : 0.0;
+  a.out = c->d_flux;
+  a.kinetic = c->rank == 0 ? 1 : 0;
+  const bool w = fast_min_image(c);
+  const bool offs = c->t.any_offsets;
+  dim3 grid(c->force_grid, c->R);
+  const int bs = c->force_warps * 32;
+  const int m = c->t.method == B2MD_METHOD_EWALD ? 2 : (c->t.method == B2MD_METHOD_REACTION_FIELD ? 1 : 0);
+#define FLUX_CASE(M)                                                                        \
+  case M:                                                                                   \
+    if (offs && w)                                                                          \
+      PROF(c, F_HEAT_FLUX, (k_heat_flux<M, true, true><<<grid, bs, 0, c->stream>>>(a)));    \
+    else if (offs)                                                                          \
+      PROF(c, F_HEAT_FLUX, (k_heat_flux<M, true, false><<<grid, bs, 0, c->stream>>>(a)));   \
+    else if (w)                                                                             \
+      PROF(c, F_HEAT_FLUX, (k_heat_flux<M, false, true><<<grid, bs, 0, c->stream>>>(a)));   \
+    else                                                                                    \
+      PROF(c, F_HEAT_FLUX, (k_heat_flux<M, false, false><<<grid, bs, 0, c->stream>>>(a)));  \
+    break;
+  switch (m) {
+    FLUX_CASE(0)
+    FLUX_CASE(1)
+    FLUX_CASE(2)
+  }
+#undef FLUX_CASE
+  if (c->world > 1 && c->comm)
+    NC(ncclAllReduce(c->d_flux, c->d_flux, size_t(kNumSums) * c->R, ncclDouble, ncclSum, c->comm,
+                     c->stream));
+  return B2MD_OK;
+}
+
+int download_flux(b2md_ctx* c, double* jq) {
+  std::vector<double> h(size_t(kNumSums) * c->R);
+  CU(cudaMemcpyAsync(h.data(), c->d_flux, sizeof(double) * h.size(), cudaMemcpyDeviceToHost,
+                     c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (int r = 0; r < c->R; ++r)
+    for (int k = 0; k < 3; ++k) jq[3 * r + k] = h[size_t(r) * kNumSums + k];
+  return B2MD_OK;
+}
+
+int check_enthalpy(const b2md_ctx* c, const double* enthalpy, int n_enthalpy, const double* jq) {
+  if (!jq || (n_enthalpy > 0 && !enthalpy))
+    return set_err(B2MD_INVALID_ARGUMENT, "heat_flux: null pointer");
+  // greenkubo.cpp:184-185
+  if (n_enthalpy != c->t.ns)
+    return set_err(B2MD_CONFIG_ERROR,
+                   "heat flux: partial molar enthalpy required for every component");
   return B2MD_OK;
 }
 
@@ -775,6 +834,7 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   }
   TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars * c->force_grid));
   TRY(dalloc(&c->d_ticket, size_t(2) * R));
+  TRY(dalloc(&c->d_flux, size_t(kNumSums) * R));
   TRY(dalloc(&c->d_error, 1));
   const int big = INT_MAX;
   CU(cudaMemcpy(c->d_error, &big, sizeof(int), cudaMemcpyHostToDevice));
@@ -868,7 +928,7 @@ void free_ctx(b2md_ctx* c) {
   void* ptrs[] = {c->d_tab,   c->d_species_of, c->d_site_begin, c->d_state, c->d_fbuf, c->d_off,
                   c->d_stage, c->d_mask,       c->d_cta_part, c->d_ticket, c->d_fixpos, c->d_pos4,   c->d_super, c->d_error, c->d_q_mol,
                   c->d_q_site, c->d_q_val,     c->d_mol_qbegin, c->d_kv,    c->d_etab,  c->d_S,
-                  c->d_uk};
+                  c->d_uk,    c->d_flux};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1049,6 +1109,42 @@ int b2md_get_state(b2md_ctx* c, double* pos, double* orient, double* vel, double
   if (torque) TRY(download_aos(c, 5, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
   TRY(download_scalars(c, energy, stats));
   CU(cudaStreamSynchronize(c->stream));
+  return B2MD_OK;
+}
+
+int b2md_heat_flux(b2md_ctx* c, const double* enthalpy, int n_enthalpy, double* jq) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "heat_flux: null context");
+  TRY(check_enthalpy(c, enthalpy, n_enthalpy, jq));
+  if (!c->state_valid)
+    return set_err(B2MD_CONFIG_ERROR, "heat_flux: set_state must precede heat_flux");
+  CU(cudaSetDevice(c->device));
+  TRY(launch_heat_flux(c, enthalpy));
+  return download_flux(c, jq);
+}
+
+int b2md_heat_flux_state(b2md_ctx* c, const double* pos, const double* orient, const double* vel,
+                         const double* ang_vel, const double* enthalpy, int n_enthalpy,
+                         double* jq) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "heat_flux: null context");
+  if (!pos || !orient || !vel || !ang_vel)
+    return set_err(B2MD_INVALID_ARGUMENT, "heat_flux: null pointer");
+  TRY(check_enthalpy(c, enthalpy, n_enthalpy, jq));
+  CU(cudaSetDevice(c->device));
+  TRY(upload_aos(c, 0, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
+  TRY(upload_aos(c, 1, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
+  TRY(upload_aos(c, 2, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
+  TRY(upload_aos(c, 3, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
+  set_wrapped(c, false);  // the reference takes the positions as given
+  TRY(launch_offsets(c));
+  const int nt = n_total(c);
+  k_stage_positions<<<(nt + 255) / 256, 256, 0, c->stream>>>(
+      c->st.px, c->st.py, c->st.pz, nt, c->t.box, 4294967296.0 / c->t.box, c->d_fixpos,
+      c->st.pos4);
+  CU(cudaGetLastError());
+  TRY(launch_search(c));
+  TRY(launch_heat_flux(c, enthalpy));
+  TRY(download_flux(c, jq));
+  c->state_valid = false;  // forces not evaluated: not an engine state
   return B2MD_OK;
 }
 

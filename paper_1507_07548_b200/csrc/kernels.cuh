@@ -770,6 +770,161 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
   finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
 }
 
+// ------------------------------------------------------------- heat flux
+// heat_flux (greenkubo.cpp:182-266), split by row instead of by pair: the
+// reference adds, per i<j pair with any site term inside rc,
+//   0.5 (f.v_i + g_ij.w_i + f.v_j - g_ji.w_j) R    and  u to pair_u[i], pair_u[j].
+// From row i's side the pair's force and torque on i are (f_i, g_i) and the
+// row's own vector R_i = min_image(com_i - com_j); from row j's side they are
+// (-f, -g_ji) with R_j = -R, so the pair term is the sum over both rows of
+//   0.5 (f_row.v_row + g_row.w_row) R_row
+// (the decomposition of the reference's own check, test_greenkubo.cpp:244-266).
+// Each row adds 0.5 (sum_p u_p) v_i + (e_kin_i - h_i) v_i; the kinetic part
+// only where `kinetic` is set (rank 0 of a sharded run: pair parts are
+// linear in the pairs, so shard partials sum to the whole).  Site terms use
+// the same orientation rules as k_force_multi; charges are plain Coulomb
+// (+ reaction field), never the Ewald real-space form (greenkubo.cpp:235-247).
+// METHOD: 0 LJ only, 1 Coulomb + reaction field, 2 plain Coulomb.
+struct FluxArgs {
+  ForceArgs f;
+  double enthalpy[kMaxSpecies];  // per species (by value: no upload)
+  double* out;             // R * kNumSums (jq in the first 3)
+  int kinetic;
+};
+
+template <int METHOD, bool OFFS, bool WRAPPED>
+__global__ void __launch_bounds__(kForceWarps * 32) k_heat_flux(FluxArgs fa) {
+  __shared__ int plist[kForceWarps][kQueue];
+  const ForceArgs& a = fa.f;
+  const SysDev& s = a.s;
+  const DevTables* __restrict__ tab = s.tab;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.y;
+  const size_t roff = size_t(r) * s.n;
+  const size_t soff = size_t(r) * s.total_sites;
+  const double4* __restrict__ p4 = a.st.pos4 + roff;
+  const double4* __restrict__ o4 = a.st.off + soff;
+  const MinImage mi = s.mi;
+  const float thr = a.thr;
+  auto mimg = [&](double d) {
+    return WRAPPED ? min_image_wrapped(d, mi.negL, thr) : min_image(d, mi);
+  };
+  const double rc2 = a.rc2;
+  double jx = 0, jy = 0, jz = 0;  // this warp's rows (lane 0)
+  const int wpb = blockDim.x >> 5;
+  for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
+    const double4 pi = p4[i];
+    const int si = s.species_of[i];
+    const int bi = s.site_begin[i];
+    const double vix = a.st.vx[roff + i], viy = a.st.vy[roff + i], viz = a.st.vz[roff + i];
+    const double wbx = a.st.wx[roff + i], wby = a.st.wy[roff + i], wbz = a.st.wz[roff + i];
+    const D3 wl = rotate_exact(a.st.qw[roff + i], a.st.qx[roff + i], a.st.qy[roff + i],
+                               a.st.qz[roff + i], {wbx, wby, wbz});
+    double tx = 0, ty = 0, tz = 0, up = 0;  // sum_p 0.5 s_p R_p, sum_p u_p
+    const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
+    for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
+      const bool lo = i < j;
+      const double4 pj = p4[j];
+      const double Rx = mimg(sub(pi.x, pj.x));
+      const double Ry = mimg(sub(pi.y, pj.y));
+      const double Rz = mimg(sub(pi.z, pj.z));
+      const int sj = s.species_of[j];
+      const int bj = s.site_begin[j];
+      const DevPairInfo pinfo = tab->pair[lo ? si * s.ns + sj : sj * s.ns + si];
+      double u = 0, fx = 0, fy = 0, fz = 0, gx = 0, gy = 0, gz = 0;
+      auto term = [&](double uu, double du_r, double inv_r2, double rx, double ry,
+                      double rz, double dix, double diy, double diz) {
+        u += uu;
+        const double fs = -du_r * inv_r2;
+        const double ex = fs * rx, ey = fs * ry, ez = fs * rz;
+        fx += ex;
+        fy += ey;
+        fz += ez;
+        gx += diy * ez - diz * ey;
+        gy += diz * ex - dix * ez;
+        gz += dix * ey - diy * ex;
+      };
+      auto site = [&](int ta, int tb, double& rx, double& ry, double& rz, double& dix,
+                      double& diy, double& diz) -> double {
+        if constexpr (!OFFS) {
+          dix = diy = diz = 0.0;
+          rx = Rx;
+          ry = Ry;
+          rz = Rz;
+        } else {
+          const int ki = bi + (lo ? ta : tb), kj = bj + (lo ? tb : ta);
+          const double4 di = o4[ki], dj = o4[kj];
+          dix = di.x;
+          diy = di.y;
+          diz = di.z;
+          if (lo) {
+            rx = sub(add(Rx, dix), dj.x);
+            ry = sub(add(Ry, diy), dj.y);
+            rz = sub(add(Rz, diz), dj.z);
+          } else {
+            rx = add(sub(Rx, dj.x), dix);
+            ry = add(sub(Ry, dj.y), diy);
+            rz = add(sub(Rz, dj.z), diz);
+          }
+        }
+        return norm2_exact(rx, ry, rz);
+      };
+      for (int q = 0; q < pinfo.lj_count; ++q) {
+        const DevLjTerm t = tab->lj[pinfo.lj_begin + q];
+        double rx, ry, rz, dix, diy, diz;
+        const double r2 = site(t.a, t.b, rx, ry, rz, dix, diy, diz);
+        if (r2 >= rc2) continue;
+        const double inv_r2 = rcp_nr(r2);
+        const double ir6 = inv_r2 * inv_r2 * inv_r2;
+        const double a12 = t.c12 * ir6 * ir6;
+        const double a6 = t.c6 * ir6;
+        term(a12 - a6, -12.0 * a12 + 6.0 * a6, inv_r2, rx, ry, rz, dix, diy, diz);
+      }
+      if constexpr (METHOD != 0) {
+        for (int q = 0; q < pinfo.qq_count; ++q) {
+          const DevQTerm t = tab->qq[pinfo.qq_begin + q];
+          double rx, ry, rz, dix, diy, diz;
+          const double r2 = site(t.a, t.b, rx, ry, rz, dix, diy, diz);
+          if (r2 >= rc2) continue;
+          const double inv_r2 = rcp_nr(r2);
+          const double uc = t.qq / sqrt(r2);
+          double uu = uc, du_r = -uc;
+          if constexpr (METHOD == 1) {
+            const double rf = t.qq * a.rf_r3inv * r2;
+            uu += rf + t.qq * a.rf_shift;
+            du_r += 2.0 * rf;
+          }
+          term(uu, du_r, inv_r2, rx, ry, rz, dix, diy, diz);
+        }
+      }
+      const double sp = 0.5 * (fx * vix + fy * viy + fz * viz + gx * wl.x + gy * wl.y + gz * wl.z);
+      tx += sp * Rx;
+      ty += sp * Ry;
+      tz += sp * Rz;
+      up += u;
+    });
+    tx = warp_sum(tx);
+    ty = warp_sum(ty);
+    tz = warp_sum(tz);
+    up = warp_sum(up);
+    if (lane == 0) {
+      double e = 0.5 * up;
+      if (fa.kinetic) {
+        const DevSpecies& sp = tab->species[si];
+        const double ek = 0.5 * sp.total_mass * (vix * vix + viy * viy + viz * viz) +
+                          0.5 * (sp.inertia[0] * wbx * wbx + sp.inertia[1] * wby * wby +
+                                 sp.inertia[2] * wbz * wbz);
+        e += ek - fa.enthalpy[si];
+      }
+      jx += tx + e * vix;
+      jy += ty + e * viy;
+      jz += tz + e * viz;
+    }
+  }
+  double v[3] = {jx, jy, jz};
+  finalize_scalars<3>(v, a.cta_part, a.ticket, fa.out, r, 0);
+}
+
 // ------------------------------------ single-species all-LJ rigid molecules
 // The general path of potentials.cpp:204-242 specialised to one species whose
 // site pairs are all LJ terms in the PairTable's (ia, ib) order

@@ -168,6 +168,14 @@ class ForceField:
     def pair_list(self) -> np.ndarray:
         return self._c.pair_list(0)
 
+    def heat_flux(self, state: SystemState, h_per_species) -> np.ndarray:
+        """tmd::heat_flux(comp, state, table, h_per_species) (src/greenkubo.cpp:182-266)
+        of `state` (positions as given) with this force field's pair table."""
+        n = self._c.n
+        return _heat_flux_state(self._c, _f64(state.pos, (n, 3)), _f64(state.orient, (n, 4)),
+                                _f64(state.vel, (n, 3)), _f64(state.ang_vel, (n, 3)),
+                                h_per_species)[0]
+
     def set_shard(self, rank: int, world: int) -> None:
         """Evaluate only `rank`'s shard of a `world`-way decomposition (partial
         results, no communicator) — b2md_set_shard."""
@@ -284,6 +292,17 @@ class Engine:
     def pair_list(self, replica: int = 0) -> np.ndarray:
         return self._c.pair_list(replica)
 
+    def heat_fluxes(self, h_per_species) -> np.ndarray:
+        """(replicas, 3) J_q of the device-resident state (what Engine::run
+        samples every n_ext steps, src/engine.cpp:235-238)."""
+        h = np.ascontiguousarray(h_per_species, dtype=np.float64).reshape(-1)
+        out = np.empty((self.replicas, 3))
+        check(_abi.lib().b2md_heat_flux(self._c.ctx, _abi.dptr(h), int(h.size), _abi.dptr(out)))
+        return out
+
+    def heat_flux(self, h_per_species) -> np.ndarray:
+        return self.heat_fluxes(h_per_species)[0]
+
     def attach_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
         check(_abi.lib().b2md_attach_nccl(self._c.ctx, unique_id, rank, world))
 
@@ -308,6 +327,20 @@ class Engine:
 
     def close(self) -> None:
         self._c.close()
+
+
+def _heat_flux_state(c: _Context, pos, orient, vel, ang_vel, h_per_species) -> np.ndarray:
+    h = np.ascontiguousarray(h_per_species, dtype=np.float64).reshape(-1)
+    out = np.empty((c.replicas, 3))
+    check(_abi.lib().b2md_heat_flux_state(c.ctx, _abi.dptr(pos), _abi.dptr(orient), _abi.dptr(vel),
+                                          _abi.dptr(ang_vel), _abi.dptr(h), int(h.size),
+                                          _abi.dptr(out)))
+    return out
+
+
+def heat_flux(ff: ForceField, state: SystemState, h_per_species) -> np.ndarray:
+    """Free-function form of tmd::heat_flux (include/tmd/greenkubo.hpp:93)."""
+    return ff.heat_flux(state, h_per_species)
 
 
 def nccl_unique_id() -> bytes:

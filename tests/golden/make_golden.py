@@ -66,6 +66,17 @@ def eval_vectors():
             pairs=ref.pair_list(st.pos), warning=np.array(ref.warning))
 
 
+def flux_vectors():
+    """tmd::heat_flux (src/greenkubo.cpp:182-266) on every eval case with
+    seeded velocities, angular velocities and enthalpies."""
+    for name, (comp, opts, st) in golden_cases.eval_cases().items():
+        vel, ang_vel, h = golden_cases.flux_inputs(name, comp)
+        ref = pyoracle.RefFF(comp, opts)
+        jq = ref.heat_flux(st.pos, st.orient, vel, ang_vel, h)
+        np.savez_compressed(OUT / f"flux_{name}.npz", pos=st.pos, orient=st.orient, vel=vel,
+                            ang_vel=ang_vel, h=h, jq=jq)
+
+
 def traj_vectors():
     for name, (comp, opts, st, dt, steps) in golden_cases.traj_cases().items():
         eng = pyoracle.RefEngine(comp, opts, dt, seed=1)
@@ -86,5 +97,6 @@ if __name__ == "__main__":
     rng_vectors()
     species_vectors()
     eval_vectors()
+    flux_vectors()
     traj_vectors()
     print("golden vectors written to", OUT)

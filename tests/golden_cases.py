@@ -96,3 +96,16 @@ def traj_cases():
         st.ang_vel[i] = (0.3 * rng.gaussian(), 0.3 * rng.gaussian(), 0.3 * rng.gaussian())
     cases["tri"] = (comp, opts, st, 0.0005, 40)
     return cases
+
+
+def flux_inputs(name, comp):
+    """Seeded velocities, angular velocities (body frame) and one enthalpy per
+    species for the heat-flux golden vectors (stored with them, so the seed
+    only fixes what make_golden.py writes)."""
+    seed = sum(name.encode()) * 7919
+    rng = np.random.default_rng(seed)
+    n = comp.molecule_count()
+    vel = rng.normal(size=(n, 3))
+    ang_vel = rng.normal(size=(n, 3))
+    h = rng.normal(size=comp.species_count()) * 2.0
+    return vel, ang_vel, h
