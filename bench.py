@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-flush", action="store_true")
+    p.add_argument("--op", default="step", choices=["step", "heat_flux"],
+                   help="step: Engine::step (the north_star path); heat_flux: tmd::heat_flux "
+                        "(SURVEY 8(f) row 1) of the set state")
     return p.parse_args()
 
 
@@ -179,6 +182,184 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+# heat_flux (greenkubo.cpp:182-266): fp64 work per visit of an in-cutoff
+# single-site pair from one row (each pair is visited from both rows):
+# min image 12, r^2 5, 1/r^2 5, LJ 9, force 5, 0.5 f.v 6, s R accumulate 6,
+# u 1, cutoff test 1  ("heat flux")
+FLUX_FLOP_PER_VISIT = 50
+FLUX_METRIC = "heat-flux J_q evaluations/s (tmd::heat_flux)"
+
+
+def flux_inputs(wl):
+    rng = np.random.default_rng(12345)
+    n = wl.comp.molecule_count() * wl.replicas
+    return rng.normal(size=(n, 3)), rng.normal(size=(n, 3)), rng.normal(size=len(wl.comp.species))
+
+
+def run_heat_flux_reference(args):
+    """tmd::heat_flux of the reference (oracle/_ref) on the host: it is serial
+    (greenkubo.cpp:196-257 has no worker split), one call per step."""
+    rank, _, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import pyoracle
+    if not pyoracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtmdref.so not built"}))
+        return
+    wl = workload(args.config, 0, 1)
+    value, k = cpu_reference_flux(wl, args.steps, 150.0)
+    line = {
+        "impl": "reference", "op": "heat_flux", "metric": FLUX_METRIC, "value": value,
+        "unit": "evals/s", "n_gpus": args.gpus, "steps": k, "warmup": 1, "ms_per_step": 1e3 / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, paper_1507_07548_b200/configs.py)",
+        "config": {"workload": f"{args.config}: {describe(wl)}"},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": 1, "kind": "reference",
+                         "sample": f"{k} tmd::heat_flux calls (serial in the reference)"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_reference_flux(wl, calls_wanted, budget_s):
+    from oracle import pyoracle
+    st = wl.states[0]
+    n = wl.comp.molecule_count()
+    vel, ang, h = flux_inputs(wl)
+    ff = pyoracle.RefFF(wl.comp, wl.opts)
+    t0 = time.perf_counter()
+    ff.heat_flux(st.pos, st.orient, vel[:n], ang[:n], h)
+    est = time.perf_counter() - t0
+    k = max(1, min(calls_wanted, int(budget_s / max(est, 1e-6))))
+    t0 = time.perf_counter()
+    for _ in range(k):
+        ff.heat_flux(st.pos, st.orient, vel[:n], ang[:n], h)
+    return k / (time.perf_counter() - t0), k
+
+
+def run_heat_flux(args):
+    """J_q of a device-resident state (b2md_heat_flux: what Engine::run samples
+    every n_ext steps), K calls each bracketed by CUDA events with an L2 flush
+    between; e2e through b2md_heat_flux_state with pinned host buffers."""
+    rank, world, local = dist_env()
+    import torch
+    import paper_1507_07548_b200 as b2
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = workload(args.config, rank, world)
+    R, n = wl.replicas, wl.comp.molecule_count()
+    eng = b2.Engine(wl.comp, wl.opts, wl.dt, device=local, replicas=R)
+    if world > 1 and args.config != "cfg4":
+        uid = [b2.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        eng.attach_nccl(uid[0], rank, world)
+    vel, ang, h = flux_inputs(wl)
+    states = wl.states
+    for r, s in enumerate(states):
+        s.vel, s.ang_vel = vel[r * n:(r + 1) * n], ang[r * n:(r + 1) * n]
+    eng.set_state(states)
+    _, stats = eng.energies()
+    pairs_total = int(sum(s.com_pairs for s in stats))
+    peak_gflops = b2.measure_fp64_peak(local)
+    stream = torch.cuda.ExternalStream(eng.stream(), device=local)
+    flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    for _ in range(max(3, args.warmup)):
+        eng.heat_fluxes(h)
+
+    def timed(k):
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        with torch.cuda.stream(stream):
+            for i in range(k):
+                starts[i].record(stream)
+                eng.heat_fluxes(h)
+                ends[i].record(stream)
+                if flush is not None:
+                    flush.zero_()
+        torch.cuda.synchronize()
+        return float(sum(a.elapsed_time(b) for a, b in zip(starts, ends)))
+
+    clocks = ClockSampler(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    total_ms = timed(args.steps)
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop()
+    if dist is not None:
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    eng.profile(True, 1)
+    timed(args.steps)
+    kt = eng.kernel_times()
+    eng.profile(False)
+    # e2e: the reference's free-function form from host buffers (state upload,
+    # site offsets, partner search, flux, 3 doubles back)
+    ff = b2.ForceField(wl.comp, wl.opts, device=local)
+    if world > 1 and args.config != "cfg4":
+        ff.set_shard(rank, world)  # partial per rank; the e2e time is what counts
+    hs = wl.states[0]
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    hs.pos, hs.orient, hs.vel, hs.ang_vel = map(pin, (hs.pos, hs.orient, hs.vel, hs.ang_vel))
+    ff.heat_flux(hs, h)
+    k_e2e = max(1, args.e2e_steps)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k_e2e):
+        ff.heat_flux(hs, h)
+    e2e_s = time.perf_counter() - t0
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    evals = args.steps * (R * world if args.config == "cfg4" else 1)
+    value = evals / (total_ms * 1e-3)
+    fl_ms, fl_n = kt.get("heat_flux", (0.0, 0))
+    avg_s = fl_ms * 1e-3 / max(1, fl_n)
+    achieved = 2 * pairs_total * FLUX_FLOP_PER_VISIT / avg_s / 1e12 if avg_s > 0 else 0.0
+    peak = peak_gflops / 1e3
+    line = {
+        "op": "heat_flux", "metric": FLUX_METRIC, "value": value, "unit": "evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak" if args.config == "cfg4" else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded generator; velocities N(0,1))",
+        "config": {"workload": f"{args.config}: {describe(wl)}",
+                   "l2": "flushed between timed calls (256 MiB memset outside the events)"
+                   if flush is not None else "not flushed",
+                   "timing": "per-call CUDA events on the library stream (kernel + 3-double readback)"},
+        "e2e": {"value": k_e2e * (R if args.config == "cfg4" else 1) / e2e_s, "unit": "evals/s",
+                "h2d_bytes_per_step": 8 * n * R * 13, "d2h_bytes_per_step": 8 * 3 * R,
+                "path": "b2md_heat_flux_state (upload, offsets, partner search, flux), pinned host buffers"},
+        "roofline": {"bound": "fp64", "kernel": f"k_heat_flux ({FLUX_FLOP_PER_VISIT} flop per pair visit, "
+                     "2 visits per in-cutoff pair; single-site count)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "launch_ms": avg_s * 1e3},
+        "kernel_ms_per_launch": {k: v[0] / max(1, v[1]) for k, v in kt.items()},
+        "gpu_launches": args.steps,
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            from oracle import pyoracle
+            if pyoracle.ref_available():
+                v, k = cpu_reference_flux(wl, 10 ** 6, args.cpu_seconds)
+                line["cpu_baseline"] = {"value": v, "unit": "evals/s", "cores": 1, "kind": "reference",
+                                        "sample": f"{k} tmd::heat_flux calls of {args.config} (serial)"}
+        except Exception as exc:
+            line["cpu_baseline"] = {"error": str(exc)}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def describe(wl):
     n = wl.comp.molecule_count()
     return (f"N={n} x {wl.replicas} replica(s), {len(wl.comp.species)} species, L={wl.comp.box_length:.6f}, "
@@ -187,6 +368,9 @@ def describe(wl):
 
 def main():
     args = parse()
+    if args.op == "heat_flux":
+        (run_heat_flux_reference if args.impl == "reference" else run_heat_flux)(args)
+        return
     if args.impl == "reference":
         run_reference_arm(args)
         return

@@ -449,25 +449,34 @@ int launch_heat_flux(b2md_ctx* c, const double* enthalpy) {
   a.kinetic = c->rank == 0 ? 1 : 0;
   const bool w = fast_min_image(c);
   const bool offs = c->t.any_offsets;
+  const bool one = c->t.ns == 1;
   dim3 grid(c->force_grid, c->R);
   const int bs = c->force_warps * 32;
   const int m = c->t.method == B2MD_METHOD_EWALD ? 2 : (c->t.method == B2MD_METHOD_REACTION_FIELD ? 1 : 0);
-#define FLUX_CASE(M)                                                                        \
-  case M:                                                                                   \
-    if (offs && w)                                                                          \
-      PROF(c, F_HEAT_FLUX, (k_heat_flux<M, true, true><<<grid, bs, 0, c->stream>>>(a)));    \
-    else if (offs)                                                                          \
-      PROF(c, F_HEAT_FLUX, (k_heat_flux<M, true, false><<<grid, bs, 0, c->stream>>>(a)));   \
-    else if (w)                                                                             \
-      PROF(c, F_HEAT_FLUX, (k_heat_flux<M, false, true><<<grid, bs, 0, c->stream>>>(a)));   \
-    else                                                                                    \
-      PROF(c, F_HEAT_FLUX, (k_heat_flux<M, false, false><<<grid, bs, 0, c->stream>>>(a)));  \
+#define FLUX_K(M, O, W)                                                                       \
+  do {                                                                                        \
+    if (one)                                                                                  \
+      PROF(c, F_HEAT_FLUX, (k_heat_flux<M, O, W, true><<<grid, bs, 0, c->stream>>>(a)));      \
+    else                                                                                      \
+      PROF(c, F_HEAT_FLUX, (k_heat_flux<M, O, W, false><<<grid, bs, 0, c->stream>>>(a)));     \
+  } while (0)
+#define FLUX_CASE(M)                  \
+  case M:                             \
+    if (offs && w)                    \
+      FLUX_K(M, true, true);          \
+    else if (offs)                    \
+      FLUX_K(M, true, false);         \
+    else if (w)                       \
+      FLUX_K(M, false, true);         \
+    else                              \
+      FLUX_K(M, false, false);        \
     break;
   switch (m) {
     FLUX_CASE(0)
     FLUX_CASE(1)
     FLUX_CASE(2)
   }
+#undef FLUX_K
 #undef FLUX_CASE
   if (c->world > 1 && c->comm)
     NC(ncclAllReduce(c->d_flux, c->d_flux, size_t(kNumSums) * c->R, ncclDouble, ncclSum, c->comm,

@@ -792,8 +792,10 @@ struct FluxArgs {
   int kinetic;
 };
 
-template <int METHOD, bool OFFS, bool WRAPPED>
-__global__ void __launch_bounds__(kForceWarps * 32) k_heat_flux(FluxArgs fa) {
+// ONE_SPECIES: the pair's term list and site numbering are row-invariant
+// (species 0 throughout; molecule j's sites start at j * n_sites).
+template <int METHOD, bool OFFS, bool WRAPPED, bool ONE_SPECIES>
+__global__ void __launch_bounds__(kForceWarps * 32, OFFS ? 2 : 4) k_heat_flux(FluxArgs fa) {
   __shared__ int plist[kForceWarps][kQueue];
   const ForceArgs& a = fa.f;
   const SysDev& s = a.s;
@@ -812,14 +814,17 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_heat_flux(FluxArgs fa) {
   const double rc2 = a.rc2;
   double jx = 0, jy = 0, jz = 0;  // this warp's rows (lane 0)
   const int wpb = blockDim.x >> 5;
+  const int nsite0 = tab->species[0].n_sites;
+  const DevPairInfo pinfo0 = tab->pair[0];
   for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
     const double4 pi = p4[i];
-    const int si = s.species_of[i];
-    const int bi = s.site_begin[i];
+    const int si = ONE_SPECIES ? 0 : s.species_of[i];
+    const int bi = ONE_SPECIES ? i * nsite0 : s.site_begin[i];
     const double vix = a.st.vx[roff + i], viy = a.st.vy[roff + i], viz = a.st.vz[roff + i];
-    const double wbx = a.st.wx[roff + i], wby = a.st.wy[roff + i], wbz = a.st.wz[roff + i];
-    const D3 wl = rotate_exact(a.st.qw[roff + i], a.st.qx[roff + i], a.st.qy[roff + i],
-                               a.st.qz[roff + i], {wbx, wby, wbz});
+    D3 wl{0.0, 0.0, 0.0};  // lab-frame angular velocity (only torques use it)
+    if constexpr (OFFS)
+      wl = rotate_exact(a.st.qw[roff + i], a.st.qx[roff + i], a.st.qy[roff + i], a.st.qz[roff + i],
+                        {a.st.wx[roff + i], a.st.wy[roff + i], a.st.wz[roff + i]});
     double tx = 0, ty = 0, tz = 0, up = 0;  // sum_p 0.5 s_p R_p, sum_p u_p
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
     for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
@@ -828,9 +833,16 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_heat_flux(FluxArgs fa) {
       const double Rx = mimg(sub(pi.x, pj.x));
       const double Ry = mimg(sub(pi.y, pj.y));
       const double Rz = mimg(sub(pi.z, pj.z));
-      const int sj = s.species_of[j];
-      const int bj = s.site_begin[j];
-      const DevPairInfo pinfo = tab->pair[lo ? si * s.ns + sj : sj * s.ns + si];
+      int bj;
+      DevPairInfo pinfo;
+      if constexpr (ONE_SPECIES) {
+        bj = j * nsite0;
+        pinfo = pinfo0;
+      } else {
+        const int sj = s.species_of[j];
+        bj = s.site_begin[j];
+        pinfo = tab->pair[lo ? si * s.ns + sj : sj * s.ns + si];
+      }
       double u = 0, fx = 0, fy = 0, fz = 0, gx = 0, gy = 0, gz = 0;
       auto term = [&](double uu, double du_r, double inv_r2, double rx, double ry,
                       double rz, double dix, double diy, double diz) {
@@ -840,9 +852,11 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_heat_flux(FluxArgs fa) {
         fx += ex;
         fy += ey;
         fz += ez;
-        gx += diy * ez - diz * ey;
-        gy += diz * ex - dix * ez;
-        gz += dix * ey - diy * ex;
+        if constexpr (OFFS) {  // centred sites: no torque
+          gx += diy * ez - diz * ey;
+          gy += diz * ex - dix * ez;
+          gz += dix * ey - diy * ex;
+        }
       };
       auto site = [&](int ta, int tb, double& rx, double& ry, double& rz, double& dix,
                       double& diy, double& diz) -> double {
@@ -869,16 +883,29 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_heat_flux(FluxArgs fa) {
         }
         return norm2_exact(rx, ry, rz);
       };
-      for (int q = 0; q < pinfo.lj_count; ++q) {
-        const DevLjTerm t = tab->lj[pinfo.lj_begin + q];
-        double rx, ry, rz, dix, diy, diz;
-        const double r2 = site(t.a, t.b, rx, ry, rz, dix, diy, diz);
-        if (r2 >= rc2) continue;
-        const double inv_r2 = rcp_nr(r2);
-        const double ir6 = inv_r2 * inv_r2 * inv_r2;
-        const double a12 = t.c12 * ir6 * ir6;
-        const double a6 = t.c6 * ir6;
-        term(a12 - a6, -12.0 * a12 + 6.0 * a6, inv_r2, rx, ry, rz, dix, diy, diz);
+      if constexpr (ONE_SPECIES && !OFFS && METHOD == 0) {
+        // one centred site: at most one LJ term, its coefficients in a.c12 /
+        // a.c6 (zero when the table has none)
+        const double r2 = norm2_exact(Rx, Ry, Rz);
+        if (r2 < rc2) {
+          const double inv_r2 = rcp_nr(r2);
+          const double ir6 = inv_r2 * inv_r2 * inv_r2;
+          const double a12 = a.c12 * ir6 * ir6;
+          const double a6 = a.c6 * ir6;
+          term(a12 - a6, -12.0 * a12 + 6.0 * a6, inv_r2, Rx, Ry, Rz, 0.0, 0.0, 0.0);
+        }
+      } else {
+        for (int q = 0; q < pinfo.lj_count; ++q) {
+          const DevLjTerm t = tab->lj[pinfo.lj_begin + q];
+          double rx, ry, rz, dix, diy, diz;
+          const double r2 = site(t.a, t.b, rx, ry, rz, dix, diy, diz);
+          if (r2 >= rc2) continue;
+          const double inv_r2 = rcp_nr(r2);
+          const double ir6 = inv_r2 * inv_r2 * inv_r2;
+          const double a12 = t.c12 * ir6 * ir6;
+          const double a6 = t.c6 * ir6;
+          term(a12 - a6, -12.0 * a12 + 6.0 * a6, inv_r2, rx, ry, rz, dix, diy, diz);
+        }
       }
       if constexpr (METHOD != 0) {
         for (int q = 0; q < pinfo.qq_count; ++q) {
@@ -897,7 +924,8 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_heat_flux(FluxArgs fa) {
           term(uu, du_r, inv_r2, rx, ry, rz, dix, diy, diz);
         }
       }
-      const double sp = 0.5 * (fx * vix + fy * viy + fz * viz + gx * wl.x + gy * wl.y + gz * wl.z);
+      const double sp = OFFS ? 0.5 * (fx * vix + fy * viy + fz * viz + gx * wl.x + gy * wl.y + gz * wl.z)
+                             : 0.5 * (fx * vix + fy * viy + fz * viz);
       tx += sp * Rx;
       ty += sp * Ry;
       tz += sp * Rz;
@@ -911,6 +939,7 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_heat_flux(FluxArgs fa) {
       double e = 0.5 * up;
       if (fa.kinetic) {
         const DevSpecies& sp = tab->species[si];
+        const double wbx = a.st.wx[roff + i], wby = a.st.wy[roff + i], wbz = a.st.wz[roff + i];
         const double ek = 0.5 * sp.total_mass * (vix * vix + viy * viy + viz * viz) +
                           0.5 * (sp.inertia[0] * wbx * wbx + sp.inertia[1] * wby * wby +
                                  sp.inertia[2] * wbz * wbz);
