@@ -360,6 +360,32 @@ def run_heat_flux(args):
         dist.destroy_process_group()
 
 
+def tile_cull_kept_fraction(eng, wl):
+    """Fraction of the upper-triangle 32x32 tiles the search's bounding-arc
+    cull keeps on the final state (the arithmetic of k_search's arcs)."""
+    L = wl.comp.box_length
+    pos = eng.state().pos % L
+    n = len(pos)
+    u = np.floor(pos * (2.0 ** 32 / L) + 0.5).astype(np.int64) % (1 << 32)
+    nb = (n + 31) // 32
+    pad = np.zeros((nb * 32, 3), dtype=np.int64)
+    pad[:n] = u
+    blk = pad.reshape(nb, 32, 3)
+    off = ((blk - blk[:, :1, :] + (1 << 31)) % (1 << 32)) - (1 << 31)
+    mn, mx = off.min(1), off.max(1)
+    c = (blk[:, 0, :] + (mn + mx) // 2) % (1 << 32)
+    h = (mx - mn + 1) // 2 + 1
+    rmax = wl.opts.cutoff + 2 * max(sp.max_extent for sp in wl.comp.species)
+    ru = rmax * 2.0 ** 32 / L
+    kept, total = 0, 0
+    for b in range(nb):
+        d = np.abs(((c[b] - c[b:] + (1 << 31)) % (1 << 32)) - (1 << 31))
+        g = np.maximum(d - h[b] - h[b:] - 2, 0).astype(float)
+        kept += int(((g * g).sum(-1) <= ru * ru * (1 + 1e-6)).sum())
+        total += nb - b
+    return kept / total
+
+
 def describe(wl):
     n = wl.comp.molecule_count()
     return (f"N={n} x {wl.replicas} replica(s), {len(wl.comp.species)} species, L={wl.comp.box_length:.6f}, "
@@ -444,8 +470,12 @@ def main():
     # the per-kernel breakdown and launch counts.  Event-record nodes stall the
     # graph pipeline, so they are kept out of the headline region.
     eng.profile(True, 2)
-    prof_ms = timed_pass(args.steps, flush)
+    timed_pass(args.steps, flush)
     kt_search = eng.kernel_times()
+    eng.profile(False)
+    eng.profile(True, 3)
+    timed_pass(args.steps, flush)
+    kt_force = eng.kernel_times()
     eng.profile(False)
     n_all = min(args.steps, 50)
     eng.profile(True, 1)
@@ -490,24 +520,37 @@ def main():
     value = replica_steps / (total_ms * 1e-3)
     e2e_value = e2e_steps * (R * world if args.config == "cfg4" else 1) / e2e_s
 
-    # ---- roofline of the dominant kernel (partner search: fp64 CUDA cores)
-    search_ms, search_launches = kt_search.get("search", (0.0, 0))
-    cand = n * (n - 1) // 2 * R
-    if world > 1 and args.config != "cfg4":
-        cand_rank = b2.shard_plan(n, b2.kvector_count(wl.opts.ewald.kmax) if wl.opts.ewald else 0,
-                                  world, rank)["candidate_pairs"]
-    else:
-        cand_rank = cand
-    avg_search_s = search_ms * 1e-3 / max(1, search_launches)
-    achieved = cand_rank * FLOP_CANDIDATE / avg_search_s / 1e12 if avg_search_s > 0 else 0.0
+    # ---- roofline of the dominant kernel: the force walk (fp64 CUDA cores).
+    # Algorithmic work: 32 flop per single-site LJ pair in
+    # cutoff; multi-site: 86 per LJ term, counted as if every term of a passing
+    # molecule pair were inside rc (an upper bound).
     peak = peak_gflops / 1e3
+    force_ms, force_launches = kt_force.get("force", (0.0, 0))
+    avg_force_s = force_ms * 1e-3 / max(1, force_launches)
+    single_site = all(sp.n_sites == 1 for sp in wl.comp.species)
+    if single_site:
+        force_flop = pairs_total * FLOP_LJ_SINGLE
+        force_note = f"{FLOP_LJ_SINGLE} flop per single-site LJ pair in cutoff"
+    else:
+        terms = max(sp.n_sites for sp in wl.comp.species) ** 2
+        force_flop = pairs_total * (2 + 86 * terms)
+        force_note = f"(2 + 86 x {terms} terms) flop per passing molecule pair (upper bound)"
+    achieved = force_flop / avg_force_s / 1e12 if avg_force_s > 0 else 0.0
     traffic = None
-    prof = ROOT / "profiles" / f"ncu_{args.config}_search.json"
+    prof = ROOT / "profiles" / f"ncu_{args.config}_force.json"
     if prof.exists():
         try:
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    # partner search: share of the step and the tiles the bounding-arc cull kept
+    search_ms, search_launches = kt_search.get("search", (0.0, 0))
+    avg_search_s = search_ms * 1e-3 / max(1, search_launches)
+    cand = n * (n - 1) // 2 * R
+    kept = tile_cull_kept_fraction(eng, wl) if single_site and R == 1 else None
+    step_s = total_ms * 1e-3 / args.steps
+    fp64_step = ((cand * FLOP_CANDIDATE + pairs_total * FLOP_LJ_SINGLE) / step_s / 1e12 / peak
+                 if single_site and world == 1 else None)
     step_kernels = sum(c for name, (ms, c) in kt.items() if name != "allreduce")
 
     line = {
@@ -539,18 +582,29 @@ def main():
                 "path": "b2md_upload_state + b2md_step + b2md_get_state, pinned host buffers"},
         "roofline": {
             "bound": "fp64",
-            "kernel": "k_search (COM partner search, 17 flop/candidate)",
+            "kernel": f"k_force_* partner walk ({force_note})",
             "achieved": achieved,
             "peak": peak,
             "unit": "TFLOP/s",
             "frac": achieved / peak if peak else None,
             "traffic": traffic,
             "peak_source": "DFMA microbenchmark measured in this run (MEASURED_PEAKS.json has no fp64 entry)",
-            "launch_ms": avg_search_s * 1e3,
-            "share_of_step": avg_search_s * 1e3 / max(1e-9, total_ms / args.steps),
-            "launch_timing": "CUDA events around k_search in a second K-step pass (same step "
-                             "structure); ncu launch list in profiles/ for the shares",
+            "launch_ms": avg_force_s * 1e3,
+            "share_of_step": avg_force_s / max(1e-12, step_s),
+            "launch_timing": "CUDA events around the force kernel only, in a second K-step pass "
+                             "(same graph step structure); ncu launch list in profiles/",
         },
+        "search": {
+            "launch_ms": avg_search_s * 1e3,
+            "share_of_step": avg_search_s / max(1e-12, step_s),
+            "candidates": cand,
+            "tile_cull_kept_fraction": kept,
+            "note": "32x32 tiles whose blocks' bounding arcs are > rmax apart are skipped (exact)",
+        },
+        "fp64_fraction_step": fp64_step,
+        "fp64_fraction_step_def": "(all n(n-1)/2 candidates x 17 + pairs in cutoff x 32) flop per "
+                                  "step / device step time / fp64 peak (SURVEY.md 8(d) convention; "
+                                  "culled candidates count as work the reference does)",
         "kernel_ms_per_launch": {k: v[0] / max(1, v[1]) for k, v in kt.items()},
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "clocks": clk,

@@ -203,6 +203,13 @@ int b2md_get_state(b2md_ctx* ctx, double* pos, double* orient, double* vel, doub
 int b2md_pair_list(b2md_ctx* ctx, int replica, int32_t* pairs, int64_t capacity,
                    int64_t* n_pairs);
 
+/* Partner-search strategy (results are identical; for tests and
+ * measurement).  fix_prefilter: the certified fixed-point prefilter of the
+ * single-species path (else the exact fp64 test on every candidate);
+ * tile_cull: skip 32x32 tiles whose molecule blocks' bounding arcs are
+ * further apart than the COM radius (fixed-point path only).  Both default 1. */
+int b2md_set_search_options(b2md_ctx* ctx, int fix_prefilter, int tile_cull);
+
 /* Green-Kubo heat flux J_q (tmd::heat_flux, include/tmd/greenkubo.hpp:93,
  * src/greenkubo.cpp:182-266) of the context's current device state: the
  * state set_state / step left (Engine::run samples it every n_ext steps,
@@ -240,8 +247,8 @@ void* b2md_stream(b2md_ctx* ctx);
 
 /* Per-kernel CUDA-event timing of the device step (bench instrumentation).
  * enable = 1 records an event pair around every launch of each kernel
- * family, enable = 2 only around the partner search (the dominant kernel;
- * least perturbation); 0 turns it off.  Single steps run as a CUDA graph whose
+ * family, enable = 2 only around the partner search, enable = 3 only around
+ * the force walk (one family at a time: least perturbation); 0 turns it off.  Single steps run as a CUDA graph whose
  * event-record nodes are re-pointed at fresh events before every launch.
  * b2md_kernel_times returns {name, total_ms, launches} rows. */
 int b2md_profile_enable(b2md_ctx* ctx, int enable);

@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -118,7 +119,7 @@ struct b2md_ctx {
   double* d_cta_part = nullptr;  // force-kernel per-CTA scalar partials
   unsigned* d_ticket = nullptr;   // 2 * R: force, ewald
   int force_grid = 1;
-  int force_warps = 8;
+  int force_warps = kForceWarps;  // warps per CTA of the partner walks
   uint32_t* d_super = nullptr;
   int n_super_tiles = 0;
   int* d_error = nullptr;
@@ -142,6 +143,7 @@ struct b2md_ctx {
   // graphs
   bool use_graphs = true;
   bool use_fix_prefilter = true;
+  bool use_tile_cull = true;
   cudaGraphExec_t step_graph = nullptr;  // forces + fused kick/kick-drift
   cudaGraphExec_t single_graph = nullptr;  // one whole step
   cudaGraphExec_t prof_graph = nullptr;    // one whole step with event-record nodes
@@ -152,7 +154,7 @@ struct b2md_ctx {
   std::vector<cudaGraphNode_t> cap_nodes;   // the event-record node of each placeholder
   // profiling
   bool profile = false;
-  int profile_level = 1;   // 1: every kernel family, 2: the partner search only
+  int profile_level = 1;   // 1: every kernel family, 2: the partner search only, 3: the force walk only
   bool prof_open = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
   size_t ev_used = 0;
@@ -189,7 +191,8 @@ void set_wrapped(b2md_ctx* c, bool w) {
 }
 
 bool prof_on(const b2md_ctx* c, int fam) {
-  return c->profile && (c->profile_level == 1 || fam == F_SEARCH);
+  return c->profile && (c->profile_level == 1 || (c->profile_level == 2 && fam == F_SEARCH) ||
+                        (c->profile_level == 3 && fam == F_FORCE));
 }
 
 int prof_begin(b2md_ctx* c, int fam) {
@@ -290,6 +293,9 @@ int launch_search(b2md_ctx* c) {
     a.fix_lo32 = lo32 > 0.0 ? uint32_t(lo32) : 0u;
     a.fix_w32 = 17u;
     if (!(r2_32 + 64.0 < two32) || lo32 <= 0.0) a.fix_ok = 0;
+    a.cull = a.fix_ok && c->use_tile_cull ? 1 : 0;
+    const double ru = rmax * two32 / L;
+    a.cull_r2 = ru * ru * (1.0 + 1e-6);
   }
   dim3 grid(c->n_super_tiles, c->R);
   const int st = c->g.st;
@@ -749,6 +755,16 @@ int setup_shard(b2md_ctx* c) {
   const int s0 = c->row_begin / c->g.st, s1 = (c->row_end + c->g.st - 1) / c->g.st;
   for (int si = s0; si < s1; ++si)
     for (int sj = si; sj < c->g.n_super; ++sj) list.push_back((uint32_t(si) << 16) | uint32_t(sj));
+  // heaviest first: with spatially ordered molecules the tiles that survive
+  // culling sit near the (periodic) diagonal; launching them first shortens
+  // the tail.  The order does not affect results.
+  const int ns = c->g.n_super;
+  auto band = [ns](uint32_t code) {
+    const int d = int(code & 0xffffu) - int(code >> 16);
+    return std::min(d, ns - d);
+  };
+  std::stable_sort(list.begin(), list.end(),
+                   [&](uint32_t x, uint32_t y) { return band(x) < band(y); });
   if (c->d_super) cudaFree(c->d_super);
   c->d_super = nullptr;
   TRY(dalloc(&c->d_super, list.size()));
@@ -840,6 +856,10 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const int rows_grid = (t.n + kForceWarps - 1) / kForceWarps;
     c->force_grid = std::max(1, std::min(rows_grid, sms * 4));
+    // tuning knobs (measurement only): warps per CTA, CTAs per replica
+    if (const char* e = std::getenv("B2MD_FORCE_WARPS"))
+      c->force_warps = std::max(1, std::min(kForceWarps, std::atoi(e)));
+    if (const char* e = std::getenv("B2MD_FORCE_GRID")) c->force_grid = std::max(1, std::atoi(e));
   }
   TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars * c->force_grid));
   TRY(dalloc(&c->d_ticket, size_t(2) * R));
@@ -1118,6 +1138,14 @@ int b2md_get_state(b2md_ctx* c, double* pos, double* orient, double* vel, double
   if (torque) TRY(download_aos(c, 5, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
   TRY(download_scalars(c, energy, stats));
   CU(cudaStreamSynchronize(c->stream));
+  return B2MD_OK;
+}
+
+int b2md_set_search_options(b2md_ctx* c, int fix_prefilter, int tile_cull) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "set_search_options: null context");
+  c->use_fix_prefilter = fix_prefilter != 0;
+  c->use_tile_cull = tile_cull != 0;
+  drop_graphs(c);  // launch arguments are baked into the graphs
   return B2MD_OK;
 }
 

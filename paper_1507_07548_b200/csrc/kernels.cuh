@@ -82,6 +82,10 @@ struct SearchArgs {
   double fix_scale;  // 2^32 / L
   uint32_t fix_lo, fix_width;  // 15-bit test (units (L/32768)^2)
   uint32_t fix_lo32, fix_w32;  // 32-bit refinement (units L^2/2^32)
+  // tile culling (fixed-point path): skip a 32x32 tile when the bounding arcs
+  // of its two molecule blocks are further apart than rmax
+  int cull;
+  double cull_r2;  // (rmax 2^32 / L)^2 (1 + 1e-6), fixed-point units squared
 };
 
 // Branch-free minimum image for |d| < L (both positions wrapped to [0, L)),
@@ -165,17 +169,19 @@ __device__ __forceinline__ bool refine_pair(uint4 pi, uint4 pj, int ig, int jg,
 
 // 32 i-rows (local tile row at `ib`) x JB column tiles c0.. : U words (row
 // ib+ii, columns c0..) to wu, L words to wl.
+// Column tiles c0 and (JB == 2) c1, not necessarily adjacent.
 template <int JB, bool DIAG, bool PARTIAL_I>
 __device__ __forceinline__ void search_tile_fix(
     const uint4* __restrict__ siu, const uint4* __restrict__ sju,
     const double* __restrict__ gx, const double* __restrict__ gy, const double* __restrict__ gz,
-    int ig0, int jg0, int ib, int c0, int I, int lane, int ST, int ilim, int jlim, int neglo,
-    int width, const FixRefine& f, const MinImage& mi, uint32_t* wu, uint32_t* wl) {
+    int ig0, int jg0, int ib, int c0, int c1, int I, int lane, int ST, int ilim, int jlim,
+    int neglo, int width, const FixRefine& f, const MinImage& mi, uint32_t* wu, uint32_t* wl) {
   uint32_t xj[JB], yj[JB], zj[JB], lw[JB], bw[JB];
   int nl[JB];
+  auto col = [&](int b) { return b == 0 ? c0 : c1; };
 #pragma unroll
   for (int b = 0; b < JB; ++b) {
-    const int jl = (c0 + b) * 32 + lane;
+    const int jl = col(b) * 32 + lane;
     const uint4 pj = sju[jl];
     xj[b] = pj.x;
     yj[b] = pj.y;
@@ -207,7 +213,7 @@ __device__ __forceinline__ void search_tile_fix(
     // rare: band members are decided exactly, lane by lane (no collectives)
     uint32_t band = bw[b] & ~lw[b] & m;
     if (band) {
-      const int jl = (c0 + b) * 32 + lane;
+      const int jl = col(b) * 32 + lane;
       const uint4 pj = sju[jl];
       while (band) {
         const int ii = __ffs(band) - 1;
@@ -219,9 +225,36 @@ __device__ __forceinline__ void search_tile_fix(
   }
 #pragma unroll
   for (int b = 0; b < JB; ++b) {
-    wl[((c0 + b) * 32 + lane) * ST + I] = lw[b];
-    wu[(ib + lane) * ST + c0 + b] = warp_transpose32(lw[b], lane);
+    wl[(col(b) * 32 + lane) * ST + I] = lw[b];
+    wu[(ib + lane) * ST + col(b)] = warp_transpose32(lw[b], lane);
   }
+}
+
+// Bounding arc of 32 fixed-point coordinates on the periodic axis (2^32 =
+// L): anchored at lane 0, the wrapping int32 offsets of all lanes lie in
+// [mn, mx], so every point is within h of the centre c.  Valid for any
+// spread (a block spanning the box gets an arc of ~the whole circle).
+__device__ __forceinline__ void bounding_arc(uint32_t u, uint32_t& c, uint32_t& h) {
+  const uint32_t anchor = __shfl_sync(0xffffffffu, u, 0);
+  const int off = int(u - anchor);
+  const int mn = __reduce_min_sync(0xffffffffu, off);
+  const int mx = __reduce_max_sync(0xffffffffu, off);
+  c = anchor + uint32_t(int((static_cast<long long>(mn) + mx) >> 1));
+  h = uint32_t((static_cast<long long>(mx) - mn + 1) >> 1) + 1u;
+}
+
+// Conservative "no pair of these two blocks is within rmax": per axis the
+// circular gap between the arcs, less 2 units for the rounding of u.
+__device__ __forceinline__ bool tiles_apart(uint4 ca, uint4 ha, uint4 cb, uint4 hb, double lim) {
+  auto gap = [](uint32_t x, uint32_t y, uint32_t hx, uint32_t hy) {
+    const long long d = llabs(static_cast<long long>(int(x - y)));
+    const long long g = d - static_cast<long long>(hx) - static_cast<long long>(hy) - 2;
+    return g > 0 ? double(g) : 0.0;
+  };
+  const double gx = gap(ca.x, cb.x, ha.x, hb.x);
+  const double gy = gap(ca.y, cb.y, ha.y, hb.y);
+  const double gz = gap(ca.z, cb.z, ha.z, hb.z);
+  return gx * gx + gy * gy + gz * gz > lim;
 }
 
 // One CTA = one super-tile (SI, SJ), SI <= SJ, of ST x ST 32-molecule tiles;
@@ -240,6 +273,7 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
   __shared__ double rmax2_s[MULTI ? kMaxSpecies * kMaxSpecies : 1];
   __shared__ __align__(16) uint32_t wu[T * ST];
   __shared__ __align__(16) uint32_t wl[T * ST];
+  __shared__ uint4 arc_c[2 * ST], arc_h[2 * ST];  // i tiles [0, ST), j tiles [ST, 2 ST)
 
   const SysDev& s = a.s;
   const int r = blockIdx.y;
@@ -291,31 +325,92 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
     refine.lo32 = a.fix_lo32;
     refine.w32 = a.fix_w32;
     refine.rc2 = a.rc2;
-    if (!diag && ilim >= 32) {
-      // hot path: uniform, compile-time trip count (no divergence emulation
-      // around the ballots)
-#pragma unroll 1
-      for (int c = 0; c < ST; c += (ST >= 2 ? 2 : 1)) {
-        if constexpr (ST >= 2)
-          search_tile_fix<2, false, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, I,
-                                           lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
-        else
-          search_tile_fix<1, false, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, I,
-                                           lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
+    // tiles kept after culling: bit c = column tile c of this warp's tile row
+    uint32_t keep = (1u << ST) - 1u;
+    if (a.cull) {
+      {
+        const uint4 p = ui[ib + lane];
+        uint4 c, h;
+        bounding_arc(p.x, c.x, h.x);
+        bounding_arc(p.y, c.y, h.y);
+        bounding_arc(p.z, c.z, h.z);
+        const uint4 q = uj[ib + lane];
+        uint4 cj, hj;
+        bounding_arc(q.x, cj.x, hj.x);
+        bounding_arc(q.y, cj.y, hj.y);
+        bounding_arc(q.z, cj.z, hj.z);
+        if (lane == 0) {
+          arc_c[I] = c;
+          arc_h[I] = h;
+          arc_c[ST + I] = cj;
+          arc_h[ST + I] = hj;
+        }
       }
-    } else if (ilim >= 32) {
-      search_tile_fix<1, true, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, I, I, lane,
+      __syncthreads();
+      uint32_t k = 0;
+      for (int c = 0; c < ST; ++c) {
+        if (!tiles_apart(arc_c[I], arc_h[I], arc_c[ST + c], arc_h[ST + c], a.cull_r2)) {
+          k |= 1u << c;
+        } else {  // no pairs: zero words (the non-diagonal path does not pre-zero)
+          wu[(ib + lane) * ST + c] = 0u;
+          wl[(c * 32 + lane) * ST + I] = 0u;
+        }
+      }
+      keep = __shfl_sync(0xffffffffu, k, 0);
+    }
+    if (!diag && n - ibase >= T) {
+      // hot path (all ST tile rows full): each tile row's kept column tiles
+      // are paired into jobs and the CTA's jobs are dealt to the warps
+      // round-robin, so culling leaves no warp idle at the final barrier.
+      // A tile's words have fixed places in wu / wl: any warp may do it.
+      __shared__ int njob_s[ST];
+      __shared__ uint32_t jobs[ST * ((ST + 1) / 2)];
+      const int nj = (__popc(keep) + 1) >> 1;
+      if (lane == 0) njob_s[I] = nj;
+      __syncthreads();
+      int base = 0, total = 0;
+      for (int w = 0; w < ST; ++w) {
+        base += w < I ? njob_s[w] : 0;
+        total += njob_s[w];
+      }
+      if (lane == 0) {
+        uint32_t k = keep;
+        for (int q = 0; q < nj; ++q) {
+          const uint32_t c0 = __ffs(k) - 1;
+          k &= k - 1u;
+          const uint32_t c1 = k ? uint32_t(__ffs(k) - 1) : 0xffu;
+          if (k) k &= k - 1u;
+          jobs[base + q] = (uint32_t(I) << 16) | (c0 << 8) | c1;
+        }
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int q = warp; q < total; q += ST) {
+        const uint32_t jb = jobs[q];
+        const int Iq = int(jb >> 16), c0 = int((jb >> 8) & 0xffu), c1 = int(jb & 0xffu);
+        if (ST >= 2 && c1 != 0xff)
+          search_tile_fix<(ST >= 2 ? 2 : 1), false, false>(ui, uj, gx, gy, gz, ibase, jbase,
+                                                           Iq * 32, c0, c1, Iq, lane, ST, 32,
+                                                           jlim, neglo, wd, refine, s.mi, wu, wl);
+        else
+          search_tile_fix<1, false, false>(ui, uj, gx, gy, gz, ibase, jbase, Iq * 32, c0, c0,
+                                           Iq, lane, ST, 32, jlim, neglo, wd, refine, s.mi, wu,
+                                           wl);
+      }
+    } else if (diag && ilim >= 32) {
+      search_tile_fix<1, true, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, I, I, I, lane,
                                       ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
       for (int c = I + 1; c < ST; ++c)
-        search_tile_fix<1, false, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, I,
-                                         lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
-    } else {  // last, partial tile row
+        if (keep >> c & 1u)
+          search_tile_fix<1, false, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, c, I,
+                                           lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
+    } else {  // last, partial tile row (arcs include the padding: conservative)
       for (int c = diag ? I : 0; c < ST; ++c) {
         if (diag && c == I)
-          search_tile_fix<1, true, true>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, I,
+          search_tile_fix<1, true, true>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, c, I,
                                          lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
-        else
-          search_tile_fix<1, false, true>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, I,
+        else if (keep >> c & 1u)
+          search_tile_fix<1, false, true>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, c, I,
                                           lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
       }
     }
@@ -389,6 +484,7 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
 // carried to the next chunk.  Partner order, hence the accumulation order, is
 // a fixed function of the bit matrix: results are reproducible.
 constexpr int kChunkWords = 32;
+constexpr int kForceWarps = 8;  // warps per CTA of the partner walks
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 #pragma unroll
@@ -406,57 +502,81 @@ template <bool DUAL = true, typename Body>
 __device__ __forceinline__ void for_each_partner(const uint32_t* __restrict__ row, int words,
                                                  int lane, int* __restrict__ q, Body&& body) {
   int fill = 0;  // warp-uniform queue length carried between chunks
-  // the next chunk's words are loaded before the current one is expanded
-  uint32_t next = lane < words ? __ldg(row + lane) : 0u;
-  for (int w0 = 0; w0 < words; w0 += kChunkWords) {
-    const uint32_t m = next;
-    next = w0 + kChunkWords + lane < words ? __ldg(row + w0 + kChunkWords + lane) : 0u;
-    const int c0 = __popc(m);
-    const int total = int(__reduce_add_sync(0xffffffffu, unsigned(c0)));
-    if (total == 0) continue;  // empty chunk
-    const int mx = int(__reduce_max_sync(0xffffffffu, unsigned(c0)));
-    if (mx * 32 > 2 * total + 128) {
-      // bits concentrated in a few words (clustered partner runs): a 32x32
-      // bit transpose gives lane b bit b of every word, i.e. partners
-      // j = (w0 + k) * 32 + b, which spreads each run across lanes
-      uint32_t t = warp_transpose32(m, lane);
-      const int c = __popc(t);
-      int off = fill + warp_incl_scan(c, lane) - c;
-      while (t) {
-        const int k = __ffs(t) - 1;
-        t &= t - 1u;
-        q[off++] = (w0 + k) * 32 + lane;
-      }
-    } else {
-      // balanced chunk: lane k expands word k (ascending j, gather-friendly)
-      uint32_t t = m;
-      int off = fill + warp_incl_scan(c0, lane) - c0;
-      while (t) {
-        q[off++] = (w0 + lane) * 32 + __ffs(t) - 1;
-        t &= t - 1u;
-      }
+  const int nchunks = (words + kChunkWords - 1) / kChunkWords;
+  for (int g0 = 0; g0 < nchunks; g0 += 64) {
+    // Occupancy pass over (up to) 64 chunks: the words are loaded with eight
+    // loads in flight and OR-reduced per chunk, so empty chunks (most of a
+    // short-cutoff row) cost no dependent memory round trip in the walk.
+    const int gn = min(64, nchunks - g0);
+    uint64_t cm = 0;
+#pragma unroll 8
+    for (int k = 0; k < gn; ++k) {
+      const int w = (g0 + k) * kChunkWords + lane;
+      const uint32_t m = w < words ? __ldg(row + w) : 0u;
+      if (__reduce_or_sync(0xffffffffu, m)) cm |= 1ull << k;
     }
-    fill += total;
-    __syncwarp();
-    int e = 0;
-    if (DUAL)
-      for (; e + 64 <= fill; e += 64) {  // two full batches: both gathers in flight
-        const int j0 = q[e + lane], j1 = q[e + 32 + lane];
-        body(j0);
-        body(j1);
-      }
-    else
-      for (; e + 64 <= fill; e += 32) body(q[e + lane]);
-    if (e + 32 <= fill) {
-      body(q[e + lane]);
-      e += 32;
+    // nonempty chunks; the next one's word is loaded (L1) before the
+    // current one is expanded
+    uint32_t next = 0;
+    if (cm) {
+      const int w = (g0 + __ffsll(static_cast<long long>(cm)) - 1) * kChunkWords + lane;
+      next = w < words ? __ldg(row + w) : 0u;
     }
-    const int rem = fill - e;  // carry the partial batch
-    const int v = lane < rem ? q[e + lane] : 0;
-    __syncwarp();
-    if (lane < rem) q[lane] = v;
-    __syncwarp();
-    fill = rem;
+    while (cm) {
+      const int c = __ffsll(static_cast<long long>(cm)) - 1;
+      cm &= cm - 1;
+      const int w0 = (g0 + c) * kChunkWords;
+      const uint32_t m = next;
+      if (cm) {
+        const int w = (g0 + __ffsll(static_cast<long long>(cm)) - 1) * kChunkWords + lane;
+        next = w < words ? __ldg(row + w) : 0u;
+      }
+      const int c0 = __popc(m);
+      const int total = int(__reduce_add_sync(0xffffffffu, unsigned(c0)));
+      const int mx = int(__reduce_max_sync(0xffffffffu, unsigned(c0)));
+      if (mx * 32 > 2 * total + 128) {
+        // bits concentrated in a few words (clustered partner runs): a 32x32
+        // bit transpose gives lane b bit b of every word, i.e. partners
+        // j = (w0 + k) * 32 + b, which spreads each run across lanes
+        uint32_t t = warp_transpose32(m, lane);
+        const int cc = __popc(t);
+        int off = fill + warp_incl_scan(cc, lane) - cc;
+        while (t) {
+          const int k = __ffs(t) - 1;
+          t &= t - 1u;
+          q[off++] = (w0 + k) * 32 + lane;
+        }
+      } else {
+        // balanced chunk: lane k expands word k (ascending j, gather-friendly)
+        uint32_t t = m;
+        int off = fill + warp_incl_scan(c0, lane) - c0;
+        while (t) {
+          q[off++] = (w0 + lane) * 32 + __ffs(t) - 1;
+          t &= t - 1u;
+        }
+      }
+      fill += total;
+      __syncwarp();
+      int e = 0;
+      if (DUAL)
+        for (; e + 64 <= fill; e += 64) {  // two full batches: both gathers in flight
+          const int j0 = q[e + lane], j1 = q[e + 32 + lane];
+          body(j0);
+          body(j1);
+        }
+      else
+        for (; e + 64 <= fill; e += 32) body(q[e + lane]);
+      if (e + 32 <= fill) {
+        body(q[e + lane]);
+        e += 32;
+      }
+      const int rem = fill - e;  // carry the partial batch
+      const int v = lane < rem ? q[e + lane] : 0;
+      __syncwarp();
+      if (lane < rem) q[lane] = v;
+      __syncwarp();
+      fill = rem;
+    }
   }
   if (lane < fill) body(q[lane]);
 }
@@ -478,7 +598,7 @@ template <int NS>
 __device__ void finalize_scalars(const double* v /* NS values, valid on lane 0 of each warp */,
                                  double* cta_part, unsigned* ticket, double* sums, int r,
                                  int sum_offset) {
-  __shared__ double red[8][NS];
+  __shared__ double red[kForceWarps][NS];
   __shared__ bool last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
@@ -539,11 +659,10 @@ struct ForceArgs {
   float thr;  // hi32(L/2) as float (min_image_wrapped)
 };
 
-constexpr int kForceWarps = 8;
 
 template <bool MULTI_SPECIES, bool WRAPPED>
 __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) {
-  __shared__ int queue[kForceWarps][kQueue];
+  __shared__ int plist[kForceWarps][kQueue];
   const SysDev& s = a.s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.y;
@@ -561,7 +680,7 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
     const int si = MULTI_SPECIES ? s.species_of[i] : 0;
     double fx = 0, fy = 0, fz = 0;
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
-    for_each_partner(row, s.words, lane, queue[warp], [&](int j) {
+    for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
       const double4 pj = p4[j];
       const double dx = mimg(sub(pi.x, pj.x));
       const double dy = mimg(sub(pi.y, pj.y));

@@ -168,6 +168,10 @@ class ForceField:
     def pair_list(self) -> np.ndarray:
         return self._c.pair_list(0)
 
+    def set_search_options(self, fix_prefilter: bool = True, tile_cull: bool = True) -> None:
+        """b2md_set_search_options: partner-search strategy (same results)."""
+        check(_abi.lib().b2md_set_search_options(self._c.ctx, int(fix_prefilter), int(tile_cull)))
+
     def heat_flux(self, state: SystemState, h_per_species) -> np.ndarray:
         """tmd::heat_flux(comp, state, table, h_per_species) (src/greenkubo.cpp:182-266)
         of `state` (positions as given) with this force field's pair table."""
@@ -291,6 +295,10 @@ class Engine:
 
     def pair_list(self, replica: int = 0) -> np.ndarray:
         return self._c.pair_list(replica)
+
+    def set_search_options(self, fix_prefilter: bool = True, tile_cull: bool = True) -> None:
+        """b2md_set_search_options: partner-search strategy (same results)."""
+        check(_abi.lib().b2md_set_search_options(self._c.ctx, int(fix_prefilter), int(tile_cull)))
 
     def heat_fluxes(self, h_per_species) -> np.ndarray:
         """(replicas, 3) J_q of the device-resident state (what Engine::run

@@ -363,3 +363,61 @@ def test_shards_sum_to_full_evaluation(case, world):
     ref = np.array([e.lj, e.elec_real, e.elec_recip, full.virial])
     assert np.all(np.abs(parts[:4] - ref) <= 1e-11 * np.maximum(1.0, np.abs(ref)))
     assert int(parts[4]) == len(pyoracle.OracleFF(comp, opts).pair_list(st.pos))
+
+
+# ------------------------------------------------ partner-search strategies
+def _search_variants(comp, opts, pos, orient):
+    out = []
+    for fix, cull in ((True, True), (True, False), (False, False)):
+        ff = b2.ForceField(comp, opts)
+        ff.set_search_options(fix, cull)
+        st = b2.SystemState(comp.molecule_count(), comp.box_length)
+        st.pos, st.orient = np.array(pos), np.array(orient)
+        ff.evaluate(st)
+        out.append((ff.pair_list(), st.force.copy(), st.torque.copy()))
+    return out
+
+
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg1", "cfg3", "lj_gas_8192", "lj_shell_4096"])
+def test_tile_cull_is_exact(cfg):
+    """Tile culling, the unculled fixed-point search and the generic fp64
+    search give the same pair list (bit-exact vs the oracle) and the same
+    forces.  lj_gas: random positions (blocks span the box, little culls);
+    lj_shell: a lattice whose spacing puts many COM distances within 1e-12
+    of rmax."""
+    if cfg.startswith("lj_gas"):
+        rng = np.random.default_rng(4)
+        n = 8192
+        wl = configs.lj_fluid_config(n, 0.8, 3.0, seed=4, steps=1, name=cfg)
+        comp, opts = wl.comp, wl.opts
+        pos = rng.uniform(0, comp.box_length, size=(n, 3))
+        orient = wl.states[0].orient
+    elif cfg.startswith("lj_shell"):
+        wl = configs.lj_fluid_config(4096, 0.8, None, seed=5, steps=1, side=16, name=cfg)
+        comp = wl.comp
+        a = comp.box_length / 16
+        opts = b2.ForceFieldOptions(cutoff=3 * a)  # lattice shells sit on rmax
+        idx = np.arange(4096)
+        pos = np.column_stack([idx // 256, (idx // 16) % 16, idx % 16]) * a + 0.5 * a
+        orient = wl.states[0].orient
+    else:
+        wl = configs.make(cfg)
+        comp, opts = wl.comp, wl.opts
+        pos, orient = wl.states[0].pos, wl.states[0].orient
+    variants = _search_variants(comp, opts, pos, orient)
+    ref_pairs = pyoracle.OracleFF(comp, opts).pair_list(pos)
+    for pairs, f, t in variants:
+        assert np.array_equal(pairs, ref_pairs)
+        check_vec(f, variants[2][1], 1e-12, "force")
+        check_vec(t, variants[2][2], 1e-12, "torque")
+
+
+def test_tile_cull_after_steps():
+    """Culling on a state the integrator moved (arcs from the device-written
+    fixed-point positions) keeps the pair list exact."""
+    wl = configs.make("cfg3")
+    eng = b2.Engine(wl.comp, wl.opts, wl.dt)
+    eng.set_state(wl.states[0])
+    eng.step(50)
+    s = eng.state()
+    assert np.array_equal(eng.pair_list(), pyoracle.OracleFF(wl.comp, wl.opts).pair_list(s.pos))
