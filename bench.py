@@ -362,10 +362,17 @@ def run_heat_flux(args):
 
 def tile_cull_kept_fraction(eng, wl):
     """Fraction of the upper-triangle 32x32 tiles the search's bounding-arc
-    cull keeps on the final state (the arithmetic of k_search's arcs)."""
+    cull keeps on the final state, re-sorted as the device orders it (the
+    arithmetic of k_search's arcs)."""
     L = wl.comp.box_length
     pos = eng.state().pos % L
     n = len(pos)
+    # the device's slot order (k_sort_keys): columns of c^2 = 32 / (rho L), x inside
+    G = max(1, min(1024, int(L / np.sqrt(32.0 / (n / L ** 3 * L)))))
+    col = np.clip((pos[:, 2] / L * G).astype(np.int64), 0, G - 1) * G + \
+        np.clip((pos[:, 1] / L * G).astype(np.int64), 0, G - 1)
+    xq = np.clip((pos[:, 0] / L * 2 ** 20).astype(np.int64), 0, 2 ** 20 - 1)
+    pos = pos[np.argsort((col << 20) | xq, kind="stable")]
     u = np.floor(pos * (2.0 ** 32 / L) + 0.5).astype(np.int64) % (1 << 32)
     nb = (n + 31) // 32
     pad = np.zeros((nb * 32, 3), dtype=np.int64)

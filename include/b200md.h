@@ -210,6 +210,15 @@ int b2md_pair_list(b2md_ctx* ctx, int replica, int32_t* pairs, int64_t capacity,
  * further apart than the COM radius (fixed-point path only).  Both default 1. */
 int b2md_set_search_options(b2md_ctx* ctx, int fix_prefilter, int tile_cull);
 
+/* Spatial ordering: internally molecules occupy slots in column order of
+ * their wrapped positions (thin x-lines of ~32 molecules, for the search's
+ * tile cull) (re-sorted by every set_state / evaluate and every
+ * `steps` steps; 0 keeps the input order).  Only summation order changes;
+ * every output is indexed as the input and pair lists keep the reference's
+ * (i, j) order.  Default: 100 for a single species with COM radius < 0.3 L
+ * (where the tile cull can use it), else 0. */
+int b2md_set_sort_interval(b2md_ctx* ctx, int steps);
+
 /* Green-Kubo heat flux J_q (tmd::heat_flux, include/tmd/greenkubo.hpp:93,
  * src/greenkubo.cpp:182-266) of the context's current device state: the
  * state set_state / step left (Engine::run samples it every n_ext steps,

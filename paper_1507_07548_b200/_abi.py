@@ -136,6 +136,7 @@ SIGNATURES = {
         [_CTX, C.c_int, C.POINTER(C.c_int32), C.c_int64, C.POINTER(C.c_int64)],
     ),
     "b2md_set_search_options": (C.c_int, [_CTX, C.c_int, C.c_int]),
+    "b2md_set_sort_interval": (C.c_int, [_CTX, C.c_int]),
     "b2md_heat_flux": (C.c_int, [_CTX, _D, C.c_int, _D]),
     "b2md_heat_flux_state": (C.c_int, [_CTX, _D, _D, _D, _D, _D, C.c_int, _D]),
     "b2md_nccl_unique_id": (C.c_int, [C.c_char_p]),

@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cub/cub.cuh>
 #include <cstdlib>
 #include <climits>
 #include <cmath>
@@ -136,6 +137,19 @@ struct b2md_ctx {
   double2* d_S = nullptr;
   double* d_uk = nullptr;
   double* d_flux = nullptr;  // R * kNumSums: heat flux totals
+  // spatial order (resort): slot tables and radix-sort buffers
+  int* d_perm = nullptr;
+  int* d_slot_of = nullptr;
+  int* d_sp_slot = nullptr;
+  int* d_sb_slot = nullptr;
+  int* d_nsites_slot = nullptr;
+  int* d_scan = nullptr;
+  unsigned long long* d_keys[2] = {nullptr, nullptr};
+  int* d_vals[2] = {nullptr, nullptr};
+  void* d_cub = nullptr;
+  size_t cub_bytes = 0;
+  int sort_interval = 100;  // steps between re-sorts (0: keep the input order)
+  int64_t steps_since_sort = 0;
   // sharding
   int rank = 0, world = 1;
   int row_begin = 0, row_end = 0, k_begin = 0, k_end = 0;
@@ -267,9 +281,7 @@ int launch_search(b2md_ctx* c) {
   if (c->n_super_tiles == 0) return B2MD_OK;
   SearchArgs a;
   a.s = c->sys;
-  a.px = c->st.px;
-  a.py = c->st.py;
-  a.pz = c->st.pz;
+  a.pos4 = c->st.pos4;
   a.mask = c->d_mask;
   a.super_tiles = c->d_super;
   a.fixpos = c->d_fixpos;
@@ -510,14 +522,62 @@ int check_enthalpy(const b2md_ctx* c, const double* enthalpy, int n_enthalpy, co
   return B2MD_OK;
 }
 
+// Spatial order: molecules are assigned slots in column order of their
+// (wrapped) positions (k_sort_keys), so 32-slot blocks stay thin lines and
+// the search's tile cull stays effective as molecules diffuse.  Rebuilds perm / slot_of / sp_slot / sb_slot; the
+// caller re-stages pos4, fixpos and the offsets before the next search.
+// Results do not depend on the order beyond summation order (pair lists are
+// exported in the reference's (i, j) order).
+int resort(b2md_ctx* c) {
+  const int nt = n_total(c), n = c->t.n;
+  const int g = (nt + 255) / 256;
+  // columns of cross-section c^2 = 32 / (rho L) (about one block each)
+  const double L = c->t.box, rho = double(n) / (L * L * L);
+  const int G = std::max(1, std::min(1024, int(L / std::sqrt(32.0 / (rho * L)))));
+  k_sort_keys<<<g, 256, 0, c->stream>>>(c->st.px, c->st.py, c->st.pz, nt, n, L, G,
+                                        c->d_keys[0], c->d_vals[0]);
+  CU(cudaGetLastError());
+  int end_bit = 40;
+  while ((1 << (end_bit - 40)) < c->R) ++end_bit;
+  size_t bytes = c->cub_bytes;
+  CU(cub::DeviceRadixSort::SortPairs(c->d_cub, bytes, c->d_keys[0], c->d_keys[1], c->d_vals[0],
+                                     c->d_vals[1], nt, 0, end_bit, c->stream));
+  k_apply_order<<<g, 256, 0, c->stream>>>(c->d_vals[1], nt, n, c->d_species_of, c->d_tab,
+                                          c->d_perm, c->d_slot_of, c->d_sp_slot,
+                                          c->d_nsites_slot);
+  CU(cudaGetLastError());
+  bytes = c->cub_bytes;
+  CU(cub::DeviceScan::ExclusiveSum(c->d_cub, bytes, c->d_nsites_slot, c->d_scan, nt, c->stream));
+  k_site_starts<<<g, 256, 0, c->stream>>>(c->d_scan, nt, n, c->t.total_sites, c->d_sb_slot);
+  CU(cudaGetLastError());
+  c->steps_since_sort = 0;
+  return B2MD_OK;
+}
+
+// resort + re-stage of what the integrator wrote in the old order
+int resort_and_stage(b2md_ctx* c) {
+  TRY(resort(c));
+  TRY(launch_offsets(c));
+  const int nt = n_total(c);
+  k_stage_positions<<<(nt + 255) / 256, 256, 0, c->stream>>>(
+      c->st.px, c->st.py, c->st.pz, nt, c->t.n, c->d_slot_of, c->t.box, 4294967296.0 / c->t.box,
+      c->d_fixpos, c->st.pos4);
+  CU(cudaGetLastError());
+  return B2MD_OK;
+}
+
+bool sort_due(const b2md_ctx* c) {
+  return c->sort_interval > 0 && c->steps_since_sort >= c->sort_interval;
+}
+
 // ForceField::evaluate (src/parallel.cpp:79-122) on the device state.
 int enqueue_forces(b2md_ctx* c, bool offsets) {
   if (offsets) {  // evaluate / set_state path: the integrator did not refresh these
     TRY(launch_offsets(c));
     const int nt = n_total(c);
     k_stage_positions<<<(nt + 255) / 256, 256, 0, c->stream>>>(
-        c->st.px, c->st.py, c->st.pz, nt, c->t.box, 4294967296.0 / c->t.box, c->d_fixpos,
-        c->st.pos4);
+        c->st.px, c->st.py, c->st.pz, nt, c->t.n, c->d_slot_of, c->t.box,
+        4294967296.0 / c->t.box, c->d_fixpos, c->st.pos4);
     CU(cudaGetLastError());
   }
   TRY(launch_search(c));
@@ -662,10 +722,14 @@ int launch_prof_graph(b2md_ctx* c) {
   return B2MD_OK;
 }
 
+// A due re-sort runs between a step's drift and its force evaluation (so the
+// bit matrix always matches the current slot order); that step is issued
+// eagerly, all others as graphs.
 int run_steps(b2md_ctx* c, int64_t nsteps) {
-  if (c->profile && c->use_graphs && nsteps == 1) return launch_prof_graph(c);
   const bool graphs = c->use_graphs && !c->profile;
-  if (graphs && nsteps == 1) {
+  if (nsteps == 1 && c->use_graphs && !sort_due(c)) {
+    ++c->steps_since_sort;
+    if (c->profile) return launch_prof_graph(c);
     TRY(build_single_step_graph(c));
     CU(cudaGraphLaunch(c->single_graph, c->stream));
     return B2MD_OK;
@@ -673,11 +737,15 @@ int run_steps(b2md_ctx* c, int64_t nsteps) {
   if (graphs) TRY(build_step_graph(c));
   TRY(launch_step_kernel(c, F_KICK_DRIFT));
   for (int64_t k = 0; k + 1 < nsteps; ++k) {
+    if (sort_due(c)) TRY(resort_and_stage(c));
+    ++c->steps_since_sort;
     if (graphs)
       CU(cudaGraphLaunch(c->step_graph, c->stream));
     else
       TRY(enqueue_loop_body(c));
   }
+  if (sort_due(c)) TRY(resort_and_stage(c));
+  ++c->steps_since_sort;
   TRY(enqueue_forces(c, false));
   TRY(launch_step_kernel(c, F_KICK));
   return B2MD_OK;
@@ -856,6 +924,10 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const int rows_grid = (t.n + kForceWarps - 1) / kForceWarps;
     c->force_grid = std::max(1, std::min(rows_grid, sms * 4));
+    // re-sort only where the search's tile cull can use the order: single
+    // species (fixed-point path) and a COM radius well below L/2
+    const double rmax = std::sqrt(t.single_site_path ? t.rc2 : t.rmax2[0]);
+    c->sort_interval = (t.ns == 1 && rmax < 0.3 * t.box) ? 100 : 0;
     // tuning knobs (measurement only): warps per CTA, CTAs per replica
     if (const char* e = std::getenv("B2MD_FORCE_WARPS"))
       c->force_warps = std::max(1, std::min(kForceWarps, std::atoi(e)));
@@ -864,6 +936,36 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars * c->force_grid));
   TRY(dalloc(&c->d_ticket, size_t(2) * R));
   TRY(dalloc(&c->d_flux, size_t(kNumSums) * R));
+  {
+    // spatial-order tables, identity until the first resort
+    TRY(dalloc(&c->d_perm, nt));
+    TRY(dalloc(&c->d_slot_of, nt));
+    TRY(dalloc(&c->d_sp_slot, nt));
+    TRY(dalloc(&c->d_sb_slot, nt));
+    TRY(dalloc(&c->d_nsites_slot, nt));
+    TRY(dalloc(&c->d_scan, nt));
+    TRY(dalloc(&c->d_keys[0], nt));
+    TRY(dalloc(&c->d_keys[1], nt));
+    TRY(dalloc(&c->d_vals[0], nt));
+    TRY(dalloc(&c->d_vals[1], nt));
+    std::vector<int> ident(nt), sp(nt), sb(nt);
+    for (size_t g = 0; g < nt; ++g) {
+      const int i = int(g % t.n);
+      ident[g] = i;
+      sp[g] = t.species_of[i];
+      sb[g] = t.site_begin[i];
+    }
+    CU(cudaMemcpy(c->d_perm, ident.data(), sizeof(int) * nt, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_slot_of, ident.data(), sizeof(int) * nt, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_sp_slot, sp.data(), sizeof(int) * nt, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_sb_slot, sb.data(), sizeof(int) * nt, cudaMemcpyHostToDevice));
+    size_t b1 = 0, b2 = 0;
+    CU(cub::DeviceRadixSort::SortPairs(nullptr, b1, c->d_keys[0], c->d_keys[1], c->d_vals[0],
+                                       c->d_vals[1], int(nt), 0, 52));
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, b2, c->d_nsites_slot, c->d_scan, int(nt)));
+    c->cub_bytes = std::max(b1, b2);
+    CU(cudaMalloc(&c->d_cub, c->cub_bytes));
+  }
   TRY(dalloc(&c->d_error, 1));
   const int big = INT_MAX;
   CU(cudaMemcpy(c->d_error, &big, sizeof(int), cudaMemcpyHostToDevice));
@@ -899,6 +1001,10 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   c->sys.species_of = c->d_species_of;
   c->sys.site_begin = c->d_site_begin;
   c->sys.tab = c->d_tab;
+  c->sys.perm = c->d_perm;
+  c->sys.slot_of = c->d_slot_of;
+  c->sys.sp_slot = c->d_sp_slot;
+  c->sys.sb_slot = c->d_sb_slot;
   MinImage& mi = c->sys.mi;
   mi.L = t.box;
   mi.negL = -t.box;
@@ -957,7 +1063,9 @@ void free_ctx(b2md_ctx* c) {
   void* ptrs[] = {c->d_tab,   c->d_species_of, c->d_site_begin, c->d_state, c->d_fbuf, c->d_off,
                   c->d_stage, c->d_mask,       c->d_cta_part, c->d_ticket, c->d_fixpos, c->d_pos4,   c->d_super, c->d_error, c->d_q_mol,
                   c->d_q_site, c->d_q_val,     c->d_mol_qbegin, c->d_kv,    c->d_etab,  c->d_S,
-                  c->d_uk,    c->d_flux};
+                  c->d_uk,    c->d_flux,  c->d_perm, c->d_slot_of, c->d_sp_slot, c->d_sb_slot,
+                  c->d_nsites_slot, c->d_scan, c->d_keys[0], c->d_keys[1], c->d_vals[0],
+                  c->d_vals[1], c->d_cub};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1054,6 +1162,7 @@ int b2md_evaluate(b2md_ctx* c, const double* pos, const double* orient, double* 
     return set_err(B2MD_INVALID_ARGUMENT, "evaluate: orientations required for multi-site species");
   }
   set_wrapped(c, false);
+  if (c->sort_interval > 0) TRY(resort(c));
   TRY(enqueue_forces(c, true));
   if (force) TRY(download_aos(c, 4, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
   if (torque) TRY(download_aos(c, 5, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
@@ -1079,6 +1188,7 @@ int b2md_set_state(b2md_ctx* c, const double* pos, const double* orient, const d
   set_wrapped(c, true);
   const int big = INT_MAX;
   CU(cudaMemcpyAsync(c->d_error, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  if (c->sort_interval > 0) TRY(resort(c));
   TRY(enqueue_forces(c, true));
   CU(cudaStreamSynchronize(c->stream));
   c->state_valid = true;
@@ -1149,6 +1259,12 @@ int b2md_set_search_options(b2md_ctx* c, int fix_prefilter, int tile_cull) {
   return B2MD_OK;
 }
 
+int b2md_set_sort_interval(b2md_ctx* c, int steps) {
+  if (!c || steps < 0) return set_err(B2MD_INVALID_ARGUMENT, "set_sort_interval: bad argument");
+  c->sort_interval = steps;
+  return B2MD_OK;
+}
+
 int b2md_heat_flux(b2md_ctx* c, const double* enthalpy, int n_enthalpy, double* jq) {
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "heat_flux: null context");
   TRY(check_enthalpy(c, enthalpy, n_enthalpy, jq));
@@ -1172,12 +1288,16 @@ int b2md_heat_flux_state(b2md_ctx* c, const double* pos, const double* orient, c
   TRY(upload_aos(c, 2, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
   TRY(upload_aos(c, 3, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
   set_wrapped(c, false);  // the reference takes the positions as given
-  TRY(launch_offsets(c));
-  const int nt = n_total(c);
-  k_stage_positions<<<(nt + 255) / 256, 256, 0, c->stream>>>(
-      c->st.px, c->st.py, c->st.pz, nt, c->t.box, 4294967296.0 / c->t.box, c->d_fixpos,
-      c->st.pos4);
-  CU(cudaGetLastError());
+  if (c->sort_interval > 0)
+    TRY(resort_and_stage(c));
+  else {
+    TRY(launch_offsets(c));
+    const int nt = n_total(c);
+    k_stage_positions<<<(nt + 255) / 256, 256, 0, c->stream>>>(
+        c->st.px, c->st.py, c->st.pz, nt, c->t.n, c->d_slot_of, c->t.box,
+        4294967296.0 / c->t.box, c->d_fixpos, c->st.pos4);
+    CU(cudaGetLastError());
+  }
   TRY(launch_search(c));
   TRY(launch_heat_flux(c, enthalpy));
   TRY(download_flux(c, jq));
@@ -1191,9 +1311,10 @@ int b2md_pair_list(b2md_ctx* c, int replica, int32_t* pairs, int64_t capacity, i
   CU(cudaSetDevice(c->device));
   const int n = c->t.n;
   const uint32_t* mask = c->d_mask + size_t(replica) * c->g.n_pad * c->g.words;
+  const int* perm = c->d_perm + size_t(replica) * n;
   int64_t* d_cnt = nullptr;
   CU(cudaMalloc(&d_cnt, sizeof(int64_t) * (n + 1)));
-  k_pair_count<<<(n + 255) / 256, 256, 0, c->stream>>>(mask, n, c->g.n_pad, c->g.words, d_cnt);
+  k_pair_count<<<(n + 255) / 256, 256, 0, c->stream>>>(mask, perm, n, c->g.words, d_cnt);
   std::vector<int64_t> cnt(n + 1, 0);
   cudaError_t e = cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -1218,7 +1339,7 @@ int b2md_pair_list(b2md_ctx* c, int replica, int32_t* pairs, int64_t capacity, i
     e = cudaMalloc(&d_pairs, sizeof(int32_t) * 2 * total);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_cnt, cnt.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) {
-      k_pair_fill<<<(n + 255) / 256, 256, 0, c->stream>>>(mask, n, c->g.words, d_cnt, d_pairs);
+      k_pair_fill<<<(n + 255) / 256, 256, 0, c->stream>>>(mask, perm, n, c->g.words, d_cnt, d_pairs);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess)
@@ -1228,6 +1349,15 @@ int b2md_pair_list(b2md_ctx* c, int replica, int32_t* pairs, int64_t capacity, i
     if (e != cudaSuccess) {
       cudaFree(d_cnt);
       return set_err(B2MD_CUDA_ERROR, cudaGetErrorString(e));
+    }
+    // each row i's partners j came in slot order: sort them (reference order)
+    for (int i = 0; i < n; ++i) {
+      const int64_t b = cnt[i], en = i + 1 < n ? cnt[i + 1] : total;
+      std::vector<int32_t> js;
+      js.reserve(size_t(en - b));
+      for (int64_t q = b; q < en; ++q) js.push_back(pairs[2 * q + 1]);
+      std::sort(js.begin(), js.end());
+      for (int64_t q = b; q < en; ++q) pairs[2 * q + 1] = js[size_t(q - b)];
     }
   }
   cudaFree(d_cnt);

@@ -47,7 +47,28 @@ struct SysDev {
   const int* species_of;  // n
   const int* site_begin;  // n + 1
   const DevTables* tab;
+  // spatial order (b2md_ctx::resort): the search, the bit matrix, pos4,
+  // fixpos and the site offsets are indexed by slot k; state arrays by the
+  // external molecule index perm[k].  All R * n, replica-major.
+  const int* perm;     // external index of slot k
+  const int* slot_of;  // slot of external molecule i
+  const int* sp_slot;  // species of slot k
+  const int* sb_slot;  // first site of slot k in slot-ordered site numbering
 };
+
+// pos4.w carries the slot's external index (integer bits; never used as a
+// double), so a partner gather yields it with the position.
+__device__ __forceinline__ double4 pack_pos(double x, double y, double z, int ext) {
+  return make_double4(x, y, z, __hiloint2double(0, ext));
+}
+__device__ __forceinline__ int ext_of(const double4& p) { return __double2loint(p.w); }
+
+// slot-ordered offset index of external molecule m's site `site` (external
+// site numbering site_begin[m] + k)
+__device__ __forceinline__ int site_slot(const SysDev& s, int r, int m, int site) {
+  const size_t ro = size_t(r) * s.n;
+  return s.sb_slot[ro + s.slot_of[ro + m]] + (site - s.site_begin[m]);
+}
 
 // ------------------------------------------------------------ site offsets
 // build_scene (potentials.cpp:106-116): off = rotate(orient, body_pos); a single
@@ -57,7 +78,7 @@ __global__ void k_offsets(SysDev s, StateDev st) {
   if (gid >= s.n * s.R) return;
   const int r = gid / s.n, i = gid - r * s.n;
   const DevSpecies& sp = s.tab->species[s.species_of[i]];
-  const int base = r * s.total_sites + s.site_begin[i];
+  const int base = r * s.total_sites + s.sb_slot[size_t(r) * s.n + s.slot_of[gid]];
   if (sp.centred) {
     st.off[base] = make_double4(0.0, 0.0, 0.0, 0.0);
     return;
@@ -72,7 +93,7 @@ __global__ void k_offsets(SysDev s, StateDev st) {
 // ----------------------------------------------------------- partner search
 struct SearchArgs {
   SysDev s;
-  const double *px, *py, *pz;
+  const double4* pos4;  // slot-ordered positions (exact fallback)
   uint32_t* mask;               // R * n_pad * words
   const uint32_t* super_tiles;  // (SI << 16) | SJ, this rank's list
   const uint4* fixpos;          // R * n: (round(x 2^32/L), .., .., in-box flag)
@@ -152,18 +173,17 @@ struct FixRefine {
 };
 
 __device__ __forceinline__ bool refine_pair(uint4 pi, uint4 pj, int ig, int jg,
-                                         const double* __restrict__ gx,
-                                         const double* __restrict__ gy,
-                                         const double* __restrict__ gz, const FixRefine& f,
+                                         const double4* __restrict__ gp, const FixRefine& f,
                                          const MinImage& mi) {
   const int dx = int(pi.x - pj.x), dy = int(pi.y - pj.y), dz = int(pi.z - pj.z);
   const uint32_t r2 =
       uint32_t(__mulhi(dx, dx)) + uint32_t(__mulhi(dy, dy)) + uint32_t(__mulhi(dz, dz));
   if (r2 < f.lo32) return true;
   if (r2 - f.lo32 >= f.w32) return false;
-  const double ex = min_image(sub(gx[ig], gx[jg]), mi);
-  const double ey = min_image(sub(gy[ig], gy[jg]), mi);
-  const double ez = min_image(sub(gz[ig], gz[jg]), mi);
+  const double4 a = gp[ig], b = gp[jg];
+  const double ex = min_image(sub(a.x, b.x), mi);
+  const double ey = min_image(sub(a.y, b.y), mi);
+  const double ez = min_image(sub(a.z, b.z), mi);
   return norm2_exact(ex, ey, ez) < f.rc2;
 }
 
@@ -172,8 +192,7 @@ __device__ __forceinline__ bool refine_pair(uint4 pi, uint4 pj, int ig, int jg,
 // Column tiles c0 and (JB == 2) c1, not necessarily adjacent.
 template <int JB, bool DIAG, bool PARTIAL_I>
 __device__ __forceinline__ void search_tile_fix(
-    const uint4* __restrict__ siu, const uint4* __restrict__ sju,
-    const double* __restrict__ gx, const double* __restrict__ gy, const double* __restrict__ gz,
+    const uint4* __restrict__ siu, const uint4* __restrict__ sju, const double4* __restrict__ gp,
     int ig0, int jg0, int ib, int c0, int c1, int I, int lane, int ST, int ilim, int jlim,
     int neglo, int width, const FixRefine& f, const MinImage& mi, uint32_t* wu, uint32_t* wl) {
   uint32_t xj[JB], yj[JB], zj[JB], lw[JB], bw[JB];
@@ -218,7 +237,7 @@ __device__ __forceinline__ void search_tile_fix(
       while (band) {
         const int ii = __ffs(band) - 1;
         band &= band - 1u;
-        if (refine_pair(siu[ib + ii], pj, ig0 + ib + ii, jg0 + jl, gx, gy, gz, f, mi))
+        if (refine_pair(siu[ib + ii], pj, ig0 + ib + ii, jg0 + jl, gp, f, mi))
           lw[b] |= 1u << ii;
       }
     }
@@ -285,9 +304,7 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
   const int n = s.n;
   const int ibase = SI * T, jbase = SJ * T;
   const size_t roff = size_t(r) * n;
-  const double* __restrict__ gx = a.px + roff;
-  const double* __restrict__ gy = a.py + roff;
-  const double* __restrict__ gz = a.pz + roff;
+  const double4* __restrict__ gp = a.pos4 + roff;
 
   bool inbox;
   {
@@ -300,8 +317,8 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
     uj[tid] = fj;
     inbox = fi.w != 0u && fj.w != 0u;
     if constexpr (MULTI) {
-      ispec[tid] = i < n ? s.species_of[i] : 0;
-      jspec[tid] = j < n ? s.species_of[j] : 0;
+      ispec[tid] = i < n ? s.sp_slot[roff + i] : 0;
+      jspec[tid] = j < n ? s.sp_slot[roff + j] : 0;
       for (int k = tid; k < s.ns * s.ns; k += T) rmax2_s[k] = s.tab->pair[k].rmax2;
     }
     if (diag || !a.fix_ok || MULTI) {  // only partially written there: merge needs zeros
@@ -389,28 +406,28 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
         const uint32_t jb = jobs[q];
         const int Iq = int(jb >> 16), c0 = int((jb >> 8) & 0xffu), c1 = int(jb & 0xffu);
         if (ST >= 2 && c1 != 0xff)
-          search_tile_fix<(ST >= 2 ? 2 : 1), false, false>(ui, uj, gx, gy, gz, ibase, jbase,
+          search_tile_fix<(ST >= 2 ? 2 : 1), false, false>(ui, uj, gp, ibase, jbase,
                                                            Iq * 32, c0, c1, Iq, lane, ST, 32,
                                                            jlim, neglo, wd, refine, s.mi, wu, wl);
         else
-          search_tile_fix<1, false, false>(ui, uj, gx, gy, gz, ibase, jbase, Iq * 32, c0, c0,
+          search_tile_fix<1, false, false>(ui, uj, gp, ibase, jbase, Iq * 32, c0, c0,
                                            Iq, lane, ST, 32, jlim, neglo, wd, refine, s.mi, wu,
                                            wl);
       }
     } else if (diag && ilim >= 32) {
-      search_tile_fix<1, true, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, I, I, I, lane,
+      search_tile_fix<1, true, false>(ui, uj, gp, ibase, jbase, ib, I, I, I, lane,
                                       ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
       for (int c = I + 1; c < ST; ++c)
         if (keep >> c & 1u)
-          search_tile_fix<1, false, false>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, c, I,
+          search_tile_fix<1, false, false>(ui, uj, gp, ibase, jbase, ib, c, c, I,
                                            lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
     } else {  // last, partial tile row (arcs include the padding: conservative)
       for (int c = diag ? I : 0; c < ST; ++c) {
         if (diag && c == I)
-          search_tile_fix<1, true, true>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, c, I,
+          search_tile_fix<1, true, true>(ui, uj, gp, ibase, jbase, ib, c, c, I,
                                          lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
         else if (keep >> c & 1u)
-          search_tile_fix<1, false, true>(ui, uj, gx, gy, gz, ibase, jbase, ib, c, c, I,
+          search_tile_fix<1, false, true>(ui, uj, gp, ibase, jbase, ib, c, c, I,
                                           lane, ST, ilim, jlim, neglo, wd, refine, s.mi, wu, wl);
       }
     }
@@ -421,15 +438,17 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
       const int jl = c * 32 + lane;
       const bool jvalid = jbase + jl < n;
       const int jg = jvalid ? jbase + jl : 0;
-      const double xj = gx[jg], yj = gy[jg], zj = gz[jg];
+      const double4 pj = gp[jg];
+      const double xj = pj.x, yj = pj.y, zj = pj.z;
       const int sj = MULTI ? jspec[jl] : 0;
       const bool diag_tile = diag && c == I;
       for (int ii = 0; ii < 32; ++ii) {
         const int il = ib + ii;
         const int ig = ii < ilim ? ibase + il : 0;
-        const double dx = min_image(sub(gx[ig], xj), mi);
-        const double dy = min_image(sub(gy[ig], yj), mi);
-        const double dz = min_image(sub(gz[ig], zj), mi);
+        const double4 pi = gp[ig];
+        const double dx = min_image(sub(pi.x, xj), mi);
+        const double dy = min_image(sub(pi.y, yj), mi);
+        const double dz = min_image(sub(pi.z, zj), mi);
         const double r2 = norm2_exact(dx, dy, dz);
         double lim;
         if constexpr (MULTI)
@@ -676,8 +695,8 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
   double u = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
   const int wpb = blockDim.x >> 5;  // warps per CTA (<= kForceWarps; fewer for small systems)
   for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
-    const double4 pi = p4[i];
-    const int si = MULTI_SPECIES ? s.species_of[i] : 0;
+    const double4 pi = p4[i];  // i, j: slots (single-site terms are symmetric)
+    const int si = MULTI_SPECIES ? s.sp_slot[roff + i] : 0;
     double fx = 0, fy = 0, fz = 0;
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
     for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
@@ -688,7 +707,7 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
       const double r2 = norm2_exact(dx, dy, dz);
       double c12 = a.c12, c6 = a.c6;
       if constexpr (MULTI_SPECIES) {
-        const int sj = s.species_of[j];
+        const int sj = s.sp_slot[roff + j];
         const DevPairInfo& pinfo = s.tab->pair[(i < j) ? si * s.ns + sj : sj * s.ns + si];
         c12 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c12 : 0.0;
         c6 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c6 : 0.0;
@@ -715,9 +734,10 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
     fy = warp_sum(fy);
     fz = warp_sum(fz);
     if (lane == 0) {
-      a.st.fx[roff + i] = fx;
-      a.st.fy[roff + i] = fy;
-      a.st.fz[roff + i] = fz;
+      const size_t e = roff + ext_of(pi);
+      a.st.fx[e] = fx;
+      a.st.fy[e] = fy;
+      a.st.fz[e] = fz;
     }
   }
   double v[kNumRowScalars] = {warp_sum(u), 0.0, 0.0, a.vderiv ? warp_sum(s1) : 0.0,
@@ -754,19 +774,20 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
   double ulj = 0, uel = 0, urf = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
   const int wpb = blockDim.x >> 5;  // warps per CTA (<= kForceWarps; fewer for small systems)
   for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
-    const double4 pi = p4[i];
-    const int si = s.species_of[i];
-    const int bi = s.site_begin[i];
+    const double4 pi = p4[i];  // i, j: slots; the reference's order is that of ext_of
+    const int ei = ext_of(pi);
+    const int si = s.sp_slot[roff + i];
+    const int bi = s.sb_slot[roff + i];
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
     for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
-      const bool lo = i < j;
       const double4 pj = p4[j];
+      const bool lo = ei < ext_of(pj);
       const double Rx = mimg(sub(pi.x, pj.x));
       const double Ry = mimg(sub(pi.y, pj.y));
       const double Rz = mimg(sub(pi.z, pj.z));
-      const int sj = s.species_of[j];
-      const int bj = s.site_begin[j];
+      const int sj = s.sp_slot[roff + j];
+      const int bj = s.sb_slot[roff + j];
       const DevPairInfo pinfo = tab->pair[lo ? si * s.ns + sj : sj * s.ns + si];
       double R2 = 0.0, s1p = 0.0, s2p = 0.0;
       if (lo) {
@@ -876,12 +897,13 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
     ty = warp_sum(ty);
     tz = warp_sum(tz);
     if (lane == 0) {
-      a.st.fx[roff + i] = fx;
-      a.st.fy[roff + i] = fy;
-      a.st.fz[roff + i] = fz;
-      a.st.tx[roff + i] = tx;
-      a.st.ty[roff + i] = ty;
-      a.st.tz[roff + i] = tz;
+      const size_t e = roff + ext_of(pi);
+      a.st.fx[e] = fx;
+      a.st.fy[e] = fy;
+      a.st.fz[e] = fz;
+      a.st.tx[e] = tx;
+      a.st.ty[e] = ty;
+      a.st.tz[e] = tz;
     }
   }
   double v[kNumRowScalars] = {warp_sum(ulj), warp_sum(uel), warp_sum(urf), warp_sum(s1),
@@ -936,19 +958,21 @@ __global__ void __launch_bounds__(kForceWarps * 32, OFFS ? 2 : 4) k_heat_flux(Fl
   const int nsite0 = tab->species[0].n_sites;
   const DevPairInfo pinfo0 = tab->pair[0];
   for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
-    const double4 pi = p4[i];
-    const int si = ONE_SPECIES ? 0 : s.species_of[i];
-    const int bi = ONE_SPECIES ? i * nsite0 : s.site_begin[i];
-    const double vix = a.st.vx[roff + i], viy = a.st.vy[roff + i], viz = a.st.vz[roff + i];
+    const double4 pi = p4[i];  // i, j: slots; the reference's order is that of ext_of
+    const int ei = ext_of(pi);
+    const size_t ge = roff + ei;
+    const int si = ONE_SPECIES ? 0 : s.sp_slot[roff + i];
+    const int bi = ONE_SPECIES ? i * nsite0 : s.sb_slot[roff + i];
+    const double vix = a.st.vx[ge], viy = a.st.vy[ge], viz = a.st.vz[ge];
     D3 wl{0.0, 0.0, 0.0};  // lab-frame angular velocity (only torques use it)
     if constexpr (OFFS)
-      wl = rotate_exact(a.st.qw[roff + i], a.st.qx[roff + i], a.st.qy[roff + i], a.st.qz[roff + i],
-                        {a.st.wx[roff + i], a.st.wy[roff + i], a.st.wz[roff + i]});
+      wl = rotate_exact(a.st.qw[ge], a.st.qx[ge], a.st.qy[ge], a.st.qz[ge],
+                        {a.st.wx[ge], a.st.wy[ge], a.st.wz[ge]});
     double tx = 0, ty = 0, tz = 0, up = 0;  // sum_p 0.5 s_p R_p, sum_p u_p
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
     for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
-      const bool lo = i < j;
       const double4 pj = p4[j];
+      const bool lo = ei < ext_of(pj);
       const double Rx = mimg(sub(pi.x, pj.x));
       const double Ry = mimg(sub(pi.y, pj.y));
       const double Rz = mimg(sub(pi.z, pj.z));
@@ -958,8 +982,8 @@ __global__ void __launch_bounds__(kForceWarps * 32, OFFS ? 2 : 4) k_heat_flux(Fl
         bj = j * nsite0;
         pinfo = pinfo0;
       } else {
-        const int sj = s.species_of[j];
-        bj = s.site_begin[j];
+        const int sj = s.sp_slot[roff + j];
+        bj = s.sb_slot[roff + j];
         pinfo = tab->pair[lo ? si * s.ns + sj : sj * s.ns + si];
       }
       double u = 0, fx = 0, fy = 0, fz = 0, gx = 0, gy = 0, gz = 0;
@@ -1058,7 +1082,7 @@ __global__ void __launch_bounds__(kForceWarps * 32, OFFS ? 2 : 4) k_heat_flux(Fl
       double e = 0.5 * up;
       if (fa.kinetic) {
         const DevSpecies& sp = tab->species[si];
-        const double wbx = a.st.wx[roff + i], wby = a.st.wy[roff + i], wbz = a.st.wz[roff + i];
+        const double wbx = a.st.wx[ge], wby = a.st.wy[ge], wbz = a.st.wz[ge];
         const double ek = 0.5 * sp.total_mass * (vix * vix + viy * viy + viz * viz) +
                           0.5 * (sp.inertia[0] * wbx * wbx + sp.inertia[1] * wby * wby +
                                  sp.inertia[2] * wbz * wbz);
@@ -1109,16 +1133,17 @@ __global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a
   double ulj = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
   const int wpb = blockDim.x >> 5;  // warps per CTA (<= kForceWarps; fewer for small systems)
   for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
-    const double4 pi = p4[i];
-    const int bi = i * NS;  // single species: site_begin[i] = i * NS
+    const double4 pi = p4[i];  // i, j: slots; the reference's order is that of ext_of
+    const int ei = ext_of(pi);
+    const int bi = i * NS;  // single species: slot-ordered sites start at i * NS
     double4 di[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) di[k] = o4[bi + k];
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
     for_each_partner<false>(row, s.words, lane, plist[warp], [&](int j) {
-      const bool lo = i < j;
       const double4 pj = p4[j];
+      const bool lo = ei < ext_of(pj);
       double4 dj[NS];
 #pragma unroll
       for (int k = 0; k < NS; ++k) dj[k] = o4[j * NS + k];
@@ -1183,12 +1208,13 @@ __global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a
     ty = warp_sum(ty);
     tz = warp_sum(tz);
     if (lane == 0) {
-      a.st.fx[roff + i] = fx;
-      a.st.fy[roff + i] = fy;
-      a.st.fz[roff + i] = fz;
-      a.st.tx[roff + i] = tx;
-      a.st.ty[roff + i] = ty;
-      a.st.tz[roff + i] = tz;
+      const size_t e = roff + ext_of(pi);
+      a.st.fx[e] = fx;
+      a.st.fy[e] = fy;
+      a.st.fz[e] = fz;
+      a.st.tx[e] = tx;
+      a.st.ty[e] = ty;
+      a.st.tz[e] = tz;
     }
   }
   double v[kNumRowScalars] = {warp_sum(ulj), 0.0, 0.0, warp_sum(s1),
@@ -1226,7 +1252,7 @@ __global__ void k_ewald_tables(EwaldArgs a) {
   const int r = gid / a.nq, q = gid - r * a.nq;
   const int m = a.q_mol[q];
   const size_t roff = size_t(r) * a.s.n;
-  const size_t soff = size_t(r) * a.s.total_sites + a.q_site[q];
+  const size_t soff = size_t(r) * a.s.total_sites + site_slot(a.s, r, m, a.q_site[q]);
   const double4 o = a.st.off[soff];
   const double p[3] = {a.st.px[roff + m] + o.x, a.st.py[roff + m] + o.y, a.st.pz[roff + m] + o.z};
   const int K = a.kmax + 1;
@@ -1314,7 +1340,7 @@ __global__ void __launch_bounds__(256) k_ewald_force(EwaldArgs a) {
   const size_t soff = size_t(r) * a.s.total_sites;
   double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
   for (int q = q0; q < q1; ++q) {
-    const int site = a.q_site[q];
+    const int site = site_slot(a.s, r, m, a.q_site[q]);
     const double4 o4 = a.st.off[soff + site];
     const double ox = o4.x, oy = o4.y, oz = o4.z;
     const double qv = a.q_val[q];
@@ -1431,12 +1457,15 @@ __device__ __forceinline__ uint4 fix_position(double x, double y, double z, doub
 // Positions as the search (fixed point) and the force kernels (packed) read
 // them; the integrator writes both itself.
 __global__ void k_stage_positions(const double* px, const double* py, const double* pz, int count,
-                                  double L, double scale, uint4* fixpos, double4* pos4) {
+                                  int n, const int* slot_of, double L, double scale,
+                                  uint4* fixpos, double4* pos4) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= count) return;
+  const int r = gid / n;
+  const size_t k = size_t(r) * n + slot_of[gid];
   const double x = px[gid], y = py[gid], z = pz[gid];
-  fixpos[gid] = fix_position(x, y, z, L, scale);
-  pos4[gid] = make_double4(x, y, z, 0.0);
+  fixpos[k] = fix_position(x, y, z, L, scale);
+  pos4[k] = pack_pos(x, y, z, gid - r * n);
 }
 
 // engine.cpp:107-127 (+ build_scene offsets for the new orientation)
@@ -1480,10 +1509,11 @@ __device__ __forceinline__ void kick_drift_one(const StepArgs& a, int gid) {
   a.st.px[gid] = px;
   a.st.py[gid] = py;
   a.st.pz[gid] = pz;
-  a.st.pos4[gid] = make_double4(px, py, pz, 0.0);
-  if (a.fixpos) a.fixpos[gid] = fix_position(px, py, pz, s.mi.L, a.fix_scale);
+  const size_t slot = size_t(r) * s.n + s.slot_of[gid];
+  a.st.pos4[slot] = pack_pos(px, py, pz, i);
+  if (a.fixpos) a.fixpos[slot] = fix_position(px, py, pz, s.mi.L, a.fix_scale);
   if (a.write_offsets) {
-    const int base = r * s.total_sites + s.site_begin[i];
+    const int base = r * s.total_sites + s.sb_slot[slot];
     if (sp.centred) {
       a.st.off[base] = make_double4(0.0, 0.0, 0.0, 0.0);
     } else {
@@ -1564,38 +1594,94 @@ __global__ void k_wrap(double* p, int count, double L) {
 // --------------------------------------------------- pair-list compaction
 // Prefix-sum compaction of the upper triangle (j > i) of the bit matrix into
 // an (i, j) list sorted by i then j: per-row popcounts, then a row scan.
-__global__ void k_pair_count(const uint32_t* mask, int n, int n_pad, int words, int64_t* row_count) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t* row = mask + size_t(i) * words;
+// Pair export (b2md_pair_list): slot row k holds external molecule
+// i = perm[k]; its partners l with perm[l] > i are the reference pairs (i, j).
+// Rows are counted / filled by external index; the host orders each row's j.
+__global__ void k_pair_count(const uint32_t* mask, const int* perm, int n, int words,
+                             int64_t* row_count) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t* row = mask + size_t(k) * words;
+  const int i = perm[k];
   int64_t c = 0;
-  const int w0 = i >> 5;
-  for (int w = w0; w < words; ++w) {
+  for (int w = 0; w < words; ++w) {
     uint32_t m = row[w];
-    if (w == w0) m &= (i & 31) == 31 ? 0u : (0xffffffffu << ((i & 31) + 1));
-    c += __popc(m);
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      c += perm[w * 32 + b] > i ? 1 : 0;
+    }
   }
   row_count[i] = c;
 }
 
-__global__ void k_pair_fill(const uint32_t* mask, int n, int words, const int64_t* row_start,
-                            int32_t* pairs) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t* row = mask + size_t(i) * words;
+__global__ void k_pair_fill(const uint32_t* mask, const int* perm, int n, int words,
+                            const int64_t* row_start, int32_t* pairs) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t* row = mask + size_t(k) * words;
+  const int i = perm[k];
   int64_t o = row_start[i];
-  const int w0 = i >> 5;
-  for (int w = w0; w < words; ++w) {
+  for (int w = 0; w < words; ++w) {
     uint32_t m = row[w];
-    if (w == w0) m &= (i & 31) == 31 ? 0u : (0xffffffffu << ((i & 31) + 1));
     while (m) {
       const int b = __ffs(m) - 1;
       m &= m - 1;
-      pairs[2 * o] = i;
-      pairs[2 * o + 1] = w * 32 + b;
-      ++o;
+      const int j = perm[w * 32 + b];
+      if (j > i) {
+        pairs[2 * o] = i;
+        pairs[2 * o + 1] = j;
+        ++o;
+      }
     }
   }
+}
+
+// ------------------------------------------------------ spatial ordering
+// Sort keys for b2md_ctx::resort: molecules are binned into G x G columns
+// along x (cross-section c x c, c^2 = 32 / (rho L): about one 32-slot block
+// per column), columns in (z, y) order, molecules by x within a column.  A
+// block is then a thin line, which is what the search's per-axis bounding-arc
+// cull rejects best, and a row's partners fall in a few runs of consecutive
+// words.  Key = (replica, column, x on 2^20 bins); values are global
+// molecule indices; the stable radix sort makes the order a deterministic
+// function of the positions.
+__global__ void k_sort_keys(const double* px, const double* py, const double* pz, int count,
+                            int n, double L, int G, unsigned long long* keys, int* vals) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= count) return;
+  auto bin = [L](double x, int nb) {
+    double f = x / L;
+    f -= floor(f);  // wrapped
+    const int c = int(f * nb);
+    return unsigned(c < 0 ? 0 : (c >= nb ? nb - 1 : c));
+  };
+  const unsigned long long col = bin(pz[gid], G) * unsigned(G) + bin(py[gid], G);
+  keys[gid] = (static_cast<unsigned long long>(gid / n) << 40) | (col << 20) |
+              bin(px[gid], 1 << 20);
+  vals[gid] = gid;
+}
+
+// sorted position p (= r n + k) -> perm, slot_of, species and site count
+__global__ void k_apply_order(const int* sorted_vals, int count, int n, const int* species_of,
+                              const DevTables* tab, int* perm, int* slot_of, int* sp_slot,
+                              int* nsites_slot) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= count) return;
+  const int g = sorted_vals[p];
+  const int r = g / n, i = g - r * n;
+  perm[p] = i;
+  slot_of[g] = p - r * n;
+  const int sp = species_of[i];
+  sp_slot[p] = sp;
+  nsites_slot[p] = tab->species[sp].n_sites;
+}
+
+// global exclusive scan -> per-replica slot-ordered first site
+__global__ void k_site_starts(const int* scan, int count, int n, int total_sites, int* sb_slot) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= count) return;
+  sb_slot[p] = scan[p] - (p / n) * total_sites;
 }
 
 // --------------------------------------------------------------- DFMA peak

@@ -168,6 +168,11 @@ class ForceField:
     def pair_list(self) -> np.ndarray:
         return self._c.pair_list(0)
 
+    def set_sort_interval(self, steps: int) -> None:
+        """b2md_set_sort_interval: re-sort period of the internal spatial order
+        (0 keeps the input order; results differ only in summation order)."""
+        check(_abi.lib().b2md_set_sort_interval(self._c.ctx, int(steps)))
+
     def set_search_options(self, fix_prefilter: bool = True, tile_cull: bool = True) -> None:
         """b2md_set_search_options: partner-search strategy (same results)."""
         check(_abi.lib().b2md_set_search_options(self._c.ctx, int(fix_prefilter), int(tile_cull)))
@@ -295,6 +300,11 @@ class Engine:
 
     def pair_list(self, replica: int = 0) -> np.ndarray:
         return self._c.pair_list(replica)
+
+    def set_sort_interval(self, steps: int) -> None:
+        """b2md_set_sort_interval: re-sort period of the internal spatial order
+        (0 keeps the input order; results differ only in summation order)."""
+        check(_abi.lib().b2md_set_sort_interval(self._c.ctx, int(steps)))
 
     def set_search_options(self, fix_prefilter: bool = True, tile_cull: bool = True) -> None:
         """b2md_set_search_options: partner-search strategy (same results)."""

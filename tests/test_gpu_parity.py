@@ -421,3 +421,78 @@ def test_tile_cull_after_steps():
     eng.step(50)
     s = eng.state()
     assert np.array_equal(eng.pair_list(), pyoracle.OracleFF(wl.comp, wl.opts).pair_list(s.pos))
+
+
+# ------------------------------------------------------- spatial ordering
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg1", "cfg2", "cfg3"])
+def test_spatial_order_evaluation(cfg):
+    """Sorted (default) and input-order evaluations: identical pair lists
+    (the oracle's), forces/torques/energies equal to summation order."""
+    wl = configs.make(cfg)
+    st0 = wl.states[0]
+    out = []
+    for interval in (100, 0):
+        ff = b2.ForceField(wl.comp, wl.opts)
+        ff.set_sort_interval(interval)
+        st = st0.copy()
+        ff.evaluate(st)
+        out.append((ff.pair_list(), st))
+    ref = pyoracle.OracleFF(wl.comp, wl.opts).evaluate(st0.pos, st0.orient)
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][0], pyoracle.OracleFF(wl.comp, wl.opts).pair_list(st0.pos))
+    for _, st in out:
+        check_vec(st.force, ref["force"], F_TOL, "force")
+        check_vec(st.torque, ref["torque"], F_TOL, "torque")
+        check_energy(st.energy, ref["energy"], st.virial, ref["virial"])
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2_small", "cfg3"])
+def test_spatial_order_resorts_during_steps(cfg):
+    """Re-sorts every 7 steps (eager steps between graph launches) keep the
+    trajectory on the oracle's, the pair list exact and the heat flux right."""
+    if cfg == "cfg2_small":
+        comp, opts, st = golden_cases.eval_cases()["water_ions"]
+        wl = None
+        dt, steps = 0.0005, 30
+        st = st.copy()
+        rng = np.random.default_rng(3)
+        st.vel = rng.normal(scale=0.05, size=(comp.molecule_count(), 3))
+        st.ang_vel = rng.normal(scale=0.05, size=(comp.molecule_count(), 3))
+    else:
+        wl = configs.make(cfg)
+        comp, opts, st, dt = wl.comp, wl.opts, wl.states[0], wl.dt
+        steps = 30
+    chunks, interval = (1, 1, 5, 9, 14), 7  # single-step graphs and multi-step runs
+    if cfg == "cfg3":  # the O(N^2) oracle step is ~1 s here
+        chunks, interval, steps = (1, 4, 7), 3, 12
+    eng = b2.Engine(comp, opts, dt)
+    eng.set_sort_interval(interval)
+    eng.set_state(st)
+    for chunk in chunks:
+        eng.step(chunk)
+    s = eng.state()
+    ora = pyoracle.OracleFF(comp, opts)
+    o = ora.run(dt, steps, st.pos, st.orient, st.vel, st.ang_vel)
+    L = comp.box_length
+    d = s.pos - o["pos"]
+    d -= L * np.round(d / L)
+    assert np.abs(d).max() / L <= T_TOL
+    assert np.array_equal(eng.pair_list(), ora.pair_list(s.pos))
+    h = np.linspace(-1.0, 1.0, len(comp.species))
+    check_vec(eng.heat_flux(h), ora.heat_flux(s.pos, s.orient, s.vel, s.ang_vel, h), 1e-10, "jq")
+
+
+def test_spatial_order_replicas():
+    wl = configs.make("cfg4", replicas=3, steps=12)
+    eng = b2.Engine(wl.comp, wl.opts, wl.dt, replicas=3)
+    eng.set_sort_interval(5)
+    eng.set_state(wl.states)
+    eng.step(12)
+    ora = pyoracle.OracleFF(wl.comp, wl.opts)
+    for r, s in enumerate(eng.states()):
+        st = wl.states[r]
+        o = ora.run(wl.dt, 12, st.pos, st.orient, st.vel, st.ang_vel)
+        d = s.pos - o["pos"]
+        d -= wl.comp.box_length * np.round(d / wl.comp.box_length)
+        assert np.abs(d).max() / wl.comp.box_length <= T_TOL
+        assert np.array_equal(eng.pair_list(r), ora.pair_list(s.pos))
