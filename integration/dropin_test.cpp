@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <numbers>
 
+#include "tmd/greenkubo.hpp"
 #include "tmd_gpu.hpp"
 
 using namespace tmd;
@@ -67,6 +68,14 @@ void compare_eval(const char* name, const SystemComposition& comp, const ForceFi
   expect(de <= 1e-9, "|dU| / |U|", de);
   const double dv = std::abs(a.virial - b.virial) / std::max(1.0, std::abs(a.virial));
   expect(dv <= 1e-9, "|dW| / |W|", dv);
+  // heat flux (greenkubo.cpp:182-266) of the same state, one enthalpy per species
+  std::vector<double> h;
+  for (int k = 0; k < comp.species_count(); ++k) h.push_back(0.3 - 0.7 * k);
+  const Vec3 jr = heat_flux(comp, st, cpu.table(), h);
+  const Vec3 jg = heat_flux(gpu, st, h);
+  const double js = std::max({1.0, std::abs(jr.x), std::abs(jr.y), std::abs(jr.z)});
+  const double dj = std::max({std::abs(jr.x - jg.x), std::abs(jr.y - jg.y), std::abs(jr.z - jg.z)}) / js;
+  expect(dj <= 1e-10, "heat flux |dJq| / max |Jq|", dj);
 }
 
 }  // namespace
@@ -106,6 +115,13 @@ int main() {
     expect(dp / comp.box_length <= 1e-9, "max |dpos| / L", dp / comp.box_length);
     const double de = std::abs(a.energy.total() - b.energy.total()) / std::abs(a.energy.total());
     expect(de <= 1e-9, "|dU| / |U|", de);
+    // J_q of the stepped states: the reference on its state, the GPU on its resident one
+    ForceField table_owner(comp, opts);
+    const Vec3 jr = heat_flux(comp, a, table_owner.table(), {0.4});
+    const Vec3 jg = gpu.heat_flux({0.4});
+    const double js = std::max({1.0, std::abs(jr.x), std::abs(jr.y), std::abs(jr.z)});
+    const double dj = std::max({std::abs(jr.x - jg.x), std::abs(jr.y - jg.y), std::abs(jr.z - jg.z)}) / js;
+    expect(dj <= 1e-9, "heat flux after 50 steps |dJq| / max |Jq|", dj);
   }
   // charged rigid dimers + LJ with reaction field (test_potentials.cpp:214-258 shape)
   {

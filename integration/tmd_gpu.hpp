@@ -141,10 +141,27 @@ class GpuForceField {
 
   const char* warning() const { return b2md_warning(ctx_.get()); }
 
+  // tmd::heat_flux(comp, state, table, h) (greenkubo.hpp:93, greenkubo.cpp:182-266)
+  // with this force field's pair table; state taken as given.
+  Vec3 heat_flux(const SystemState& state, const std::vector<double>& h_per_species) {
+    Vec3 jq;
+    b2md_detail::check(b2md_heat_flux_state(ctx_.get(), &state.pos[0].x, &state.orient[0].w,
+                                            &state.vel[0].x, &state.ang_vel[0].x,
+                                            h_per_species.data(),
+                                            static_cast<int>(h_per_species.size()), &jq.x));
+    return jq;
+  }
+
  private:
   const SystemComposition& comp_;
   b2md_detail::Context ctx_;
 };
+
+// Free-function form next to tmd::heat_flux.
+inline Vec3 heat_flux(GpuForceField& ff, const SystemState& state,
+                      const std::vector<double>& h_per_species) {
+  return ff.heat_flux(state, h_per_species);
+}
 
 // The step path of tmd::Engine (engine.hpp:52-112), device resident.
 class GpuEngine {
@@ -174,6 +191,15 @@ class GpuEngine {
     b2md_detail::from_c(e, s.energy);
     s.virial = st.virial;
     return s;
+  }
+
+  // J_q of the resident state, as Engine::run samples it every n_ext steps
+  // (engine.cpp:235-238)
+  Vec3 heat_flux(const std::vector<double>& h_per_species) const {
+    Vec3 jq;
+    b2md_detail::check(b2md_heat_flux(ctx_.get(), h_per_species.data(),
+                                      static_cast<int>(h_per_species.size()), &jq.x));
+    return jq;
   }
 
  private:
