@@ -50,9 +50,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-flush", action="store_true")
-    p.add_argument("--op", default="step", choices=["step", "heat_flux"],
-                   help="step: Engine::step (the north_star path); heat_flux: tmd::heat_flux "
-                        "(SURVEY 8(f) row 1) of the set state")
+    p.add_argument("--op", default="step", choices=["step", "heat_flux", "rdf"],
+                   help="step: Engine::step (the north_star path); heat_flux: tmd::heat_flux, "
+                        "rdf: RdfHistogram::accumulate (SURVEY 8(f) rows 1-2) of the set state")
     return p.parse_args()
 
 
@@ -182,12 +182,26 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------- sampler ops
+# SURVEY.md 8(f) rows measured like the step: device value on the resident
+# state, e2e through the host-buffer C-ABI call, roofline on the op's kernel,
+# the reference's own CPU implementation as the baseline.
+#
 # heat_flux (greenkubo.cpp:182-266): fp64 work per visit of an in-cutoff
 # single-site pair from one row (each pair is visited from both rows):
 # min image 12, r^2 5, 1/r^2 5, LJ 9, force 5, 0.5 f.v 6, s R accumulate 6,
 # u 1, cutoff test 1  ("heat flux")
 FLUX_FLOP_PER_VISIT = 50
-FLUX_METRIC = "heat-flux J_q evaluations/s (tmd::heat_flux)"
+# RdfHistogram::accumulate (structure.cpp:60-73): per intermolecular site pair
+# min image 12 (3 x sub, div, round, mul-sub), norm2 5, sqrt 1, div 1
+RDF_FLOP_PER_PAIR = 19
+OPS = {
+    "heat_flux": {"metric": "heat-flux J_q evaluations/s (tmd::heat_flux)", "unit": "evals/s",
+                  "family": "heat_flux"},
+    "rdf": {"metric": "RDF histogram accumulations/s (tmd::RdfHistogram::accumulate)",
+            "unit": "snapshots/s", "family": "rdf"},
+}
+RDF_BIN_WIDTH = 0.02  # SimulationPlan::rdf_bin_width default (engine.hpp:34)
 
 
 def flux_inputs(wl):
@@ -196,9 +210,37 @@ def flux_inputs(wl):
     return rng.normal(size=(n, 3)), rng.normal(size=(n, 3)), rng.normal(size=len(wl.comp.species))
 
 
-def run_heat_flux_reference(args):
-    """tmd::heat_flux of the reference (oracle/_ref) on the host: it is serial
-    (greenkubo.cpp:196-257 has no worker split), one call per step."""
+def rdf_site_pairs(wl):
+    """Intermolecular pairs of RDF sampling sites (LJ and dummy) per replica."""
+    per_species = [sum(1 for s in sp.sites if int(s.kind) != 1) for sp in wl.comp.species]
+    sites = [per_species[k] for k in wl.comp.species_index()]
+    tot = sum(sites)
+    return (tot * tot - sum(x * x for x in sites)) // 2
+
+
+def cpu_reference_op(op, wl, calls_wanted, budget_s):
+    """The reference's own serial implementation of the op (oracle/_ref)."""
+    from oracle import pyoracle
+    st = wl.states[0]
+    n = wl.comp.molecule_count()
+    vel, ang, h = flux_inputs(wl)
+    ff = pyoracle.RefFF(wl.comp, wl.opts)
+    if op == "heat_flux":
+        call = lambda: ff.heat_flux(st.pos, st.orient, vel[:n], ang[:n], h)
+    else:
+        rdf = pyoracle.RefRdf(ff, RDF_BIN_WIDTH, 0.5 * wl.comp.box_length)
+        call = lambda: rdf.accumulate(st.pos, st.orient)
+    t0 = time.perf_counter()
+    call()
+    est = time.perf_counter() - t0
+    k = max(1, min(calls_wanted, int(budget_s / max(est, 1e-6))))
+    t0 = time.perf_counter()
+    for _ in range(k):
+        call()
+    return k / (time.perf_counter() - t0), k
+
+
+def run_op_reference(args):
     rank, _, _ = dist_env()
     if rank != 0:
         return
@@ -207,40 +249,25 @@ def run_heat_flux_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtmdref.so not built"}))
         return
     wl = workload(args.config, 0, 1)
-    value, k = cpu_reference_flux(wl, args.steps, 150.0)
+    spec = OPS[args.op]
+    value, k = cpu_reference_op(args.op, wl, args.steps, 150.0)
     line = {
-        "impl": "reference", "op": "heat_flux", "metric": FLUX_METRIC, "value": value,
-        "unit": "evals/s", "n_gpus": args.gpus, "steps": k, "warmup": 1, "ms_per_step": 1e3 / value,
+        "impl": "reference", "op": args.op, "metric": spec["metric"], "value": value,
+        "unit": spec["unit"], "n_gpus": args.gpus, "steps": k, "warmup": 1, "ms_per_step": 1e3 / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, paper_1507_07548_b200/configs.py)",
         "config": {"workload": f"{args.config}: {describe(wl)}"},
-        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": 1, "kind": "reference",
-                         "sample": f"{k} tmd::heat_flux calls (serial in the reference)"},
-        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": value, "unit": spec["unit"], "cores": 1, "kind": "reference",
+                         "sample": f"{k} calls of the reference's {args.op} (serial in the reference)"},
+        "e2e": {"value": value, "unit": spec["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_reference_flux(wl, calls_wanted, budget_s):
-    from oracle import pyoracle
-    st = wl.states[0]
-    n = wl.comp.molecule_count()
-    vel, ang, h = flux_inputs(wl)
-    ff = pyoracle.RefFF(wl.comp, wl.opts)
-    t0 = time.perf_counter()
-    ff.heat_flux(st.pos, st.orient, vel[:n], ang[:n], h)
-    est = time.perf_counter() - t0
-    k = max(1, min(calls_wanted, int(budget_s / max(est, 1e-6))))
-    t0 = time.perf_counter()
-    for _ in range(k):
-        ff.heat_flux(st.pos, st.orient, vel[:n], ang[:n], h)
-    return k / (time.perf_counter() - t0), k
-
-
-def run_heat_flux(args):
-    """J_q of a device-resident state (b2md_heat_flux: what Engine::run samples
-    every n_ext steps), K calls each bracketed by CUDA events with an L2 flush
-    between; e2e through b2md_heat_flux_state with pinned host buffers."""
+def run_op(args):
+    """A sampler op on the device-resident state (what Engine::run calls every
+    n_ext / rdf_stride steps), K calls each bracketed by CUDA events with an L2
+    flush between; e2e through the host-state C-ABI entry with pinned buffers."""
     rank, world, local = dist_env()
     import torch
     import paper_1507_07548_b200 as b2
@@ -250,9 +277,11 @@ def run_heat_flux(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = workload(args.config, rank, world)
+    spec = OPS[args.op]
     R, n = wl.replicas, wl.comp.molecule_count()
+    L = wl.comp.box_length
     eng = b2.Engine(wl.comp, wl.opts, wl.dt, device=local, replicas=R)
-    if world > 1 and args.config != "cfg4":
+    if world > 1 and args.config != "cfg4" and args.op == "heat_flux":
         uid = [b2.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         eng.attach_nccl(uid[0], rank, world)
@@ -266,8 +295,10 @@ def run_heat_flux(args):
     peak_gflops = b2.measure_fp64_peak(local)
     stream = torch.cuda.ExternalStream(eng.stream(), device=local)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    rdf = b2.RdfHistogram(eng, RDF_BIN_WIDTH, 0.5 * L) if args.op == "rdf" else None
+    op_call = (lambda: eng.heat_fluxes(h)) if args.op == "heat_flux" else (lambda: rdf.accumulate())
     for _ in range(max(3, args.warmup)):
-        eng.heat_fluxes(h)
+        op_call()
 
     def timed(k):
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
@@ -275,7 +306,7 @@ def run_heat_flux(args):
         with torch.cuda.stream(stream):
             for i in range(k):
                 starts[i].record(stream)
-                eng.heat_fluxes(h)
+                op_call()
                 ends[i].record(stream)
                 if flush is not None:
                     flush.zero_()
@@ -299,20 +330,26 @@ def run_heat_flux(args):
     timed(args.steps)
     kt = eng.kernel_times()
     eng.profile(False)
-    # e2e: the reference's free-function form from host buffers (state upload,
-    # site offsets, partner search, flux, 3 doubles back)
+    # e2e: the reference's host-state form (upload + device work + result back)
     ff = b2.ForceField(wl.comp, wl.opts, device=local)
-    if world > 1 and args.config != "cfg4":
+    if world > 1 and args.config != "cfg4" and args.op == "heat_flux":
         ff.set_shard(rank, world)  # partial per rank; the e2e time is what counts
     hs = wl.states[0]
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
     hs.pos, hs.orient, hs.vel, hs.ang_vel = map(pin, (hs.pos, hs.orient, hs.vel, hs.ang_vel))
-    ff.heat_flux(hs, h)
+    if args.op == "heat_flux":
+        e2e_call = lambda: ff.heat_flux(hs, h)
+        h2d, d2h = 8 * n * 13, 8 * 3
+    else:
+        rdf_h = b2.RdfHistogram(ff, RDF_BIN_WIDTH, 0.5 * L)
+        e2e_call = lambda: (rdf_h.accumulate(hs), rdf_h.counts())
+        h2d, d2h = 8 * n * 7, 8 * rdf_h._pairs * rdf_h.bins()
+    e2e_call()
     k_e2e = max(1, args.e2e_steps)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(k_e2e):
-        ff.heat_flux(hs, h)
+        e2e_call()
     e2e_s = time.perf_counter() - t0
     if rank != 0:
         if dist is not None:
@@ -320,12 +357,19 @@ def run_heat_flux(args):
         return
     evals = args.steps * (R * world if args.config == "cfg4" else 1)
     value = evals / (total_ms * 1e-3)
-    fl_ms, fl_n = kt.get("heat_flux", (0.0, 0))
-    avg_s = fl_ms * 1e-3 / max(1, fl_n)
-    achieved = 2 * pairs_total * FLUX_FLOP_PER_VISIT / avg_s / 1e12 if avg_s > 0 else 0.0
+    k_ms, k_n = kt.get(spec["family"], (0.0, 0))
+    avg_s = k_ms * 1e-3 / max(1, k_n)
+    if args.op == "heat_flux":
+        work = 2 * pairs_total * FLUX_FLOP_PER_VISIT
+        kernel = f"k_heat_flux ({FLUX_FLOP_PER_VISIT} flop per pair visit, 2 visits per in-cutoff pair)"
+    else:
+        work = rdf_site_pairs(wl) * R * RDF_FLOP_PER_PAIR
+        kernel = (f"k_rdf_pairs ({RDF_FLOP_PER_PAIR} flop per intermolecular site pair, "
+                  f"bin width {RDF_BIN_WIDTH}, r_max L/2)")
+    achieved = work / avg_s / 1e12 if avg_s > 0 else 0.0
     peak = peak_gflops / 1e3
     line = {
-        "op": "heat_flux", "metric": FLUX_METRIC, "value": value, "unit": "evals/s",
+        "op": args.op, "metric": spec["metric"], "value": value, "unit": spec["unit"],
         "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
         "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if args.config == "cfg4" else "strong", "vs_baseline": None,
@@ -333,26 +377,25 @@ def run_heat_flux(args):
         "config": {"workload": f"{args.config}: {describe(wl)}",
                    "l2": "flushed between timed calls (256 MiB memset outside the events)"
                    if flush is not None else "not flushed",
-                   "timing": "per-call CUDA events on the library stream (kernel + 3-double readback)"},
-        "e2e": {"value": k_e2e * (R if args.config == "cfg4" else 1) / e2e_s, "unit": "evals/s",
-                "h2d_bytes_per_step": 8 * n * R * 13, "d2h_bytes_per_step": 8 * 3 * R,
-                "path": "b2md_heat_flux_state (upload, offsets, partner search, flux), pinned host buffers"},
-        "roofline": {"bound": "fp64", "kernel": f"k_heat_flux ({FLUX_FLOP_PER_VISIT} flop per pair visit, "
-                     "2 visits per in-cutoff pair; single-site count)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak if peak else None, "traffic": None,
+                   "timing": "per-call CUDA events on the library stream (kernels + small readback)"},
+        "e2e": {"value": k_e2e * (R if args.config == "cfg4" else 1) / e2e_s, "unit": spec["unit"],
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": ("b2md_heat_flux_state" if args.op == "heat_flux" else
+                         "b2md_rdf_accumulate_state + b2md_rdf_counts") + ", pinned host buffers"},
+        "roofline": {"bound": "fp64", "kernel": kernel, "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
                      "launch_ms": avg_s * 1e3},
         "kernel_ms_per_launch": {k: v[0] / max(1, v[1]) for k, v in kt.items()},
-        "gpu_launches": args.steps,
+        "gpu_launches": int(sum(c for _, c in kt.values())),
         "clocks": clk,
     }
     if not args.no_cpu_baseline and world == 1:
         try:
             from oracle import pyoracle
             if pyoracle.ref_available():
-                v, k = cpu_reference_flux(wl, 10 ** 6, args.cpu_seconds)
-                line["cpu_baseline"] = {"value": v, "unit": "evals/s", "cores": 1, "kind": "reference",
-                                        "sample": f"{k} tmd::heat_flux calls of {args.config} (serial)"}
+                v, k = cpu_reference_op(args.op, wl, 10 ** 6, args.cpu_seconds)
+                line["cpu_baseline"] = {"value": v, "unit": spec["unit"], "cores": 1, "kind": "reference",
+                                        "sample": f"{k} calls of the reference's {args.op} on {args.config} (serial)"}
         except Exception as exc:
             line["cpu_baseline"] = {"error": str(exc)}
     print(json.dumps(line), flush=True)
@@ -401,8 +444,8 @@ def describe(wl):
 
 def main():
     args = parse()
-    if args.op == "heat_flux":
-        (run_heat_flux_reference if args.impl == "reference" else run_heat_flux)(args)
+    if args.op != "step":
+        (run_op_reference if args.impl == "reference" else run_op)(args)
         return
     if args.impl == "reference":
         run_reference_arm(args)

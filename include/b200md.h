@@ -237,6 +237,29 @@ int b2md_heat_flux_state(b2md_ctx* ctx, const double* pos, const double* orient,
                          const double* vel, const double* ang_vel, const double* enthalpy,
                          int n_enthalpy, double* jq);
 
+/* Radial distribution histograms: tmd::RdfHistogram (include/tmd/structure.hpp:
+ * 29-67, src/structure.cpp:10-76) over a context's composition, one histogram
+ * per replica, accumulated on the device.  Sampling sites are every LJ and
+ * dummy site (charge-only sites skipped); site types are numbered in
+ * (species, site) order; counts are uint64 [pair][bin] with pair(ta <= tb) =
+ * ta*T - ta(ta+1)/2 + tb, exactly the reference's (integer, bit-exact).
+ * create fails like the constructor: bin_width <= 0 or r_max > L/2 (+1e-12)
+ * is B2MD_CONFIG_ERROR.  finalize / first_minimum / solvation_number are
+ * host arithmetic on these counts (structure.cpp:78-194). */
+typedef struct b2md_rdf b2md_rdf;
+int b2md_rdf_create(b2md_ctx* ctx, double bin_width, double r_max, b2md_rdf** out);
+void b2md_rdf_destroy(b2md_rdf* rdf);
+int b2md_rdf_shape(const b2md_rdf* rdf, int* n_types, int* bins, int* n_pairs);
+int b2md_rdf_types(const b2md_rdf* rdf, int* species, int* site);
+/* accumulate (structure.cpp:38-76) of the context's device state, every replica */
+int b2md_rdf_accumulate(b2md_rdf* rdf);
+/* ... of host positions / orientations (AoS, n_replicas systems, as given);
+ * replaces the context's device state (an Engine needs a new set_state). */
+int b2md_rdf_accumulate_state(b2md_rdf* rdf, const double* pos, const double* orient);
+int b2md_rdf_counts(const b2md_rdf* rdf, int replica, uint64_t* counts, int64_t* snapshots);
+/* restore counts (RdfHistogram::deserialize, structure.cpp:142-153); NULL zeroes */
+int b2md_rdf_set_counts(b2md_rdf* rdf, int replica, const uint64_t* counts, int64_t snapshots);
+
 /* Multi-GPU row sharding (one process per GPU).  b2md_nccl_unique_id fills a
  * 128-byte ncclUniqueId on the root; every rank then calls b2md_attach_nccl
  * with the broadcast id.  After attaching, each rank evaluates only its shard

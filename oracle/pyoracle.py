@@ -52,6 +52,11 @@ def oracle_lib():
         L.oracle_pair_list.restype = C.c_int64
         L.oracle_wrap.argtypes = [C.c_int, C.c_double, _D]
         L.oracle_heat_flux.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, C.c_int, _D]
+        L.oracle_rdf_create.argtypes = [C.c_void_p, C.c_double, C.c_double, C.POINTER(C.c_void_p)]
+        L.oracle_rdf_destroy.argtypes = [C.c_void_p]
+        L.oracle_rdf_accumulate.argtypes = [C.c_void_p, _D, _D]
+        L.oracle_rdf_shape.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.oracle_rdf_counts.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int64)]
         L.oracle_step.argtypes = [C.c_void_p, C.c_double, C.c_int64, _D, _D, _D, _D, _D, _D,
                                   C.POINTER(_abi.b2md_energy), C.POINTER(_abi.b2md_eval_stats)]
         _oracle = L
@@ -79,6 +84,17 @@ def ref_lib():
         L.ref_pair_list.argtypes = [C.c_void_p, _D, C.POINTER(C.c_int32), C.c_int64]
         L.ref_pair_list.restype = C.c_int64
         L.ref_heat_flux.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, C.c_int, _D]
+        L.ref_rdf_create.argtypes = [C.c_void_p, C.c_double, C.c_double, C.POINTER(C.c_void_p)]
+        L.ref_rdf_destroy.argtypes = [C.c_void_p]
+        L.ref_rdf_accumulate.argtypes = [C.c_void_p, C.c_void_p, _D, _D]
+        L.ref_rdf_serialize.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+        L.ref_rdf_serialize.restype = C.c_int64
+        L.ref_rdf_finalize.argtypes = [C.c_void_p, _D, C.c_int64]
+        L.ref_rdf_finalize.restype = C.c_int64
+        L.ref_first_minimum.argtypes = [_D, _D, C.c_int]
+        L.ref_first_minimum.restype = C.c_double
+        L.ref_solvation_number.argtypes = [C.c_double, _D, C.c_int, C.c_double, C.c_double]
+        L.ref_solvation_number.restype = C.c_double
         L.ref_engine_create.argtypes = [C.POINTER(_abi.b2md_composition), C.POINTER(_abi.b2md_ff_options), C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]
         L.ref_engine_destroy.argtypes = [C.c_void_p]
         L.ref_engine_set_state.argtypes = [C.c_void_p, _D, _D, _D, _D]
@@ -264,3 +280,106 @@ class RefEngine:
         out["energy"] = EnergyBreakdown.from_c(e)
         out["virial"] = float(v[0])
         return out
+
+
+class OracleRdf:
+    """oracle_rdf_*: the C restatement of tmd::RdfHistogram accumulate."""
+
+    def __init__(self, ff: "OracleFF", bin_width: float, r_max: float):
+        self.ff = ff
+        self.lib = ff.lib
+        h = C.c_void_p()
+        _check(self.lib, "oracle", self.lib.oracle_rdf_create(ff.h, bin_width, r_max, C.byref(h)))
+        self.h = h
+        t, b, p = C.c_int(), C.c_int(), C.c_int()
+        self.lib.oracle_rdf_shape(self.h, C.byref(t), C.byref(b), C.byref(p))
+        self.n_types, self.bins, self.n_pairs = t.value, b.value, p.value
+
+    def __del__(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.oracle_rdf_destroy(self.h)
+            self.h = None
+
+    def accumulate(self, pos, orient):
+        n = self.ff.n
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(n, 3)
+        orient = np.ascontiguousarray(orient, dtype=np.float64).reshape(n, 4)
+        _check(self.lib, "oracle", self.lib.oracle_rdf_accumulate(self.h, _d(pos), _d(orient)))
+
+    def counts(self):
+        out = np.zeros((self.n_pairs, self.bins), dtype=np.uint64)
+        snaps = C.c_int64()
+        self.lib.oracle_rdf_counts(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(snaps))
+        return out, snaps.value
+
+
+class RefRdf:
+    """The unmodified tmd::RdfHistogram (oracle/_ref)."""
+
+    def __init__(self, ff: "RefFF", bin_width: float, r_max: float):
+        self.ff = ff
+        self.lib = ff.lib
+        h = C.c_void_p()
+        _check(self.lib, "ref", self.lib.ref_rdf_create(ff.h, bin_width, r_max, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.ref_rdf_destroy(self.h)
+            self.h = None
+
+    def accumulate(self, pos, orient):
+        n = self.ff.n
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(n, 3)
+        orient = np.ascontiguousarray(orient, dtype=np.float64).reshape(n, 4)
+        _check(self.lib, "ref", self.lib.ref_rdf_accumulate(self.h, self.ff.h, _d(pos), _d(orient)))
+
+    def serialize(self) -> bytes:
+        n = self.lib.ref_rdf_serialize(self.h, None, 0)
+        buf = C.create_string_buffer(int(n))
+        self.lib.ref_rdf_serialize(self.h, buf, n)
+        return buf.raw
+
+    def counts(self):
+        """Counts parsed from RdfHistogram::serialize (structure.cpp:130-140)."""
+        b = self.serialize()
+        bins = int(np.frombuffer(b, np.uint32, 1, 16)[0])
+        snaps = int(np.frombuffer(b, np.int64, 1, 20)[0])
+        npairs = int(np.frombuffer(b, np.uint64, 1, 28)[0])
+        out = np.zeros((npairs, bins), dtype=np.uint64)
+        o = 36
+        for p in range(npairs):
+            nb = int(np.frombuffer(b, np.uint64, 1, o)[0])
+            out[p] = np.frombuffer(b, np.uint64, nb, o + 8)
+            o += 8 + 8 * nb
+        return out, snaps
+
+    def finalize(self):
+        n = self.lib.ref_rdf_finalize(self.h, None, 0)
+        if n < 0:
+            raise OracleError(2, self.lib.ref_last_error().decode())
+        v = np.zeros(int(n))
+        self.lib.ref_rdf_finalize(self.h, _d(v), n)
+        tables, o = [], 0
+        while o < len(v):
+            sa, sb, dens, bw, snaps, nb = v[o:o + 6]
+            nb = int(nb)
+            body = v[o + 6:o + 6 + 3 * nb].reshape(nb, 3)
+            tables.append({"species_a": int(sa), "species_b": int(sb), "partner_density": dens,
+                           "bin_width": bw, "snapshots": int(snaps), "r_mid": body[:, 0].copy(),
+                           "g": body[:, 1].copy(), "n_cum": body[:, 2].copy()})
+            o += 6 + 3 * nb
+        return tables
+
+
+def ref_first_minimum(r_mid, g):
+    L = ref_lib()
+    r_mid = np.ascontiguousarray(r_mid, dtype=np.float64)
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    return L.ref_first_minimum(_d(r_mid), _d(g), len(g))
+
+
+def ref_solvation_number(bin_width, g, partner_density, r_min):
+    L = ref_lib()
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    return L.ref_solvation_number(bin_width, _d(g), len(g), partner_density, r_min)

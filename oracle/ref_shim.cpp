@@ -16,7 +16,9 @@
 #include <vector>
 
 #include "tmd/engine.hpp"
+#include "tmd/checkpoint.hpp"
 #include "tmd/greenkubo.hpp"
+#include "tmd/structure.hpp"
 #include "tmd/parallel.hpp"
 #include "../include/b200md.h"
 
@@ -338,4 +340,66 @@ extern "C" int ref_heat_flux(void* h, const double* pos, const double* orient, c
     jq[2] = j.z;
     return B2MD_OK;
   });
+}
+
+// ---------------------------------------------- tmd::RdfHistogram (structure.cpp)
+extern "C" int ref_rdf_create(void* ffh, double bin_width, double r_max, void** out) {
+  return guarded([&]() -> int {
+    auto* f = static_cast<RefFF*>(ffh);
+    *out = new tmd::RdfHistogram(f->comp, bin_width, r_max);
+    return B2MD_OK;
+  });
+}
+
+extern "C" void ref_rdf_destroy(void* h) { delete static_cast<tmd::RdfHistogram*>(h); }
+
+extern "C" int ref_rdf_accumulate(void* h, void* ffh, const double* pos, const double* orient) {
+  return guarded([&]() -> int {
+    auto* f = static_cast<RefFF*>(ffh);
+    tmd::SystemState st;
+    st.box_length = f->comp.box_length;
+    get_state(st, f->comp.molecule_count(), pos, orient, nullptr, nullptr);
+    static_cast<tmd::RdfHistogram*>(h)->accumulate(st);
+    return B2MD_OK;
+  });
+}
+
+// RdfHistogram::serialize bytes (structure.cpp:130-140); returns the length
+extern "C" int64_t ref_rdf_serialize(void* h, char* buf, int64_t cap) {
+  tmd::ByteWriter w;
+  static_cast<tmd::RdfHistogram*>(h)->serialize(w);
+  const std::string& d = w.data();
+  if (buf && cap >= static_cast<int64_t>(d.size())) std::memcpy(buf, d.data(), d.size());
+  return static_cast<int64_t>(d.size());
+}
+
+// RdfHistogram::finalize (structure.cpp:78-128), flattened per table:
+// species_a, species_b, partner_density, bin_width, snapshots, bins, then
+// bins x (r_mid, g, n_cum).  Returns the number of doubles.
+extern "C" int64_t ref_rdf_finalize(void* h, double* out, int64_t cap) {
+  std::vector<double> v;
+  try {
+    for (const auto& t : static_cast<tmd::RdfHistogram*>(h)->finalize()) {
+      v.insert(v.end(), {double(t.species_a), double(t.species_b), t.partner_density, t.bin_width,
+                         double(t.snapshots), double(t.g.size())});
+      for (std::size_t b = 0; b < t.g.size(); ++b) v.insert(v.end(), {t.r_mid[b], t.g[b], t.n_cum[b]});
+    }
+  } catch (const std::exception& e) {
+    fail(B2MD_CONFIG_ERROR, e.what());
+    return -1;
+  }
+  if (out && cap >= static_cast<int64_t>(v.size())) std::memcpy(out, v.data(), v.size() * 8);
+  return static_cast<int64_t>(v.size());
+}
+
+extern "C" double ref_first_minimum(const double* r_mid, const double* g, int n) {
+  return tmd::first_minimum(std::vector<double>(r_mid, r_mid + n), std::vector<double>(g, g + n));
+}
+
+extern "C" double ref_solvation_number(double bin_width, const double* g, int n,
+                                       double partner_density, double r_min) {
+  tmd::RdfTable t;
+  t.bin_width = bin_width;
+  t.g.assign(g, g + n);
+  return tmd::solvation_number(t, partner_density, r_min);
 }

@@ -1073,3 +1073,137 @@ int oracle_heat_flux(oracle_ff* ff, const double* pos, const double* orient, con
   free(w_lab);
   return B2MD_OK;
 }
+
+/* ------------------------------------------------ RdfHistogram, structure.cpp */
+
+struct oracle_rdf {
+  const oracle_ff* ff;
+  double bin_width, r_max;
+  int bins, n_types;
+  int* type_species; /* per type */
+  int* type_site;
+  int* type_of_site;       /* per (species, site), -1 for charge sites */
+  int* species_type_begin; /* ns + 1 */
+  uint64_t* counts;        /* n_pairs * bins */
+  int64_t snapshots;
+};
+
+/* structure.cpp:10-36 */
+int oracle_rdf_create(const oracle_ff* ff, double bin_width, double r_max, oracle_rdf** out) {
+  if (!ff || !out) return fail(B2MD_INVALID_ARGUMENT, "rdf: null pointer");
+  if (bin_width <= 0.0) return fail(B2MD_CONFIG_ERROR, "rdf: bin width must be positive");
+  if (r_max > 0.5 * ff->box + 1e-12)
+    return fail(B2MD_CONFIG_ERROR, "rdf: r_max exceeds half the box length");
+  oracle_rdf* r = (oracle_rdf*)calloc(1, sizeof *r);
+  r->ff = ff;
+  r->bin_width = bin_width;
+  r->r_max = r_max;
+  r->bins = (int)ceil(r_max / bin_width);
+  int total = 0;
+  for (int s = 0; s < ff->ns; ++s) total += ff->species[s].n_sites;
+  r->type_of_site = (int*)malloc(sizeof(int) * (size_t)(total > 0 ? total : 1));
+  r->type_species = (int*)malloc(sizeof(int) * (size_t)(total > 0 ? total : 1));
+  r->type_site = (int*)malloc(sizeof(int) * (size_t)(total > 0 ? total : 1));
+  r->species_type_begin = (int*)malloc(sizeof(int) * (size_t)(ff->ns + 1));
+  int k_all = 0;
+  for (int s = 0; s < ff->ns; ++s) {
+    r->species_type_begin[s] = k_all;
+    const b2md_species* sp = &ff->species[s];
+    for (int k = 0; k < sp->n_sites; ++k, ++k_all) {
+      if (sp->sites[k].kind == B2MD_SITE_CHARGE) {
+        r->type_of_site[k_all] = -1;
+      } else {
+        r->type_of_site[k_all] = r->n_types;
+        r->type_species[r->n_types] = s;
+        r->type_site[r->n_types] = k;
+        ++r->n_types;
+      }
+    }
+  }
+  r->species_type_begin[ff->ns] = k_all;
+  const int t = r->n_types;
+  r->counts = (uint64_t*)calloc((size_t)(t * (t + 1) / 2) * (size_t)(r->bins > 0 ? r->bins : 1),
+                                sizeof(uint64_t));
+  *out = r;
+  return B2MD_OK;
+}
+
+void oracle_rdf_destroy(oracle_rdf* r) {
+  if (!r) return;
+  free(r->type_species);
+  free(r->type_site);
+  free(r->type_of_site);
+  free(r->species_type_begin);
+  free(r->counts);
+  free(r);
+}
+
+/* structure.hpp:51-54 */
+static int rdf_pair_index(const oracle_rdf* r, int ta, int tb) {
+  return ta * r->n_types - ta * (ta + 1) / 2 + tb;
+}
+
+/* structure.cpp:38-76 */
+int oracle_rdf_accumulate(oracle_rdf* r, const double* pos, const double* orient) {
+  if (!r || !pos || !orient) return fail(B2MD_INVALID_ARGUMENT, "rdf: null pointer");
+  const oracle_ff* ff = r->ff;
+  const int n = ff->n;
+  const double r_max2 = r->r_max * r->r_max;
+  int cap = 0;
+  for (int m = 0; m < n; ++m) cap += ff->species[species_of_molecule(ff, m)].n_sites;
+  vec3* site_pos = (vec3*)malloc(sizeof(vec3) * (size_t)(cap > 0 ? cap : 1));
+  int* site_type = (int*)malloc(sizeof(int) * (size_t)(cap > 0 ? cap : 1));
+  int* mol_begin = (int*)malloc(sizeof(int) * (size_t)(n + 1));
+  int ns = 0;
+  for (int m = 0; m < n; ++m) {
+    mol_begin[m] = ns;
+    const int s = species_of_molecule(ff, m);
+    const b2md_species* sp = &ff->species[s];
+    for (int k = 0; k < sp->n_sites; ++k) {
+      const int t = r->type_of_site[r->species_type_begin[s] + k];
+      if (t < 0) continue;
+      const vec3 b = v3(sp->sites[k].body_pos[0], sp->sites[k].body_pos[1], sp->sites[k].body_pos[2]);
+      site_pos[ns] = vadd(load3(pos, m), rotate(load4(orient, m), b));
+      site_type[ns] = t;
+      ++ns;
+    }
+  }
+  mol_begin[n] = ns;
+  for (int mi = 0; mi < n; ++mi) {
+    for (int mj = mi + 1; mj < n; ++mj) {
+      for (int a = mol_begin[mi]; a < mol_begin[mi + 1]; ++a) {
+        for (int b = mol_begin[mj]; b < mol_begin[mj + 1]; ++b) {
+          const vec3 d = minimum_image(vsub(site_pos[a], site_pos[b]), ff->box);
+          const double d2 = vnorm2(d);
+          if (d2 >= r_max2) continue;
+          const int bin = (int)(sqrt(d2) / r->bin_width);
+          if (bin >= r->bins) continue;
+          const int ta = site_type[a] < site_type[b] ? site_type[a] : site_type[b];
+          const int tb = site_type[a] < site_type[b] ? site_type[b] : site_type[a];
+          ++r->counts[(size_t)rdf_pair_index(r, ta, tb) * (size_t)r->bins + (size_t)bin];
+        }
+      }
+    }
+  }
+  ++r->snapshots;
+  free(site_pos);
+  free(site_type);
+  free(mol_begin);
+  return B2MD_OK;
+}
+
+int oracle_rdf_shape(const oracle_rdf* r, int* n_types, int* bins, int* n_pairs) {
+  if (!r) return fail(B2MD_INVALID_ARGUMENT, "rdf: null pointer");
+  if (n_types) *n_types = r->n_types;
+  if (bins) *bins = r->bins;
+  if (n_pairs) *n_pairs = r->n_types * (r->n_types + 1) / 2;
+  return B2MD_OK;
+}
+
+int oracle_rdf_counts(const oracle_rdf* r, uint64_t* counts, int64_t* snapshots) {
+  if (!r) return fail(B2MD_INVALID_ARGUMENT, "rdf: null pointer");
+  const size_t nc = (size_t)(r->n_types * (r->n_types + 1) / 2) * (size_t)r->bins;
+  if (counts) memcpy(counts, r->counts, sizeof(uint64_t) * nc);
+  if (snapshots) *snapshots = r->snapshots;
+  return B2MD_OK;
+}

@@ -69,6 +69,17 @@ int oracle_step(oracle_ff* ff, double dt, int64_t nsteps, double* pos, double* o
 int oracle_heat_flux(oracle_ff* ff, const double* pos, const double* orient, const double* vel,
                      const double* ang_vel, const double* enthalpy, int n_enthalpy, double* jq);
 
+/* RdfHistogram (include/tmd/structure.hpp:29-67, src/structure.cpp:10-76):
+ * integer site-pair histograms per unordered site-type pair. */
+typedef struct oracle_rdf oracle_rdf;
+int oracle_rdf_create(const oracle_ff* ff, double bin_width, double r_max, oracle_rdf** out);
+void oracle_rdf_destroy(oracle_rdf* rdf);
+/* structure.cpp:38-76 */
+int oracle_rdf_accumulate(oracle_rdf* rdf, const double* pos, const double* orient);
+int oracle_rdf_shape(const oracle_rdf* rdf, int* n_types, int* bins, int* n_pairs);
+/* counts[pair * bins + bin] */
+int oracle_rdf_counts(const oracle_rdf* rdf, uint64_t* counts, int64_t* snapshots);
+
 #ifdef __cplusplus
 }
 #endif

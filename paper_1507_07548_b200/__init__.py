@@ -16,6 +16,8 @@ from .forcefield import (
     nccl_unique_id,
     shard_plan,
 )
+from .structure import (RdfHistogram, RdfTable, finalize_tables, first_minimum, rdf_site_types,
+                        serialize_counts, solvation_number)
 from .model import (
     ElectrostaticsMethod,
     EnergyBreakdown,

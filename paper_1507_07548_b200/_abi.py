@@ -139,6 +139,14 @@ SIGNATURES = {
     "b2md_set_sort_interval": (C.c_int, [_CTX, C.c_int]),
     "b2md_heat_flux": (C.c_int, [_CTX, _D, C.c_int, _D]),
     "b2md_heat_flux_state": (C.c_int, [_CTX, _D, _D, _D, _D, _D, C.c_int, _D]),
+    "b2md_rdf_create": (C.c_int, [_CTX, C.c_double, C.c_double, C.POINTER(C.c_void_p)]),
+    "b2md_rdf_destroy": (None, [C.c_void_p]),
+    "b2md_rdf_shape": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "b2md_rdf_types": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "b2md_rdf_accumulate": (C.c_int, [C.c_void_p]),
+    "b2md_rdf_accumulate_state": (C.c_int, [C.c_void_p, _D, _D]),
+    "b2md_rdf_counts": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_int64)]),
+    "b2md_rdf_set_counts": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.c_int64]),
     "b2md_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "b2md_attach_nccl": (C.c_int, [_CTX, C.c_char_p, C.c_int, C.c_int]),
     "b2md_set_shard": (C.c_int, [_CTX, C.c_int, C.c_int]),

@@ -17,6 +17,7 @@
 
 #include "../../include/b200md.h"
 #include "kernels.cuh"
+#include "rdf.cuh"
 #include "model.hpp"
 #include "search_geometry.hpp"
 
@@ -88,10 +89,10 @@ __global__ void k_soa_to_aos(double* aos, int count, int width, const double* d0
 }
 
 enum Family { F_OFFSETS, F_SEARCH, F_FORCE, F_EWALD_TAB, F_EWALD_SK, F_EWALD_F, F_KICK_KICK_DRIFT,
-              F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_HEAT_FLUX, F_COUNT };
+              F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_HEAT_FLUX, F_RDF, F_COUNT };
 const char* kFamilyName[F_COUNT] = {"offsets",  "search", "force",   "ewald_tables", "ewald_sk",
                                     "ewald_force", "kick_kick_drift", "kick_drift", "kick", "allreduce",
-                                    "heat_flux"};
+                                    "heat_flux", "rdf"};
 
 }  // namespace
 
@@ -1361,6 +1362,246 @@ int b2md_pair_list(b2md_ctx* c, int replica, int32_t* pairs, int64_t capacity, i
     }
   }
   cudaFree(d_cnt);
+  return B2MD_OK;
+}
+
+// ---------------------------------------------------------------- RDF
+// tmd::RdfHistogram (include/tmd/structure.hpp:29-67) over a context: one
+// histogram per replica, accumulated on the device (rdf.cuh).
+struct b2md_rdf {
+  b2md_ctx* ctx = nullptr;
+  double bin_width = 0.0, r_max = 0.0;
+  int bins = 0, n_types = 0, n_pairs = 0, S = 0;
+  std::vector<int> type_species, type_site;
+  std::vector<int64_t> snapshots;  // per replica
+  int* d_site_mol = nullptr;
+  int* d_site_k = nullptr;
+  int* d_site_type = nullptr;
+  double4* d_sites = nullptr;
+  uint4* d_fix = nullptr;
+  unsigned long long* d_counts = nullptr;
+};
+
+namespace {
+
+void rdf_free(b2md_rdf* h) {
+  if (!h) return;
+  void* ptrs[] = {h->d_site_mol, h->d_site_k, h->d_site_type, h->d_sites, h->d_fix, h->d_counts};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete h;
+}
+
+// structure.cpp:38-76 on the context's device positions / orientations
+int rdf_launch(b2md_rdf* h) {
+  b2md_ctx* c = h->ctx;
+  for (auto& s : h->snapshots) ++s;
+  if (h->S == 0 || h->n_pairs == 0 || h->bins == 0) return B2MD_OK;
+  RdfArgs a;
+  a.s = c->sys;
+  a.px = c->st.px;
+  a.py = c->st.py;
+  a.pz = c->st.pz;
+  a.qw = c->st.qw;
+  a.qx = c->st.qx;
+  a.qy = c->st.qy;
+  a.qz = c->st.qz;
+  a.site_mol = h->d_site_mol;
+  a.site_k = h->d_site_k;
+  a.site_type = h->d_site_type;
+  a.S = h->S;
+  a.n_types = h->n_types;
+  a.bins = h->bins;
+  a.n_pairs = h->n_pairs;
+  a.rmax2 = h->r_max * h->r_max;  // structure.cpp:41
+  a.bin_width = h->bin_width;
+  a.sites = h->d_sites;
+  a.fix = h->d_fix;
+  a.counts = h->d_counts;
+  a.L = c->t.box;
+  {
+    // fp32 fast-path margins (rdf.cuh, k_rdf_pairs): relative 2e-6 on d2
+    // (bound 5.4e-7: nine fp32 roundings) plus the fixed-point quantisation
+    // (<= 1 unit of L/2^32 per axis: |dd| <= sqrt(3) units, 4 taken); the
+    // thresholds' own fp32 rounding is covered by the extra 1e-6
+    const double L = c->t.box, unit = L / 4294967296.0;
+    const double r2 = a.rmax2, rm = h->r_max, dd = 4.0 * unit;
+    a.scale = float(unit);
+    a.rmax2_lo = float((r2 * (1.0 - 2e-6) - 2.0 * rm * dd) * (1.0 - 1e-6));
+    a.rmax2_hi = float((r2 * (1.0 + 2e-6) + 2.0 * rm * dd + dd * dd) * (1.0 + 1e-6));
+    a.inv_bw_f = float(1.0 / h->bin_width);
+    a.bin_abs = float(2.0 * dd / h->bin_width + 1e-6);
+  }
+  const int total = h->S * c->R;
+  k_rdf_stage<<<(total + 255) / 256, 256, 0, c->stream>>>(a);
+  CU(cudaGetLastError());
+  a.inv_bw = 1.0 / h->bin_width;
+  // tile side: the largest of 256 / 128 / 64 that still gives ~2 CTAs per SM
+  const int nc = h->n_pairs * h->bins;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  auto ctas = [&](int t) {
+    const long nb = (h->S + t - 1) / t;
+    return nb * (nb + 1) / 2 * c->R;
+  };
+  const int T = ctas(256) >= 2 * sms ? 256 : (ctas(128) >= 2 * sms ? 128 : 64);
+  const int nb = (h->S + T - 1) / T;
+  const dim3 grid(nb, nb, c->R);
+  // a per-CTA shared histogram pays when the tile's pairs outnumber its counters
+  const bool shared = nc <= kRdfSharedCounters && T * T >= 4 * nc;
+  const size_t sm = shared ? sizeof(unsigned) * nc : 0;
+#define RDF_LAUNCH(TT)                                                                   \
+  if (shared)                                                                            \
+    PROF(c, F_RDF, (k_rdf_pairs<TT, true><<<grid, TT, sm, c->stream>>>(a)));             \
+  else                                                                                   \
+    PROF(c, F_RDF, (k_rdf_pairs<TT, false><<<grid, TT, 0, c->stream>>>(a)));
+  if (T == 256) {
+    RDF_LAUNCH(256)
+  } else if (T == 128) {
+    RDF_LAUNCH(128)
+  } else {
+    RDF_LAUNCH(64)
+  }
+#undef RDF_LAUNCH
+  return B2MD_OK;
+}
+
+}  // namespace
+
+int b2md_rdf_create(b2md_ctx* c, double bin_width, double r_max, b2md_rdf** out) {
+  if (!c || !out) return set_err(B2MD_INVALID_ARGUMENT, "rdf: null pointer");
+  // structure.cpp:12-14
+  if (bin_width <= 0.0) return set_err(B2MD_CONFIG_ERROR, "rdf: bin width must be positive");
+  if (r_max > 0.5 * c->t.box + 1e-12)
+    return set_err(B2MD_CONFIG_ERROR, "rdf: r_max exceeds half the box length");
+  CU(cudaSetDevice(c->device));
+  auto* h = new b2md_rdf;
+  h->ctx = c;
+  h->bin_width = bin_width;
+  h->r_max = r_max;
+  h->bins = static_cast<int>(std::ceil(r_max / bin_width));
+  // structure.cpp:17-32: types in (species, site) order, charge sites skipped
+  std::vector<int> type_of(c->t.ns * B2MD_MAX_SITES, -1);
+  for (int s = 0; s < c->t.ns; ++s) {
+    const b2md_species& sp = c->t.species[s];
+    for (int k = 0; k < sp.n_sites; ++k) {
+      if (sp.sites[k].kind == B2MD_SITE_CHARGE) continue;
+      type_of[s * B2MD_MAX_SITES + k] = h->n_types++;
+      h->type_species.push_back(s);
+      h->type_site.push_back(k);
+    }
+  }
+  h->n_pairs = h->n_types * (h->n_types + 1) / 2;
+  std::vector<int> site_mol, site_k, site_type;
+  for (int m = 0; m < c->t.n; ++m) {
+    const int s = c->t.species_of[m];
+    for (int k = 0; k < c->t.species[s].n_sites; ++k) {
+      const int t = type_of[s * B2MD_MAX_SITES + k];
+      if (t < 0) continue;
+      site_mol.push_back(m);
+      site_k.push_back(k);
+      site_type.push_back(t);
+    }
+  }
+  h->S = static_cast<int>(site_mol.size());
+  h->snapshots.assign(c->R, 0);
+  int rc = B2MD_OK;
+  const size_t nc = size_t(h->n_pairs) * h->bins * c->R;
+  if (h->S > 0) {
+    rc = dalloc(&h->d_site_mol, h->S);
+    if (!rc) rc = dalloc(&h->d_site_k, h->S);
+    if (!rc) rc = dalloc(&h->d_site_type, h->S);
+    if (!rc) rc = dalloc(&h->d_sites, size_t(h->S) * c->R);
+    if (!rc) rc = dalloc(&h->d_fix, size_t(h->S) * c->R);
+    if (!rc) {
+      cudaMemcpy(h->d_site_mol, site_mol.data(), sizeof(int) * h->S, cudaMemcpyHostToDevice);
+      cudaMemcpy(h->d_site_k, site_k.data(), sizeof(int) * h->S, cudaMemcpyHostToDevice);
+      cudaMemcpy(h->d_site_type, site_type.data(), sizeof(int) * h->S, cudaMemcpyHostToDevice);
+    }
+  }
+  if (!rc && nc > 0) {
+    rc = dalloc(&h->d_counts, nc);
+    if (!rc && cudaMemset(h->d_counts, 0, sizeof(unsigned long long) * nc) != cudaSuccess)
+      rc = set_err(B2MD_CUDA_ERROR, "rdf: memset failed");
+  }
+  if (rc) {
+    rdf_free(h);
+    return rc;
+  }
+  *out = h;
+  return B2MD_OK;
+}
+
+void b2md_rdf_destroy(b2md_rdf* h) {
+  if (h && h->ctx) cudaSetDevice(h->ctx->device);
+  rdf_free(h);
+}
+
+int b2md_rdf_shape(const b2md_rdf* h, int* n_types, int* bins, int* n_pairs) {
+  if (!h) return set_err(B2MD_INVALID_ARGUMENT, "rdf: null handle");
+  if (n_types) *n_types = h->n_types;
+  if (bins) *bins = h->bins;
+  if (n_pairs) *n_pairs = h->n_pairs;
+  return B2MD_OK;
+}
+
+int b2md_rdf_types(const b2md_rdf* h, int* species, int* site) {
+  if (!h) return set_err(B2MD_INVALID_ARGUMENT, "rdf: null handle");
+  for (int t = 0; t < h->n_types; ++t) {
+    if (species) species[t] = h->type_species[t];
+    if (site) site[t] = h->type_site[t];
+  }
+  return B2MD_OK;
+}
+
+int b2md_rdf_accumulate(b2md_rdf* h) {
+  if (!h) return set_err(B2MD_INVALID_ARGUMENT, "rdf: null handle");
+  CU(cudaSetDevice(h->ctx->device));
+  return rdf_launch(h);
+}
+
+int b2md_rdf_accumulate_state(b2md_rdf* h, const double* pos, const double* orient) {
+  if (!h || !pos || !orient) return set_err(B2MD_INVALID_ARGUMENT, "rdf: null pointer");
+  b2md_ctx* c = h->ctx;
+  CU(cudaSetDevice(c->device));
+  TRY(upload_aos(c, 0, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
+  TRY(upload_aos(c, 1, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
+  c->state_valid = false;  // positions replaced: not an engine state any more
+  TRY(rdf_launch(h));
+  CU(cudaStreamSynchronize(c->stream));
+  return B2MD_OK;
+}
+
+int b2md_rdf_counts(const b2md_rdf* h, int replica, uint64_t* counts, int64_t* snapshots) {
+  if (!h) return set_err(B2MD_INVALID_ARGUMENT, "rdf: null handle");
+  if (replica < 0 || replica >= h->ctx->R) return set_err(B2MD_INVALID_ARGUMENT, "rdf: bad replica");
+  b2md_ctx* c = h->ctx;
+  CU(cudaSetDevice(c->device));
+  const size_t nc = size_t(h->n_pairs) * h->bins;
+  if (counts && nc > 0) {
+    CU(cudaMemcpyAsync(counts, h->d_counts + replica * nc, sizeof(uint64_t) * nc,
+                       cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+  }
+  if (snapshots) *snapshots = h->snapshots[replica];
+  return B2MD_OK;
+}
+
+int b2md_rdf_set_counts(b2md_rdf* h, int replica, const uint64_t* counts, int64_t snapshots) {
+  if (!h) return set_err(B2MD_INVALID_ARGUMENT, "rdf: null handle");
+  if (replica < 0 || replica >= h->ctx->R) return set_err(B2MD_INVALID_ARGUMENT, "rdf: bad replica");
+  b2md_ctx* c = h->ctx;
+  CU(cudaSetDevice(c->device));
+  const size_t nc = size_t(h->n_pairs) * h->bins;
+  if (nc > 0) {
+    if (counts)
+      CU(cudaMemcpyAsync(h->d_counts + replica * nc, counts, sizeof(uint64_t) * nc,
+                         cudaMemcpyHostToDevice, c->stream));
+    else
+      CU(cudaMemsetAsync(h->d_counts + replica * nc, 0, sizeof(uint64_t) * nc, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+  }
+  h->snapshots[replica] = snapshots;
   return B2MD_OK;
 }
 

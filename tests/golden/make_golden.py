@@ -77,6 +77,31 @@ def flux_vectors():
                             ang_vel=ang_vel, h=h, jq=jq)
 
 
+def rdf_vectors():
+    """tmd::RdfHistogram (structure.cpp:10-153) on every eval case: counts,
+    serialize bytes and finalize tables of two snapshots, and first_minimum /
+    solvation_number of each table."""
+    for name, (comp, opts, st) in golden_cases.eval_cases().items():
+        bw, rmax, snaps = golden_cases.rdf_inputs(name, comp, st)
+        ref = pyoracle.RefRdf(pyoracle.RefFF(comp, opts), bw, rmax)
+        for pos, orient in snaps:
+            ref.accumulate(pos, orient)
+        counts, n_snap = ref.counts()
+        tables = ref.finalize()
+        flat = np.concatenate([np.concatenate([[t["species_a"], t["species_b"], t["partner_density"],
+                                                t["bin_width"], t["snapshots"], len(t["g"])],
+                                               np.column_stack([t["r_mid"], t["g"], t["n_cum"]]).ravel()])
+                               for t in tables]) if tables else np.zeros(0)
+        fmin = np.array([pyoracle.ref_first_minimum(t["r_mid"], t["g"]) for t in tables])
+        solv = np.array([pyoracle.ref_solvation_number(t["bin_width"], t["g"], t["partner_density"],
+                                                       0.6 * rmax) for t in tables])
+        np.savez_compressed(
+            OUT / f"rdf_{name}.npz", bin_width=bw, r_max=rmax,
+            pos=np.stack([p for p, _ in snaps]), orient=np.stack([o for _, o in snaps]),
+            counts=counts, snapshots=n_snap, serialized=np.frombuffer(ref.serialize(), np.uint8),
+            finalize=flat, first_minimum=fmin, solvation_number=solv)
+
+
 def traj_vectors():
     for name, (comp, opts, st, dt, steps) in golden_cases.traj_cases().items():
         eng = pyoracle.RefEngine(comp, opts, dt, seed=1)
@@ -98,5 +123,6 @@ if __name__ == "__main__":
     species_vectors()
     eval_vectors()
     flux_vectors()
+    rdf_vectors()
     traj_vectors()
     print("golden vectors written to", OUT)

@@ -109,3 +109,16 @@ def flux_inputs(name, comp):
     ang_vel = rng.normal(size=(n, 3))
     h = rng.normal(size=comp.species_count()) * 2.0
     return vel, ang_vel, h
+
+
+def rdf_inputs(name, comp, st):
+    """Two seeded snapshots (the case's state and a displaced / re-oriented
+    copy), bin width and r_max = L/2 (the engine's choice, engine.cpp:204)."""
+    seed = sum(name.encode()) * 104729
+    rng = np.random.default_rng(seed)
+    n = comp.molecule_count()
+    pos2 = st.pos + rng.normal(scale=0.3, size=(n, 3))
+    q = rng.normal(size=(n, 4))
+    orient2 = q / np.linalg.norm(q, axis=1, keepdims=True)
+    L = comp.box_length
+    return L / 150.0, 0.5 * L, [(st.pos, st.orient), (pos2, orient2)]
