@@ -237,6 +237,22 @@ int b2md_heat_flux_state(b2md_ctx* ctx, const double* pos, const double* orient,
                          const double* vel, const double* ang_vel, const double* enthalpy,
                          int n_enthalpy, double* jq);
 
+/* Checkpoint state block: the device-resident part of
+ * tmd::Engine::checkpoint_bytes (src/engine.cpp:432-441) — u32 n, f64
+ * box_length, then per molecule pos.xyz, orient.wxyz, vel.xyz, ang_vel.xyz
+ * (13 x f64), little-endian; 12 + 104 n bytes.  save packs replica `replica`
+ * on the device.  restore is restore_dynamic's state part (engine.cpp:
+ * 479-491) followed by its compute_forces() (engine.cpp:540; no wrap), for
+ * one replica; the other replicas keep their state.  Errors as the
+ * reference: B2MD_IO_ERROR "checkpoint: molecule count mismatch", the
+ * ByteReader's "checkpoint: truncated or corrupted data (need N bytes at
+ * offset M)"; a box length different from the composition's is also
+ * B2MD_IO_ERROR.  The rest of the container (header, counters, RNG,
+ * statistics, samplers) is host data: paper_1507_07548_b200/checkpoint.py. */
+size_t b2md_state_block_size(const b2md_ctx* ctx);
+int b2md_save_state_block(b2md_ctx* ctx, int replica, uint8_t* buf, size_t cap);
+int b2md_restore_state_block(b2md_ctx* ctx, int replica, const uint8_t* buf, size_t len);
+
 /* Radial distribution histograms: tmd::RdfHistogram (include/tmd/structure.hpp:
  * 29-67, src/structure.cpp:10-76) over a context's composition, one histogram
  * per replica, accumulated on the device.  Sampling sites are every LJ and

@@ -95,6 +95,14 @@ def ref_lib():
         L.ref_first_minimum.restype = C.c_double
         L.ref_solvation_number.argtypes = [C.c_double, _D, C.c_int, C.c_double, C.c_double]
         L.ref_solvation_number.restype = C.c_double
+        L.ref_engine_checkpoint.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+        L.ref_engine_checkpoint.restype = C.c_int64
+        L.ref_engine_restore.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+        L.ref_run_sampled_checkpoint.argtypes = [
+            C.POINTER(_abi.b2md_composition), C.POINTER(_abi.b2md_ff_options), C.c_double, C.c_uint64,
+            C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, _D, C.c_int, C.c_int, C.c_int,
+            C.c_double, C.c_char_p, C.c_char_p, C.c_int64]
+        L.ref_run_sampled_checkpoint.restype = C.c_int64
         L.ref_engine_create.argtypes = [C.POINTER(_abi.b2md_composition), C.POINTER(_abi.b2md_ff_options), C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]
         L.ref_engine_destroy.argtypes = [C.c_void_p]
         L.ref_engine_set_state.argtypes = [C.c_void_p, _D, _D, _D, _D]
@@ -268,6 +276,15 @@ class RefEngine:
         arr = [np.ascontiguousarray(a, dtype=np.float64) for a in (pos, orient, vel, ang_vel)]
         _check(self.lib, "ref", self.lib.ref_engine_set_state(self.h, *[_d(a) for a in arr]))
 
+    def checkpoint_bytes(self) -> bytes:
+        n = self.lib.ref_engine_checkpoint(self.h, None, 0)
+        buf = C.create_string_buffer(int(n))
+        self.lib.ref_engine_checkpoint(self.h, buf, n)
+        return buf.raw
+
+    def restore(self, data: bytes) -> None:
+        _check(self.lib, "ref", self.lib.ref_engine_restore(self.h, data, len(data)))
+
     def step(self, n=1):
         _check(self.lib, "ref", self.lib.ref_engine_step(self.h, n))
 
@@ -383,3 +400,22 @@ def ref_solvation_number(bin_width, g, partner_density, r_min):
     L = ref_lib()
     g = np.ascontiguousarray(g, dtype=np.float64)
     return L.ref_solvation_number(bin_width, _d(g), len(g), partner_density, r_min)
+
+
+def ref_run_sampled_checkpoint(comp, opts, dt, seed, n_equil, n_prod, *, n_ext=1, corr_length=20,
+                               n_blocks=4, flags=0, enthalpy=(), residence=(0, 0, 0.0),
+                               config_text=""):
+    """tmd::Engine::run with samplers, then Engine::checkpoint_bytes (bytes)."""
+    L = ref_lib()
+    cc, keep = comp.to_c()
+    oc = opts.to_c()
+    h = np.ascontiguousarray(enthalpy, dtype=np.float64).reshape(-1)
+    args = (C.byref(cc), C.byref(oc), dt, seed, n_equil, n_prod, n_ext, corr_length, n_blocks, flags,
+            _d(h) if h.size else None, int(h.size), residence[0], residence[1], float(residence[2]),
+            config_text.encode())
+    n = L.ref_run_sampled_checkpoint(*args, None, 0)
+    if n < 0:
+        raise OracleError(2, L.ref_last_error().decode())
+    buf = C.create_string_buffer(int(n))
+    L.ref_run_sampled_checkpoint(*args, buf, n)
+    return buf.raw

@@ -403,3 +403,66 @@ extern "C" double ref_solvation_number(double bin_width, const double* g, int n,
   t.g.assign(g, g + n);
   return tmd::solvation_number(t, partner_density, r_min);
 }
+
+// ------------------------------------------- Engine checkpoints (engine.cpp:420-541)
+extern "C" int64_t ref_engine_checkpoint(void* h, char* buf, int64_t cap) {
+  const std::string d = static_cast<RefEngine*>(h)->eng->checkpoint_bytes();
+  if (buf && cap >= static_cast<int64_t>(d.size())) std::memcpy(buf, d.data(), d.size());
+  return static_cast<int64_t>(d.size());
+}
+
+// What a restart does with a checkpoint file: the container header (magic,
+// version, embedded config text — written by checkpoint_bytes, engine.cpp:
+// 421-423), then Engine::restore_dynamic for the rest.
+extern "C" int ref_engine_restore(void* h, const char* buf, int64_t len) {
+  return guarded([&]() -> int {
+    tmd::ByteReader r(std::string(buf, static_cast<std::size_t>(len)));
+    char magic[8];
+    r.bytes(magic, 8);
+    if (std::string(magic, 8) != "TMDCKPT1") throw tmd::IoError("checkpoint: bad magic");
+    if (r.u32() != 1) throw tmd::IoError("checkpoint: unsupported version");
+    (void)r.str();
+    static_cast<RefEngine*>(h)->eng->restore_dynamic(r);
+    return B2MD_OK;
+  });
+}
+
+// Engine::run with samplers (engine.cpp:197-300), then checkpoint_bytes: a
+// checkpoint with every sampler section.  flags: 1 massieu, 2 rdf, 4 self
+// diffusion, 8 electric conductivity, 16 thermal conductivity, 32 residence.
+extern "C" int64_t ref_run_sampled_checkpoint(const b2md_composition* comp,
+                                              const b2md_ff_options* opts, double dt,
+                                              uint64_t seed, int64_t n_equil, int64_t n_prod,
+                                              int n_ext, int corr_length, int n_blocks, int flags,
+                                              const double* enthalpy, int n_enthalpy,
+                                              int res_solute, int res_solvent, double res_radius,
+                                              const char* config_text, char* buf, int64_t cap) {
+  std::string d;
+  const int rc = guarded([&]() -> int {
+    tmd::SimulationPlan plan;
+    plan.dt = dt;
+    plan.n_equilibration = n_equil;
+    plan.n_production = n_prod;
+    plan.n_ext = n_ext;
+    plan.corr_length = corr_length;
+    plan.n_blocks = n_blocks;
+    plan.sample_massieu = flags & 1;
+    plan.sample_rdf = flags & 2;
+    plan.sample_self_diffusion = flags & 4;
+    plan.sample_electric_conductivity = flags & 8;
+    plan.sample_thermal_conductivity = flags & 16;
+    plan.sample_residence = flags & 32;
+    plan.enthalpy.assign(enthalpy, enthalpy + n_enthalpy);
+    plan.residence_solute = res_solute;
+    plan.residence_solvent = res_solvent;
+    plan.residence_radius = res_radius;
+    plan.config_text = config_text ? config_text : "";
+    tmd::Engine eng(to_comp(*comp), to_opts(*opts), plan, seed);
+    (void)eng.run();
+    d = eng.checkpoint_bytes();
+    return B2MD_OK;
+  });
+  if (rc) return -1;
+  if (buf && cap >= static_cast<int64_t>(d.size())) std::memcpy(buf, d.data(), d.size());
+  return static_cast<int64_t>(d.size());
+}

@@ -139,6 +139,9 @@ SIGNATURES = {
     "b2md_set_sort_interval": (C.c_int, [_CTX, C.c_int]),
     "b2md_heat_flux": (C.c_int, [_CTX, _D, C.c_int, _D]),
     "b2md_heat_flux_state": (C.c_int, [_CTX, _D, _D, _D, _D, _D, C.c_int, _D]),
+    "b2md_state_block_size": (C.c_size_t, [_CTX]),
+    "b2md_save_state_block": (C.c_int, [_CTX, C.c_int, C.c_char_p, C.c_size_t]),
+    "b2md_restore_state_block": (C.c_int, [_CTX, C.c_int, C.c_char_p, C.c_size_t]),
     "b2md_rdf_create": (C.c_int, [_CTX, C.c_double, C.c_double, C.POINTER(C.c_void_p)]),
     "b2md_rdf_destroy": (None, [C.c_void_p]),
     "b2md_rdf_shape": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),

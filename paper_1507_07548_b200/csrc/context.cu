@@ -1365,6 +1365,75 @@ int b2md_pair_list(b2md_ctx* c, int replica, int32_t* pairs, int64_t capacity, i
   return B2MD_OK;
 }
 
+// ------------------------------------------------------ checkpoint state
+// The device-resident part of Engine::checkpoint_bytes (engine.cpp:432-441):
+// u32 n, f64 box_length, then 13 f64 per molecule, little-endian (the
+// ByteWriter of checkpoint.hpp:15-38 writes raw host bytes; x86-64 and the
+// GPU hosts here are little-endian).
+size_t b2md_state_block_size(const b2md_ctx* c) { return c ? 12 + size_t(104) * c->t.n : 0; }
+
+int b2md_save_state_block(b2md_ctx* c, int replica, uint8_t* buf, size_t cap) {
+  if (!c || !buf) return set_err(B2MD_INVALID_ARGUMENT, "save_state_block: null pointer");
+  if (replica < 0 || replica >= c->R)
+    return set_err(B2MD_INVALID_ARGUMENT, "save_state_block: bad replica");
+  const int n = c->t.n;
+  if (cap < b2md_state_block_size(c))
+    return set_err(B2MD_INVALID_ARGUMENT, "save_state_block: buffer too small");
+  CU(cudaSetDevice(c->device));
+  const uint32_t nn = uint32_t(n);
+  const double box = c->t.box;
+  std::memcpy(buf, &nn, 4);
+  std::memcpy(buf + 4, &box, 8);
+  k_pack_state<<<(n + 255) / 256, 256, 0, c->stream>>>(c->st, n, replica, c->d_stage);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(buf + 12, c->d_stage, sizeof(double) * 13 * n, cudaMemcpyDeviceToHost,
+                     c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return B2MD_OK;
+}
+
+int b2md_restore_state_block(b2md_ctx* c, int replica, const uint8_t* buf, size_t len) {
+  if (!c || !buf) return set_err(B2MD_INVALID_ARGUMENT, "restore_state_block: null pointer");
+  if (replica < 0 || replica >= c->R)
+    return set_err(B2MD_INVALID_ARGUMENT, "restore_state_block: bad replica");
+  // ByteReader::need (checkpoint.hpp:87-91) and engine.cpp:479-480
+  auto truncated = [&](size_t need, size_t at) {
+    return set_err(B2MD_IO_ERROR, "checkpoint: truncated or corrupted data (need " +
+                                      std::to_string(need) + " bytes at offset " +
+                                      std::to_string(at) + ")");
+  };
+  if (len < 4) return truncated(4, 0);
+  uint32_t nn = 0;
+  std::memcpy(&nn, buf, 4);
+  if (int(nn) != c->t.n) return set_err(B2MD_IO_ERROR, "checkpoint: molecule count mismatch");
+  if (len < 12) return truncated(8, 4);
+  double box = 0.0;
+  std::memcpy(&box, buf + 4, 8);
+  if (box != c->t.box)  // the context's tables are built for the composition's box
+    return set_err(B2MD_IO_ERROR, "checkpoint: box length does not match the composition");
+  const int n = c->t.n;
+  for (int i = 0; i < n; ++i)
+    if (len < 12 + size_t(104) * (i + 1)) {
+      const size_t at = 12 + size_t(104) * i;
+      return truncated(8, at + ((len - at) / 8) * 8);
+    }
+  CU(cudaSetDevice(c->device));
+  CU(cudaMemcpyAsync(c->d_stage, buf + 12, sizeof(double) * 13 * n, cudaMemcpyHostToDevice,
+                     c->stream));
+  k_unpack_state<<<(n + 255) / 256, 256, 0, c->stream>>>(c->st, n, replica, c->d_stage);
+  CU(cudaGetLastError());
+  // restore_dynamic ends with compute_forces() (engine.cpp:540): no wrap
+  set_wrapped(c, false);
+  const int big = INT_MAX;
+  CU(cudaMemcpyAsync(c->d_error, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  if (c->sort_interval > 0) TRY(resort(c));
+  TRY(enqueue_forces(c, true));
+  CU(cudaStreamSynchronize(c->stream));
+  set_wrapped(c, true);  // steps wrap before every later evaluation
+  c->state_valid = true;
+  return B2MD_OK;
+}
+
 // ---------------------------------------------------------------- RDF
 // tmd::RdfHistogram (include/tmd/structure.hpp:29-67) over a context: one
 // histogram per replica, accumulated on the device (rdf.cuh).

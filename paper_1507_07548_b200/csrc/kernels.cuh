@@ -1637,6 +1637,50 @@ __global__ void k_pair_fill(const uint32_t* mask, const int* perm, int n, int wo
   }
 }
 
+// ------------------------------------------------------- checkpoint state
+// Engine::checkpoint_bytes' per-molecule record (engine.cpp:434-440):
+// pos.xyz, orient.wxyz, vel.xyz, ang_vel.xyz as 13 f64, molecule-major.
+__global__ void k_pack_state(StateDev st, int n, int r, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t g = size_t(r) * n + i;
+  double* o = out + size_t(i) * 13;
+  o[0] = st.px[g];
+  o[1] = st.py[g];
+  o[2] = st.pz[g];
+  o[3] = st.qw[g];
+  o[4] = st.qx[g];
+  o[5] = st.qy[g];
+  o[6] = st.qz[g];
+  o[7] = st.vx[g];
+  o[8] = st.vy[g];
+  o[9] = st.vz[g];
+  o[10] = st.wx[g];
+  o[11] = st.wy[g];
+  o[12] = st.wz[g];
+}
+
+// Engine::restore_dynamic's state loop (engine.cpp:483-491)
+__global__ void k_unpack_state(StateDev st, int n, int r, const double* in) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t g = size_t(r) * n + i;
+  const double* o = in + size_t(i) * 13;
+  st.px[g] = o[0];
+  st.py[g] = o[1];
+  st.pz[g] = o[2];
+  st.qw[g] = o[3];
+  st.qx[g] = o[4];
+  st.qy[g] = o[5];
+  st.qz[g] = o[6];
+  st.vx[g] = o[7];
+  st.vy[g] = o[8];
+  st.vz[g] = o[9];
+  st.wx[g] = o[10];
+  st.wy[g] = o[11];
+  st.wz[g] = o[12];
+}
+
 // ------------------------------------------------------ spatial ordering
 // Sort keys for b2md_ctx::resort: molecules are binned into G x G columns
 // along x (cross-section c x c, c^2 = 32 / (rho L): about one 32-slot block

@@ -102,6 +102,41 @@ def rdf_vectors():
             finalize=flat, first_minimum=fmin, solvation_number=solv)
 
 
+def checkpoint_vectors():
+    """tmd::Engine::checkpoint_bytes (engine.cpp:420-462): two sampled runs
+    (Engine::run with every sampler section the reference has) and a fresh
+    engine after set_state; plus the reference's restore error on truncated
+    copies of one of them."""
+    cases = golden_cases.eval_cases()
+    comp, opts, st = cases["water_ions"]
+    a = pyoracle.ref_run_sampled_checkpoint(comp, opts, 0.0005, 7, 20, 40, n_ext=2, corr_length=6,
+                                            n_blocks=4, flags=62, enthalpy=[-1.0, 0.5, 0.7],
+                                            residence=(1, 0, 0.0),
+                                            config_text="[system]\nexample = true\n")
+    comp, opts, st = cases["rf"]
+    b = pyoracle.ref_run_sampled_checkpoint(comp, opts, 0.001, 3, 10, 30, n_ext=1, corr_length=5,
+                                            n_blocks=3, flags=1 | 2 | 4 | 16, enthalpy=[0.3],
+                                            config_text="rf")
+    comp, opts, st = cases["two_clj"]
+    eng = pyoracle.RefEngine(comp, opts, 0.002, seed=5)
+    eng.set_state(st.pos, st.orient, st.vel, st.ang_vel)
+    fresh = eng.checkpoint_bytes()
+    # the reference's restore of truncated water-ions copies
+    comp_w, opts_w, _ = cases["water_ions"]
+    cuts = [9, 40, 200, 1000, len(a) // 2, len(a) - 3]
+    msgs = []
+    for cut in cuts:
+        e = pyoracle.RefEngine(comp_w, opts_w, 0.0005, seed=7)
+        try:
+            e.restore(a[:cut])
+            msgs.append("")
+        except pyoracle.OracleError as exc:
+            msgs.append(str(exc))
+    np.savez_compressed(OUT / "ckpt.npz", sampled_water=np.frombuffer(a, np.uint8),
+                        sampled_rf=np.frombuffer(b, np.uint8), fresh_two_clj=np.frombuffer(fresh, np.uint8),
+                        fresh_seed=5, cuts=np.array(cuts), cut_messages=np.array(msgs))
+
+
 def traj_vectors():
     for name, (comp, opts, st, dt, steps) in golden_cases.traj_cases().items():
         eng = pyoracle.RefEngine(comp, opts, dt, seed=1)
@@ -124,5 +159,6 @@ if __name__ == "__main__":
     eval_vectors()
     flux_vectors()
     rdf_vectors()
+    checkpoint_vectors()
     traj_vectors()
     print("golden vectors written to", OUT)
