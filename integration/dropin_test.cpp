@@ -122,6 +122,36 @@ int main() {
     const double js = std::max({1.0, std::abs(jr.x), std::abs(jr.y), std::abs(jr.z)});
     const double dj = std::max({std::abs(jr.x - jg.x), std::abs(jr.y - jg.y), std::abs(jr.z - jg.z)}) / js;
     expect(dj <= 1e-9, "heat flux after 50 steps |dJq| / max |Jq|", dj);
+
+    // RDF: GPU counts finalized by the reference's own RdfHistogram, on a
+    // host state and on the GPU engine's resident state (b = its download)
+    RdfHistogram cpu2(comp, 0.05, 0.5 * comp.box_length);
+    GpuRdfHistogram gpu2(comp, gpu, 0.05, 0.5 * comp.box_length);
+    cpu2.accumulate(a);
+    gpu2.accumulate(a);
+    cpu2.accumulate(b);
+    gpu2.accumulate();
+    const auto tc = cpu2.finalize(), tg = gpu2.finalize();
+    double dg = tc.size() == tg.size() ? 0.0 : 1.0;
+    for (std::size_t t = 0; t < tc.size() && t < tg.size(); ++t)
+      for (std::size_t k = 0; k < tc[t].g.size(); ++k)
+        dg = std::max({dg, std::abs(tc[t].g[k] - tg[t].g[k]), std::abs(tc[t].n_cum[k] - tg[t].n_cum[k])});
+    expect(dg == 0.0, "RDF tables (GPU counts) vs reference, max |d|", dg);
+
+    // checkpoint state block: a fresh pair of engines on the same state
+    Engine ref2(comp, opts, plan, 7);
+    GpuEngine gpu3(comp, opts, 0.002);
+    ref2.set_state(st);
+    gpu3.set_state(st);
+    const std::string full = ref2.checkpoint_bytes();
+    const std::string block = gpu3.checkpoint_state_block();
+    const std::size_t off = 8 + 4 + 8 + plan.config_text.size() + 3 * 8 + 4 * 8;  // engine.cpp:421-429
+    const bool same = full.compare(off, block.size(), block) == 0;
+    expect(same, "checkpoint state block == reference bytes", same ? 0.0 : 1.0);
+    gpu3.restore_state_block(block);
+    const SystemState r3 = gpu3.state();
+    const double dfr = max_diff(r3.force, ref2.state().force) / std::max(1.0, max_abs(ref2.state().force));
+    expect(dfr <= 1e-10, "forces after state-block restore", dfr);
   }
   // charged rigid dimers + LJ with reaction field (test_potentials.cpp:214-258 shape)
   {

@@ -16,7 +16,9 @@
 
 #include "b200md.h"
 #include "tmd/engine.hpp"
+#include "tmd/checkpoint.hpp"
 #include "tmd/parallel.hpp"
+#include "tmd/structure.hpp"
 
 namespace tmd {
 
@@ -140,6 +142,7 @@ class GpuForceField {
   }
 
   const char* warning() const { return b2md_warning(ctx_.get()); }
+  b2md_ctx* context() const { return ctx_.get(); }
 
   // tmd::heat_flux(comp, state, table, h) (greenkubo.hpp:93, greenkubo.cpp:182-266)
   // with this force field's pair table; state taken as given.
@@ -193,6 +196,21 @@ class GpuEngine {
     return s;
   }
 
+  b2md_ctx* context() const { return ctx_.get(); }
+
+  // checkpoint state block (engine.cpp:432-441) of the device state, for
+  // Engine::checkpoint_bytes; restore = restore_dynamic's state part + forces
+  std::string checkpoint_state_block() const {
+    std::string buf(b2md_state_block_size(ctx_.get()), '\0');
+    b2md_detail::check(b2md_save_state_block(ctx_.get(), 0, reinterpret_cast<std::uint8_t*>(&buf[0]),
+                                             buf.size()));
+    return buf;
+  }
+  void restore_state_block(const std::string& block) {
+    b2md_detail::check(b2md_restore_state_block(
+        ctx_.get(), 0, reinterpret_cast<const std::uint8_t*>(block.data()), block.size()));
+  }
+
   // J_q of the resident state, as Engine::run samples it every n_ext steps
   // (engine.cpp:235-238)
   Vec3 heat_flux(const std::vector<double>& h_per_species) const {
@@ -205,6 +223,56 @@ class GpuEngine {
  private:
   SystemComposition comp_;
   b2md_detail::Context ctx_;
+};
+
+// RdfHistogram (structure.hpp:29-67) accumulated on the GPU.  The counts
+// are the reference's (bit-exact); finalize() hands them to the reference's
+// own class through its deserialize (structure.cpp:142-153), so tables,
+// first_minimum and solvation_number are the reference's arithmetic.
+class GpuRdfHistogram {
+ public:
+  template <typename Owner>  // GpuForceField or GpuEngine
+  GpuRdfHistogram(const SystemComposition& comp, Owner& owner, double bin_width, double r_max)
+      : comp_(comp), bin_width_(bin_width), r_max_(r_max) {
+    b2md_detail::check(b2md_rdf_create(owner.context(), bin_width, r_max, &h_));
+    b2md_detail::check(b2md_rdf_shape(h_, nullptr, &bins_, &pairs_));
+  }
+  ~GpuRdfHistogram() { b2md_rdf_destroy(h_); }
+  GpuRdfHistogram(const GpuRdfHistogram&) = delete;
+  GpuRdfHistogram& operator=(const GpuRdfHistogram&) = delete;
+
+  void accumulate(const SystemState& s) {  // structure.cpp:38-76
+    b2md_detail::check(b2md_rdf_accumulate_state(h_, &s.pos[0].x, &s.orient[0].w));
+  }
+  void accumulate() { b2md_detail::check(b2md_rdf_accumulate(h_)); }  // resident state
+
+  // the reference histogram holding the GPU counts (RdfHistogram::serialize layout)
+  RdfHistogram to_reference() const {
+    std::vector<std::uint64_t> counts(std::size_t(pairs_) * bins_);
+    std::int64_t snaps = 0;
+    b2md_detail::check(b2md_rdf_counts(h_, 0, counts.data(), &snaps));
+    ByteWriter w;
+    w.f64(bin_width_);
+    w.f64(r_max_);
+    w.u32(static_cast<std::uint32_t>(bins_));
+    w.i64(snaps);
+    w.u64(static_cast<std::uint64_t>(pairs_));
+    for (int p = 0; p < pairs_; ++p) {
+      w.u64(static_cast<std::uint64_t>(bins_));
+      for (int b = 0; b < bins_; ++b) w.u64(counts[std::size_t(p) * bins_ + b]);
+    }
+    RdfHistogram h(comp_, bin_width_, r_max_);
+    ByteReader r(w.data());
+    h.deserialize(r);
+    return h;
+  }
+  std::vector<RdfTable> finalize() const { return to_reference().finalize(); }
+
+ private:
+  const SystemComposition& comp_;
+  double bin_width_, r_max_;
+  int bins_ = 0, pairs_ = 0;
+  b2md_rdf* h_ = nullptr;
 };
 
 }  // namespace tmd
