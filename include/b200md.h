@@ -219,6 +219,14 @@ int b2md_set_search_options(b2md_ctx* ctx, int fix_prefilter, int tile_cull);
  * (where the tile cull can use it), else 0. */
 int b2md_set_sort_interval(b2md_ctx* ctx, int steps);
 
+/* Step structure (same results bit for bit; for tests and measurement):
+ * fused_kick = 1 runs the end-of-step half kick (engine.cpp:131-142) in the
+ * force kernel's row epilogue whenever a molecule's force is final there (no
+ * Ewald reciprocal term, no multi-GPU all-reduce).  Default: 1 below 4096
+ * molecules in total (one launch less per step), 0 above (the epilogue kick
+ * lengthens warps that own several rows). */
+int b2md_set_step_options(b2md_ctx* ctx, int fused_kick);
+
 /* Green-Kubo heat flux J_q (tmd::heat_flux, include/tmd/greenkubo.hpp:93,
  * src/greenkubo.cpp:182-266) of the context's current device state: the
  * state set_state / step left (Engine::run samples it every n_ext steps,

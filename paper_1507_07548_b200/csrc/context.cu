@@ -159,6 +159,7 @@ struct b2md_ctx {
   bool use_graphs = true;
   bool use_fix_prefilter = true;
   bool use_tile_cull = true;
+  bool use_fused_kick = true;  // end-of-step half kick inside the force kernel
   cudaGraphExec_t step_graph = nullptr;  // forces + fused kick/kick-drift
   cudaGraphExec_t single_graph = nullptr;  // one whole step
   cudaGraphExec_t prof_graph = nullptr;    // one whole step with event-record nodes
@@ -355,7 +356,17 @@ ForceArgs force_args(b2md_ctx* c) {
   a.vderiv = c->t.vderiv ? 1 : 0;
   const int hh = hi32(0.5 * c->t.box);
   std::memcpy(&a.thr, &hh, 4);
+  a.kick_dt = 0.0;
+  a.error_mol = c->d_error;
   return a;
+}
+
+// The end-of-step half kick can run in the force kernel's row epilogue when
+// a molecule's force is final there: no Ewald reciprocal term still to add
+// and no cross-rank all-reduce.
+bool kick_fusable(const b2md_ctx* c) {
+  return c->engine && c->use_fused_kick && !(c->t.ewald && c->nq > 0) &&
+         !(c->world > 1 && c->comm);
 }
 
 // positions known to lie in [0, L) (set_state / step wrap them) and every
@@ -368,8 +379,9 @@ bool fast_min_image(const b2md_ctx* c) {
   return !(c->t.single_site_path && !(c->t.rc2 < h * h));
 }
 
-int launch_force(b2md_ctx* c) {
+int launch_force(b2md_ctx* c, bool kick) {
   ForceArgs a = force_args(c);
+  if (kick) a.kick_dt = c->dt;
   const bool w = fast_min_image(c);
   dim3 grid(c->force_grid, c->R);
   const int bs = c->force_warps * 32;
@@ -572,7 +584,7 @@ bool sort_due(const b2md_ctx* c) {
 }
 
 // ForceField::evaluate (src/parallel.cpp:79-122) on the device state.
-int enqueue_forces(b2md_ctx* c, bool offsets) {
+int enqueue_forces(b2md_ctx* c, bool offsets, bool kick = false) {
   if (offsets) {  // evaluate / set_state path: the integrator did not refresh these
     TRY(launch_offsets(c));
     const int nt = n_total(c);
@@ -582,7 +594,7 @@ int enqueue_forces(b2md_ctx* c, bool offsets) {
     CU(cudaGetLastError());
   }
   TRY(launch_search(c));
-  TRY(launch_force(c));
+  TRY(launch_force(c, kick));
   TRY(launch_ewald(c));
   TRY(launch_allreduce(c));
   return B2MD_OK;
@@ -603,7 +615,9 @@ StepArgs step_args(b2md_ctx* c) {
 // Engine::step (src/engine.cpp:102-143).  A run of k steps is issued as
 //   kick_drift, [forces, kick+kick_drift] x (k-1), forces, kick
 // where the bracket is one CUDA graph (the second half-kick of step s and the
-// first of step s+1 share one launch).
+// first of step s+1 share one launch), or, when the kick fuses into the force
+// kernel (kick_fusable),
+//   kick_drift, [forces+kick, kick_drift] x (k-1), forces+kick.
 int launch_step_kernel(b2md_ctx* c, int fam) {
   StepArgs a = step_args(c);
   const int nt = n_total(c);
@@ -619,8 +633,17 @@ int launch_step_kernel(b2md_ctx* c, int fam) {
 }
 
 int enqueue_loop_body(b2md_ctx* c) {
-  TRY(enqueue_forces(c, false));
-  TRY(launch_step_kernel(c, F_KICK_KICK_DRIFT));
+  const bool fused = kick_fusable(c);
+  TRY(enqueue_forces(c, false, fused));
+  TRY(launch_step_kernel(c, fused ? F_KICK_DRIFT : F_KICK_KICK_DRIFT));
+  return B2MD_OK;
+}
+
+// forces + the end-of-step half kick
+int enqueue_forces_and_kick(b2md_ctx* c) {
+  const bool fused = kick_fusable(c);
+  TRY(enqueue_forces(c, false, fused));
+  if (!fused) TRY(launch_step_kernel(c, F_KICK));
   return B2MD_OK;
 }
 
@@ -645,8 +668,7 @@ int build_single_step_graph(b2md_ctx* c) {
   if (c->single_graph) return B2MD_OK;
   CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   int rc = launch_step_kernel(c, F_KICK_DRIFT);
-  if (!rc) rc = enqueue_forces(c, false);
-  if (!rc) rc = launch_step_kernel(c, F_KICK);
+  if (!rc) rc = enqueue_forces_and_kick(c);
   cudaGraph_t graph;
   cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
   if (rc) return rc;
@@ -665,8 +687,7 @@ int build_prof_graph(b2md_ctx* c) {
   CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   c->capturing_prof = true;
   int rc = launch_step_kernel(c, F_KICK_DRIFT);
-  if (!rc) rc = enqueue_forces(c, false);
-  if (!rc) rc = launch_step_kernel(c, F_KICK);
+  if (!rc) rc = enqueue_forces_and_kick(c);
   c->capturing_prof = false;
   cudaGraph_t graph;
   cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
@@ -747,8 +768,7 @@ int run_steps(b2md_ctx* c, int64_t nsteps) {
   }
   if (sort_due(c)) TRY(resort_and_stage(c));
   ++c->steps_since_sort;
-  TRY(enqueue_forces(c, false));
-  TRY(launch_step_kernel(c, F_KICK));
+  TRY(enqueue_forces_and_kick(c));
   return B2MD_OK;
 }
 
@@ -933,6 +953,11 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     if (const char* e = std::getenv("B2MD_FORCE_WARPS"))
       c->force_warps = std::max(1, std::min(kForceWarps, std::atoi(e)));
     if (const char* e = std::getenv("B2MD_FORCE_GRID")) c->force_grid = std::max(1, std::atoi(e));
+    // the fused kick runs on each row's lane 0: it pays for small systems
+    // (one launch less), but lengthens every warp's critical path when warps
+    // own several rows (measured: cfg0/cfg1 +3-7%, cfg3/cfg4 -2-4%)
+    c->use_fused_kick = size_t(t.n) * R < 4096;
+    if (const char* e = std::getenv("B2MD_FUSED_KICK")) c->use_fused_kick = std::atoi(e) != 0;
   }
   TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars * c->force_grid));
   TRY(dalloc(&c->d_ticket, size_t(2) * R));
@@ -1257,6 +1282,13 @@ int b2md_set_search_options(b2md_ctx* c, int fix_prefilter, int tile_cull) {
   c->use_fix_prefilter = fix_prefilter != 0;
   c->use_tile_cull = tile_cull != 0;
   drop_graphs(c);  // launch arguments are baked into the graphs
+  return B2MD_OK;
+}
+
+int b2md_set_step_options(b2md_ctx* c, int fused_kick) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "set_step_options: null context");
+  c->use_fused_kick = fused_kick != 0;
+  drop_graphs(c);
   return B2MD_OK;
 }
 

@@ -676,7 +676,14 @@ struct ForceArgs {
   double rf_r3inv, rf_shift;
   int vderiv;
   float thr;  // hi32(L/2) as float (min_image_wrapped)
+  // fused end-of-step half kick (kick_one) in the row epilogue: dt > 0 when
+  // the forces are complete after this kernel (no Ewald term, no all-reduce)
+  double kick_dt;
+  int* error_mol;
 };
+
+struct StepArgs;
+__device__ __forceinline__ void fused_kick(const ForceArgs& a, size_t gid);
 
 
 template <bool MULTI_SPECIES, bool WRAPPED>
@@ -738,6 +745,7 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
       a.st.fx[e] = fx;
       a.st.fy[e] = fy;
       a.st.fz[e] = fz;
+      if (a.kick_dt > 0.0) fused_kick(a, e);
     }
   }
   double v[kNumRowScalars] = {warp_sum(u), 0.0, 0.0, a.vderiv ? warp_sum(s1) : 0.0,
@@ -904,6 +912,7 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
       a.st.tx[e] = tx;
       a.st.ty[e] = ty;
       a.st.tz[e] = tz;
+      if (a.kick_dt > 0.0) fused_kick(a, e);
     }
   }
   double v[kNumRowScalars] = {warp_sum(ulj), warp_sum(uel), warp_sum(urf), warp_sum(s1),
@@ -1215,6 +1224,7 @@ __global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a
       a.st.tx[e] = tx;
       a.st.ty[e] = ty;
       a.st.tz[e] = tz;
+      if (a.kick_dt > 0.0) fused_kick(a, e);
     }
   }
   double v[kNumRowScalars] = {warp_sum(ulj), 0.0, 0.0, warp_sum(s1),
@@ -1552,6 +1562,21 @@ __device__ __forceinline__ bool kick_one(const StepArgs& a, int gid) {
   return isfinite(a.st.px[gid]) && isfinite(a.st.py[gid]) && isfinite(a.st.pz[gid]) &&
          isfinite(vx) && isfinite(vy) && isfinite(vz) && isfinite(w0) && isfinite(w1) &&
          isfinite(w2) && isfinite(a.st.qw[gid]);
+}
+
+// k_kick's work for one molecule inside a force kernel's row epilogue: its
+// force and torque were just written by this thread (engine.cpp:131-142)
+__device__ __forceinline__ void fused_kick(const ForceArgs& f, size_t gid) {
+  if (*f.error_mol != 0x7fffffff) return;  // state frozen after a failed step
+  StepArgs a;
+  a.s = f.s;
+  a.st = f.st;
+  a.dt = f.kick_dt;
+  a.error_mol = f.error_mol;
+  a.write_offsets = 0;
+  a.fixpos = nullptr;
+  a.fix_scale = 0.0;
+  if (!kick_one(a, int(gid))) atomicMin(f.error_mol, int(gid));
 }
 
 // first half of a step: half kick, drift, rotate, wrap, offsets

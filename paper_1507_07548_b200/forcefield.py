@@ -310,6 +310,11 @@ class Engine:
         """b2md_set_search_options: partner-search strategy (same results)."""
         check(_abi.lib().b2md_set_search_options(self._c.ctx, int(fix_prefilter), int(tile_cull)))
 
+    def set_step_options(self, fused_kick: bool = True) -> None:
+        """b2md_set_step_options: end-of-step kick fused into the force kernel
+        (same results bit for bit)."""
+        check(_abi.lib().b2md_set_step_options(self._c.ctx, int(fused_kick)))
+
     # --- checkpoint / restart (engine.cpp:420-541)
     def state_block(self, replica: int = 0) -> bytes:
         """The state block of Engine::checkpoint_bytes (engine.cpp:432-441),

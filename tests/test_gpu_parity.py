@@ -496,3 +496,22 @@ def test_spatial_order_replicas():
         d -= wl.comp.box_length * np.round(d / wl.comp.box_length)
         assert np.abs(d).max() / wl.comp.box_length <= T_TOL
         assert np.array_equal(eng.pair_list(r), ora.pair_list(s.pos))
+
+
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg1", "cfg2", "cfg3"])
+def test_fused_kick_bit_identical(cfg):
+    """The end-of-step half kick in the force kernel's epilogue (single-step
+    graphs, multi-step graphs, eager re-sort steps) gives the separate-kernel
+    trajectory bit for bit (cfg2 has an Ewald term: never fused)."""
+    wl = configs.make(cfg)
+    out = []
+    for fused in (True, False):
+        eng = b2.Engine(wl.comp, wl.opts, wl.dt)
+        eng.set_step_options(fused)
+        eng.set_sort_interval(4 if cfg == "cfg3" else 0)
+        eng.set_state(wl.states[0])
+        for k in (1, 1, 6, 3):
+            eng.step(k)
+        s = eng.state()
+        out.append(np.hstack([s.pos, s.orient, s.vel, s.ang_vel, s.force, s.torque]))
+    assert np.array_equal(out[0], out[1])
