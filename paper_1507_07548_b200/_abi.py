@@ -172,6 +172,24 @@ def library_path() -> Path:
     return Path(os.environ.get("B2MD_LIBRARY", str(LIB_PATH)))
 
 
+def _prefer_python_nccl() -> None:
+    """NCCL is loaded by the library at first multi-GPU use; point it at the
+    NCCL of this Python environment's PyTorch (nvidia-nccl wheel) so a later
+    `import torch` finds the same, compatible library in the process."""
+    if os.environ.get("B2MD_NCCL_LIBRARY"):
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        cand = Path(base) / "lib" / "libnccl.so.2"
+        if cand.exists():
+            os.environ["B2MD_NCCL_LIBRARY"] = str(cand)
+            return
+
+
 def lib():
     """Load libb200md.so (fails loudly when it has not been built)."""
     global _lib
@@ -182,6 +200,7 @@ def lib():
                 f"b200md native library missing at {path}; build it with "
                 "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
             )
+        _prefer_python_nccl()
         handle = C.CDLL(str(path), mode=C.RTLD_GLOBAL)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(handle, name)

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cub/cub.cuh>
 #include <cstdlib>
@@ -40,12 +42,48 @@ int set_err(int code, const std::string& msg) {
                                           " at " #expr);                                  \
   } while (0)
 
+// NCCL is resolved at first multi-GPU use (dlopen), not linked: a process
+// that loads another NCCL first (e.g. PyTorch's bundled one) keeps it.
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+int nccl_load() {
+  if (g_nccl.loaded) return B2MD_OK;
+  // an explicit library (the Python package points it at the NCCL its PyTorch
+  // uses, so both share one), else one already in the process, else the system's
+  void* h = nullptr;
+  if (const char* path = std::getenv("B2MD_NCCL_LIBRARY")) h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return set_err(B2MD_CUDA_ERROR, std::string("NCCL not available: ") + dlerror());
+  auto sym = [&](const char* name) { return dlsym(h, name); };
+  g_nccl.GetUniqueId = reinterpret_cast<decltype(g_nccl.GetUniqueId)>(sym("ncclGetUniqueId"));
+  g_nccl.CommInitRank = reinterpret_cast<decltype(g_nccl.CommInitRank)>(sym("ncclCommInitRank"));
+  g_nccl.AllReduce = reinterpret_cast<decltype(g_nccl.AllReduce)>(sym("ncclAllReduce"));
+  g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(sym("ncclCommDestroy"));
+  g_nccl.GetErrorString = reinterpret_cast<decltype(g_nccl.GetErrorString)>(sym("ncclGetErrorString"));
+  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy ||
+      !g_nccl.GetErrorString)
+    return set_err(B2MD_CUDA_ERROR, "NCCL: missing symbols");
+  g_nccl.loaded = true;
+  return B2MD_OK;
+}
+
 #define NC(expr)                                                                        \
   do {                                                                                  \
     ncclResult_t r_ = (expr);                                                           \
     if (r_ != ncclSuccess)                                                              \
-      return set_err(B2MD_CUDA_ERROR, std::string("NCCL error: ") + ncclGetErrorString(r_) + \
-                                          " at " #expr);                                \
+      return set_err(B2MD_CUDA_ERROR, std::string("NCCL error: ") +                     \
+                                          g_nccl.GetErrorString(r_) + " at " #expr);    \
   } while (0)
 
 #define TRY(expr)          \
@@ -86,6 +124,32 @@ __global__ void k_soa_to_aos(double* aos, int count, int width, const double* d0
   aos[size_t(i) * width + 1] = d1[i];
   aos[size_t(i) * width + 2] = d2[i];
   if (width == 4) aos[size_t(i) * width + 3] = d3[i];
+}
+
+// Up to six AoS host arrays (pinned, device-accessible) <-> SoA device arrays
+// in one launch: the transfer is the kernel's own PCIe / C2C traffic (no
+// staging copy, one launch per direction).  grid.y = array.
+struct AosBatch {
+  const double* src[6];  // upload: host AoS
+  double* dst[6];        // download: host AoS
+  double* d[6][4];       // SoA components
+  int width[6];
+  int n_arrays;
+  int count;
+};
+__global__ void k_aos_batch_upload(AosBatch b) {
+  const int k = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b.count) return;
+  const int w = b.width[k];
+  const double* a = b.src[k] + size_t(i) * w;
+  for (int c = 0; c < w; ++c) b.d[k][c][i] = a[c];
+}
+__global__ void k_aos_batch_download(AosBatch b) {
+  const int k = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b.count) return;
+  const int w = b.width[k];
+  double* a = b.dst[k] + size_t(i) * w;
+  for (int c = 0; c < w; ++c) a[c] = b.d[k][c][i];
 }
 
 enum Family { F_OFFSETS, F_SEARCH, F_FORCE, F_EWALD_TAB, F_EWALD_SK, F_EWALD_F, F_KICK_KICK_DRIFT,
@@ -179,6 +243,7 @@ struct b2md_ctx {
   int64_t prof_n[F_COUNT] = {};
   // host scratch
   std::vector<double> h_sums;
+  double* h_sums_pinned = nullptr;  // energy sums read-back (cudaMallocHost)
   std::string warning;
 };
 
@@ -464,7 +529,7 @@ int launch_allreduce(b2md_ctx* c) {
   if (c->world <= 1 || !c->comm) return B2MD_OK;
   const size_t count = size_t(6) * n_total(c) + size_t(kNumSums) * c->R;
   TRY(prof_begin(c, F_ALLREDUCE));
-  NC(ncclAllReduce(c->d_fbuf, c->d_fbuf, count, ncclDouble, ncclSum, c->comm, c->stream));
+  NC(g_nccl.AllReduce(c->d_fbuf, c->d_fbuf, count, ncclDouble, ncclSum, c->comm, c->stream));
   TRY(prof_end(c));
   return B2MD_OK;
 }
@@ -510,7 +575,7 @@ int launch_heat_flux(b2md_ctx* c, const double* enthalpy) {
 #undef FLUX_K
 #undef FLUX_CASE
   if (c->world > 1 && c->comm)
-    NC(ncclAllReduce(c->d_flux, c->d_flux, size_t(kNumSums) * c->R, ncclDouble, ncclSum, c->comm,
+    NC(g_nccl.AllReduce(c->d_flux, c->d_flux, size_t(kNumSums) * c->R, ncclDouble, ncclSum, c->comm,
                      c->stream));
   return B2MD_OK;
 }
@@ -826,14 +891,93 @@ void assemble(const b2md_ctx* c, const double* sums, b2md_energy* e, b2md_eval_s
 
 int download_scalars(b2md_ctx* c, b2md_energy* e, b2md_eval_stats* st) {
   if (!e && !st) return B2MD_OK;
-  c->h_sums.resize(size_t(kNumSums) * c->R);
-  CU(cudaMemcpyAsync(c->h_sums.data(), c->d_fbuf + size_t(6) * n_total(c),
-                     sizeof(double) * kNumSums * c->R, cudaMemcpyDeviceToHost, c->stream));
+  const size_t bytes = sizeof(double) * kNumSums * c->R;
+  if (!c->h_sums_pinned) CU(cudaMallocHost(&c->h_sums_pinned, bytes));
+  CU(cudaMemcpyAsync(c->h_sums_pinned, c->d_fbuf + size_t(6) * n_total(c), bytes,
+                     cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   for (int r = 0; r < c->R; ++r)
-    assemble(c, c->h_sums.data() + size_t(r) * kNumSums, e ? e + r : nullptr, st ? st + r : nullptr);
+    assemble(c, c->h_sums_pinned + size_t(r) * kNumSums, e ? e + r : nullptr, st ? st + r : nullptr);
   return B2MD_OK;
 }
+
+// A host pointer the device can access directly (pinned / registered memory
+// under unified addressing); nullptr for pageable memory.
+const double* device_view(const double* host) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost && at.devicePointer
+             ? static_cast<const double*>(at.devicePointer) : nullptr;
+}
+
+struct AosSpec {
+  const double* host;
+  int width;
+  double* d[4];
+};
+
+// Host AoS <-> device SoA for several arrays.  Small transfers (< 1 MiB in
+// total, latency-bound) from device-accessible (pinned) host memory are one
+// zero-copy launch; larger ones go through the copy engines into the staging
+// slots plus one batched conversion launch (device-initiated PCIe reads
+// measured ~10 GB/s against the DMA engines' bandwidth).
+constexpr size_t kZeroCopyMaxBytes = size_t(1) << 20;
+
+int move_arrays(b2md_ctx* c, const AosSpec* spec, int n, bool upload) {
+  if (n == 0) return B2MD_OK;
+  const int nt = n_total(c);
+  size_t bytes = 0;
+  for (int k = 0; k < n; ++k) bytes += sizeof(double) * spec[k].width * size_t(nt);
+  AosBatch b{};
+  b.count = nt;
+  b.n_arrays = n;
+  bool direct = bytes < kZeroCopyMaxBytes;
+  for (int k = 0; k < n && direct; ++k) {
+    const double* v = device_view(spec[k].host);
+    if (!v) direct = false;
+    b.src[k] = v;
+    b.dst[k] = const_cast<double*>(v);
+  }
+  for (int k = 0; k < n; ++k) {
+    b.width[k] = spec[k].width;
+    for (int q = 0; q < 4; ++q) b.d[k][q] = spec[k].d[q];
+  }
+  const dim3 grid((nt + 255) / 256, n);
+  if (direct) {
+    if (upload)
+      k_aos_batch_upload<<<grid, 256, 0, c->stream>>>(b);
+    else
+      k_aos_batch_download<<<grid, 256, 0, c->stream>>>(b);
+    CU(cudaGetLastError());
+    return B2MD_OK;
+  }
+  // staged: slot k of d_stage holds array k (4 nt doubles per slot)
+  for (int k = 0; k < n; ++k) {
+    double* stage = c->d_stage + size_t(k) * 4 * nt;
+    b.src[k] = stage;
+    b.dst[k] = stage;
+  }
+  if (upload) {
+    for (int k = 0; k < n; ++k)
+      CU(cudaMemcpyAsync(c->d_stage + size_t(k) * 4 * nt, spec[k].host,
+                         sizeof(double) * spec[k].width * nt, cudaMemcpyHostToDevice, c->stream));
+    k_aos_batch_upload<<<grid, 256, 0, c->stream>>>(b);
+    CU(cudaGetLastError());
+  } else {
+    k_aos_batch_download<<<grid, 256, 0, c->stream>>>(b);
+    CU(cudaGetLastError());
+    for (int k = 0; k < n; ++k)
+      CU(cudaMemcpyAsync(const_cast<double*>(spec[k].host), c->d_stage + size_t(k) * 4 * nt,
+                         sizeof(double) * spec[k].width * nt, cudaMemcpyDeviceToHost, c->stream));
+  }
+  return B2MD_OK;
+}
+
+int upload_arrays(b2md_ctx* c, const AosSpec* spec, int n) { return move_arrays(c, spec, n, true); }
+int download_arrays(b2md_ctx* c, const AosSpec* spec, int n) { return move_arrays(c, spec, n, false); }
 
 int setup_shard(b2md_ctx* c) {
   int64_t cand = 0;
@@ -1085,7 +1229,8 @@ void free_ctx(b2md_ctx* c) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
   }
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm) g_nccl.CommDestroy(c->comm);
+  if (c->h_sums_pinned) cudaFreeHost(c->h_sums_pinned);
   void* ptrs[] = {c->d_tab,   c->d_species_of, c->d_site_begin, c->d_state, c->d_fbuf, c->d_off,
                   c->d_stage, c->d_mask,       c->d_cta_part, c->d_ticket, c->d_fixpos, c->d_pos4,   c->d_super, c->d_error, c->d_q_mol,
                   c->d_q_site, c->d_q_val,     c->d_mol_qbegin, c->d_kv,    c->d_etab,  c->d_S,
@@ -1250,12 +1395,15 @@ int b2md_upload_state(b2md_ctx* c, const double* pos, const double* orient, cons
                       const double* ang_vel, const double* force, const double* torque) {
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "upload_state: null context");
   CU(cudaSetDevice(c->device));
-  if (pos) TRY(upload_aos(c, 0, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
-  if (orient) TRY(upload_aos(c, 1, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
-  if (vel) TRY(upload_aos(c, 2, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
-  if (ang_vel) TRY(upload_aos(c, 3, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
-  if (force) TRY(upload_aos(c, 4, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
-  if (torque) TRY(upload_aos(c, 5, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
+  AosSpec spec[6];
+  int n = 0;
+  if (pos) spec[n++] = {pos, 3, {c->st.px, c->st.py, c->st.pz, nullptr}};
+  if (orient) spec[n++] = {orient, 4, {c->st.qw, c->st.qx, c->st.qy, c->st.qz}};
+  if (vel) spec[n++] = {vel, 3, {c->st.vx, c->st.vy, c->st.vz, nullptr}};
+  if (ang_vel) spec[n++] = {ang_vel, 3, {c->st.wx, c->st.wy, c->st.wz, nullptr}};
+  if (force) spec[n++] = {force, 3, {c->st.fx, c->st.fy, c->st.fz, nullptr}};
+  if (torque) spec[n++] = {torque, 3, {c->st.tx, c->st.ty, c->st.tz, nullptr}};
+  TRY(upload_arrays(c, spec, n));
   // steps wrap before every evaluation, so step-time forces may use the fast path
   set_wrapped(c, true);
   c->state_valid = true;
@@ -1266,12 +1414,15 @@ int b2md_get_state(b2md_ctx* c, double* pos, double* orient, double* vel, double
                    double* force, double* torque, b2md_energy* energy, b2md_eval_stats* stats) {
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "get_state: null context");
   CU(cudaSetDevice(c->device));
-  if (pos) TRY(download_aos(c, 0, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
-  if (orient) TRY(download_aos(c, 1, orient, 4, c->st.qw, c->st.qx, c->st.qy, c->st.qz));
-  if (vel) TRY(download_aos(c, 2, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
-  if (ang_vel) TRY(download_aos(c, 3, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
-  if (force) TRY(download_aos(c, 4, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
-  if (torque) TRY(download_aos(c, 5, torque, 3, c->st.tx, c->st.ty, c->st.tz, nullptr));
+  AosSpec spec[6];
+  int n = 0;
+  if (pos) spec[n++] = {pos, 3, {c->st.px, c->st.py, c->st.pz, nullptr}};
+  if (orient) spec[n++] = {orient, 4, {c->st.qw, c->st.qx, c->st.qy, c->st.qz}};
+  if (vel) spec[n++] = {vel, 3, {c->st.vx, c->st.vy, c->st.vz, nullptr}};
+  if (ang_vel) spec[n++] = {ang_vel, 3, {c->st.wx, c->st.wy, c->st.wz, nullptr}};
+  if (force) spec[n++] = {force, 3, {c->st.fx, c->st.fy, c->st.fz, nullptr}};
+  if (torque) spec[n++] = {torque, 3, {c->st.tx, c->st.ty, c->st.tz, nullptr}};
+  TRY(download_arrays(c, spec, n));
   TRY(download_scalars(c, energy, stats));
   CU(cudaStreamSynchronize(c->stream));
   return B2MD_OK;
@@ -1709,7 +1860,8 @@ int b2md_rdf_set_counts(b2md_rdf* h, int replica, const uint64_t* counts, int64_
 int b2md_nccl_unique_id(char id[128]) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
   ncclUniqueId u;
-  NC(ncclGetUniqueId(&u));
+  TRY(nccl_load());
+  NC(g_nccl.GetUniqueId(&u));
   std::memcpy(id, &u, 128);
   return B2MD_OK;
 }
@@ -1718,14 +1870,15 @@ int b2md_attach_nccl(b2md_ctx* c, const char id[128], int rank, int world) {
   if (!c || !id || world < 1 || rank < 0 || rank >= world)
     return set_err(B2MD_INVALID_ARGUMENT, "attach_nccl: bad argument");
   CU(cudaSetDevice(c->device));
+  if (world > 1) TRY(nccl_load());
   if (c->comm) {
-    ncclCommDestroy(c->comm);
+    g_nccl.CommDestroy(c->comm);
     c->comm = nullptr;
   }
   if (world > 1) {
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
-    NC(ncclCommInitRank(&c->comm, world, u, rank));
+    NC(g_nccl.CommInitRank(&c->comm, world, u, rank));
   }
   c->rank = rank;
   c->world = world;
@@ -1738,7 +1891,7 @@ int b2md_set_shard(b2md_ctx* c, int rank, int world) {
     return set_err(B2MD_INVALID_ARGUMENT, "set_shard: bad argument");
   CU(cudaSetDevice(c->device));
   if (c->comm) {
-    ncclCommDestroy(c->comm);
+    g_nccl.CommDestroy(c->comm);
     c->comm = nullptr;
   }
   c->rank = rank;

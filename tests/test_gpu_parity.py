@@ -515,3 +515,26 @@ def test_fused_kick_bit_identical(cfg):
         s = eng.state()
         out.append(np.hstack([s.pos, s.orient, s.vel, s.ang_vel, s.force, s.torque]))
     assert np.array_equal(out[0], out[1])
+
+
+def test_pinned_and_pageable_transfers_agree():
+    """b2md_upload_state / b2md_get_state: pinned host buffers take the
+    one-launch zero-copy path, pageable ones the staged copies; same bits."""
+    import torch
+    wl = configs.make("cfg1")
+    st = wl.states[0]
+    n = wl.comp.molecule_count()
+    outs = []
+    for pinned in (True, False):
+        eng = b2.Engine(wl.comp, wl.opts, wl.dt)
+        eng.set_state(st)
+        mk = (lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()) if pinned \
+            else (lambda a: np.ascontiguousarray(a).copy())
+        bufs = [mk(x) for x in (st.pos, st.orient, st.vel, st.ang_vel, np.zeros((n, 3)), np.zeros((n, 3)))]
+        eng.get_state_raw(*bufs)
+        for _ in range(3):
+            eng.upload_state_raw(*bufs)
+            eng.step(1)
+            eng.get_state_raw(*bufs)
+        outs.append(np.hstack([np.array(b) for b in bufs]))
+    assert np.array_equal(outs[0], outs[1])
