@@ -186,6 +186,7 @@ struct b2md_ctx {
   unsigned* d_ticket = nullptr;   // 2 * R: force, ewald
   int force_grid = 1;
   int force_warps = kForceWarps;  // warps per CTA of the partner walks
+  int force_split = 1;            // warps per row in the force walks (1, 2, 4, 8)
   uint32_t* d_super = nullptr;
   int n_super_tiles = 0;
   int* d_error = nullptr;
@@ -434,6 +435,17 @@ bool kick_fusable(const b2md_ctx* c) {
          !(c->world > 1 && c->comm);
 }
 
+// k_force_rigid applies: a single species whose site pairs are all LJ terms
+// in the PairTable's (ia, ib) order, no charges, 2 or 3 sites; returns the
+// site count (0: not applicable)
+int rigid_sites(const ModelTables& t) {
+  if (t.single_site_path || t.ns != 1 || !t.qq[0].empty()) return 0;
+  const int ns = t.species[0].n_sites;
+  bool full = int(t.lj[0].size()) == ns * ns;
+  for (int k = 0; full && k < ns * ns; ++k) full = t.lj[0][k].a == k / ns && t.lj[0][k].b == k % ns;
+  return full && (ns == 2 || ns == 3) ? ns : 0;
+}
+
 // positions known to lie in [0, L) (set_state / step wrap them) and every
 // listed pair's components far from L/2: the branch-free minimum image is exact
 bool fast_min_image(const b2md_ctx* c) {
@@ -447,25 +459,24 @@ bool fast_min_image(const b2md_ctx* c) {
 int launch_force(b2md_ctx* c, bool kick) {
   ForceArgs a = force_args(c);
   if (kick) a.kick_dt = c->dt;
+  a.split = c->force_split;
   const bool w = fast_min_image(c);
+  const bool sp = c->force_split > 1;
   dim3 grid(c->force_grid, c->R);
   const int bs = c->force_warps * 32;
-#define FORCE_LAUNCH(K, ...)                                                        \
-  do {                                                                              \
-    if (w)                                                                          \
-      PROF(c, F_FORCE, (K<__VA_ARGS__, true><<<grid, bs, 0, c->stream>>>(a)));      \
-    else                                                                            \
-      PROF(c, F_FORCE, (K<__VA_ARGS__, false><<<grid, bs, 0, c->stream>>>(a)));     \
+#define FORCE_LAUNCH(K, ...)                                                              \
+  do {                                                                                    \
+    if (w && sp)                                                                          \
+      PROF(c, F_FORCE, (K<__VA_ARGS__, true, true><<<grid, bs, 0, c->stream>>>(a)));      \
+    else if (w)                                                                           \
+      PROF(c, F_FORCE, (K<__VA_ARGS__, true, false><<<grid, bs, 0, c->stream>>>(a)));     \
+    else if (sp)                                                                          \
+      PROF(c, F_FORCE, (K<__VA_ARGS__, false, true><<<grid, bs, 0, c->stream>>>(a)));     \
+    else                                                                                  \
+      PROF(c, F_FORCE, (K<__VA_ARGS__, false, false><<<grid, bs, 0, c->stream>>>(a)));    \
   } while (0)
   // single species, every site pair an LJ term in (ia, ib) order, no charges
-  int rigid_ns = 0;
-  if (!c->t.single_site_path && c->t.ns == 1 && c->t.qq[0].empty()) {
-    const int ns = c->t.species[0].n_sites;
-    bool full = int(c->t.lj[0].size()) == ns * ns;
-    for (int k = 0; full && k < ns * ns; ++k)
-      full = c->t.lj[0][k].a == k / ns && c->t.lj[0][k].b == k % ns;
-    if (full && (ns == 2 || ns == 3)) rigid_ns = ns;
-  }
+  const int rigid_ns = rigid_sites(c->t);
   if (c->t.single_site_path) {
     if (c->t.ns > 1)
       FORCE_LAUNCH(k_force_single, true);
@@ -1087,7 +1098,20 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const int rows_grid = (t.n + kForceWarps - 1) / kForceWarps;
+    // row split: two warps per row for the general multi-site kernel
+    // (charge terms: erfc / exp per site pair) when its rows do not fill the
+    // resident warps (16 per SM at 128 registers).  Measured (steps/s): cfg2
+    // S=1 4.2k, S=2 5.0k, S=4 4.7k; the LJ-only walks lose at any split
+    // (cfg0 S=4 -23%, cfg1 S=2 -17%, cfg4 S=2 -18%: duplicated expansion
+    // outweighs the extra warps).
+    const bool multi_kernel = !t.single_site_path && rigid_sites(t) == 0;
+    const long resident = long(sms) * 16;
+    int S = multi_kernel && long(t.n) * R < resident ? 2 : 1;
+    if (const char* e = std::getenv("B2MD_FORCE_SPLIT")) S = std::max(1, std::min(kForceWarps, std::atoi(e)));
+    while (kForceWarps % S) --S;
+    c->force_split = S;
+    const int rpc = kForceWarps / S;
+    const int rows_grid = (t.n + rpc - 1) / rpc;
     c->force_grid = std::max(1, std::min(rows_grid, sms * 4));
     // re-sort only where the search's tile cull can use the order: single
     // species (fixed-point path) and a COM radius well below L/2

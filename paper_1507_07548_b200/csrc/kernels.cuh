@@ -517,10 +517,16 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 // Queue capacity per warp: a carried partial batch (< 32) + one chunk (<= 1024).
 constexpr int kQueue = kChunkWords * 32 + 32;
 
+// Row split (part, nparts > 1): the nparts warps of a row all expand it and
+// warp `part` evaluates the batches with index = part mod nparts, so short
+// rows of small systems still occupy the GPU; each batch is evaluated by
+// exactly one warp.
 template <bool DUAL = true, typename Body>
 __device__ __forceinline__ void for_each_partner(const uint32_t* __restrict__ row, int words,
-                                                 int lane, int* __restrict__ q, Body&& body) {
+                                                 int lane, int* __restrict__ q, Body&& body,
+                                                 int part = 0, int nparts = 1) {
   int fill = 0;  // warp-uniform queue length carried between chunks
+  int bk = 0;    // batches of this row so far (row split)
   const int nchunks = (words + kChunkWords - 1) / kChunkWords;
   for (int g0 = 0; g0 < nchunks; g0 += 64) {
     // Occupancy pass over (up to) 64 chunks: the words are loaded with eight
@@ -577,17 +583,22 @@ __device__ __forceinline__ void for_each_partner(const uint32_t* __restrict__ ro
       fill += total;
       __syncwarp();
       int e = 0;
-      if (DUAL)
-        for (; e + 64 <= fill; e += 64) {  // two full batches: both gathers in flight
-          const int j0 = q[e + lane], j1 = q[e + 32 + lane];
-          body(j0);
-          body(j1);
+      if (nparts > 1) {
+        for (; e + 32 <= fill; e += 32, ++bk)
+          if (bk % nparts == part) body(q[e + lane]);
+      } else {
+        if (DUAL)
+          for (; e + 64 <= fill; e += 64) {  // two full batches: both gathers in flight
+            const int j0 = q[e + lane], j1 = q[e + 32 + lane];
+            body(j0);
+            body(j1);
+          }
+        else
+          for (; e + 64 <= fill; e += 32) body(q[e + lane]);
+        if (e + 32 <= fill) {
+          body(q[e + lane]);
+          e += 32;
         }
-      else
-        for (; e + 64 <= fill; e += 32) body(q[e + lane]);
-      if (e + 32 <= fill) {
-        body(q[e + lane]);
-        e += 32;
       }
       const int rem = fill - e;  // carry the partial batch
       const int v = lane < rem ? q[e + lane] : 0;
@@ -597,7 +608,26 @@ __device__ __forceinline__ void for_each_partner(const uint32_t* __restrict__ ro
       fill = rem;
     }
   }
-  if (lane < fill) body(q[lane]);
+  if (lane < fill && bk % nparts == part) body(q[lane]);
+}
+
+// Row-split epilogue: the parts of row group `rl` are summed in part order
+// (deterministic) by part 0; returns true on the lane that owns the totals.
+template <int NV>
+__device__ __forceinline__ bool combine_parts(double (&v)[NV], double (*slab)[NV], int warp,
+                                              int lane, int S) {
+  if (lane == 0)
+    for (int k = 0; k < NV; ++k) slab[warp][k] = v[k];
+  __syncthreads();
+  const bool owner = warp % S == 0 && lane == 0;
+  if (owner)
+    for (int k = 0; k < NV; ++k) {
+      double t = slab[warp][k];
+      for (int p = 1; p < S; ++p) t += slab[warp + p][k];
+      v[k] = t;
+    }
+  __syncthreads();  // the slab is rewritten by the next row group
+  return owner;
 }
 
 // 1/x to ~1 ulp without the IEEE-division slow path: hardware reciprocal
@@ -680,13 +710,14 @@ struct ForceArgs {
   // the forces are complete after this kernel (no Ewald term, no all-reduce)
   double kick_dt;
   int* error_mol;
+  int split;  // warps per row (row-split kernels)
 };
 
 struct StepArgs;
 __device__ __forceinline__ void fused_kick(const ForceArgs& a, size_t gid);
 
 
-template <bool MULTI_SPECIES, bool WRAPPED>
+template <bool MULTI_SPECIES, bool WRAPPED, bool SPLIT>
 __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) {
   __shared__ int plist[kForceWarps][kQueue];
   const SysDev& s = a.s;
@@ -701,11 +732,20 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
   };
   double u = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
   const int wpb = blockDim.x >> 5;  // warps per CTA (<= kForceWarps; fewer for small systems)
-  for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
+  // row groups: S warps per row when SPLIT (S divides the CTA's warps)
+  const int S = SPLIT ? a.split : 1;
+  const int rpc = wpb / S, rl = warp / S, part = warp % S;
+  __shared__ double slab[SPLIT ? kForceWarps : 1][3];
+  for (int base = blockIdx.x * rpc;; base += gridDim.x * rpc) {
+    if (SPLIT ? base >= s.n : base + rl >= s.n) break;  // CTA-uniform when SPLIT
+    const int i_ = base + rl;
+    const bool has = i_ < s.n;
+    const int i = has ? i_ : 0;
     const double4 pi = p4[i];  // i, j: slots (single-site terms are symmetric)
     const int si = MULTI_SPECIES ? s.sp_slot[roff + i] : 0;
     double fx = 0, fy = 0, fz = 0;
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
+    if (has)
     for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
       const double4 pj = p4[j];
       const double dx = mimg(sub(pi.x, pj.x));
@@ -736,11 +776,19 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
         s2 += 156.0 * a12 - 42.0 * a6;
         cnt += 1.0;
       }
-    });
+    }, part, S);
     fx = warp_sum(fx);
     fy = warp_sum(fy);
     fz = warp_sum(fz);
-    if (lane == 0) {
+    bool own = lane == 0 && has;
+    if constexpr (SPLIT) {
+      double vv[3] = {fx, fy, fz};
+      own = combine_parts<3>(vv, slab, warp, lane, S) && has;
+      fx = vv[0];
+      fy = vv[1];
+      fz = vv[2];
+    }
+    if (own) {
       const size_t e = roff + ext_of(pi);
       a.st.fx[e] = fx;
       a.st.fy[e] = fy;
@@ -762,7 +810,7 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_single(ForceArgs a) 
 // so the site cutoff r2 < rc2 is decided on the reference's bits either way;
 // force on i is fs*rv and torque d_i x (fs*rv).
 // METHOD: 0 none, 1 reaction field, 2 ewald real space.
-template <int METHOD, bool WRAPPED>
+template <int METHOD, bool WRAPPED, bool SPLIT>
 __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
   __shared__ int plist[kForceWarps][kQueue];
   const SysDev& s = a.s;
@@ -781,13 +829,22 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
   const double rc2 = a.rc2;
   double ulj = 0, uel = 0, urf = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
   const int wpb = blockDim.x >> 5;  // warps per CTA (<= kForceWarps; fewer for small systems)
-  for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
+  // row groups: S warps per row when SPLIT (S divides the CTA's warps)
+  const int S = SPLIT ? a.split : 1;
+  const int rpc = wpb / S, rl = warp / S, part = warp % S;
+  __shared__ double slab[SPLIT ? kForceWarps : 1][6];
+  for (int base = blockIdx.x * rpc;; base += gridDim.x * rpc) {
+    if (SPLIT ? base >= s.n : base + rl >= s.n) break;  // CTA-uniform when SPLIT
+    const int i_ = base + rl;
+    const bool has = i_ < s.n;
+    const int i = has ? i_ : 0;
     const double4 pi = p4[i];  // i, j: slots; the reference's order is that of ext_of
     const int ei = ext_of(pi);
     const int si = s.sp_slot[roff + i];
     const int bi = s.sb_slot[roff + i];
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
+    if (has)
     for_each_partner(row, s.words, lane, plist[warp], [&](int j) {
       const double4 pj = p4[j];
       const bool lo = ei < ext_of(pj);
@@ -897,14 +954,25 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
       }
       s1 += s1p;
       s2 += s2p;
-    });
+    }, part, S);
     fx = warp_sum(fx);
     fy = warp_sum(fy);
     fz = warp_sum(fz);
     tx = warp_sum(tx);
     ty = warp_sum(ty);
     tz = warp_sum(tz);
-    if (lane == 0) {
+    bool own = lane == 0 && has;
+    if constexpr (SPLIT) {
+      double vv[6] = {fx, fy, fz, tx, ty, tz};
+      own = combine_parts<6>(vv, slab, warp, lane, S) && has;
+      fx = vv[0];
+      fy = vv[1];
+      fz = vv[2];
+      tx = vv[3];
+      ty = vv[4];
+      tz = vv[5];
+    }
+    if (own) {
       const size_t e = roff + ext_of(pi);
       a.st.fx[e] = fx;
       a.st.fy[e] = fy;
@@ -1114,7 +1182,7 @@ __global__ void __launch_bounds__(kForceWarps * 32, OFFS ? 2 : 4) k_heat_flux(Fl
 // offsets sit in registers; each partner's site offsets are gathered once per
 // pair (not once per term).  Same arithmetic and orientation rules as
 // k_force_multi.
-template <int NS, bool WRAPPED>
+template <int NS, bool WRAPPED, bool SPLIT>
 __global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a) {
   __shared__ int plist[kForceWarps][kQueue];
   const SysDev& s = a.s;
@@ -1141,7 +1209,15 @@ __global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a
   const double rc2 = a.rc2;
   double ulj = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
   const int wpb = blockDim.x >> 5;  // warps per CTA (<= kForceWarps; fewer for small systems)
-  for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
+  // row groups: S warps per row when SPLIT (S divides the CTA's warps)
+  const int S = SPLIT ? a.split : 1;
+  const int rpc = wpb / S, rl = warp / S, part = warp % S;
+  __shared__ double slab[SPLIT ? kForceWarps : 1][6];
+  for (int base = blockIdx.x * rpc;; base += gridDim.x * rpc) {
+    if (SPLIT ? base >= s.n : base + rl >= s.n) break;  // CTA-uniform when SPLIT
+    const int i_ = base + rl;
+    const bool has = i_ < s.n;
+    const int i = has ? i_ : 0;
     const double4 pi = p4[i];  // i, j: slots; the reference's order is that of ext_of
     const int ei = ext_of(pi);
     const int bi = i * NS;  // single species: slot-ordered sites start at i * NS
@@ -1150,6 +1226,7 @@ __global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a
     for (int k = 0; k < NS; ++k) di[k] = o4[bi + k];
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
     const uint32_t* row = a.mask + (size_t(r) * s.n_pad + i) * s.words;
+    if (has)
     for_each_partner<false>(row, s.words, lane, plist[warp], [&](int j) {
       const double4 pj = p4[j];
       const bool lo = ei < ext_of(pj);
@@ -1209,14 +1286,25 @@ __global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a
         }
       s1 += s1p;
       s2 += s2p;
-    });
+    }, part, S);
     fx = warp_sum(fx);
     fy = warp_sum(fy);
     fz = warp_sum(fz);
     tx = warp_sum(tx);
     ty = warp_sum(ty);
     tz = warp_sum(tz);
-    if (lane == 0) {
+    bool own = lane == 0 && has;
+    if constexpr (SPLIT) {
+      double vv[6] = {fx, fy, fz, tx, ty, tz};
+      own = combine_parts<6>(vv, slab, warp, lane, S) && has;
+      fx = vv[0];
+      fy = vv[1];
+      fz = vv[2];
+      tx = vv[3];
+      ty = vv[4];
+      tz = vv[5];
+    }
+    if (own) {
       const size_t e = roff + ext_of(pi);
       a.st.fx[e] = fx;
       a.st.fy[e] = fy;
