@@ -245,6 +245,18 @@ int b2md_heat_flux_state(b2md_ctx* ctx, const double* pos, const double* orient,
                          const double* vel, const double* ang_vel, const double* enthalpy,
                          int n_enthalpy, double* jq);
 
+/* Thermostat and kinetic energies (src/engine.cpp:145-160, src/model.cpp:
+ * 304-330).  kinetic_energy: kinetic_energy_trans / _rot of every replica
+ * (fixed-order device reduction).  apply_thermostat: Engine::apply_thermostat
+ * (isokinetic rescale to the composition's temperature) on every replica;
+ * B2MD_NUMERICAL_ERROR "thermostat: zero translational (rotational) kinetic
+ * energy" as the reference throws.  step_thermostat: Engine::run's loop —
+ * steps numbered done+1 .. done+nsteps of the phase, the rescale after each
+ * step whose number is a multiple of `interval` (<= 0: none). */
+int b2md_kinetic_energy(b2md_ctx* ctx, double* ke_trans, double* ke_rot);
+int b2md_apply_thermostat(b2md_ctx* ctx);
+int b2md_step_thermostat(b2md_ctx* ctx, int64_t nsteps, int interval, int64_t done);
+
 /* Checkpoint state block: the device-resident part of
  * tmd::Engine::checkpoint_bytes (src/engine.cpp:432-441) — u32 n, f64
  * box_length, then per molecule pos.xyz, orient.wxyz, vel.xyz, ang_vel.xyz

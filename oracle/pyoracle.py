@@ -51,6 +51,8 @@ def oracle_lib():
         L.oracle_pair_list.argtypes = [C.c_void_p, _D, C.POINTER(C.c_int32), C.c_int64]
         L.oracle_pair_list.restype = C.c_int64
         L.oracle_wrap.argtypes = [C.c_int, C.c_double, _D]
+        L.oracle_kinetic_energy.argtypes = [C.c_void_p, _D, _D, _D]
+        L.oracle_apply_thermostat.argtypes = [C.c_void_p, _D, _D]
         L.oracle_heat_flux.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, C.c_int, _D]
         L.oracle_rdf_create.argtypes = [C.c_void_p, C.c_double, C.c_double, C.POINTER(C.c_void_p)]
         L.oracle_rdf_destroy.argtypes = [C.c_void_p]
@@ -83,6 +85,8 @@ def ref_lib():
         L.ref_evaluate.argtypes = [C.c_void_p, _D, _D, _D, _D, C.POINTER(_abi.b2md_energy), _D]
         L.ref_pair_list.argtypes = [C.c_void_p, _D, C.POINTER(C.c_int32), C.c_int64]
         L.ref_pair_list.restype = C.c_int64
+        L.ref_engine_apply_thermostat.argtypes = [C.c_void_p]
+        L.ref_kinetic_energy.argtypes = [C.c_void_p, _D, _D, _D]
         L.ref_heat_flux.argtypes = [C.c_void_p, _D, _D, _D, _D, _D, C.c_int, _D]
         L.ref_rdf_create.argtypes = [C.c_void_p, C.c_double, C.c_double, C.POINTER(C.c_void_p)]
         L.ref_rdf_destroy.argtypes = [C.c_void_p]
@@ -162,6 +166,10 @@ class _FF:
     def warning(self) -> str:
         return getattr(self.lib, self.prefix + "_ff_warning")(self.h).decode()
 
+    def kinetic_energy(self, vel, ang_vel):
+        """kinetic_energy_trans / _rot (model.cpp:304-319)."""
+        return _kinetic(self, vel, ang_vel)
+
     def pair_list(self, pos) -> np.ndarray:
         pos = np.ascontiguousarray(pos, dtype=np.float64)
         fn = getattr(self.lib, self.prefix + "_pair_list")
@@ -183,10 +191,25 @@ def _heat_flux(ff, pos, orient, vel, ang_vel, enthalpy):
     return out
 
 
+def _kinetic(ff, vel, ang_vel):
+    v = np.ascontiguousarray(vel, dtype=np.float64).reshape(ff.n, 3)
+    w = np.ascontiguousarray(ang_vel, dtype=np.float64).reshape(ff.n, 3)
+    out = np.zeros(2)
+    _check(ff.lib, ff.prefix, getattr(ff.lib, ff.prefix + "_kinetic_energy")(ff.h, _d(v), _d(w), _d(out)))
+    return out
+
+
 class OracleFF(_FF):
     """C restatement (serial ForceField::evaluate + Engine::step)."""
 
     prefix = "oracle"
+
+    def apply_thermostat(self, vel, ang_vel):
+        """Engine::apply_thermostat on copies; returns (vel, ang_vel)."""
+        v = np.array(vel, dtype=np.float64).reshape(self.n, 3)
+        w = np.array(ang_vel, dtype=np.float64).reshape(self.n, 3)
+        _check(self.lib, "oracle", self.lib.oracle_apply_thermostat(self.h, _d(v), _d(w)))
+        return v, w
 
     def heat_flux(self, pos, orient, vel, ang_vel, enthalpy):
         return _heat_flux(self, pos, orient, vel, ang_vel, enthalpy)
@@ -281,6 +304,9 @@ class RefEngine:
         buf = C.create_string_buffer(int(n))
         self.lib.ref_engine_checkpoint(self.h, buf, n)
         return buf.raw
+
+    def apply_thermostat(self) -> None:
+        _check(self.lib, "ref", self.lib.ref_engine_apply_thermostat(self.h))
 
     def restore(self, data: bytes) -> None:
         _check(self.lib, "ref", self.lib.ref_engine_restore(self.h, data, len(data)))
@@ -418,4 +444,32 @@ def ref_run_sampled_checkpoint(comp, opts, dt, seed, n_equil, n_prod, *, n_ext=1
         raise OracleError(2, L.ref_last_error().decode())
     buf = C.create_string_buffer(int(n))
     L.ref_run_sampled_checkpoint(*args, buf, n)
+    return buf.raw
+
+
+def ref_derivative_accumulator(temperature, volume, n_mol, n_blocks, expected, samples) -> bytes:
+    """tmd::DerivativeAccumulator fed `samples` (k x 3), serialized."""
+    L = ref_lib()
+    L.ref_derivative_accumulator.argtypes = [C.c_double, C.c_double, C.c_int64, C.c_int, C.c_int64, _D,
+                                             C.c_int, C.c_char_p, C.c_int64]
+    L.ref_derivative_accumulator.restype = C.c_int64
+    smp = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 3)
+    args = (temperature, volume, n_mol, n_blocks, expected, _d(smp), len(smp))
+    n = L.ref_derivative_accumulator(*args, None, 0)
+    if n < 0:
+        raise OracleError(2, L.ref_last_error().decode())
+    buf = C.create_string_buffer(int(n))
+    L.ref_derivative_accumulator(*args, buf, n)
+    return buf.raw
+
+
+def ref_block_stat(n_blocks, expected, x) -> bytes:
+    """tmd::BlockStat fed `x`, serialized."""
+    L = ref_lib()
+    L.ref_block_stat.argtypes = [C.c_int, C.c_int64, _D, C.c_int, C.c_char_p, C.c_int64]
+    L.ref_block_stat.restype = C.c_int64
+    xs = np.ascontiguousarray(x, dtype=np.float64)
+    n = L.ref_block_stat(n_blocks, expected, _d(xs), len(xs), None, 0)
+    buf = C.create_string_buffer(int(n))
+    L.ref_block_stat(n_blocks, expected, _d(xs), len(xs), buf, n)
     return buf.raw

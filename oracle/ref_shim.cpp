@@ -466,3 +466,55 @@ extern "C" int64_t ref_run_sampled_checkpoint(const b2md_composition* comp,
   if (buf && cap >= static_cast<int64_t>(d.size())) std::memcpy(buf, d.data(), d.size());
   return static_cast<int64_t>(d.size());
 }
+
+// ------------------------------------------------ thermostat (engine.cpp:145-160)
+extern "C" int ref_engine_apply_thermostat(void* h) {
+  return guarded([&]() -> int {
+    static_cast<RefEngine*>(h)->eng->apply_thermostat();
+    return B2MD_OK;
+  });
+}
+
+extern "C" int ref_kinetic_energy(void* ffh, const double* vel, const double* ang_vel, double* out) {
+  return guarded([&]() -> int {
+    auto* f = static_cast<RefFF*>(ffh);
+    tmd::SystemState st;
+    get_state(st, f->comp.molecule_count(), nullptr, nullptr, vel, ang_vel);
+    out[0] = tmd::kinetic_energy_trans(f->comp, st);
+    out[1] = tmd::kinetic_energy_rot(f->comp, st);
+    return B2MD_OK;
+  });
+}
+
+// ---------------------- scalar accumulators (massieu.cpp:9-70, results.hpp:21-51)
+#include "tmd/massieu.hpp"
+#include "tmd/results.hpp"
+
+extern "C" int64_t ref_derivative_accumulator(double temperature, double volume, int64_t n_mol,
+                                              int n_blocks, int64_t expected,
+                                              const double* samples, int k, char* buf,
+                                              int64_t cap) {
+  std::string d;
+  const int rc = guarded([&]() -> int {
+    tmd::DerivativeAccumulator a(temperature, volume, n_mol, n_blocks, expected);
+    for (int i = 0; i < k; ++i) a.add(samples[3 * i], samples[3 * i + 1], samples[3 * i + 2]);
+    tmd::ByteWriter w;
+    a.serialize(w);
+    d = w.data();
+    return B2MD_OK;
+  });
+  if (rc) return -1;
+  if (buf && cap >= static_cast<int64_t>(d.size())) std::memcpy(buf, d.data(), d.size());
+  return static_cast<int64_t>(d.size());
+}
+
+extern "C" int64_t ref_block_stat(int n_blocks, int64_t expected, const double* x, int k, char* buf,
+                                  int64_t cap) {
+  tmd::BlockStat b(n_blocks, expected);
+  for (int i = 0; i < k; ++i) b.add(x[i]);
+  tmd::ByteWriter w;
+  b.serialize(w);
+  const std::string& d = w.data();
+  if (buf && cap >= static_cast<int64_t>(d.size())) std::memcpy(buf, d.data(), d.size());
+  return static_cast<int64_t>(d.size());
+}

@@ -1207,3 +1207,44 @@ int oracle_rdf_counts(const oracle_rdf* r, uint64_t* counts, int64_t* snapshots)
   if (snapshots) *snapshots = r->snapshots;
   return B2MD_OK;
 }
+
+/* ------------------------------------------------------------- thermostat */
+
+/* model.cpp:304-319 */
+int oracle_kinetic_energy(const oracle_ff* ff, const double* vel, const double* ang_vel, double* out) {
+  if (!ff || !vel || !ang_vel || !out) return fail(B2MD_INVALID_ARGUMENT, "kinetic_energy: null pointer");
+  double kt = 0.0, kr = 0.0;
+  for (int i = 0; i < ff->n; ++i) {
+    const b2md_species* sp = &ff->species[species_of_molecule(ff, i)];
+    kt += 0.5 * sp->total_mass * vnorm2(load3(vel, i));
+  }
+  for (int i = 0; i < ff->n; ++i) {
+    const b2md_species* sp = &ff->species[species_of_molecule(ff, i)];
+    const double* I = sp->inertia_principal;
+    const vec3 w = load3(ang_vel, i);
+    kr += 0.5 * (I[0] * w.x * w.x + I[1] * w.y * w.y + I[2] * w.z * w.z);
+  }
+  out[0] = kt;
+  out[1] = kr;
+  return B2MD_OK;
+}
+
+/* engine.cpp:145-160 with translational_dof / rotational_dof (model.cpp:321-330) */
+int oracle_apply_thermostat(const oracle_ff* ff, double* vel, double* ang_vel) {
+  double ke[2];
+  int rc = oracle_kinetic_energy(ff, vel, ang_vel, ke);
+  if (rc) return rc;
+  const double T = ff->temperature;
+  const int dof_t = 3 * ff->n - 3;
+  if (ke[0] <= 0.0) return fail(B2MD_NUMERICAL_ERROR, "thermostat: zero translational kinetic energy");
+  const double scale_t = sqrt(0.5 * dof_t * T / ke[0]);
+  for (int i = 0; i < 3 * ff->n; ++i) vel[i] *= scale_t;
+  int dof_r = 0;
+  for (int s = 0; s < ff->ns; ++s) dof_r += ff->counts[s] * ff->species[s].rotational_dof;
+  if (dof_r > 0) {
+    if (ke[1] <= 0.0) return fail(B2MD_NUMERICAL_ERROR, "thermostat: zero rotational kinetic energy");
+    const double scale_r = sqrt(0.5 * dof_r * T / ke[1]);
+    for (int i = 0; i < 3 * ff->n; ++i) ang_vel[i] *= scale_r;
+  }
+  return B2MD_OK;
+}

@@ -69,6 +69,11 @@ int oracle_step(oracle_ff* ff, double dt, int64_t nsteps, double* pos, double* o
 int oracle_heat_flux(oracle_ff* ff, const double* pos, const double* orient, const double* vel,
                      const double* ang_vel, const double* enthalpy, int n_enthalpy, double* jq);
 
+/* kinetic_energy_trans / _rot (src/model.cpp:304-319): out[2] */
+int oracle_kinetic_energy(const oracle_ff* ff, const double* vel, const double* ang_vel, double* out);
+/* Engine::apply_thermostat (src/engine.cpp:145-160), in place */
+int oracle_apply_thermostat(const oracle_ff* ff, double* vel, double* ang_vel);
+
 /* RdfHistogram (include/tmd/structure.hpp:29-67, src/structure.cpp:10-76):
  * integer site-pair histograms per unordered site-type pair. */
 typedef struct oracle_rdf oracle_rdf;

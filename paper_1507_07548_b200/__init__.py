@@ -17,6 +17,7 @@ from .forcefield import (
     shard_plan,
 )
 from .checkpoint import BlockStat, ByteReader, ByteWriter, EngineCheckpoint
+from .sampling import DerivativeAccumulator, accumulate_scalars
 from .structure import (RdfHistogram, RdfTable, finalize_tables, first_minimum, rdf_site_types,
                         serialize_counts, solvation_number)
 from .model import (

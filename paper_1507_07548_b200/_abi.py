@@ -140,6 +140,9 @@ SIGNATURES = {
     "b2md_set_step_options": (C.c_int, [_CTX, C.c_int]),
     "b2md_heat_flux": (C.c_int, [_CTX, _D, C.c_int, _D]),
     "b2md_heat_flux_state": (C.c_int, [_CTX, _D, _D, _D, _D, _D, C.c_int, _D]),
+    "b2md_kinetic_energy": (C.c_int, [_CTX, _D, _D]),
+    "b2md_apply_thermostat": (C.c_int, [_CTX]),
+    "b2md_step_thermostat": (C.c_int, [_CTX, C.c_int64, C.c_int, C.c_int64]),
     "b2md_state_block_size": (C.c_size_t, [_CTX]),
     "b2md_save_state_block": (C.c_int, [_CTX, C.c_int, C.c_char_p, C.c_size_t]),
     "b2md_restore_state_block": (C.c_int, [_CTX, C.c_int, C.c_char_p, C.c_size_t]),

@@ -203,6 +203,8 @@ struct b2md_ctx {
   double2* d_S = nullptr;
   double* d_uk = nullptr;
   double* d_flux = nullptr;  // R * kNumSums: heat flux totals
+  double2* d_ke = nullptr;    // R: (kinetic_energy_trans, kinetic_energy_rot)
+  int* d_thermo_err = nullptr;  // R: thermostat failure code (0 ok)
   // spatial order (resort): slot tables and radix-sort buffers
   int* d_perm = nullptr;
   int* d_slot_of = nullptr;
@@ -1130,6 +1132,9 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars * c->force_grid));
   TRY(dalloc(&c->d_ticket, size_t(2) * R));
   TRY(dalloc(&c->d_flux, size_t(kNumSums) * R));
+  TRY(dalloc(&c->d_ke, R));
+  TRY(dalloc(&c->d_thermo_err, R));
+  CU(cudaMemset(c->d_thermo_err, 0, sizeof(int) * R));
   {
     // spatial-order tables, identity until the first resort
     TRY(dalloc(&c->d_perm, nt));
@@ -1260,7 +1265,7 @@ void free_ctx(b2md_ctx* c) {
                   c->d_q_site, c->d_q_val,     c->d_mol_qbegin, c->d_kv,    c->d_etab,  c->d_S,
                   c->d_uk,    c->d_flux,  c->d_perm, c->d_slot_of, c->d_sp_slot, c->d_sb_slot,
                   c->d_nsites_slot, c->d_scan, c->d_keys[0], c->d_keys[1], c->d_vals[0],
-                  c->d_vals[1], c->d_cub};
+                  c->d_vals[1], c->d_cub, c->d_ke, c->d_thermo_err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1570,6 +1575,100 @@ int b2md_pair_list(b2md_ctx* c, int replica, int32_t* pairs, int64_t capacity, i
   }
   cudaFree(d_cnt);
   return B2MD_OK;
+}
+
+// ------------------------------------------------------------ thermostat
+// model.cpp:321-330
+int dof_trans(const b2md_ctx* c) { return 3 * c->t.n - 3; }
+int dof_rot(const b2md_ctx* c) {
+  int dof = 0;
+  for (int m = 0; m < c->t.n; ++m) dof += c->t.species[c->t.species_of[m]].rotational_dof;
+  return dof;
+}
+
+int launch_kinetic(b2md_ctx* c) {
+  k_kinetic<<<c->R, kKeThreads, 0, c->stream>>>(c->sys, c->st, c->d_ke);
+  CU(cudaGetLastError());
+  return B2MD_OK;
+}
+
+// Engine::apply_thermostat (engine.cpp:145-160) on every replica, on the stream
+int launch_thermostat(b2md_ctx* c) {
+  TRY(launch_kinetic(c));
+  ThermoArgs a;
+  a.s = c->sys;
+  a.st = c->st;
+  a.ke = c->d_ke;
+  a.err = c->d_thermo_err;
+  a.temperature = c->t.temperature;
+  a.dof_t = dof_trans(c);
+  a.dof_r = dof_rot(c);
+  const int nt = n_total(c);
+  k_thermostat<<<(nt + 255) / 256, 256, 0, c->stream>>>(a);
+  CU(cudaGetLastError());
+  return B2MD_OK;
+}
+
+int check_thermostat(b2md_ctx* c) {
+  std::vector<int> err(c->R, 0);
+  CU(cudaMemcpyAsync(err.data(), c->d_thermo_err, sizeof(int) * c->R, cudaMemcpyDeviceToHost,
+                     c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (int r = 0; r < c->R; ++r)
+    if (err[r]) {
+      CU(cudaMemset(c->d_thermo_err, 0, sizeof(int) * c->R));
+      return set_err(B2MD_NUMERICAL_ERROR, err[r] == 1
+                                               ? "thermostat: zero translational kinetic energy"
+                                               : "thermostat: zero rotational kinetic energy");
+    }
+  return B2MD_OK;
+}
+
+int b2md_kinetic_energy(b2md_ctx* c, double* ke_trans, double* ke_rot) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "kinetic_energy: null context");
+  CU(cudaSetDevice(c->device));
+  TRY(launch_kinetic(c));
+  std::vector<double2> ke(c->R);
+  CU(cudaMemcpyAsync(ke.data(), c->d_ke, sizeof(double2) * c->R, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (int r = 0; r < c->R; ++r) {
+    if (ke_trans) ke_trans[r] = ke[r].x;
+    if (ke_rot) ke_rot[r] = ke[r].y;
+  }
+  return B2MD_OK;
+}
+
+int b2md_apply_thermostat(b2md_ctx* c) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "apply_thermostat: null context");
+  if (!c->state_valid) return set_err(B2MD_CONFIG_ERROR, "engine: set_state must precede step");
+  CU(cudaSetDevice(c->device));
+  TRY(launch_thermostat(c));
+  return check_thermostat(c);
+}
+
+// Engine::run's thermostatted loop (engine.cpp:273-296): steps numbered
+// done+1 .. done+nsteps of the current phase, the rescale after every step
+// whose number is a multiple of `interval` (<= 0: none).
+int b2md_step_thermostat(b2md_ctx* c, int64_t nsteps, int interval, int64_t done) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "step: null context");
+  if (!c->engine) return set_err(B2MD_CONFIG_ERROR, "engine: time step must be positive");
+  if (!c->state_valid) return set_err(B2MD_CONFIG_ERROR, "engine: set_state must precede step");
+  if (nsteps <= 0) return B2MD_OK;
+  CU(cudaSetDevice(c->device));
+  if (interval <= 0) {
+    TRY(run_steps(c, nsteps));
+    return check_error_flag(c);
+  }
+  for (int64_t k = 0; k < nsteps;) {
+    const int64_t step_no = done + k;                      // steps already taken
+    const int64_t to_next = interval - step_no % interval;  // steps to the next rescale
+    const int64_t chunk = std::min<int64_t>(to_next, nsteps - k);
+    TRY(run_steps(c, chunk));
+    k += chunk;
+    if ((done + k) % interval == 0) TRY(launch_thermostat(c));
+  }
+  TRY(check_error_flag(c));
+  return check_thermostat(c);
 }
 
 // ------------------------------------------------------ checkpoint state

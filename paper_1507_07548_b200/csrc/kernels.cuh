@@ -1750,6 +1750,73 @@ __global__ void k_pair_fill(const uint32_t* mask, const int* perm, int n, int wo
   }
 }
 
+// ------------------------------------------------------------ thermostat
+// kinetic_energy_trans / kinetic_energy_rot (model.cpp:304-319) per replica:
+// one CTA per replica, thread-strided partial sums in a fixed order and a
+// fixed tree (deterministic; the reference's serial order differs only in
+// rounding).  out[r] = {ke_t, ke_r}.
+constexpr int kKeThreads = 512;
+__global__ void __launch_bounds__(kKeThreads) k_kinetic(SysDev s, StateDev st, double2* out) {
+  __shared__ double red_t[kKeThreads], red_r[kKeThreads];
+  const int r = blockIdx.x, tid = threadIdx.x;
+  double kt = 0.0, kr = 0.0;
+  for (int i = tid; i < s.n; i += kKeThreads) {
+    const size_t g = size_t(r) * s.n + i;
+    const DevSpecies& sp = s.tab->species[s.species_of[i]];
+    kt += 0.5 * sp.total_mass * norm2_exact(st.vx[g], st.vy[g], st.vz[g]);
+    const double wx = st.wx[g], wy = st.wy[g], wz = st.wz[g];
+    kr += 0.5 * (sp.inertia[0] * wx * wx + sp.inertia[1] * wy * wy + sp.inertia[2] * wz * wz);
+  }
+  red_t[tid] = kt;
+  red_r[tid] = kr;
+  __syncthreads();
+  for (int w = kKeThreads / 2; w > 0; w >>= 1) {
+    if (tid < w) {
+      red_t[tid] += red_t[tid + w];
+      red_r[tid] += red_r[tid + w];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) out[r] = make_double2(red_t[0], red_r[0]);
+}
+
+// Engine::apply_thermostat (engine.cpp:145-160): isokinetic rescale of the
+// translational and (dof_r > 0) rotational velocities to the target T.
+// A zero kinetic energy is the reference's NumericalError: error code
+// 1 (translational) / 2 (rotational) per replica in err[r], state unchanged.
+struct ThermoArgs {
+  SysDev s;
+  StateDev st;
+  const double2* ke;
+  int* err;
+  double temperature;
+  int dof_t, dof_r;
+};
+__global__ void k_thermostat(ThermoArgs a) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= a.s.n * a.s.R) return;
+  const int r = gid / a.s.n;
+  const double2 ke = a.ke[r];
+  if (ke.x <= 0.0) {
+    if (gid == r * a.s.n) a.err[r] = 1;
+    return;
+  }
+  if (a.dof_r > 0 && ke.y <= 0.0) {
+    if (gid == r * a.s.n) a.err[r] = 2;
+    return;
+  }
+  const double st_ = sqrt(0.5 * a.dof_t * a.temperature / ke.x);
+  a.st.vx[gid] *= st_;
+  a.st.vy[gid] *= st_;
+  a.st.vz[gid] *= st_;
+  if (a.dof_r > 0) {
+    const double sr = sqrt(0.5 * a.dof_r * a.temperature / ke.y);
+    a.st.wx[gid] *= sr;
+    a.st.wy[gid] *= sr;
+    a.st.wz[gid] *= sr;
+  }
+}
+
 // ------------------------------------------------------- checkpoint state
 // Engine::checkpoint_bytes' per-molecule record (engine.cpp:434-440):
 // pos.xyz, orient.wxyz, vel.xyz, ang_vel.xyz as 13 f64, molecule-major.

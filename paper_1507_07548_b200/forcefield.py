@@ -315,6 +315,25 @@ class Engine:
         (same results bit for bit)."""
         check(_abi.lib().b2md_set_step_options(self._c.ctx, int(fused_kick)))
 
+    # --- thermostat (engine.cpp:145-160, 273-296) and kinetic energies
+    def kinetic_energies(self) -> tuple[np.ndarray, np.ndarray]:
+        """(kinetic_energy_trans, kinetic_energy_rot) of every replica
+        (model.cpp:304-319), reduced on the device."""
+        kt = np.zeros(self.replicas)
+        kr = np.zeros(self.replicas)
+        check(_abi.lib().b2md_kinetic_energy(self._c.ctx, _abi.dptr(kt), _abi.dptr(kr)))
+        return kt, kr
+
+    def apply_thermostat(self) -> None:
+        """Engine::apply_thermostat: isokinetic rescale to the composition's
+        temperature (every replica)."""
+        check(_abi.lib().b2md_apply_thermostat(self._c.ctx))
+
+    def step_thermostat(self, nsteps: int, interval: int, done: int = 0) -> None:
+        """Engine::run's loop: steps done+1 .. done+nsteps of a phase with the
+        rescale after each step whose number is a multiple of `interval`."""
+        check(_abi.lib().b2md_step_thermostat(self._c.ctx, int(nsteps), int(interval), int(done)))
+
     # --- checkpoint / restart (engine.cpp:420-541)
     def state_block(self, replica: int = 0) -> bytes:
         """The state block of Engine::checkpoint_bytes (engine.cpp:432-441),

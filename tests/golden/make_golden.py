@@ -137,6 +137,24 @@ def checkpoint_vectors():
                         fresh_seed=5, cuts=np.array(cuts), cut_messages=np.array(msgs))
 
 
+def sampling_vectors():
+    """tmd::DerivativeAccumulator (massieu.cpp:9-70) and tmd::BlockStat
+    (results.hpp:21-51) fed seeded samples, serialized by the reference."""
+    rng = np.random.default_rng(2718)
+    out = {}
+    cases = [(1, 0, 5), (4, 20, 20), (4, 10, 23), (7, 30, 13), (3, 1, 4)]
+    for k, (nb, expected, count) in enumerate(cases):
+        smp = rng.normal(size=(count, 3)) * [50.0, 3.0, 0.2] + [-900.0, 4.0, 0.5]
+        x = rng.normal(size=count)
+        out[f"da_{k}_samples"] = smp
+        out[f"da_{k}_bytes"] = np.frombuffer(
+            pyoracle.ref_derivative_accumulator(1.5, 812.0, 256, nb, expected, smp), np.uint8)
+        out[f"bs_{k}_x"] = x
+        out[f"bs_{k}_bytes"] = np.frombuffer(pyoracle.ref_block_stat(nb, expected, x), np.uint8)
+    out["cases"] = np.array(cases)
+    np.savez_compressed(OUT / "sampling.npz", **out)
+
+
 def traj_vectors():
     for name, (comp, opts, st, dt, steps) in golden_cases.traj_cases().items():
         eng = pyoracle.RefEngine(comp, opts, dt, seed=1)
@@ -160,5 +178,6 @@ if __name__ == "__main__":
     flux_vectors()
     rdf_vectors()
     checkpoint_vectors()
+    sampling_vectors()
     traj_vectors()
     print("golden vectors written to", OUT)
