@@ -247,6 +247,7 @@ struct b2md_ctx {
   // host scratch
   std::vector<double> h_sums;
   double* h_sums_pinned = nullptr;  // energy sums read-back (cudaMallocHost)
+
   std::string warning;
 };
 
@@ -902,15 +903,25 @@ void assemble(const b2md_ctx* c, const double* sums, b2md_energy* e, b2md_eval_s
   }
 }
 
-int download_scalars(b2md_ctx* c, b2md_energy* e, b2md_eval_stats* st) {
-  if (!e && !st) return B2MD_OK;
+// energy sums -> pinned host scratch (queued; read after the caller's sync)
+int enqueue_scalars(b2md_ctx* c) {
   const size_t bytes = sizeof(double) * kNumSums * c->R;
   if (!c->h_sums_pinned) CU(cudaMallocHost(&c->h_sums_pinned, bytes));
   CU(cudaMemcpyAsync(c->h_sums_pinned, c->d_fbuf + size_t(6) * n_total(c), bytes,
                      cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
+  return B2MD_OK;
+}
+
+void assemble_all(b2md_ctx* c, b2md_energy* e, b2md_eval_stats* st) {
   for (int r = 0; r < c->R; ++r)
     assemble(c, c->h_sums_pinned + size_t(r) * kNumSums, e ? e + r : nullptr, st ? st + r : nullptr);
+}
+
+int download_scalars(b2md_ctx* c, b2md_energy* e, b2md_eval_stats* st) {
+  if (!e && !st) return B2MD_OK;
+  TRY(enqueue_scalars(c));
+  CU(cudaStreamSynchronize(c->stream));
+  assemble_all(c, e, st);
   return B2MD_OK;
 }
 
@@ -967,7 +978,9 @@ int move_arrays(b2md_ctx* c, const AosSpec* spec, int n, bool upload) {
     CU(cudaGetLastError());
     return B2MD_OK;
   }
-  // staged: slot k of d_stage holds array k (4 nt doubles per slot)
+  // staged: slot k of d_stage holds array k (4 nt doubles per slot).  (Side
+  // copy streams and cached transfer graphs were measured: no gain — the
+  // copies run at the link's bandwidth, cfg3 2.5 MB in ~48 us per direction.)
   for (int k = 0; k < n; ++k) {
     double* stage = c->d_stage + size_t(k) * 4 * nt;
     b.src[k] = stage;
@@ -1452,8 +1465,9 @@ int b2md_get_state(b2md_ctx* c, double* pos, double* orient, double* vel, double
   if (force) spec[n++] = {force, 3, {c->st.fx, c->st.fy, c->st.fz, nullptr}};
   if (torque) spec[n++] = {torque, 3, {c->st.tx, c->st.ty, c->st.tz, nullptr}};
   TRY(download_arrays(c, spec, n));
-  TRY(download_scalars(c, energy, stats));
-  CU(cudaStreamSynchronize(c->stream));
+  if (energy || stats) TRY(enqueue_scalars(c));
+  CU(cudaStreamSynchronize(c->stream));  // one sync for arrays and sums
+  if (energy || stats) assemble_all(c, energy, stats);
   return B2MD_OK;
 }
 
