@@ -530,7 +530,17 @@ int launch_ewald(b2md_ctx* c) {
   PROF(c, F_EWALD_TAB, (k_ewald_tables<<<(nt + 127) / 128, 128, 0, c->stream>>>(a)));
   if (a.nk > 0) {
     PROF(c, F_EWALD_SK, (k_ewald_sk<<<dim3(a.nk, c->R), 256, 0, c->stream>>>(a)));
-    PROF(c, F_EWALD_F, (k_ewald_force<<<dim3((c->t.n + 7) / 8, c->R), 256, 0, c->stream>>>(a)));
+    // k-split: P warps per molecule so that molecules x P reach ~16 warps per SM
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    int P = 1;
+    while (P < 8 && long(c->t.n) * c->R * P < long(sms) * 16) P *= 2;
+    if (const char* e = std::getenv("B2MD_EWALD_KPARTS")) P = std::max(1, std::min(8, std::atoi(e)));
+    while (8 % P) --P;
+    a.kparts = P;
+    const int mpc = 8 / P;
+    PROF(c, F_EWALD_F,
+         (k_ewald_force<<<dim3((c->t.n + mpc - 1) / mpc, c->R), 256, 0, c->stream>>>(a)));
   } else {
     for (int r = 0; r < c->R; ++r)
       CU(cudaMemsetAsync(sums_ptr(c) + size_t(r) * kNumSums + kNumRowScalars, 0, sizeof(double),

@@ -1341,6 +1341,7 @@ struct EwaldArgs {
   unsigned* ticket;     // R
   double* sums;         // R * kNumSums
   int nk_total;
+  int kparts;           // warps per molecule in k_ewald_force (1, 2, 4, 8)
   double two_pi_over_L;
 };
 
@@ -1395,6 +1396,7 @@ __global__ void __launch_bounds__(256) k_ewald_sk(EwaldArgs a) {
   const int K = a.kmax + 1;
   const double2* base = a.tab + size_t(r) * 3 * K * a.nq;
   double sre = 0.0, sim = 0.0;
+#pragma unroll 4
   for (int q = threadIdx.x; q < a.nq; q += blockDim.x) {
     const double2 e = site_phase(base, K, a.nq, q, k);
     sre += e.x * a.q_val[q];
@@ -1424,15 +1426,19 @@ __global__ void __launch_bounds__(256) k_ewald_sk(EwaldArgs a) {
   finalize_scalars<1>(v, a.uk, a.ticket, a.sums, r, kNumRowScalars);
 }
 
-// ewald.cpp:171-178: one warp per molecule with charges; lanes over k; adds
-// F and torque = off x F into the (already written) real-space totals.
+// ewald.cpp:171-178: P = a.kparts warps per molecule with charges, warp part
+// p takes the k-vectors p*32 + lane, +32P, ...; the parts' forces and
+// torques (= off x F) are summed in part order (deterministic) and added to
+// the (already written) real-space totals.  P > 1 puts short systems' few
+// molecules on enough warps to hide the table gathers.
 __global__ void __launch_bounds__(256) k_ewald_force(EwaldArgs a) {
-  const int m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  __shared__ double slab[8][6];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = a.kparts;
+  const int m = blockIdx.x * ((blockDim.x >> 5) / P) + warp / P, part = warp % P;
   const int r = blockIdx.y;
-  if (m >= a.s.n) return;
-  const int q0 = a.mol_qbegin[m], q1 = a.mol_qbegin[m + 1];
-  if (q0 == q1) return;
+  const bool in = m < a.s.n;
+  const int q0 = in ? a.mol_qbegin[m] : 0, q1 = in ? a.mol_qbegin[m + 1] : 0;
   const int K = a.kmax + 1;
   const double2* base = a.tab + size_t(r) * 3 * K * a.nq;
   const size_t soff = size_t(r) * a.s.total_sites;
@@ -1443,7 +1449,7 @@ __global__ void __launch_bounds__(256) k_ewald_force(EwaldArgs a) {
     const double ox = o4.x, oy = o4.y, oz = o4.z;
     const double qv = a.q_val[q];
     double sfx = 0, sfy = 0, sfz = 0;
-    for (int kk = a.k_begin + lane; kk < a.k_begin + a.nk; kk += 32) {
+    for (int kk = a.k_begin + part * 32 + lane; kk < a.k_begin + a.nk; kk += 32 * P) {
       const DevKVec k = a.kv[kk];
       const double2 e = site_phase(base, K, a.nq, q, k);
       const double2 S = a.S[size_t(r) * a.nk_total + kk];
@@ -1460,20 +1466,17 @@ __global__ void __launch_bounds__(256) k_ewald_force(EwaldArgs a) {
     ty += oz * sfx - ox * sfz;
     tz += ox * sfy - oy * sfx;
   }
-  fx = warp_sum(fx);
-  fy = warp_sum(fy);
-  fz = warp_sum(fz);
-  tx = warp_sum(tx);
-  ty = warp_sum(ty);
-  tz = warp_sum(tz);
-  if (lane == 0) {
+  double v[6] = {warp_sum(fx), warp_sum(fy), warp_sum(fz), warp_sum(tx), warp_sum(ty), warp_sum(tz)};
+  bool own = lane == 0;
+  if (P > 1) own = combine_parts<6>(v, slab, warp, lane, P);
+  if (own && in && q0 != q1) {
     const size_t roff = size_t(r) * a.s.n;
-    a.st.fx[roff + m] += fx;
-    a.st.fy[roff + m] += fy;
-    a.st.fz[roff + m] += fz;
-    a.st.tx[roff + m] += tx;
-    a.st.ty[roff + m] += ty;
-    a.st.tz[roff + m] += tz;
+    a.st.fx[roff + m] += v[0];
+    a.st.fy[roff + m] += v[1];
+    a.st.fz[roff + m] += v[2];
+    a.st.tx[roff + m] += v[3];
+    a.st.ty[roff + m] += v[4];
+    a.st.tz[roff + m] += v[5];
   }
 }
 
