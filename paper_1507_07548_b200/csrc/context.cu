@@ -422,6 +422,25 @@ ForceArgs force_args(b2md_ctx* c) {
   a.two_alpha_over_sqrt_pi = 2.0 * c->t.alpha / std::sqrt(3.14159265358979323846);
   a.rf_r3inv = c->t.rf_r3inv;
   a.rf_shift = c->t.rf_shift;
+  // erfcx Chebyshev interpolation (kernels.cuh, erfcx_cheb): nodes in
+  // u, t = t_lo + (u + 1)(1 - t_lo)/2, x = 2 (1/t - 1)
+  {
+    const int N = kErfcxDeg + 1;
+    const double t_lo = 1.0 / (1.0 + 0.5 * kErfcxMax);
+    double f[kErfcxDeg + 1];
+    for (int k = 0; k < N; ++k) {
+      const double u = std::cos(3.14159265358979323846 * (k + 0.5) / N);
+      const double t = t_lo + 0.5 * (u + 1.0) * (1.0 - t_lo);
+      const double x = 2.0 * (1.0 / t - 1.0);
+      f[k] = std::erfc(x) * std::exp(x * x);
+    }
+    for (int j = 0; j < N; ++j) {
+      double sum = 0.0;
+      for (int k = 0; k < N; ++k) sum += f[k] * std::cos(3.14159265358979323846 * j * (k + 0.5) / N);
+      a.erfcx_c[j] = (j == 0 ? 1.0 : 2.0) * sum / N;
+    }
+    a.erfcx_tlo = t_lo;
+  }
   a.vderiv = c->t.vderiv ? 1 : 0;
   const int hh = hi32(0.5 * c->t.box);
   std::memcpy(&a.thr, &hh, 4);

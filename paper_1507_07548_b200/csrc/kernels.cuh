@@ -504,6 +504,8 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
 // a fixed function of the bit matrix: results are reproducible.
 constexpr int kChunkWords = 32;
 constexpr int kForceWarps = 8;  // warps per CTA of the partner walks
+constexpr double kErfcxMax = 6.0;
+constexpr int kErfcxDeg = 18;
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 #pragma unroll
@@ -630,6 +632,21 @@ __device__ __forceinline__ bool combine_parts(double (&v)[NV], double (*slab)[NV
   return owner;
 }
 
+// erfcx(x) for 0 <= x < kErfcxMax: Clenshaw sum of the Chebyshev series in
+// u = 2 (t - t_lo) / (1 - t_lo) - 1, t = 1 / (1 + x/2)
+__device__ __forceinline__ double erfcx_cheb(double x, const double* c, double t_lo) {
+  const double t = 1.0 / (1.0 + 0.5 * x);
+  const double u = 2.0 * (t - t_lo) / (1.0 - t_lo) - 1.0;
+  double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+  for (int j = kErfcxDeg; j >= 1; --j) {
+    const double b0 = fma(2.0 * u, b1, c[j] - b2);
+    b2 = b1;
+    b1 = b0;
+  }
+  return fma(u, b1, c[0] - b2);
+}
+
 // 1/x to ~1 ulp without the IEEE-division slow path: hardware reciprocal
 // seed + two Newton steps (force arithmetic; tolerance 1e-10).
 __device__ __forceinline__ double rcp_nr(double x) {
@@ -704,6 +721,11 @@ struct ForceArgs {
   double rc2;
   double alpha, two_alpha_over_sqrt_pi;
   double rf_r3inv, rf_shift;
+  // erfcx(x) = erfc(x) exp(x^2) on [0, kErfcxMax] as a Chebyshev series in
+  // t = 1 / (1 + x/2) (host-interpolated, ~1e-14 relative): the Ewald
+  // real-space term then shares exp(-x^2) with its force factor
+  double erfcx_c[19];
+  double erfcx_tlo;
   int vderiv;
   float thr;  // hi32(L/2) as float (min_image_wrapped)
   // fused end-of-step half kick (kick_one) in the row epilogue: dt > 0 when
@@ -918,8 +940,13 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
           const double rr = sqrt(r2);
           double uu, du_r, d2u_r2 = 0.0, rfu = 0.0;
           if constexpr (METHOD == 2) {
-            const double e = erfc(a.alpha * rr) * t.qq / rr;
-            const double g = t.qq * a.two_alpha_over_sqrt_pi * exp(-a.alpha * a.alpha * r2);
+            // potentials.cpp:252-258: erfc(alpha r) qq / r and the force factor
+            // qq 2 alpha/sqrt(pi) exp(-alpha^2 r^2), one exponential for both
+            const double x = a.alpha * rr;
+            const double ex = exp(-x * x);
+            const double ec = x < kErfcxMax ? ex * erfcx_cheb(x, a.erfcx_c, a.erfcx_tlo) : erfc(x);
+            const double e = ec * t.qq / rr;
+            const double g = t.qq * a.two_alpha_over_sqrt_pi * ex;
             uu = e;
             du_r = -(e + g);
           } else {
