@@ -84,7 +84,7 @@ __device__ __forceinline__ double norm2_exact(double x, double y, double z) {
 // the reference's d - L*1.0.  Anything within the margins (probability
 // ~1e-6 per axis) or beyond 1.5L, and NaN/Inf, takes the exact IEEE
 // divide + round-half-even path.  The compares run on the integer pipe.
-__device__ __noinline__ double min_image_exact_slow(double d, double L) {
+static __device__ __noinline__ double min_image_exact_slow(double d, double L) {
   const double n = rint(__ddiv_rn(d, L));
   return sub(d, mul(L, n));
 }

@@ -73,7 +73,7 @@ __device__ __forceinline__ int site_slot(const SysDev& s, int r, int m, int site
 // ------------------------------------------------------------ site offsets
 // build_scene (potentials.cpp:106-116): off = rotate(orient, body_pos); a single
 // centred site has offset exactly 0.
-__global__ void k_offsets(SysDev s, StateDev st) {
+static __global__ void k_offsets(SysDev s, StateDev st) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= s.n * s.R) return;
   const int r = gid / s.n, i = gid - r * s.n;
@@ -1372,7 +1372,7 @@ struct EwaldArgs {
   double two_pi_over_L;
 };
 
-__global__ void k_ewald_tables(EwaldArgs a) {
+static __global__ void k_ewald_tables(EwaldArgs a) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= a.nq * a.s.R) return;
   const int r = gid / a.nq, q = gid - r * a.nq;
@@ -1416,7 +1416,7 @@ __device__ __forceinline__ double2 site_phase(const double2* base, int K, int nq
 
 // ewald.cpp:163-169: one CTA per (k, replica), fixed-order block reduction;
 // U_recip = sum_k 0.5 coeff |S|^2 finalized by the last CTA (sums[7]).
-__global__ void __launch_bounds__(256) k_ewald_sk(EwaldArgs a) {
+static __global__ void __launch_bounds__(256) k_ewald_sk(EwaldArgs a) {
   const int kk = a.k_begin + blockIdx.x;
   const int r = blockIdx.y;
   const DevKVec k = a.kv[kk];
@@ -1458,7 +1458,7 @@ __global__ void __launch_bounds__(256) k_ewald_sk(EwaldArgs a) {
 // torques (= off x F) are summed in part order (deterministic) and added to
 // the (already written) real-space totals.  P > 1 puts short systems' few
 // molecules on enough warps to hide the table gathers.
-__global__ void __launch_bounds__(256) k_ewald_force(EwaldArgs a) {
+static __global__ void __launch_bounds__(256) k_ewald_force(EwaldArgs a) {
   __shared__ double slab[8][6];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = a.kparts;
@@ -1523,7 +1523,7 @@ __device__ __forceinline__ double dot4x(const double a[4], const double b[4]) {
 }
 
 // free_rotate (engine.cpp:28-59), reference operation order, no FMA.
-__device__ void free_rotate_dev(double q[4], double L[3], const double I[3], double dt) {
+static __device__ void free_rotate_dev(double q[4], double L[3], const double I[3], double dt) {
   double p[4] = {0.0, 0.0, 0.0, 0.0};
   for (int k = 1; k <= 3; ++k) {
     const double pk = L[k - 1];
@@ -1584,7 +1584,7 @@ __device__ __forceinline__ uint4 fix_position(double x, double y, double z, doub
 
 // Positions as the search (fixed point) and the force kernels (packed) read
 // them; the integrator writes both itself.
-__global__ void k_stage_positions(const double* px, const double* py, const double* pz, int count,
+static __global__ void k_stage_positions(const double* px, const double* py, const double* pz, int count,
                                   int n, const int* slot_of, double L, double scale,
                                   uint4* fixpos, double4* pos4) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1698,7 +1698,7 @@ __device__ __forceinline__ void fused_kick(const ForceArgs& f, size_t gid) {
 }
 
 // first half of a step: half kick, drift, rotate, wrap, offsets
-__global__ void __launch_bounds__(256) k_kick_drift(StepArgs a) {
+static __global__ void __launch_bounds__(256) k_kick_drift(StepArgs a) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= a.s.n * a.s.R) return;
   if (*a.error_mol != 0x7fffffff) return;  // state frozen after a failed step
@@ -1706,7 +1706,7 @@ __global__ void __launch_bounds__(256) k_kick_drift(StepArgs a) {
 }
 
 // second half of a step: half kick + check_finite
-__global__ void __launch_bounds__(256) k_kick(StepArgs a) {
+static __global__ void __launch_bounds__(256) k_kick(StepArgs a) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= a.s.n * a.s.R) return;
   if (*a.error_mol != 0x7fffffff) return;
@@ -1717,7 +1717,7 @@ __global__ void __launch_bounds__(256) k_kick(StepArgs a) {
 // A molecule that fails check_finite stops the run; the others may already
 // have started step k+1, so the failing molecule index is recorded and the
 // host reports the failure (the reference throws at the end of step k).
-__global__ void __launch_bounds__(256) k_kick_kick_drift(StepArgs a) {
+static __global__ void __launch_bounds__(256) k_kick_kick_drift(StepArgs a) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= a.s.n * a.s.R) return;
   if (*a.error_mol != 0x7fffffff) return;
@@ -1729,7 +1729,7 @@ __global__ void __launch_bounds__(256) k_kick_kick_drift(StepArgs a) {
 }
 
 // wrap (model.cpp:279-286) for set_state
-__global__ void k_wrap(double* p, int count, double L) {
+static __global__ void k_wrap(double* p, int count, double L) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid < count) p[gid] = wrap1(p[gid], L);
 }
@@ -1740,7 +1740,7 @@ __global__ void k_wrap(double* p, int count, double L) {
 // Pair export (b2md_pair_list): slot row k holds external molecule
 // i = perm[k]; its partners l with perm[l] > i are the reference pairs (i, j).
 // Rows are counted / filled by external index; the host orders each row's j.
-__global__ void k_pair_count(const uint32_t* mask, const int* perm, int n, int words,
+static __global__ void k_pair_count(const uint32_t* mask, const int* perm, int n, int words,
                              int64_t* row_count) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
@@ -1758,7 +1758,7 @@ __global__ void k_pair_count(const uint32_t* mask, const int* perm, int n, int w
   row_count[i] = c;
 }
 
-__global__ void k_pair_fill(const uint32_t* mask, const int* perm, int n, int words,
+static __global__ void k_pair_fill(const uint32_t* mask, const int* perm, int n, int words,
                             const int64_t* row_start, int32_t* pairs) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
@@ -1786,7 +1786,7 @@ __global__ void k_pair_fill(const uint32_t* mask, const int* perm, int n, int wo
 // fixed tree (deterministic; the reference's serial order differs only in
 // rounding).  out[r] = {ke_t, ke_r}.
 constexpr int kKeThreads = 512;
-__global__ void __launch_bounds__(kKeThreads) k_kinetic(SysDev s, StateDev st, double2* out) {
+static __global__ void __launch_bounds__(kKeThreads) k_kinetic(SysDev s, StateDev st, double2* out) {
   __shared__ double red_t[kKeThreads], red_r[kKeThreads];
   const int r = blockIdx.x, tid = threadIdx.x;
   double kt = 0.0, kr = 0.0;
@@ -1822,7 +1822,7 @@ struct ThermoArgs {
   double temperature;
   int dof_t, dof_r;
 };
-__global__ void k_thermostat(ThermoArgs a) {
+static __global__ void k_thermostat(ThermoArgs a) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= a.s.n * a.s.R) return;
   const int r = gid / a.s.n;
@@ -1850,7 +1850,7 @@ __global__ void k_thermostat(ThermoArgs a) {
 // ------------------------------------------------------- checkpoint state
 // Engine::checkpoint_bytes' per-molecule record (engine.cpp:434-440):
 // pos.xyz, orient.wxyz, vel.xyz, ang_vel.xyz as 13 f64, molecule-major.
-__global__ void k_pack_state(StateDev st, int n, int r, double* out) {
+static __global__ void k_pack_state(StateDev st, int n, int r, double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const size_t g = size_t(r) * n + i;
@@ -1871,7 +1871,7 @@ __global__ void k_pack_state(StateDev st, int n, int r, double* out) {
 }
 
 // Engine::restore_dynamic's state loop (engine.cpp:483-491)
-__global__ void k_unpack_state(StateDev st, int n, int r, const double* in) {
+static __global__ void k_unpack_state(StateDev st, int n, int r, const double* in) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const size_t g = size_t(r) * n + i;
@@ -1900,7 +1900,7 @@ __global__ void k_unpack_state(StateDev st, int n, int r, const double* in) {
 // words.  Key = (replica, column, x on 2^20 bins); values are global
 // molecule indices; the stable radix sort makes the order a deterministic
 // function of the positions.
-__global__ void k_sort_keys(const double* px, const double* py, const double* pz, int count,
+static __global__ void k_sort_keys(const double* px, const double* py, const double* pz, int count,
                             int n, double L, int G, unsigned long long* keys, int* vals) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= count) return;
@@ -1917,7 +1917,7 @@ __global__ void k_sort_keys(const double* px, const double* py, const double* pz
 }
 
 // sorted position p (= r n + k) -> perm, slot_of, species and site count
-__global__ void k_apply_order(const int* sorted_vals, int count, int n, const int* species_of,
+static __global__ void k_apply_order(const int* sorted_vals, int count, int n, const int* species_of,
                               const DevTables* tab, int* perm, int* slot_of, int* sp_slot,
                               int* nsites_slot) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1932,14 +1932,14 @@ __global__ void k_apply_order(const int* sorted_vals, int count, int n, const in
 }
 
 // global exclusive scan -> per-replica slot-ordered first site
-__global__ void k_site_starts(const int* scan, int count, int n, int total_sites, int* sb_slot) {
+static __global__ void k_site_starts(const int* scan, int count, int n, int total_sites, int* sb_slot) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= count) return;
   sb_slot[p] = scan[p] - (p / n) * total_sites;
 }
 
 // --------------------------------------------------------------- DFMA peak
-__global__ void k_dfma_peak(double* out, int iters, double a, double b) {
+static __global__ void k_dfma_peak(double* out, int iters, double a, double b) {
   double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5,
          x6 = x0 + 6, x7 = x0 + 7;
   for (int i = 0; i < iters; ++i) {

@@ -38,7 +38,7 @@ struct RdfArgs {
 };
 
 // structure.cpp:45-58: site_pos = pos[m] + rotate(orient[m], body_pos)
-__global__ void k_rdf_stage(RdfArgs a) {
+static __global__ void k_rdf_stage(RdfArgs a) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= a.S * a.s.R) return;
   const int r = e / a.S, q = e - r * a.S;
@@ -76,7 +76,7 @@ __device__ __forceinline__ int rdf_bin(double d2, double bin_width, double inv_b
 
 // The reference's decision for one site pair (structure.cpp:62-67), exactly;
 // returns the bin or -1 (outside r_max or beyond the last bin).
-__device__ __noinline__ int rdf_exact(double4 pa, double4 pb, const RdfArgs& a) {
+static __device__ __noinline__ int rdf_exact(double4 pa, double4 pb, const RdfArgs& a) {
   const MinImage mi = a.s.mi;
   const double dx = min_image(sub(pa.x, pb.x), mi);
   const double dy = min_image(sub(pa.y, pb.y), mi);
