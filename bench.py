@@ -552,7 +552,7 @@ def main():
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         eng.upload_state_raw(hp, hq, hv, hw, hf, ht)
-        eng.step(1)
+        eng.step_async(1)  # its NumericalError is reported by get_state
         eng.get_state_raw(hp, hq, hv, hw, hf, ht)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -629,7 +629,7 @@ def main():
         "pairs_in_cutoff_per_step": pairs_total,
         "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "path": "b2md_upload_state + b2md_step + b2md_get_state, pinned host buffers"},
+                "path": "b2md_upload_state + b2md_step_async + b2md_get_state (one host sync), pinned host buffers"},
         "roofline": {
             "bound": "fp64",
             "kernel": f"k_force_* partner walk ({force_note})",

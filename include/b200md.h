@@ -181,7 +181,9 @@ int b2md_set_state(b2md_ctx* ctx, const double* pos, const double* orient, const
 int b2md_step(b2md_ctx* ctx, int64_t nsteps);
 
 /* Enqueue `nsteps` steps without waiting (device-resident step loop);
- * b2md_sync waits for them and reports a NumericalError like b2md_step. */
+ * b2md_sync waits for them and reports a NumericalError like b2md_step, and
+ * so does the next b2md_get_state (its download carries the error flag, so
+ * upload -> step_async -> get_state costs one host round trip). */
 int b2md_step_async(b2md_ctx* ctx, int64_t nsteps);
 int b2md_sync(b2md_ctx* ctx);
 

@@ -173,6 +173,8 @@ struct b2md_ctx {
   // host scratch
   std::vector<double> h_sums;
   double* h_sums_pinned = nullptr;  // energy sums read-back (cudaMallocHost)
+  int* h_flag = nullptr;            // error flag read-back (cudaMallocHost)
+  bool async_pending = false;       // b2md_step_async not yet checked
 
   std::string warning;
 };
@@ -196,6 +198,7 @@ int run_steps(b2md_ctx* c, int64_t nsteps);
 int upload_aos(b2md_ctx* c, int slot, const double* host, int width, double* d0, double* d1,
                double* d2, double* d3);
 int check_error_flag(b2md_ctx* c);
+int error_from_flag(b2md_ctx* c, int flag);
 
 #define PROF(ctx, fam, launch)      \
   do {                              \

@@ -303,6 +303,32 @@ def test_nan_is_fatal():  # test_engine.cpp:232-245
         eng.step()
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_nan_deferred_to_get_state(pinned):
+    """step_async defers the NumericalError to the next get_state (the flag
+    rides with the download, zero-copy or staged), reported once."""
+    comp = systems.lj_fluid(4, 6.0)
+    eng = b2.Engine(comp, systems.lj_opts(2.5), 0.01)
+    st = systems.random_state(comp, 2, 0.9)
+    st.vel[2] = (np.nan, 0, 0)
+    eng.set_state(st)
+    import torch
+    alloc = ((lambda s: torch.empty(s, dtype=torch.float64, pin_memory=True).numpy()) if pinned
+             else (lambda s: np.empty(s)))
+    bufs = [alloc((4, 3)), alloc((4, 4)), alloc((4, 3))]
+    eng.step_async(1)
+    with pytest.raises(b2.NumericalError, match="non-finite state for molecule 2"):
+        eng.get_state_raw(*bufs)
+    assert np.isnan(bufs[2][2, 0])
+    eng.get_state_raw(*bufs)  # already reported
+    ok = systems.random_state(comp, 2, 0.9)
+    eng2 = b2.Engine(comp, systems.lj_opts(2.5), 0.01)
+    eng2.set_state(ok)
+    eng2.step_async(3)
+    eng2.get_state_raw(*bufs)
+    eng2.step(1)
+
+
 def test_set_state_wraps():  # engine.cpp:91-98
     comp = systems.lj_fluid(20, 6.0)
     st = systems.random_state(comp, 11, 0.9)
@@ -517,24 +543,38 @@ def test_fused_kick_bit_identical(cfg):
     assert np.array_equal(out[0], out[1])
 
 
-def test_pinned_and_pageable_transfers_agree():
-    """b2md_upload_state / b2md_get_state: pinned host buffers take the
-    one-launch zero-copy path, pageable ones the staged copies; same bits."""
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg3"])
+def test_pinned_and_pageable_transfers_agree(cfg):
+    """b2md_upload_state / b2md_get_state: 16-byte-aligned pinned host
+    buffers take the one-launch zero-copy path, pageable and unaligned pinned
+    ones the staged copies; same bits."""
     import torch
-    wl = configs.make("cfg1")
+    wl = configs.make(cfg)
     st = wl.states[0]
     n = wl.comp.molecule_count()
+
+    def pinned(a, offset):
+        a = np.ascontiguousarray(a)
+        raw = torch.empty(a.size + 1, dtype=torch.float64, pin_memory=True).numpy()
+        v = raw[offset:offset + a.size].reshape(a.shape)
+        v[...] = a
+        return v
+
     outs = []
-    for pinned in (True, False):
+    for mode in ("pinned", "pinned_unaligned", "pageable"):
         eng = b2.Engine(wl.comp, wl.opts, wl.dt)
         eng.set_state(st)
-        mk = (lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()) if pinned \
-            else (lambda a: np.ascontiguousarray(a).copy())
+        mk = {"pinned": lambda a: pinned(a, 0), "pinned_unaligned": lambda a: pinned(a, 1),
+              "pageable": lambda a: np.ascontiguousarray(a).copy()}[mode]
         bufs = [mk(x) for x in (st.pos, st.orient, st.vel, st.ang_vel, np.zeros((n, 3)), np.zeros((n, 3)))]
+        assert all((b.ctypes.data % 16 != 0) == (mode == "pinned_unaligned") for b in bufs)
         eng.get_state_raw(*bufs)
-        for _ in range(3):
+        for k in range(3):
             eng.upload_state_raw(*bufs)
-            eng.step(1)
+            if k == 1:
+                eng.step_async(1)
+            else:
+                eng.step(1)
             eng.get_state_raw(*bufs)
         outs.append(np.hstack([np.array(b) for b in bufs]))
-    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
