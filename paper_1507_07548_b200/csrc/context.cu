@@ -41,7 +41,7 @@ int nccl_load() {
 
 const char* kFamilyName[F_COUNT] = {"offsets",  "search", "force",   "ewald_tables", "ewald_sk",
                                     "ewald_force", "kick_kick_drift", "kick_drift", "kick", "allreduce",
-                                    "heat_flux", "rdf"};
+                                    "heat_flux", "rdf", "cluster"};
 
 // AoS <-> SoA staging kernels (host layout Vec3 / Quat of include/tmd/geom.hpp)
 static __global__ void k_aos_to_soa(const double* aos, int count, int width, double* d0, double* d1,
@@ -152,7 +152,7 @@ void set_wrapped(b2md_ctx* c, bool w) {
 }
 
 bool prof_on(const b2md_ctx* c, int fam) {
-  return c->profile && (c->profile_level == 1 || (c->profile_level == 2 && fam == F_SEARCH) ||
+  return c->profile && (c->profile_level == 1 || (c->profile_level == 2 && (fam == F_SEARCH || fam == F_CLUSTER)) ||
                         (c->profile_level == 3 && fam == F_FORCE));
 }
 
@@ -266,7 +266,15 @@ int launch_search(b2md_ctx* c) {
       return set_err(B2MD_INVALID_ARGUMENT, "bad super-tile size");
   }
 #undef SEARCH_CASE
+  c->mask_valid = true;
   return B2MD_OK;
+}
+
+// The bit matrix of the current positions for its consumers (pair export,
+// heat flux): the cluster walk does not build it.
+int ensure_mask(b2md_ctx* c) {
+  if (c->mask_valid) return B2MD_OK;
+  return launch_search(c);
 }
 
 double* sums_ptr(b2md_ctx* c) { return c->d_fbuf + size_t(6) * n_total(c); }
@@ -346,7 +354,58 @@ bool fast_min_image(const b2md_ctx* c) {
   return !(c->t.single_site_path && !(c->t.rc2 < h * h));
 }
 
+// The cluster walk (cluster.cuh) replaces search + bit-matrix walk for the
+// single-site path on one shard (the walk is not sharded: with b2md_set_shard
+// the bit-matrix path computes this rank's partial terms).  Any positions:
+// clusters with a member outside [0, L) are never culled, and the exact
+// minimum image replaces the wrapped one when positions are not wrapped
+// (same bits), so the hit sequence -- and the summation order -- is the same
+// either way: restarts from unwrapped checkpoints stay bit-exact.
+bool cluster_path(const b2md_ctx* c) {
+  return c->use_cluster && c->nc > 0 && c->t.single_site_path && c->world <= 1;
+}
+
+int launch_cluster_force(b2md_ctx* c, bool kick) {
+  ClusterArgs ca;
+  ca.n = c->t.n;
+  ca.nc = c->nc;
+  ca.nsup = c->nsup;
+  ca.fixpos = c->d_fixpos;
+  ca.arcs = c->d_carc;
+  ca.half = c->d_chalf;
+  ca.sup_arcs = c->d_sarc;
+  ca.sup_half = c->d_shalf;
+  ca.list = c->d_clist;
+  ca.count = c->d_ccount;
+  const double ru = std::sqrt(c->t.rc2) * 4294967296.0 / c->t.box;
+  ca.lim = float(ru * ru * (1.0 + 1e-5));
+  ca.lim_pair = float((ru + 4.0) * (ru + 4.0) * (1.0 + 1e-5));
+  const int R = c->R, tot = R * c->nc;
+  PROF(c, F_CLUSTER, (k_cluster_arcs<<<(R * c->nsup * 32 + 255) / 256, 256, 0, c->stream>>>(ca, R)));
+  PROF(c, F_CLUSTER, (k_cluster_list<<<(tot * 32 + 255) / 256, 256, 0, c->stream>>>(ca, R)));
+  ForceArgs a = force_args(c);
+  if (kick) a.kick_dt = c->dt;
+  dim3 grid(c->force_grid, R);
+  const int bs = c->force_warps * 32;
+  const bool w = fast_min_image(c), m = c->t.ns > 1, v = a.vderiv != 0;
+#define CLUSTER_LAUNCH(M, W, V) \
+  if (m == M && w == W && v == V) \
+    PROF(c, F_FORCE, (k_force_cluster<M, W, V><<<grid, bs, 0, c->stream>>>(a, ca)));
+  CLUSTER_LAUNCH(false, true, false)
+  CLUSTER_LAUNCH(false, true, true)
+  CLUSTER_LAUNCH(false, false, false)
+  CLUSTER_LAUNCH(false, false, true)
+  CLUSTER_LAUNCH(true, true, false)
+  CLUSTER_LAUNCH(true, true, true)
+  CLUSTER_LAUNCH(true, false, false)
+  CLUSTER_LAUNCH(true, false, true)
+#undef CLUSTER_LAUNCH
+  c->mask_valid = false;
+  return B2MD_OK;
+}
+
 int launch_force(b2md_ctx* c, bool kick) {
+  if (cluster_path(c)) return launch_cluster_force(c, kick);
   ForceArgs a = force_args(c);
   if (kick) a.kick_dt = c->dt;
   a.split = c->force_split;
@@ -454,9 +513,13 @@ int launch_allreduce(b2md_ctx* c) {
 int resort(b2md_ctx* c) {
   const int nt = n_total(c), n = c->t.n;
   const int g = (nt + 255) / 256;
-  // columns of cross-section c^2 = 32 / (rho L) (about one block each)
+  // columns of cross-section c^2 = 32 / (rho L) (about one 32-slot block
+  // each: thin search tiles); for the cluster walk c = (kCS / rho)^(1/3), so
+  // kCS consecutive slots make a compact cluster
   const double L = c->t.box, rho = double(n) / (L * L * L);
-  const int G = std::max(1, std::min(1024, int(L / std::sqrt(32.0 / (rho * L)))));
+  const double side = c->use_cluster && c->nc > 0 ? std::cbrt(double(kCS) / rho)
+                                                  : std::sqrt(32.0 / (rho * L));
+  const int G = std::max(1, std::min(1024, int(L / side)));
   k_sort_keys<<<g, 256, 0, c->stream>>>(c->st.px, c->st.py, c->st.pz, nt, n, L, G,
                                         c->d_keys[0], c->d_vals[0]);
   CU(cudaGetLastError());
@@ -474,6 +537,7 @@ int resort(b2md_ctx* c) {
   k_site_starts<<<g, 256, 0, c->stream>>>(c->d_scan, nt, n, c->t.total_sites, c->d_sb_slot);
   CU(cudaGetLastError());
   c->steps_since_sort = 0;
+  c->mask_valid = false;  // slot-indexed
   return B2MD_OK;
 }
 
@@ -503,7 +567,7 @@ int enqueue_forces(b2md_ctx* c, bool offsets, bool kick) {
         4294967296.0 / c->t.box, c->d_fixpos, c->st.pos4);
     CU(cudaGetLastError());
   }
-  TRY(launch_search(c));
+  if (!cluster_path(c)) TRY(launch_search(c));
   TRY(launch_force(c, kick));
   TRY(launch_ewald(c));
   TRY(launch_allreduce(c));
@@ -876,6 +940,7 @@ int setup_shard(b2md_ctx* c) {
   c->n_super_tiles = int(list.size());
   // a fresh bit matrix: only this rank's tiles are ever written afterwards
   CU(cudaMemset(c->d_mask, 0, sizeof(uint32_t) * size_t(c->R) * c->g.n_pad * c->g.words));
+  c->mask_valid = false;
   drop_graphs(c);
   return B2MD_OK;
 }
@@ -976,6 +1041,16 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     // species (fixed-point path) and a COM radius well below L/2
     const double rmax = std::sqrt(t.single_site_path ? t.rc2 : t.rmax2[0]);
     c->sort_interval = (t.ns == 1 && rmax < 0.3 * t.box) ? 100 : 0;
+    // cluster walk (single-site path) where its cull pays: a cutoff well
+    // below L/2 (cfg0's rc = 0.45 L culls nothing; measured 24.6k vs 32k
+    // steps/s there); compact clusters need a fresher order than search
+    // tiles.  B2MD_CLUSTER=0 disables it, =2 forces it (tests, measurement).
+    int cl_mode = 1;
+    if (const char* e = std::getenv("B2MD_CLUSTER")) cl_mode = std::atoi(e);
+    if (t.single_site_path && (cl_mode == 2 || (cl_mode == 1 && rmax < 0.3 * t.box))) {
+      c->nc = (t.n + kCS - 1) / kCS;
+      if (rmax < 0.3 * t.box) c->sort_interval = 20;
+    }
     // tuning knobs (measurement only): warps per CTA, CTAs per replica
     if (const char* e = std::getenv("B2MD_FORCE_WARPS"))
       c->force_warps = std::max(1, std::min(kForceWarps, std::atoi(e)));
@@ -987,6 +1062,15 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     if (const char* e = std::getenv("B2MD_FUSED_KICK")) c->use_fused_kick = std::atoi(e) != 0;
   }
   TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars * c->force_grid));
+  if (c->nc > 0) {
+    c->nsup = (c->nc + kSC - 1) / kSC;
+    TRY(dalloc(&c->d_carc, size_t(R) * c->nc));
+    TRY(dalloc(&c->d_chalf, size_t(R) * c->nc));
+    TRY(dalloc(&c->d_sarc, size_t(R) * c->nsup));
+    TRY(dalloc(&c->d_shalf, size_t(R) * c->nsup));
+    TRY(dalloc(&c->d_clist, size_t(R) * c->nc * c->nc));
+    TRY(dalloc(&c->d_ccount, size_t(R) * c->nc));
+  }
   TRY(dalloc(&c->d_ticket, size_t(2) * R));
   TRY(dalloc(&c->d_flux, size_t(kNumSums) * R));
   TRY(dalloc(&c->d_ke, R));
@@ -1123,7 +1207,8 @@ void free_ctx(b2md_ctx* c) {
                   c->d_q_site, c->d_q_val,     c->d_mol_qbegin, c->d_kv,    c->d_etab,  c->d_S,
                   c->d_uk,    c->d_flux,  c->d_perm, c->d_slot_of, c->d_sp_slot, c->d_sb_slot,
                   c->d_nsites_slot, c->d_scan, c->d_keys[0], c->d_keys[1], c->d_vals[0],
-                  c->d_vals[1], c->d_cub, c->d_ke, c->d_thermo_err};
+                  c->d_vals[1], c->d_cub, c->d_ke, c->d_thermo_err, c->d_carc, c->d_clist,
+                  c->d_ccount, c->d_chalf, c->d_sarc, c->d_shalf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1302,6 +1387,7 @@ int b2md_upload_state(b2md_ctx* c, const double* pos, const double* orient, cons
   if (force) spec[n++] = {force, 3, {c->st.fx, c->st.fy, c->st.fz, nullptr}};
   if (torque) spec[n++] = {torque, 3, {c->st.tx, c->st.ty, c->st.tz, nullptr}};
   TRY(upload_arrays(c, spec, n));
+  if (pos) c->mask_valid = false;
   // steps wrap before every evaluation, so step-time forces may use the fast path
   set_wrapped(c, true);
   c->state_valid = true;
@@ -1360,6 +1446,7 @@ int b2md_pair_list(b2md_ctx* c, int replica, int32_t* pairs, int64_t capacity, i
   if (replica < 0 || replica >= c->R) return set_err(B2MD_INVALID_ARGUMENT, "pair_list: bad replica");
   CU(cudaSetDevice(c->device));
   const int n = c->t.n;
+  TRY(ensure_mask(c));
   const uint32_t* mask = c->d_mask + size_t(replica) * c->g.n_pad * c->g.words;
   const int* perm = c->d_perm + size_t(replica) * n;
   int64_t* d_cnt = nullptr;

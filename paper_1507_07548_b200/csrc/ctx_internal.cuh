@@ -20,6 +20,7 @@
 #include "../../include/b200md.h"
 #include "kernels.cuh"
 #include "rdf.cuh"
+#include "cluster.cuh"
 #include "model.hpp"
 #include "search_geometry.hpp"
 
@@ -79,7 +80,7 @@ int dalloc(T** p, size_t count) {
 }
 
 enum Family { F_OFFSETS, F_SEARCH, F_FORCE, F_EWALD_TAB, F_EWALD_SK, F_EWALD_F, F_KICK_KICK_DRIFT,
-              F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_HEAT_FLUX, F_RDF, F_COUNT };
+              F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_HEAT_FLUX, F_RDF, F_CLUSTER, F_COUNT };
 extern const char* kFamilyName[F_COUNT];
 
 }  // namespace b2md_host
@@ -107,7 +108,17 @@ struct b2md_ctx {
   double4* d_pos4 = nullptr;  // R * n packed positions
   double* d_stage = nullptr;  // AoS staging: 6 slots of 4*R*n (one per array, no reuse waits)
   uint32_t* d_mask = nullptr;
-  uint4* d_fixpos = nullptr;  // fixed-point positions (search prefilter)
+  uint4* d_fixpos = nullptr;  // fixed-point positions (search prefilter, cluster arcs)
+  bool mask_valid = false;    // d_mask holds the current positions' partners
+  // cluster walk of the single-site path (cluster.cuh)
+  bool use_cluster = true;
+  int nc = 0, nsup = 0;       // clusters, super-clusters per replica
+  uint4* d_carc = nullptr;    // R * nc arc centres
+  float4* d_chalf = nullptr;  // R * nc arc half extents
+  uint4* d_sarc = nullptr;    // R * nsup
+  float4* d_shalf = nullptr;  // R * nsup
+  int* d_clist = nullptr;     // R * nc * nc
+  int* d_ccount = nullptr;    // R * nc
   double* d_cta_part = nullptr;  // force-kernel per-CTA scalar partials
   unsigned* d_ticket = nullptr;   // 2 * R: force, ewald
   int force_grid = 1;
@@ -189,6 +200,8 @@ int prof_begin(b2md_ctx* c, int fam);
 int prof_end(b2md_ctx* c);
 int launch_offsets(b2md_ctx* c);
 int launch_search(b2md_ctx* c);
+int ensure_mask(b2md_ctx* c);
+bool cluster_path(const b2md_ctx* c);
 ForceArgs force_args(b2md_ctx* c);
 bool fast_min_image(const b2md_ctx* c);
 int resort(b2md_ctx* c);

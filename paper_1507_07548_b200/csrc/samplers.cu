@@ -84,6 +84,7 @@ int b2md_heat_flux(b2md_ctx* c, const double* enthalpy, int n_enthalpy, double* 
   if (!c->state_valid)
     return set_err(B2MD_CONFIG_ERROR, "heat_flux: set_state must precede heat_flux");
   CU(cudaSetDevice(c->device));
+  TRY(ensure_mask(c));
   TRY(launch_heat_flux(c, enthalpy));
   return download_flux(c, jq);
 }

@@ -164,6 +164,66 @@ def test_sizes_and_partial_tiles(n):
     check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
 
 
+@pytest.mark.parametrize("mode", ["0", "2"])
+@pytest.mark.parametrize("n", [1, 2, 7, 9, 100, 1537, 4100])
+def test_single_site_walks(monkeypatch, mode, n):
+    """Both single-site walks -- the cluster walk (B2MD_CLUSTER=2 forces it)
+    and the search + bit-matrix walk (=0) -- reproduce the oracle's pairs,
+    forces and energies at any size (one partial cluster, rc ~ L/2, ...)."""
+    monkeypatch.setenv("B2MD_CLUSTER", mode)
+    box = (n / 0.7) ** (1.0 / 3.0) if n > 8 else 8.0
+    rc = min(2.5, 0.5 * box)
+    if n > 8:
+        wl = configs.lj_fluid_config(n, n / box ** 3, rc, seed=n + 1)
+        comp, opts, st = wl.comp, wl.opts, wl.states[0]
+    else:
+        comp, opts = systems.lj_fluid(n, box), systems.lj_opts(rc)
+        st = systems.random_state(comp, n, 0.9)
+    o = pyoracle.OracleFF(comp, opts)
+    ref = o.evaluate(st.pos, st.orient)
+    ff, out = gpu_eval(comp, opts, st.pos, st.orient)
+    assert np.array_equal(ff.pair_list(), o.pair_list(st.pos))
+    check_vec(out.force, ref["force"])
+    check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+    assert ff.last_stats.com_pairs == ref["com_pairs"]
+
+
+def test_cluster_walk_unwrapped_positions(monkeypatch):
+    """The cluster walk on positions outside [0, L) (ForceField::evaluate
+    takes them as given): such clusters are never culled, the exact minimum
+    image decides."""
+    monkeypatch.setenv("B2MD_CLUSTER", "2")
+    wl = configs.lj_fluid_config(600, 0.7, 2.5, seed=3)
+    L = wl.comp.box_length
+    st = wl.states[0]
+    rng = np.random.default_rng(5)
+    pos = st.pos + L * rng.integers(-3, 4, size=st.pos.shape)
+    o = pyoracle.OracleFF(wl.comp, wl.opts)
+    ref = o.evaluate(pos, st.orient)
+    ff, out = gpu_eval(wl.comp, wl.opts, pos, st.orient)
+    assert np.array_equal(ff.pair_list(), o.pair_list(pos))
+    check_vec(out.force, ref["force"])
+    check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+
+
+def test_cfg3_trajectory_with_resorts():
+    """cfg3 (cluster walk, re-sorted every 20 steps) for 25 steps against the
+    oracle, and bit-identical when repeated (fixed summation order)."""
+    wl = configs.make("cfg3")
+    st = wl.states[0]
+    outs = []
+    for _ in range(2):
+        eng = b2.Engine(wl.comp, wl.opts, wl.dt)
+        eng.set_state(st)
+        eng.step(25)
+        outs.append(eng.state())
+    ref = pyoracle.OracleFF(wl.comp, wl.opts).run(wl.dt, 25, st.pos, st.orient, st.vel, st.ang_vel)
+    compare_states(outs[0], ref, wl.comp.box_length)
+    check_energy(outs[0].energy, ref["energy"], outs[0].virial, ref["virial"])
+    assert np.array_equal(outs[0].pos, outs[1].pos) and np.array_equal(outs[0].vel, outs[1].vel)
+    assert np.array_equal(eng.pair_list(), pyoracle.OracleFF(wl.comp, wl.opts).pair_list(ref["pos"]))
+
+
 def test_min_image_ties_and_far_images():
     """Separations exactly L/2 (round-half-even ties), positions several
     boxes away (nearbyint = +-2, +-3) and negative coordinates."""
