@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kForceWarps * 32, B2MD_CLUSTER_MINB) k_force_c
   const unsigned lt = (1u << lane) - 1u;
   int* __restrict__ wj = qj[warp];
   int* __restrict__ wsv = sv_list[warp];
-  double u = 0, vir = 0, s1 = 0, s2 = 0;
+  double A12 = 0, A6 = 0;  // sum over this warp's pairs (i < j side)
   int cnt = 0;
   const int wpb = blockDim.x >> 5;
   for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
@@ -226,15 +226,13 @@ __global__ void __launch_bounds__(kForceWarps * 32, B2MD_CLUSTER_MINB) k_force_c
       fx += gx;
       fy += gy;
       fz += gz;
-      if (i < j) {
-        u += a12 - a6;
-        vir += dx * gx + dy * gy + dz * gz;
-        if (VDERIV) {
-          s1 += du_r;
-          s2 += 156.0 * a12 - 42.0 * a6;
-        }
-        ++cnt;
-      }
+      // the pair's scalars (i < j side) are linear in a12, a6 -- u = a12 - a6,
+      // s1 = du_r, s2 = 156 a12 - 42 a6, and dot(R, f) = fs r2 = -du_r --
+      // so their sums are taken from sum a12, sum a6 in the epilogue
+      const double w = i < j ? 1.0 : 0.0;
+      A12 = fma(w, a12, A12);
+      A6 = fma(w, a6, A6);
+      cnt += i < j;
     };
     // queued slot q on this lane (on: the lane holds an entry)
     auto eval = [&](int q, bool on) {
@@ -313,8 +311,11 @@ __global__ void __launch_bounds__(kForceWarps * 32, B2MD_CLUSTER_MINB) k_force_c
       if (a.kick_dt > 0.0) fused_kick(a, e);
     }
   }
-  double v[kNumRowScalars] = {warp_sum(u), 0.0, 0.0, VDERIV ? warp_sum(s1) : 0.0,
-                              VDERIV ? warp_sum(s2) : 0.0, warp_sum(vir), warp_sum(double(cnt))};
+  A12 = warp_sum(A12);
+  A6 = warp_sum(A6);
+  const double s1 = -12.0 * A12 + 6.0 * A6;  // sum du_r
+  double v[kNumRowScalars] = {A12 - A6, 0.0, 0.0, VDERIV ? s1 : 0.0,
+                              VDERIV ? 156.0 * A12 - 42.0 * A6 : 0.0, -s1, warp_sum(double(cnt))};
   finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
 }
 

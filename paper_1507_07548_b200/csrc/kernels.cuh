@@ -1571,6 +1571,9 @@ struct StepArgs {
 };
 
 __device__ __forceinline__ double wrap1(double x, double L) {
+  // inside (0, L (1 - 2^-40)): x / L rounds below 1, floor is 0 and the
+  // reference's x - L * 0 is x itself -- no division
+  if (x > 0.0 && x < L * (1.0 - 9.094947017729282e-13)) return x;  // (-0.0 -> +0.0 below)
   return sub(x, mul(L, floor(__ddiv_rn(x, L))));  // model.cpp:282
 }
 
