@@ -75,53 +75,74 @@ __device__ __forceinline__ float arc_half(int mn, int mx) {
   return float((static_cast<long long>(mx) - mn + 1) >> 1) + 1.0f;
 }
 
-// One warp per (replica, super-cluster); lane L owns cluster 32 s + L (its
-// kCS slots): the cluster's arc from offsets to its first member, the
-// super-cluster's from offsets to the warp's first slot.  A member outside
-// [0, L) (fixed point saturated) makes its arcs whole-circle: never culled.
-static __global__ void __launch_bounds__(256) k_cluster_arcs(ClusterArgs a, int R) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= R * a.nsup) return;  // warp-uniform
-  const int r = w / a.nsup, sc = w - r * a.nsup;
+// One CTA per (replica, super-cluster), one thread per slot: a cluster is 8
+// consecutive lanes (offsets to its first member, min/max by a 3-level xor
+// shuffle), the super-cluster the whole CTA (offsets to its first slot,
+// warp REDUX then shared memory).  A member outside [0, L) (fixed point
+// saturated) makes its arcs whole-circle: never culled.
+static __global__ void __launch_bounds__(kSC * kCS) k_cluster_arcs(ClusterArgs a, int R) {
+  static_assert(kSC * kCS == 256 && kCS == 8, "one CTA of 256 slots per super-cluster");
+  __shared__ int red[8][6];
+  __shared__ int sin_[8];
+  const int r = blockIdx.x / a.nsup, sc = blockIdx.x - r * a.nsup;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint4* f = a.fixpos + size_t(r) * a.n;
-  const int cl = sc * kSC + lane;
-  const int k0 = cl * kCS, k1 = min(a.n, k0 + kCS);
-  const uint4 wa = f[sc * kSC * kCS];  // warp anchor (exists: sc < nsup)
-  uint4 u0 = wa;
-  bool in = true;
-  int mnx = 0, mxx = 0, mny = 0, mxy = 0, mnz = 0, mxz = 0;          // cluster
-  int smnx = INT_MAX, smxx = INT_MIN, smny = INT_MAX, smxy = INT_MIN, smnz = INT_MAX, smxz = INT_MIN;
-  if (k0 < k1) {
-    u0 = f[k0];
-    for (int k = k0; k < k1; ++k) {
-      const uint4 u = f[k];
-      in = in && u.w != 0u;
-      const int ox = int(u.x - u0.x), oy = int(u.y - u0.y), oz = int(u.z - u0.z);
-      mnx = min(mnx, ox), mxx = max(mxx, ox);
-      mny = min(mny, oy), mxy = max(mxy, oy);
-      mnz = min(mnz, oz), mxz = max(mxz, oz);
-      const int px = int(u.x - wa.x), py = int(u.y - wa.y), pz = int(u.z - wa.z);
-      smnx = min(smnx, px), smxx = max(smxx, px);
-      smny = min(smny, py), smxy = max(smxy, py);
-      smnz = min(smnz, pz), smxz = max(smxz, pz);
-    }
+  const int k = sc * kSC * kCS + threadIdx.x;  // slot
+  const bool valid = k < a.n;
+  const uint4 wa = f[sc * kSC * kCS];           // super-cluster anchor
+  const uint4 u = f[valid ? k : sc * kSC * kCS];
+  const unsigned full = 0xffffffffu;
+  const int src = lane & ~(kCS - 1);
+  const uint4 u0 = make_uint4(__shfl_sync(full, u.x, src), __shfl_sync(full, u.y, src),
+                              __shfl_sync(full, u.z, src), 0u);
+  // invalid slots repeat the cluster anchor (offset 0, in-box as the anchor)
+  int mnx = valid ? int(u.x - u0.x) : 0, mny = valid ? int(u.y - u0.y) : 0;
+  int mnz = valid ? int(u.z - u0.z) : 0;
+  int mxx = mnx, mxy = mny, mxz = mnz;
+  int in = valid ? int(u.w != 0u) : 1;
+#pragma unroll
+  for (int o = 1; o < kCS; o <<= 1) {
+    mnx = min(mnx, __shfl_xor_sync(full, mnx, o)), mxx = max(mxx, __shfl_xor_sync(full, mxx, o));
+    mny = min(mny, __shfl_xor_sync(full, mny, o)), mxy = max(mxy, __shfl_xor_sync(full, mxy, o));
+    mnz = min(mnz, __shfl_xor_sync(full, mnz, o)), mxz = max(mxz, __shfl_xor_sync(full, mxz, o));
+    in &= __shfl_xor_sync(full, in, o);
+  }
+  const int cl = k / kCS;
+  if ((lane & (kCS - 1)) == 0 && cl < a.nc) {
     const size_t g = size_t(r) * a.nc + cl;
     a.arcs[g] = make_uint4(arc_centre(u0.x, mnx, mxx), arc_centre(u0.y, mny, mxy),
                            arc_centre(u0.z, mnz, mxz), 0u);
     a.half[g] = in ? make_float4(arc_half(mnx, mxx), arc_half(mny, mxy), arc_half(mnz, mxz), 0.0f)
                    : make_float4(3e9f, 3e9f, 3e9f, 0.0f);
   }
-  const unsigned all = 0xffffffffu;
-  in = __all_sync(all, in);
-  smnx = __reduce_min_sync(all, smnx), smxx = __reduce_max_sync(all, smxx);
-  smny = __reduce_min_sync(all, smny), smxy = __reduce_max_sync(all, smxy);
-  smnz = __reduce_min_sync(all, smnz), smxz = __reduce_max_sync(all, smxz);
+  // super-cluster: offsets to wa over the valid slots
+  const int px = valid ? int(u.x - wa.x) : 0, py = valid ? int(u.y - wa.y) : 0;
+  const int pz = valid ? int(u.z - wa.z) : 0;
+  const int v[6] = {__reduce_min_sync(full, px), __reduce_max_sync(full, px),
+                    __reduce_min_sync(full, py), __reduce_max_sync(full, py),
+                    __reduce_min_sync(full, pz), __reduce_max_sync(full, pz)};
+  const int win = __all_sync(full, in != 0);
   if (lane == 0) {
-    a.sup_arcs[w] = make_uint4(arc_centre(wa.x, smnx, smxx), arc_centre(wa.y, smny, smxy),
-                               arc_centre(wa.z, smnz, smxz), 0u);
-    a.sup_half[w] = in ? make_float4(arc_half(smnx, smxx), arc_half(smny, smxy),
-                                     arc_half(smnz, smxz), 0.0f)
-                       : make_float4(3e9f, 3e9f, 3e9f, 0.0f);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) red[warp][q] = v[q];
+    sin_[warp] = win;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int m[6] = {red[0][0], red[0][1], red[0][2], red[0][3], red[0][4], red[0][5]};
+    int all_in = sin_[0];
+    for (int w = 1; w < 8; ++w) {
+      m[0] = min(m[0], red[w][0]), m[1] = max(m[1], red[w][1]);
+      m[2] = min(m[2], red[w][2]), m[3] = max(m[3], red[w][3]);
+      m[4] = min(m[4], red[w][4]), m[5] = max(m[5], red[w][5]);
+      all_in &= sin_[w];
+    }
+    const size_t g = size_t(r) * a.nsup + sc;
+    a.sup_arcs[g] = make_uint4(arc_centre(wa.x, m[0], m[1]), arc_centre(wa.y, m[2], m[3]),
+                               arc_centre(wa.z, m[4], m[5]), 0u);
+    a.sup_half[g] = all_in ? make_float4(arc_half(m[0], m[1]), arc_half(m[2], m[3]),
+                                         arc_half(m[4], m[5]), 0.0f)
+                           : make_float4(3e9f, 3e9f, 3e9f, 0.0f);
   }
 }
 
@@ -316,6 +337,235 @@ __global__ void __launch_bounds__(kForceWarps * 32, B2MD_CLUSTER_MINB) k_force_c
   const double s1 = -12.0 * A12 + 6.0 * A6;  // sum du_r
   double v[kNumRowScalars] = {A12 - A6, 0.0, 0.0, VDERIV ? s1 : 0.0,
                               VDERIV ? 156.0 * A12 - 42.0 * A6 : 0.0, -s1, warp_sum(double(cnt))};
+  finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
+}
+
+// ---------------------------------------------------------------------------
+// Cluster-pair walk: one warp per i-group (kGR = 4 consecutive slots, half a
+// cluster); lane = (j-member jl = lane >> 2, row il = lane & 3), so one warp
+// step takes a whole j-cluster against the group, each j position loaded once
+// for its 4 rows.  The group's own arc (from its 4 fixed-point points) is
+// culled against the super-cluster arcs, then against the clusters of each
+// surviving super-cluster -- no list buffer, no list kernel.  Every lane of a
+// step computes its pair's R = minimum_image(x_i - x_j), r2 = norm2(R) on the
+// reference's bits (potentials.cpp:156-161); a step with no r2 < rc2 in the
+// warp ends there, otherwise all lanes run the LJ terms (162-178) with the
+// out-of-range lanes zeroed (ir6 = 0 => no force, no energy).  A lane's row
+// is fixed, so its force accumulates in registers; the 8 lanes of a row are
+// summed by a fixed xor tree at the end (no atomics, deterministic).
+// Each pair is visited from both rows with bit-identical r2, so the LJ sums
+// are taken over all visits and halved (u, s1, s2, virial, pair count).
+constexpr int kGR = 4;       // rows per i-group
+constexpr int kGWarps = 4;   // warps per CTA
+constexpr int kGSplit = 1;   // warps per i-group (alternate cluster pairs; fixed-order combine)
+constexpr int kGList = 256;  // per-warp chunk of surviving clusters (+1: odd-tail pad)
+constexpr int kGDepth = 4;   // staged cluster pairs in flight per warp (power of 2)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(unsigned smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <bool MULTI_SPECIES, bool WRAPPED, bool VDERIV>
+__global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, ClusterArgs ca) {
+  __shared__ int clist[kGWarps][kGList + 1];
+  __shared__ __align__(128) double4 stage[kGWarps][kGDepth][2][kCS];
+  const SysDev& s = a.s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.y;
+  const size_t roff = size_t(r) * s.n;
+  const double4* __restrict__ p4 = a.st.pos4 + roff;
+  const uint4* __restrict__ fx4 = ca.fixpos + roff;
+  const uint4* __restrict__ arcs = ca.arcs + size_t(r) * ca.nc;
+  const float4* __restrict__ half = ca.half + size_t(r) * ca.nc;
+  const uint4* __restrict__ sarcs = ca.sup_arcs + size_t(r) * ca.nsup;
+  const float4* __restrict__ shalf = ca.sup_half + size_t(r) * ca.nsup;
+  const MinImage mi = s.mi;
+  const float thr = a.thr;
+  auto mimg = [&](double d) {
+    return WRAPPED ? min_image_wrapped(d, mi.negL, thr) : min_image(d, mi);
+  };
+  const double rc2 = a.rc2;
+  const float lim = ca.lim;
+  const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+  const int n = s.n;
+  const int g0 = ((blockIdx.x * kGWarps + warp) / kGSplit) * kGR;  // the group's first slot
+  const int part = warp % kGSplit;
+  __shared__ double comb[kGWarps][kGR][3];
+  int eidx = -1;  // lanes < kGR: the row's external index
+  int* __restrict__ wl = clist[warp];
+  // sums over all visits: single species B12 = sum ir6^2, B6 = sum ir6
+  // (a12 = c12 B12, a6 = c6 B6); mixtures sum a12, a6 directly
+  double B12 = 0, B6 = 0;
+  int cnt = 0;
+  if (g0 < n) {  // warp-uniform
+    const int il = lane & (kGR - 1), jl = lane >> 2;
+    const int i = g0 + il;
+    const bool iv = i < n;
+    const int ic = iv ? i : g0;  // clamped row
+    const uint4 fi = fx4[ic];
+    const double4 pi = p4[ic];
+    const int si = MULTI_SPECIES ? s.sp_slot[roff + ic] : 0;
+    // the group's arc (offsets from lane 0's point; lanes repeat the 4 rows)
+    uint4 gc;
+    float4 gh;
+    {
+      const uint4 f0 = make_uint4(__shfl_sync(full, fi.x, 0), __shfl_sync(full, fi.y, 0),
+                                  __shfl_sync(full, fi.z, 0), 0u);
+      const int ox = int(fi.x - f0.x), oy = int(fi.y - f0.y), oz = int(fi.z - f0.z);
+      const int mnx = __reduce_min_sync(full, ox), mxx = __reduce_max_sync(full, ox);
+      const int mny = __reduce_min_sync(full, oy), mxy = __reduce_max_sync(full, oy);
+      const int mnz = __reduce_min_sync(full, oz), mxz = __reduce_max_sync(full, oz);
+      const bool in = __all_sync(full, fi.w != 0u);
+      gc = make_uint4(arc_centre(f0.x, mnx, mxx), arc_centre(f0.y, mny, mxy),
+                      arc_centre(f0.z, mnz, mxz), 0u);
+      gh = in ? make_float4(arc_half(mnx, mxx), arc_half(mny, mxy), arc_half(mnz, mxz), 0.0f)
+              : make_float4(3e9f, 3e9f, 3e9f, 0.0f);
+    }
+    double fx = 0, fy = 0, fz = 0;
+    // one lane's pair: distance on the reference's bits, then the terms
+    auto dist = [&](const double4& pj, double& dx, double& dy, double& dz) {
+      dx = mimg(sub(pi.x, pj.x));
+      dy = mimg(sub(pi.y, pj.y));
+      dz = mimg(sub(pi.z, pj.z));
+      return norm2_exact(dx, dy, dz);
+    };
+    auto terms = [&](int j, bool in, double r2, double dx, double dy, double dz) {
+      const double inv_r2 = rcp_nr(in ? r2 : 1.0);
+      const double t6 = inv_r2 * inv_r2 * inv_r2;
+      const double ir6 = in ? t6 : 0.0;
+      double fs;
+      if constexpr (MULTI_SPECIES) {
+        const int sj = s.sp_slot[roff + j];
+        const DevPairInfo& pinfo = s.tab->pair[(i < j) ? si * s.ns + sj : sj * s.ns + si];
+        const double c12 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c12 : 0.0;
+        const double c6 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c6 : 0.0;
+        const double a12 = c12 * ir6 * ir6, a6 = c6 * ir6;
+        fs = (12.0 * a12 - 6.0 * a6) * inv_r2;  // -du_r / r2
+        B12 += a12;
+        B6 += a6;
+      } else {
+        fs = fma(ir6, a.c12x12, -a.c6x6) * ir6 * inv_r2;
+        B12 = fma(ir6, ir6, B12);
+        B6 += ir6;
+      }
+      fx = fma(fs, dx, fx);
+      fy = fma(fs, dy, fy);
+      fz = fma(fs, dz, fz);
+      cnt += in;
+    };
+    // staging ring: slot k holds a cluster pair as 512 contiguous bytes;
+    // lane L copies bytes [16 L, 16 L + 16) (lanes 0-15 the first cluster's
+    // 8 double4, lanes 16-31 the second's)
+    const unsigned ring = smem_u32(&stage[warp][0][0][0]) + 16u * lane;
+    const char* __restrict__ src0 = reinterpret_cast<const char*>(p4) + 16 * (lane & 15);
+    const int half_sel = lane >> 4;
+    const int ilim = iv ? n : 0;  // j < ilim: a real partner slot of a real row
+    // surviving clusters, in chunks of <= kGList: super-cluster batch sb
+    // (ballot sv), then each super-cluster's clusters (ballot, compacted)
+    int sb = 0;
+    unsigned sv = 0u;
+    for (;;) {
+      int nl = 0;
+      for (;;) {
+        if (sv == 0u) {
+          if (sb >= ca.nsup) break;
+          const bool near = sb + lane < ca.nsup && arcs_near(gc, gh, sarcs[sb + lane], shalf[sb + lane], lim);
+          sv = __ballot_sync(full, near);
+          sb += 32;
+          continue;
+        }
+        if (nl > kGList - 32) break;
+        const int sc = sb - 32 + __ffs(sv) - 1;
+        sv &= sv - 1u;
+        const int jc = sc * kSC + lane;
+        const bool keep = jc < ca.nc && arcs_near(gc, gh, arcs[jc], half[jc], lim);
+        const unsigned cv = __ballot_sync(full, keep);
+        if (keep) wl[nl + __popc(cv & lt)] = jc;
+        nl += __popc(cv);
+      }
+      if (nl == 0) break;
+      if (lane == 0) wl[nl] = ca.nc;  // odd tail: a cluster past the end (all j >= n)
+      __syncwarp();
+      const int nsteps = (nl + 1) >> 1;
+      int next = part;     // next pair to stage (this warp takes every kGSplit-th)
+      unsigned wslot = 0;  // its ring slot (bytes)
+      auto issue = [&]() {
+        const int e = 2 * next + half_sel;
+        if (next < nsteps && e < nl) cp_async16(ring + wslot, src0 + size_t(wl[e]) * (kCS * 32));
+        cp_async_commit();
+        next += kGSplit;
+        wslot = (wslot + 512u) & (512u * kGDepth - 1u);
+      };
+#pragma unroll
+      for (int k = 0; k < kGDepth - 1; ++k) issue();
+      const double4* rs = &stage[warp][0][0][jl];
+      int k = 0;
+      for (int st = part; st < nsteps; st += kGSplit, ++k) {
+        issue();
+        cp_async_wait<kGDepth - 1>();
+        __syncwarp();
+        const int slot = k & (kGDepth - 1);
+        const int ja = wl[2 * st] * kCS + jl, jb = wl[2 * st + 1] * kCS + jl;
+        const bool va = ja < ilim && ja != i;
+        const bool vb = jb < ilim && jb != i;
+        double ax, ay, az, bx, by, bz;
+        const double ra = dist(rs[slot * 2 * kCS], ax, ay, az);
+        const double rb = dist(rs[slot * 2 * kCS + kCS], bx, by, bz);
+        __syncwarp();  // the slot's reads are consumed before it is refilled
+        const bool ina = va && ra < rc2, inb = vb && rb < rc2;  // potentials.cpp:161
+        if (__ballot_sync(full, ina || inb) == 0u) continue;
+        terms(ja, ina, ra, ax, ay, az);
+        terms(jb, inb, rb, bx, by, bz);
+      }
+      cp_async_wait<0>();
+      __syncwarp();  // wl and the ring are rewritten by the next chunk
+    }
+    // a row's 8 lanes (il fixed, jl = lane >> 2): fixed xor tree
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      fx += __shfl_xor_sync(full, fx, o);
+      fy += __shfl_xor_sync(full, fy, o);
+      fz += __shfl_xor_sync(full, fz, o);
+    }
+    if (lane < kGR) {
+      comb[warp][lane][0] = fx;
+      comb[warp][lane][1] = fy;
+      comb[warp][lane][2] = fz;
+      if (iv) eidx = ext_of(pi);
+    }
+  }
+  // the group's kGSplit partial forces, summed in warp order
+  __syncthreads();
+  if (part == 0 && lane < kGR && eidx >= 0) {
+    double sx = comb[warp][lane][0], sy = comb[warp][lane][1], sz = comb[warp][lane][2];
+#pragma unroll
+    for (int p = 1; p < kGSplit; ++p) {
+      sx += comb[warp + p][lane][0];
+      sy += comb[warp + p][lane][1];
+      sz += comb[warp + p][lane][2];
+    }
+    const size_t e = roff + eidx;
+    a.st.fx[e] = sx;
+    a.st.fy[e] = sy;
+    a.st.fz[e] = sz;
+    if (a.kick_dt > 0.0) fused_kick(a, e);
+  }
+  // every pair was visited twice (bit-identical terms): halve the sums
+  double A12 = 0.5 * warp_sum(B12), A6 = 0.5 * warp_sum(B6);
+  if constexpr (!MULTI_SPECIES) {
+    A12 *= a.c12;
+    A6 *= a.c6;
+  }
+  const double s1 = -12.0 * A12 + 6.0 * A6;  // sum du_r
+  double v[kNumRowScalars] = {A12 - A6, 0.0, 0.0, VDERIV ? s1 : 0.0,
+                              VDERIV ? 156.0 * A12 - 42.0 * A6 : 0.0, -s1,
+                              0.5 * warp_sum(double(cnt))};
   finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
 }
 

@@ -289,9 +289,13 @@ ForceArgs force_args(b2md_ctx* c) {
   a.sums = sums_ptr(c);
   a.c12 = 0.0;
   a.c6 = 0.0;
+  a.c12x12 = 0.0;
+  a.c6x6 = 0.0;
   if (!c->t.lj.empty() && !c->t.lj[0].empty()) {
     a.c12 = c->t.lj[0][0].c12;
     a.c6 = c->t.lj[0][0].c6;
+    a.c12x12 = 12.0 * a.c12;
+    a.c6x6 = 6.0 * a.c6;
   }
   a.rc2 = c->t.rc2;
   a.alpha = c->t.alpha;
@@ -361,6 +365,12 @@ bool fast_min_image(const b2md_ctx* c) {
 // minimum image replaces the wrapped one when positions are not wrapped
 // (same bits), so the hit sequence -- and the summation order -- is the same
 // either way: restarts from unwrapped checkpoints stay bit-exact.
+// CTAs of the cluster-pair walk: kGWarps i-groups of kGR slots each
+int cpair_grid(const b2md_ctx* c) {
+  const int groups = (c->t.n + kGR - 1) / kGR;
+  return (groups * kGSplit + kGWarps - 1) / kGWarps;
+}
+
 bool cluster_path(const b2md_ctx* c) {
   return c->use_cluster && c->nc > 0 && c->t.single_site_path && c->world <= 1;
 }
@@ -381,13 +391,30 @@ int launch_cluster_force(b2md_ctx* c, bool kick) {
   ca.lim = float(ru * ru * (1.0 + 1e-5));
   ca.lim_pair = float((ru + 4.0) * (ru + 4.0) * (1.0 + 1e-5));
   const int R = c->R, tot = R * c->nc;
-  PROF(c, F_CLUSTER, (k_cluster_arcs<<<(R * c->nsup * 32 + 255) / 256, 256, 0, c->stream>>>(ca, R)));
-  PROF(c, F_CLUSTER, (k_cluster_list<<<(tot * 32 + 255) / 256, 256, 0, c->stream>>>(ca, R)));
+  PROF(c, F_CLUSTER, (k_cluster_arcs<<<R * c->nsup, kSC * kCS, 0, c->stream>>>(ca, R)));
   ForceArgs a = force_args(c);
   if (kick) a.kick_dt = c->dt;
+  const bool w = fast_min_image(c), m = c->t.ns > 1, v = a.vderiv != 0;
+  if (c->cluster_kernel == 1) {
+    dim3 pgrid(cpair_grid(c), R);
+#define CPAIR_LAUNCH(M, W, V) \
+  if (m == M && w == W && v == V) \
+    PROF(c, F_FORCE, (k_force_cpair<M, W, V><<<pgrid, kGWarps * 32, 0, c->stream>>>(a, ca)));
+    CPAIR_LAUNCH(false, true, false)
+    CPAIR_LAUNCH(false, true, true)
+    CPAIR_LAUNCH(false, false, false)
+    CPAIR_LAUNCH(false, false, true)
+    CPAIR_LAUNCH(true, true, false)
+    CPAIR_LAUNCH(true, true, true)
+    CPAIR_LAUNCH(true, false, false)
+    CPAIR_LAUNCH(true, false, true)
+#undef CPAIR_LAUNCH
+    c->mask_valid = false;
+    return B2MD_OK;
+  }
+  PROF(c, F_CLUSTER, (k_cluster_list<<<(tot * 32 + 255) / 256, 256, 0, c->stream>>>(ca, R)));
   dim3 grid(c->force_grid, R);
   const int bs = c->force_warps * 32;
-  const bool w = fast_min_image(c), m = c->t.ns > 1, v = a.vderiv != 0;
 #define CLUSTER_LAUNCH(M, W, V) \
   if (m == M && w == W && v == V) \
     PROF(c, F_FORCE, (k_force_cluster<M, W, V><<<grid, bs, 0, c->stream>>>(a, ca)));
@@ -1015,7 +1042,7 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   TRY(dalloc(&c->d_state, 13 * nt));
   TRY(dalloc(&c->d_fbuf, 6 * nt + size_t(kNumSums) * R));
   TRY(dalloc(&c->d_off, size_t(t.total_sites) * R));
-  TRY(dalloc(&c->d_pos4, nt));
+  TRY(dalloc(&c->d_pos4, nt + kCS));  // + a cluster: the cluster walk stages whole clusters
   TRY(dalloc(&c->d_stage, 6 * 4 * nt));
   TRY(dalloc(&c->d_mask, size_t(R) * c->g.n_pad * c->g.words));
   TRY(dalloc(&c->d_fixpos, nt));
@@ -1059,17 +1086,28 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     // (one launch less), but lengthens every warp's critical path when warps
     // own several rows (measured: cfg0/cfg1 +3-7%, cfg3/cfg4 -2-4%)
     c->use_fused_kick = size_t(t.n) * R < 4096;
+    if (c->nc > 0) {
+      // B2MD_CLUSTER_KERNEL=0: the row walk (k_force_cluster, measurement only)
+      c->cluster_kernel = 1;
+      if (const char* e = std::getenv("B2MD_CLUSTER_KERNEL")) c->cluster_kernel = std::atoi(e);
+      // the cluster-pair walk ends with 4 rows per warp written by 4 lanes:
+      // the kick costs those lanes a few loads, not a serial row epilogue
+      if (c->cluster_kernel == 1) c->use_fused_kick = true;
+    }
     if (const char* e = std::getenv("B2MD_FUSED_KICK")) c->use_fused_kick = std::atoi(e) != 0;
   }
-  TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars * c->force_grid));
+  TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars *
+                                 std::max(c->force_grid, c->nc > 0 ? cpair_grid(c) : 0)));
   if (c->nc > 0) {
     c->nsup = (c->nc + kSC - 1) / kSC;
     TRY(dalloc(&c->d_carc, size_t(R) * c->nc));
     TRY(dalloc(&c->d_chalf, size_t(R) * c->nc));
     TRY(dalloc(&c->d_sarc, size_t(R) * c->nsup));
     TRY(dalloc(&c->d_shalf, size_t(R) * c->nsup));
-    TRY(dalloc(&c->d_clist, size_t(R) * c->nc * c->nc));
-    TRY(dalloc(&c->d_ccount, size_t(R) * c->nc));
+    if (c->cluster_kernel == 0) {
+      TRY(dalloc(&c->d_clist, size_t(R) * c->nc * c->nc));
+      TRY(dalloc(&c->d_ccount, size_t(R) * c->nc));
+    }
   }
   TRY(dalloc(&c->d_ticket, size_t(2) * R));
   TRY(dalloc(&c->d_flux, size_t(kNumSums) * R));

@@ -718,6 +718,7 @@ struct ForceArgs {
   unsigned* ticket;  // R
   double* sums;      // R * kNumSums
   double c12, c6;    // single-species LJ term (PairTable lj[0])
+  double c12x12, c6x6;  // 12 c12, 6 c6 (kernel constants, not registers)
   double rc2;
   double alpha, two_alpha_over_sqrt_pi;
   double rf_r3inv, rf_shift;

@@ -188,6 +188,50 @@ def test_single_site_walks(monkeypatch, mode, n):
     assert ff.last_stats.com_pairs == ref["com_pairs"]
 
 
+@pytest.mark.parametrize("kernel", ["0", "1"])
+@pytest.mark.parametrize("n", [9, 300, 2053])
+def test_cluster_kernels_single_site_mixture(monkeypatch, kernel, n):
+    """Both cluster walks (=1 the cluster-pair walk, =0 the row walk) on a
+    two-species single-site mixture (species-pair LJ terms, Lorentz-Berthelot,
+    potentials.cpp:64-69): pairs, forces, energies and a short trajectory."""
+    monkeypatch.setenv("B2MD_CLUSTER", "2")
+    monkeypatch.setenv("B2MD_CLUSTER_KERNEL", kernel)
+    na = n // 3
+    box = (n / 0.7) ** (1.0 / 3.0)
+    comp = b2.SystemComposition([b2.build_species("a", [b2.make_lj_site(0, 0, 0, 1.0, 1.0, 1.0)]),
+                                 b2.build_species("b", [b2.make_lj_site(0, 0, 0, 0.9, 1.3, 2.0)])],
+                                [na, n - na], box, 1.0)
+    opts = systems.lj_opts(min(2.5, 0.45 * box))
+    st = systems.random_state(comp, n, 0.8)
+    o = pyoracle.OracleFF(comp, opts)
+    ref = o.evaluate(st.pos, st.orient)
+    ff, out = gpu_eval(comp, opts, st.pos, st.orient)
+    assert np.array_equal(ff.pair_list(), o.pair_list(st.pos))
+    check_vec(out.force, ref["force"])
+    check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+    dt, steps = 0.002, 10
+    eng = b2.Engine(comp, opts, dt)
+    eng.set_state(st)
+    eng.step(steps)
+    got = eng.state()
+    tr = o.run(dt, steps, st.pos, st.orient, st.vel, st.ang_vel)
+    compare_states(got, tr, box)
+
+
+@pytest.mark.parametrize("kernel", ["0", "1"])
+def test_cluster_kernels_agree_cfg3(monkeypatch, kernel):
+    """cfg3 through each cluster walk: oracle pairs, forces and energies."""
+    monkeypatch.setenv("B2MD_CLUSTER_KERNEL", kernel)
+    wl = configs.make("cfg3")
+    st = wl.states[0]
+    o = pyoracle.OracleFF(wl.comp, wl.opts)
+    ref = o.evaluate(st.pos, st.orient)
+    ff, out = gpu_eval(wl.comp, wl.opts, st.pos, st.orient)
+    assert np.array_equal(ff.pair_list(), o.pair_list(st.pos))
+    check_vec(out.force, ref["force"])
+    check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+
+
 def test_cluster_walk_unwrapped_positions(monkeypatch):
     """The cluster walk on positions outside [0, L) (ForceField::evaluate
     takes them as given): such clusters are never culled, the exact minimum
