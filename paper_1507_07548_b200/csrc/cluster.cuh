@@ -12,16 +12,8 @@
 // x inside), so kCS consecutive slots form a compact cluster.  Per step:
 //   k_cluster_arcs  bounding arcs of every cluster (and of every kSC-cluster
 //                   super-cluster) on the periodic fixed-point circle;
-//   k_cluster_list  per i-cluster, the clusters whose arcs come within rc
-//                   (one warp per i-cluster: super-clusters first, then their
-//                   clusters; ballot-compacted, ascending);
-//   k_force_cluster one warp per row i: the row's point-vs-arc filter over
-//                   its cluster's list, then 4 clusters x 8 members = 32
-//                   candidates per warp step under a conservative fixed-point
-//                   bound; the maybes are ballot-compacted into a per-warp
-//                   ring queue and decided + evaluated 32 at a time on the
-//                   reference's fp64 bits with every lane busy.
-// Summation order is fixed (list, survivor and lane order), so results are
+//   k_force_cpair   one warp per half cluster against whole j-clusters (below).
+// Summation order is fixed (cluster and lane order), so results are
 // deterministic; culls only ever keep extra candidates.
 #pragma once
 
@@ -29,11 +21,8 @@
 
 namespace b2md {
 
-#ifndef B2MD_CLUSTER_MINB
-#define B2MD_CLUSTER_MINB 4
-#endif
 constexpr int kCS = 8;          // molecules (consecutive slots) per cluster
-constexpr int kSC = 32;         // clusters per super-cluster (list kernel's first cull)
+constexpr int kSC = 32;         // clusters per super-cluster (the first cull)
 constexpr int kRing = 128;      // per-warp queue (< 64 carried + 64 new)
 constexpr float kArcMargin = 2048.0f;  // fixed-point units: float rounding + coordinate rounding
 
@@ -44,10 +33,7 @@ struct ClusterArgs {
   float4* half;                 // R * nc: arc half extents (fixed-point units)
   uint4* sup_arcs;              // R * nsup
   float4* sup_half;             // R * nsup
-  int* list;                    // R * nc * nc: candidate clusters of each i-cluster
-  int* count;                   // R * nc
   float lim;                    // (rc 2^32 / L)^2 (1 + 1e-5): cull radius^2
-  float lim_pair;               // (rc 2^32 / L + 4)^2 (1 + 1e-5): stage-1 pair bound
 };
 
 // Lower bound of the circle distance between two arcs (centres x, y, half
@@ -146,200 +132,6 @@ static __global__ void __launch_bounds__(kSC * kCS) k_cluster_arcs(ClusterArgs a
   }
 }
 
-// One warp per (replica, i-cluster): the clusters (itself included) whose
-// arcs come within rc, ascending -- super-clusters first, then the clusters
-// of each surviving super-cluster.
-static __global__ void __launch_bounds__(256) k_cluster_list(ClusterArgs a, int R) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= R * a.nc) return;  // warp-uniform
-  const int r = w / a.nc;
-  const uint4* __restrict__ arcs = a.arcs + size_t(r) * a.nc;
-  const float4* __restrict__ half = a.half + size_t(r) * a.nc;
-  const uint4* __restrict__ sarcs = a.sup_arcs + size_t(r) * a.nsup;
-  const float4* __restrict__ shalf = a.sup_half + size_t(r) * a.nsup;
-  const uint4 ci = a.arcs[w];
-  const float4 hi = a.half[w];
-  int* __restrict__ out = a.list + size_t(w) * a.nc;
-  const unsigned lt = (1u << lane) - 1u;
-  int cnt = 0;
-  for (int s0 = 0; s0 < a.nsup; s0 += 32) {
-    bool near = false;
-    if (s0 + lane < a.nsup) near = arcs_near(ci, hi, sarcs[s0 + lane], shalf[s0 + lane], a.lim);
-    unsigned sv = __ballot_sync(0xffffffffu, near);
-    while (sv) {
-      const int sc = s0 + __ffs(sv) - 1;
-      sv &= sv - 1u;
-      const int j = sc * kSC + lane;
-      const bool keep = j < a.nc && arcs_near(ci, hi, arcs[j], half[j], a.lim);
-      const unsigned b = __ballot_sync(0xffffffffu, keep);
-      if (keep) out[cnt + __popc(b & lt)] = j;
-      cnt += __popc(b);
-    }
-  }
-  if (lane == 0) a.count[w] = cnt;
-}
-
-// One warp per row (slot) i.  WRAPPED: positions in [0, L) and rc < L/2
-// (min_image_wrapped); else the exact minimum image (same bits).
-// Stage 1 (every candidate, 32 per warp step): the wrapping int32 difference
-// of the fixed-point positions is the minimum image to 1 unit; its fp32 norm
-// is compared with (rc + 4 units)^2 (1 + 1e-5) -- a conservative "may be
-// within rc" (the rounding of the coordinates, the float conversions and
-// sums are all inside the margins).  Maybes (the hits, plus a ~1e-5 shell)
-// are ballot-compacted into the warp's ring queue of slots.
-// Stage 2 (32 queued maybes at a time, every lane busy): the reference's
-// R = minimum_image(x_i - x_j), r2 = norm2(R) on its own bits, the pair kept
-// iff r2 < rc2 (potentials.cpp:159-161), and its terms (162-178).
-template <bool MULTI_SPECIES, bool WRAPPED, bool VDERIV>
-__global__ void __launch_bounds__(kForceWarps * 32, B2MD_CLUSTER_MINB) k_force_cluster(ForceArgs a, ClusterArgs ca) {
-  __shared__ int qj[kForceWarps][kRing];      // queued candidate slots (ring)
-  __shared__ int sv_list[kForceWarps][32];    // surviving clusters of a list batch
-  const SysDev& s = a.s;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = blockIdx.y;
-  const size_t roff = size_t(r) * s.n;
-  const double4* __restrict__ p4 = a.st.pos4 + roff;
-  const uint4* __restrict__ fx4 = ca.fixpos + roff;
-  const uint4* __restrict__ arcs = ca.arcs + size_t(r) * ca.nc;
-  const float4* __restrict__ half = ca.half + size_t(r) * ca.nc;
-  const MinImage mi = s.mi;
-  const float thr = a.thr;
-  auto mimg = [&](double d) {
-    return WRAPPED ? min_image_wrapped(d, mi.negL, thr) : min_image(d, mi);
-  };
-  const double rc2 = a.rc2;
-  const float lim_pair = ca.lim_pair;
-  const unsigned lt = (1u << lane) - 1u;
-  int* __restrict__ wj = qj[warp];
-  int* __restrict__ wsv = sv_list[warp];
-  double A12 = 0, A6 = 0;  // sum over this warp's pairs (i < j side)
-  int cnt = 0;
-  const int wpb = blockDim.x >> 5;
-  for (int i = blockIdx.x * wpb + warp; i < s.n; i += gridDim.x * wpb) {
-    const double4 pi = p4[i];
-    const uint4 fi = fx4[i];
-    const int si = MULTI_SPECIES ? s.sp_slot[roff + i] : 0;
-    const int ic = i / kCS;
-    const int* __restrict__ list = ca.list + (size_t(r) * ca.nc + ic) * ca.nc;
-    const int nl = ca.count[size_t(r) * ca.nc + ic];
-    double fx = 0, fy = 0, fz = 0;
-    // stage 2 for candidate slot j (position pj) on this lane
-    auto terms = [&](int j, const double4& pj, bool on) {
-      const double dx = mimg(sub(pi.x, pj.x));
-      const double dy = mimg(sub(pi.y, pj.y));
-      const double dz = mimg(sub(pi.z, pj.z));
-      const double r2 = norm2_exact(dx, dy, dz);
-      if (!(on && r2 < rc2)) return;  // potentials.cpp:161
-      double c12 = a.c12, c6 = a.c6;
-      if constexpr (MULTI_SPECIES) {
-        const int sj = s.sp_slot[roff + j];
-        const DevPairInfo& pinfo = s.tab->pair[(i < j) ? si * s.ns + sj : sj * s.ns + si];
-        c12 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c12 : 0.0;
-        c6 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c6 : 0.0;
-      }
-      const double inv_r2 = rcp_nr(r2);
-      const double ir6 = inv_r2 * inv_r2 * inv_r2;
-      const double a12 = c12 * ir6 * ir6;
-      const double a6 = c6 * ir6;
-      const double du_r = -12.0 * a12 + 6.0 * a6;
-      const double fs = -du_r * inv_r2;
-      const double gx = fs * dx, gy = fs * dy, gz = fs * dz;
-      fx += gx;
-      fy += gy;
-      fz += gz;
-      // the pair's scalars (i < j side) are linear in a12, a6 -- u = a12 - a6,
-      // s1 = du_r, s2 = 156 a12 - 42 a6, and dot(R, f) = fs r2 = -du_r --
-      // so their sums are taken from sum a12, sum a6 in the epilogue
-      const double w = i < j ? 1.0 : 0.0;
-      A12 = fma(w, a12, A12);
-      A6 = fma(w, a6, A6);
-      cnt += i < j;
-    };
-    // queued slot q on this lane (on: the lane holds an entry)
-    auto eval = [&](int q, bool on) {
-      const int j = on ? wj[q] : i;
-      terms(j, p4[j], on);
-    };
-    // two full batches, both gathers in flight
-    auto eval2 = [&](int qa, int qb) {
-      const int ja = wj[qa], jb = wj[qb];
-      const double4 pa = p4[ja], pb = p4[jb];
-      terms(ja, pa, true);
-      terms(jb, pb, true);
-    };
-    int head = 0, tail = 0;  // warp-uniform ring counters, tail - head < kRing
-    for (int l0 = 0; l0 < nl; l0 += 32) {
-      // the row's own cull: this point against each listed cluster's arc;
-      // survivors compacted (ascending) into the warp's cluster list
-      bool keep = false;
-      int jc = 0;
-      if (l0 + lane < nl) {
-        jc = list[l0 + lane];
-        keep = arcs_near(fi, make_float4(0.0f, 0.0f, 0.0f, 0.0f), arcs[jc], half[jc], ca.lim);
-      }
-      const unsigned sv = __ballot_sync(0xffffffffu, keep);
-      if (keep) wsv[__popc(sv & lt)] = jc;
-      __syncwarp();
-      const int nsv = __popc(sv);
-      // stage 1, 8 surviving clusters per step (two loads in flight):
-      // lane = (cluster lane >> 3, member lane & 7) of each half
-      for (int g0 = 0; g0 < nsv; g0 += 8) {
-        const int ta = g0 + (lane >> 3), tb = ta + 4;
-        const int ja = wsv[ta & 31] * kCS + (lane & 7);
-        const int jb = wsv[tb & 31] * kCS + (lane & 7);
-        const bool va = ta < nsv && ja < s.n && ja != i;
-        const bool vb = tb < nsv && jb < s.n && jb != i;
-        const uint4 fa = fx4[va ? ja : i];
-        const uint4 fb = fx4[vb ? jb : i];
-        // (a saturated fixed point -- position outside [0, L) -- always passes)
-        auto maybe = [&](uint4 fj) {
-          const float ex = float(int(fi.x - fj.x));
-          const float ey = float(int(fi.y - fj.y));
-          const float ez = float(int(fi.z - fj.z));
-          return !(fi.w & fj.w) || ex * ex + ey * ey + ez * ez <= lim_pair;
-        };
-        const bool ma = va && maybe(fa), mbb = vb && maybe(fb);
-        const unsigned ba = __ballot_sync(0xffffffffu, ma);
-        const unsigned bb = __ballot_sync(0xffffffffu, mbb);
-        if (ma) wj[(tail + __popc(ba & lt)) & (kRing - 1)] = ja;
-        tail += __popc(ba);
-        if (mbb) wj[(tail + __popc(bb & lt)) & (kRing - 1)] = jb;
-        tail += __popc(bb);
-        if (tail - head >= 64) {
-          __syncwarp();
-          eval2((head + lane) & (kRing - 1), (head + 32 + lane) & (kRing - 1));
-          head += 64;
-          __syncwarp();
-        }
-      }
-      __syncwarp();  // wsv is rewritten by the next batch
-    }
-    __syncwarp();
-    if (tail - head >= 32) {
-      eval((head + lane) & (kRing - 1), true);
-      head += 32;
-    }
-    eval((head + lane) & (kRing - 1), lane < tail - head);
-    __syncwarp();
-    fx = warp_sum(fx);
-    fy = warp_sum(fy);
-    fz = warp_sum(fz);
-    if (lane == 0) {
-      const size_t e = roff + ext_of(pi);
-      a.st.fx[e] = fx;
-      a.st.fy[e] = fy;
-      a.st.fz[e] = fz;
-      if (a.kick_dt > 0.0) fused_kick(a, e);
-    }
-  }
-  A12 = warp_sum(A12);
-  A6 = warp_sum(A6);
-  const double s1 = -12.0 * A12 + 6.0 * A6;  // sum du_r
-  double v[kNumRowScalars] = {A12 - A6, 0.0, 0.0, VDERIV ? s1 : 0.0,
-                              VDERIV ? 156.0 * A12 - 42.0 * A6 : 0.0, -s1, warp_sum(double(cnt))};
-  finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
-}
-
 // ---------------------------------------------------------------------------
 // Cluster-pair walk: one warp per i-group (kGR = 4 consecutive slots, half a
 // cluster); lane = (j-member jl = lane >> 2, row il = lane & 3), so one warp
@@ -356,8 +148,7 @@ __global__ void __launch_bounds__(kForceWarps * 32, B2MD_CLUSTER_MINB) k_force_c
 // Each pair is visited from both rows with bit-identical r2, so the LJ sums
 // are taken over all visits and halved (u, s1, s2, virial, pair count).
 constexpr int kGR = 4;       // rows per i-group
-constexpr int kGWarps = 4;   // warps per CTA
-constexpr int kGSplit = 1;   // warps per i-group (alternate cluster pairs; fixed-order combine)
+constexpr int kGWarps = 4;   // warps (i-groups) per CTA
 constexpr int kGList = 256;  // per-warp chunk of surviving clusters (+1: odd-tail pad)
 constexpr int kGDepth = 4;   // staged cluster pairs in flight per warp (power of 2)
 
@@ -394,10 +185,7 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
   const float lim = ca.lim;
   const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
   const int n = s.n;
-  const int g0 = ((blockIdx.x * kGWarps + warp) / kGSplit) * kGR;  // the group's first slot
-  const int part = warp % kGSplit;
-  __shared__ double comb[kGWarps][kGR][3];
-  int eidx = -1;  // lanes < kGR: the row's external index
+  const int g0 = (blockIdx.x * kGWarps + warp) * kGR;  // the group's first slot
   int* __restrict__ wl = clist[warp];
   // sums over all visits: single species B12 = sum ir6^2, B6 = sum ir6
   // (a12 = c12 B12, a6 = c6 B6); mixtures sum a12, a6 directly
@@ -490,27 +278,28 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
         nl += __popc(cv);
       }
       if (nl == 0) break;
-      if (lane == 0) wl[nl] = ca.nc;  // odd tail: a cluster past the end (all j >= n)
+      // odd tail: a cluster past the end (all j >= n; staged from pos4's
+      // zeroed padding or the next replica, so every lane's r2 is finite)
+      if (lane == 0) wl[nl] = ca.nc;
       __syncwarp();
       const int nsteps = (nl + 1) >> 1;
-      int next = part;     // next pair to stage (this warp takes every kGSplit-th)
+      int next = 0;        // next pair to stage
       unsigned wslot = 0;  // its ring slot (bytes)
       auto issue = [&]() {
         const int e = 2 * next + half_sel;
-        if (next < nsteps && e < nl) cp_async16(ring + wslot, src0 + size_t(wl[e]) * (kCS * 32));
+        if (next < nsteps) cp_async16(ring + wslot, src0 + size_t(wl[e]) * (kCS * 32));
         cp_async_commit();
-        next += kGSplit;
+        ++next;
         wslot = (wslot + 512u) & (512u * kGDepth - 1u);
       };
 #pragma unroll
       for (int k = 0; k < kGDepth - 1; ++k) issue();
       const double4* rs = &stage[warp][0][0][jl];
-      int k = 0;
-      for (int st = part; st < nsteps; st += kGSplit, ++k) {
+      for (int st = 0; st < nsteps; ++st) {
         issue();
         cp_async_wait<kGDepth - 1>();
         __syncwarp();
-        const int slot = k & (kGDepth - 1);
+        const int slot = st & (kGDepth - 1);
         const int ja = wl[2 * st] * kCS + jl, jb = wl[2 * st + 1] * kCS + jl;
         const bool va = ja < ilim && ja != i;
         const bool vb = jb < ilim && jb != i;
@@ -533,28 +322,13 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
       fy += __shfl_xor_sync(full, fy, o);
       fz += __shfl_xor_sync(full, fz, o);
     }
-    if (lane < kGR) {
-      comb[warp][lane][0] = fx;
-      comb[warp][lane][1] = fy;
-      comb[warp][lane][2] = fz;
-      if (iv) eidx = ext_of(pi);
+    if (lane < kGR && iv) {
+      const size_t e = roff + ext_of(pi);
+      a.st.fx[e] = fx;
+      a.st.fy[e] = fy;
+      a.st.fz[e] = fz;
+      if (a.kick_dt > 0.0) fused_kick(a, e);
     }
-  }
-  // the group's kGSplit partial forces, summed in warp order
-  __syncthreads();
-  if (part == 0 && lane < kGR && eidx >= 0) {
-    double sx = comb[warp][lane][0], sy = comb[warp][lane][1], sz = comb[warp][lane][2];
-#pragma unroll
-    for (int p = 1; p < kGSplit; ++p) {
-      sx += comb[warp + p][lane][0];
-      sy += comb[warp + p][lane][1];
-      sz += comb[warp + p][lane][2];
-    }
-    const size_t e = roff + eidx;
-    a.st.fx[e] = sx;
-    a.st.fy[e] = sy;
-    a.st.fz[e] = sz;
-    if (a.kick_dt > 0.0) fused_kick(a, e);
   }
   // every pair was visited twice (bit-identical terms): halve the sums
   double A12 = 0.5 * warp_sum(B12), A6 = 0.5 * warp_sum(B6);

@@ -368,7 +368,7 @@ bool fast_min_image(const b2md_ctx* c) {
 // CTAs of the cluster-pair walk: kGWarps i-groups of kGR slots each
 int cpair_grid(const b2md_ctx* c) {
   const int groups = (c->t.n + kGR - 1) / kGR;
-  return (groups * kGSplit + kGWarps - 1) / kGWarps;
+  return (groups + kGWarps - 1) / kGWarps;
 }
 
 bool cluster_path(const b2md_ctx* c) {
@@ -385,48 +385,26 @@ int launch_cluster_force(b2md_ctx* c, bool kick) {
   ca.half = c->d_chalf;
   ca.sup_arcs = c->d_sarc;
   ca.sup_half = c->d_shalf;
-  ca.list = c->d_clist;
-  ca.count = c->d_ccount;
   const double ru = std::sqrt(c->t.rc2) * 4294967296.0 / c->t.box;
   ca.lim = float(ru * ru * (1.0 + 1e-5));
-  ca.lim_pair = float((ru + 4.0) * (ru + 4.0) * (1.0 + 1e-5));
-  const int R = c->R, tot = R * c->nc;
+  const int R = c->R;
   PROF(c, F_CLUSTER, (k_cluster_arcs<<<R * c->nsup, kSC * kCS, 0, c->stream>>>(ca, R)));
   ForceArgs a = force_args(c);
   if (kick) a.kick_dt = c->dt;
   const bool w = fast_min_image(c), m = c->t.ns > 1, v = a.vderiv != 0;
-  if (c->cluster_kernel == 1) {
-    dim3 pgrid(cpair_grid(c), R);
+  dim3 pgrid(cpair_grid(c), R);
 #define CPAIR_LAUNCH(M, W, V) \
   if (m == M && w == W && v == V) \
     PROF(c, F_FORCE, (k_force_cpair<M, W, V><<<pgrid, kGWarps * 32, 0, c->stream>>>(a, ca)));
-    CPAIR_LAUNCH(false, true, false)
-    CPAIR_LAUNCH(false, true, true)
-    CPAIR_LAUNCH(false, false, false)
-    CPAIR_LAUNCH(false, false, true)
-    CPAIR_LAUNCH(true, true, false)
-    CPAIR_LAUNCH(true, true, true)
-    CPAIR_LAUNCH(true, false, false)
-    CPAIR_LAUNCH(true, false, true)
+  CPAIR_LAUNCH(false, true, false)
+  CPAIR_LAUNCH(false, true, true)
+  CPAIR_LAUNCH(false, false, false)
+  CPAIR_LAUNCH(false, false, true)
+  CPAIR_LAUNCH(true, true, false)
+  CPAIR_LAUNCH(true, true, true)
+  CPAIR_LAUNCH(true, false, false)
+  CPAIR_LAUNCH(true, false, true)
 #undef CPAIR_LAUNCH
-    c->mask_valid = false;
-    return B2MD_OK;
-  }
-  PROF(c, F_CLUSTER, (k_cluster_list<<<(tot * 32 + 255) / 256, 256, 0, c->stream>>>(ca, R)));
-  dim3 grid(c->force_grid, R);
-  const int bs = c->force_warps * 32;
-#define CLUSTER_LAUNCH(M, W, V) \
-  if (m == M && w == W && v == V) \
-    PROF(c, F_FORCE, (k_force_cluster<M, W, V><<<grid, bs, 0, c->stream>>>(a, ca)));
-  CLUSTER_LAUNCH(false, true, false)
-  CLUSTER_LAUNCH(false, true, true)
-  CLUSTER_LAUNCH(false, false, false)
-  CLUSTER_LAUNCH(false, false, true)
-  CLUSTER_LAUNCH(true, true, false)
-  CLUSTER_LAUNCH(true, true, true)
-  CLUSTER_LAUNCH(true, false, false)
-  CLUSTER_LAUNCH(true, false, true)
-#undef CLUSTER_LAUNCH
   c->mask_valid = false;
   return B2MD_OK;
 }
@@ -1042,7 +1020,9 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   TRY(dalloc(&c->d_state, 13 * nt));
   TRY(dalloc(&c->d_fbuf, 6 * nt + size_t(kNumSums) * R));
   TRY(dalloc(&c->d_off, size_t(t.total_sites) * R));
-  TRY(dalloc(&c->d_pos4, nt + kCS));  // + a cluster: the cluster walk stages whole clusters
+  // + two clusters: the cluster walk stages whole clusters (and a pad cluster)
+  TRY(dalloc(&c->d_pos4, nt + 2 * kCS));
+  CU(cudaMemset(c->d_pos4, 0, sizeof(double4) * (nt + 2 * kCS)));
   TRY(dalloc(&c->d_stage, 6 * 4 * nt));
   TRY(dalloc(&c->d_mask, size_t(R) * c->g.n_pad * c->g.words));
   TRY(dalloc(&c->d_fixpos, nt));
@@ -1086,14 +1066,9 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     // (one launch less), but lengthens every warp's critical path when warps
     // own several rows (measured: cfg0/cfg1 +3-7%, cfg3/cfg4 -2-4%)
     c->use_fused_kick = size_t(t.n) * R < 4096;
-    if (c->nc > 0) {
-      // B2MD_CLUSTER_KERNEL=0: the row walk (k_force_cluster, measurement only)
-      c->cluster_kernel = 1;
-      if (const char* e = std::getenv("B2MD_CLUSTER_KERNEL")) c->cluster_kernel = std::atoi(e);
-      // the cluster-pair walk ends with 4 rows per warp written by 4 lanes:
-      // the kick costs those lanes a few loads, not a serial row epilogue
-      if (c->cluster_kernel == 1) c->use_fused_kick = true;
-    }
+    // the cluster-pair walk ends with 4 rows per warp written by 4 lanes:
+    // the kick costs those lanes a few loads, not a serial row epilogue
+    if (c->nc > 0) c->use_fused_kick = true;
     if (const char* e = std::getenv("B2MD_FUSED_KICK")) c->use_fused_kick = std::atoi(e) != 0;
   }
   TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars *
@@ -1104,10 +1079,6 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     TRY(dalloc(&c->d_chalf, size_t(R) * c->nc));
     TRY(dalloc(&c->d_sarc, size_t(R) * c->nsup));
     TRY(dalloc(&c->d_shalf, size_t(R) * c->nsup));
-    if (c->cluster_kernel == 0) {
-      TRY(dalloc(&c->d_clist, size_t(R) * c->nc * c->nc));
-      TRY(dalloc(&c->d_ccount, size_t(R) * c->nc));
-    }
   }
   TRY(dalloc(&c->d_ticket, size_t(2) * R));
   TRY(dalloc(&c->d_flux, size_t(kNumSums) * R));
@@ -1245,8 +1216,8 @@ void free_ctx(b2md_ctx* c) {
                   c->d_q_site, c->d_q_val,     c->d_mol_qbegin, c->d_kv,    c->d_etab,  c->d_S,
                   c->d_uk,    c->d_flux,  c->d_perm, c->d_slot_of, c->d_sp_slot, c->d_sb_slot,
                   c->d_nsites_slot, c->d_scan, c->d_keys[0], c->d_keys[1], c->d_vals[0],
-                  c->d_vals[1], c->d_cub, c->d_ke, c->d_thermo_err, c->d_carc, c->d_clist,
-                  c->d_ccount, c->d_chalf, c->d_sarc, c->d_shalf};
+                  c->d_vals[1], c->d_cub, c->d_ke, c->d_thermo_err, c->d_carc,
+                  c->d_chalf, c->d_sarc, c->d_shalf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);

@@ -117,9 +117,6 @@ struct b2md_ctx {
   float4* d_chalf = nullptr;  // R * nc arc half extents
   uint4* d_sarc = nullptr;    // R * nsup
   float4* d_shalf = nullptr;  // R * nsup
-  int cluster_kernel = 1;     // 1: cluster-pair walk (k_force_cpair), 0: row walk
-  int* d_clist = nullptr;     // R * nc * nc
-  int* d_ccount = nullptr;    // R * nc
   double* d_cta_part = nullptr;  // force-kernel per-CTA scalar partials
   unsigned* d_ticket = nullptr;   // 2 * R: force, ewald
   int force_grid = 1;

@@ -683,22 +683,29 @@ __device__ void finalize_scalars(const double* v /* NS values, valid on lane 0 o
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // fixed-order totals; __ldcg (L2, not a possibly stale L1) lets the loads
-  // of a thread's column slice be in flight together
-  for (int k = 0; k < NS; ++k) {
-    const double* col = cta_part + (size_t(r) * NS + k) * nblk;
-    double t = 0.0;
-#pragma unroll 4
-    for (int b = threadIdx.x; b < nblk; b += blockDim.x) t += __ldcg(col + b);
-    t = warp_sum(t);
-    __syncthreads();
-    if (lane == 0) red[warp][0] = t;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tt = 0.0;
-      for (int w = 0; w < nw; ++w) tt += red[w][0];
-      sums[size_t(r) * kNumSums + sum_offset + k] = tt;
-    }
+  // fixed-order totals: every thread sums its strided slice of all NS
+  // columns at once (__ldcg: L2, not a possibly stale L1; all loads in
+  // flight together), then one fixed shuffle tree and warp-order sum
+  double t[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) t[k] = 0.0;
+  const double* base = cta_part + size_t(r) * NS * nblk;
+#pragma unroll 2
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) t[k] += __ldcg(base + size_t(k) * nblk + b);
+  }
+#pragma unroll
+  for (int k = 0; k < NS; ++k) t[k] = warp_sum(t[k]);
+  __syncthreads();  // red is reused
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NS; ++k) red[warp][k] = t[k];
+  __syncthreads();
+  if (threadIdx.x < NS) {
+    double tt = 0.0;
+    for (int w = 0; w < nw; ++w) tt += red[w][threadIdx.x];
+    sums[size_t(r) * kNumSums + sum_offset + threadIdx.x] = tt;
   }
   if (threadIdx.x == 0) ticket[r] = 0u;  // re-armed for the next launch / graph replay
 }
