@@ -66,17 +66,20 @@ __device__ __forceinline__ float arc_half(int mn, int mx) {
 // shuffle), the super-cluster the whole CTA (offsets to its first slot,
 // warp REDUX then shared memory).  A member outside [0, L) (fixed point
 // saturated) makes its arcs whole-circle: never culled.
-static __global__ void __launch_bounds__(kSC * kCS) k_cluster_arcs(ClusterArgs a, int R) {
+// The arcs of one super-cluster's clusters and of the super-cluster itself
+// from the fixed-point position u of slot sc * 256 + threadIdx.x (valid: the
+// slot exists).  Called by all 256 threads of the CTA.
+__device__ __forceinline__ void cluster_arcs_block(const ClusterArgs& a, int r, int sc, uint4 u,
+                                                   bool valid) {
   static_assert(kSC * kCS == 256 && kCS == 8, "one CTA of 256 slots per super-cluster");
   __shared__ int red[8][6];
   __shared__ int sin_[8];
-  const int r = blockIdx.x / a.nsup, sc = blockIdx.x - r * a.nsup;
+  __shared__ uint4 anchor;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint4* f = a.fixpos + size_t(r) * a.n;
-  const int k = sc * kSC * kCS + threadIdx.x;  // slot
-  const bool valid = k < a.n;
-  const uint4 wa = f[sc * kSC * kCS];           // super-cluster anchor
-  const uint4 u = f[valid ? k : sc * kSC * kCS];
+  if (threadIdx.x == 0) anchor = u;  // slot sc * 256 always exists
+  __syncthreads();
+  const uint4 wa = anchor;           // super-cluster anchor
+  if (!valid) u = wa;
   const unsigned full = 0xffffffffu;
   const int src = lane & ~(kCS - 1);
   const uint4 u0 = make_uint4(__shfl_sync(full, u.x, src), __shfl_sync(full, u.y, src),
@@ -93,7 +96,7 @@ static __global__ void __launch_bounds__(kSC * kCS) k_cluster_arcs(ClusterArgs a
     mnz = min(mnz, __shfl_xor_sync(full, mnz, o)), mxz = max(mxz, __shfl_xor_sync(full, mxz, o));
     in &= __shfl_xor_sync(full, in, o);
   }
-  const int cl = k / kCS;
+  const int cl = (sc * kSC * kCS + threadIdx.x) / kCS;
   if ((lane & (kCS - 1)) == 0 && cl < a.nc) {
     const size_t g = size_t(r) * a.nc + cl;
     a.arcs[g] = make_uint4(arc_centre(u0.x, mnx, mxx), arc_centre(u0.y, mny, mxy),
@@ -130,6 +133,42 @@ static __global__ void __launch_bounds__(kSC * kCS) k_cluster_arcs(ClusterArgs a
                                          arc_half(m[4], m[5]), 0.0f)
                            : make_float4(3e9f, 3e9f, 3e9f, 0.0f);
   }
+}
+
+// One CTA per (replica, super-cluster), one thread per slot: arcs from the
+// staged fixed-point positions (after a re-sort or a state upload).
+static __global__ void __launch_bounds__(kSC * kCS) k_cluster_arcs(ClusterArgs a, int R) {
+  const int r = blockIdx.x / a.nsup, sc = blockIdx.x - r * a.nsup;
+  const int k = sc * kSC * kCS + threadIdx.x;  // slot
+  const bool valid = k < a.n;
+  const uint4 u = a.fixpos[size_t(r) * a.n + (valid ? k : sc * kSC * kCS)];
+  cluster_arcs_block(a, r, sc, u, valid);
+}
+
+// The step's first half (k_kick_drift, or the end-of-step kick fused with
+// the next drift, k_kick_kick_drift) over slot-ordered threads, with the
+// cluster arcs of the new positions in the same launch: one CTA per
+// (replica, super-cluster), thread = slot, molecule perm[slot].  A frozen
+// state (failed step) only re-derives the arcs.
+template <bool KICK_FIRST>
+static __global__ void __launch_bounds__(kSC * kCS) k_step_drift_arcs(StepArgs sa, ClusterArgs a) {
+  const int r = blockIdx.x / a.nsup, sc = blockIdx.x - r * a.nsup;
+  const int k = sc * kSC * kCS + threadIdx.x;  // slot
+  const bool valid = k < a.n;
+  const size_t p = size_t(r) * a.n + (valid ? k : sc * kSC * kCS);
+  uint4 u;
+  const int gid = r * a.n + sa.s.perm[p];  // loaded with the error flag
+  if (valid && *sa.error_mol == 0x7fffffff) {
+    bool ok = true;
+    if constexpr (KICK_FIRST) {
+      ok = kick_one(sa, gid);
+      if (!ok) atomicMin(sa.error_mol, gid);
+    }
+    u = ok ? kick_drift_one(sa, gid) : a.fixpos[p];
+  } else {
+    u = a.fixpos[p];
+  }
+  cluster_arcs_block(a, r, sc, u, valid);
 }
 
 // ---------------------------------------------------------------------------

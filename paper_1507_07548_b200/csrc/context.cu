@@ -375,7 +375,7 @@ bool cluster_path(const b2md_ctx* c) {
   return c->use_cluster && c->nc > 0 && c->t.single_site_path && c->world <= 1;
 }
 
-int launch_cluster_force(b2md_ctx* c, bool kick) {
+ClusterArgs cluster_args(const b2md_ctx* c) {
   ClusterArgs ca;
   ca.n = c->t.n;
   ca.nc = c->nc;
@@ -387,8 +387,22 @@ int launch_cluster_force(b2md_ctx* c, bool kick) {
   ca.sup_half = c->d_shalf;
   const double ru = std::sqrt(c->t.rc2) * 4294967296.0 / c->t.box;
   ca.lim = float(ru * ru * (1.0 + 1e-5));
+  return ca;
+}
+
+// Cluster arcs are derived wherever fixed-point positions are written: by
+// the step's drift kernel (k_step_drift_arcs) and, here, after staging (a
+// re-sort, evaluate / set_state / restore).
+int launch_cluster_arcs(b2md_ctx* c) {
+  if (!cluster_path(c)) return B2MD_OK;
+  const ClusterArgs ca = cluster_args(c);
+  PROF(c, F_CLUSTER, (k_cluster_arcs<<<c->R * c->nsup, kSC * kCS, 0, c->stream>>>(ca, c->R)));
+  return B2MD_OK;
+}
+
+int launch_cluster_force(b2md_ctx* c, bool kick) {
+  const ClusterArgs ca = cluster_args(c);
   const int R = c->R;
-  PROF(c, F_CLUSTER, (k_cluster_arcs<<<R * c->nsup, kSC * kCS, 0, c->stream>>>(ca, R)));
   ForceArgs a = force_args(c);
   if (kick) a.kick_dt = c->dt;
   const bool w = fast_min_image(c), m = c->t.ns > 1, v = a.vderiv != 0;
@@ -555,6 +569,7 @@ int resort_and_stage(b2md_ctx* c) {
       c->st.px, c->st.py, c->st.pz, nt, c->t.n, c->d_slot_of, c->t.box, 4294967296.0 / c->t.box,
       c->d_fixpos, c->st.pos4);
   CU(cudaGetLastError());
+  TRY(launch_cluster_arcs(c));
   return B2MD_OK;
 }
 
@@ -571,6 +586,7 @@ int enqueue_forces(b2md_ctx* c, bool offsets, bool kick) {
         c->st.px, c->st.py, c->st.pz, nt, c->t.n, c->d_slot_of, c->t.box,
         4294967296.0 / c->t.box, c->d_fixpos, c->st.pos4);
     CU(cudaGetLastError());
+    TRY(launch_cluster_arcs(c));
   }
   if (!cluster_path(c)) TRY(launch_search(c));
   TRY(launch_force(c, kick));
@@ -602,6 +618,14 @@ int launch_step_kernel(b2md_ctx* c, int fam) {
   const int nt = n_total(c);
   // small CTAs: 16k molecules must still spread over all 148 SMs
   const int bs = 64, g = (nt + bs - 1) / bs;
+  if (fam != F_KICK && cluster_path(c)) {  // slot-ordered, with the cluster arcs
+    const ClusterArgs ca = cluster_args(c);
+    if (fam == F_KICK_DRIFT)
+      PROF(c, fam, (k_step_drift_arcs<false><<<c->R * c->nsup, kSC * kCS, 0, c->stream>>>(a, ca)));
+    else
+      PROF(c, fam, (k_step_drift_arcs<true><<<c->R * c->nsup, kSC * kCS, 0, c->stream>>>(a, ca)));
+    return B2MD_OK;
+  }
   if (fam == F_KICK_DRIFT)
     PROF(c, fam, (k_kick_drift<<<g, bs, 0, c->stream>>>(a)));
   else if (fam == F_KICK)

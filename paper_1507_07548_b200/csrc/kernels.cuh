@@ -77,7 +77,7 @@ static __global__ void k_offsets(SysDev s, StateDev st) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= s.n * s.R) return;
   const int r = gid / s.n, i = gid - r * s.n;
-  const DevSpecies& sp = s.tab->species[s.species_of[i]];
+  const DevSpecies& sp = s.tab->species[s.ns == 1 ? 0 : s.species_of[i]];
   const int base = r * s.total_sites + s.sb_slot[size_t(r) * s.n + s.slot_of[gid]];
   if (sp.centred) {
     st.off[base] = make_double4(0.0, 0.0, 0.0, 0.0);
@@ -1608,10 +1608,11 @@ static __global__ void k_stage_positions(const double* px, const double* py, con
 }
 
 // engine.cpp:107-127 (+ build_scene offsets for the new orientation)
-__device__ __forceinline__ void kick_drift_one(const StepArgs& a, int gid) {
+// returns the new fixed-point position (zero without a.fixpos)
+__device__ __forceinline__ uint4 kick_drift_one(const StepArgs& a, int gid) {
   const SysDev& s = a.s;
   const int r = gid / s.n, i = gid - r * s.n;
-  const DevSpecies& sp = s.tab->species[s.species_of[i]];
+  const DevSpecies& sp = s.tab->species[s.ns == 1 ? 0 : s.species_of[i]];
   const double dt = a.dt, half = mul(0.5, dt);
   const double c = __ddiv_rn(half, sp.total_mass);
   const double vx = add(a.st.vx[gid], mul(a.st.fx[gid], c));
@@ -1650,7 +1651,11 @@ __device__ __forceinline__ void kick_drift_one(const StepArgs& a, int gid) {
   a.st.pz[gid] = pz;
   const size_t slot = size_t(r) * s.n + s.slot_of[gid];
   a.st.pos4[slot] = pack_pos(px, py, pz, i);
-  if (a.fixpos) a.fixpos[slot] = fix_position(px, py, pz, s.mi.L, a.fix_scale);
+  uint4 fix = make_uint4(0u, 0u, 0u, 0u);
+  if (a.fixpos) {
+    fix = fix_position(px, py, pz, s.mi.L, a.fix_scale);
+    a.fixpos[slot] = fix;
+  }
   if (a.write_offsets) {
     const int base = r * s.total_sites + s.sb_slot[slot];
     if (sp.centred) {
@@ -1662,13 +1667,14 @@ __device__ __forceinline__ void kick_drift_one(const StepArgs& a, int gid) {
       }
     }
   }
+  return fix;
 }
 
 // engine.cpp:131-142; returns check_finite (model.cpp:288-302)
 __device__ __forceinline__ bool kick_one(const StepArgs& a, int gid) {
   const SysDev& s = a.s;
   const int i = gid % s.n;
-  const DevSpecies& sp = s.tab->species[s.species_of[i]];
+  const DevSpecies& sp = s.tab->species[s.ns == 1 ? 0 : s.species_of[i]];
   const double half = mul(0.5, a.dt);
   const double c = __ddiv_rn(half, sp.total_mass);
   const double vx = add(a.st.vx[gid], mul(a.st.fx[gid], c));
@@ -1803,7 +1809,7 @@ static __global__ void __launch_bounds__(kKeThreads) k_kinetic(SysDev s, StateDe
   double kt = 0.0, kr = 0.0;
   for (int i = tid; i < s.n; i += kKeThreads) {
     const size_t g = size_t(r) * s.n + i;
-    const DevSpecies& sp = s.tab->species[s.species_of[i]];
+    const DevSpecies& sp = s.tab->species[s.ns == 1 ? 0 : s.species_of[i]];
     kt += 0.5 * sp.total_mass * norm2_exact(st.vx[g], st.vy[g], st.vz[g]);
     const double wx = st.wx[g], wy = st.wy[g], wz = st.wz[g];
     kr += 0.5 * (sp.inertia[0] * wx * wx + sp.inertia[1] * wy * wy + sp.inertia[2] * wz * wz);
