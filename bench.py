@@ -578,7 +578,16 @@ def main():
     force_ms, force_launches = kt_force.get("force", (0.0, 0))
     avg_force_s = force_ms * 1e-3 / max(1, force_launches)
     single_site = all(sp.n_sites == 1 for sp in wl.comp.species)
-    if single_site:
+    cand = n * (n - 1) // 2 * R
+    # cluster walk: no search launches -- the force kernel decides every
+    # candidate pair itself (partner search fused into the LJ kernel), so its
+    # algorithmic work is the search's plus the forces'
+    fused_search = single_site and kt_search.get("search", (0.0, 0))[1] == 0
+    if fused_search:
+        force_flop = cand * FLOP_CANDIDATE + pairs_total * FLOP_LJ_SINGLE
+        force_note = (f"k_force_cpair: partner search fused with LJ; {FLOP_CANDIDATE} flop per "
+                      f"candidate pair i<j decided + {FLOP_LJ_SINGLE} per pair in cutoff")
+    elif single_site:
         force_flop = pairs_total * FLOP_LJ_SINGLE
         force_note = f"{FLOP_LJ_SINGLE} flop per single-site LJ pair in cutoff"
     else:
@@ -587,17 +596,19 @@ def main():
         force_note = f"(2 + 86 x {terms} terms) flop per passing molecule pair (upper bound)"
     achieved = force_flop / avg_force_s / 1e12 if avg_force_s > 0 else 0.0
     traffic = None
+    executed = None
     prof = ROOT / "profiles" / f"ncu_{args.config}_force.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            pj = json.loads(prof.read_text())
+            traffic = pj.get("dram_bytes_per_launch")
+            executed = pj.get("fp64_pipe_pct")
         except Exception:
             traffic = None
     # partner search: share of the step and the tiles the bounding-arc cull kept
     search_ms, search_launches = kt_search.get("search", (0.0, 0))
     avg_search_s = search_ms * 1e-3 / max(1, search_launches)
-    cand = n * (n - 1) // 2 * R
-    kept = tile_cull_kept_fraction(eng, wl) if single_site and R == 1 else None
+    kept = tile_cull_kept_fraction(eng, wl) if single_site and R == 1 and not fused_search else None
     step_s = total_ms * 1e-3 / args.steps
     fp64_step = ((cand * FLOP_CANDIDATE + pairs_total * FLOP_LJ_SINGLE) / step_s / 1e12 / peak
                  if single_site and world == 1 else None)
@@ -641,16 +652,25 @@ def main():
             "peak_source": "DFMA microbenchmark measured in this run (MEASURED_PEAKS.json has no fp64 entry)",
             "launch_ms": avg_force_s * 1e3,
             "share_of_step": avg_force_s / max(1e-12, step_s),
+            "fp64_pipe_pct_executed": executed,
+            "executed_note": "ncu sm__pipe_fp64_cycles_active of the same kernel (profiles/): the fp64 "
+                             "work actually issued, vs the algorithmic count above",
             "launch_timing": "CUDA events around the force kernel only, in a second K-step pass "
                              "(same graph step structure); ncu launch list in profiles/",
         },
-        "search": {
+        "search": ({
+            "launch_ms": None,
+            "candidates": cand,
+            "note": "fused into the force kernel (cluster walk): clusters of 8 slots whose bounding "
+                    "arcs are > rc apart are skipped (exact); the rest are decided on the "
+                    "reference's fp64 r2 per pair",
+        } if fused_search else {
             "launch_ms": avg_search_s * 1e3,
             "share_of_step": avg_search_s / max(1e-12, step_s),
             "candidates": cand,
             "tile_cull_kept_fraction": kept,
             "note": "32x32 tiles whose blocks' bounding arcs are > rmax apart are skipped (exact)",
-        },
+        }),
         "fp64_fraction_step": fp64_step,
         "fp64_fraction_step_def": "(all n(n-1)/2 candidates x 17 + pairs in cutoff x 32) flop per "
                                   "step / device step time / fp64 peak (SURVEY.md 8(d) convention; "
