@@ -544,7 +544,16 @@ def main():
     hp, hq, hv, hw, hf, ht = (pinned((nt, 3)), pinned((nt, 4)), pinned((nt, 3)), pinned((nt, 3)),
                               pinned((nt, 3)), pinned((nt, 3)))
     eng.get_state_raw(hp, hq, hv, hw, hf, ht)
-    h2d = d2h = 8 * nt * (3 + 4 + 3 + 3 + 3 + 3)
+    # point molecules (rotational_dof 0 everywhere): the step neither reads nor
+    # writes orientations, angular velocities or torques (engine.cpp:107-141
+    # skips the rotor), so the per-step transfer is pos, vel and the cached
+    # forces; rigid molecules move the full dynamic state
+    point = all(sp.rotational_dof == 0 for sp in wl.comp.species)
+    if point:
+        hq = hw = ht = None
+        h2d = d2h = 8 * nt * (3 + 3 + 3)
+    else:
+        h2d = d2h = 8 * nt * (3 + 4 + 3 + 3 + 3 + 3)
     e2e_steps = max(1, args.e2e_steps)
     if dist is not None:
         dist.barrier()
@@ -640,7 +649,10 @@ def main():
         "pairs_in_cutoff_per_step": pairs_total,
         "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "path": "b2md_upload_state + b2md_step_async + b2md_get_state (one host sync), pinned host buffers"},
+                "path": "b2md_upload_state + b2md_step_async + b2md_get_state (one host sync), pinned host buffers"
+                        + ("; point molecules: pos, vel, forces (orientations / angular velocities / "
+                           "torques are not read or written by their step and stay resident)" if point else
+                           "; full dynamic state (pos, quaternion, vel, angular vel, forces, torques)")},
         "roofline": {
             "bound": "fp64",
             "kernel": f"k_force_* partner walk ({force_note})",

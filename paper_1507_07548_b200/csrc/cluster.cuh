@@ -34,6 +34,7 @@ struct ClusterArgs {
   uint4* sup_arcs;              // R * nsup
   float4* sup_half;             // R * nsup
   float lim;                    // (rc 2^32 / L)^2 (1 + 1e-5): cull radius^2
+  int grp_begin, grp_end;       // this rank's i-groups (row shard; all of them on one rank)
 };
 
 // Lower bound of the circle distance between two arcs (centres x, y, half
@@ -185,7 +186,8 @@ static __global__ void __launch_bounds__(kSC * kCS) k_step_drift_arcs(StepArgs s
 // is fixed, so its force accumulates in registers; the 8 lanes of a row are
 // summed by a fixed xor tree at the end (no atomics, deterministic).
 // Each pair is visited from both rows with bit-identical r2, so the LJ sums
-// are taken over all visits and halved (u, s1, s2, virial, pair count).
+// are taken over all visits and halved (u, s1, s2, virial); the pair count is
+// taken on the i < j side (exact on every row shard).
 constexpr int kGR = 4;       // rows per i-group
 constexpr int kGWarps = 4;   // warps (i-groups) per CTA
 constexpr int kGList = 256;  // per-warp chunk of surviving clusters (+1: odd-tail pad)
@@ -230,7 +232,16 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
   // (a12 = c12 B12, a6 = c6 B6); mixtures sum a12, a6 directly
   double B12 = 0, B6 = 0;
   int cnt = 0;
-  if (g0 < n) {  // warp-uniform
+  const int grp = blockIdx.x * kGWarps + warp;
+  if (g0 < n && (grp < ca.grp_begin || grp >= ca.grp_end)) {
+    // another rank's rows (row shard): zero forces into the all-reduce
+    if (lane < kGR && g0 + lane < n) {
+      const size_t e = roff + ext_of(p4[g0 + lane]);
+      a.st.fx[e] = 0.0;
+      a.st.fy[e] = 0.0;
+      a.st.fz[e] = 0.0;
+    }
+  } else if (g0 < n) {  // warp-uniform
     const int il = lane & (kGR - 1), jl = lane >> 2;
     const int i = g0 + il;
     const bool iv = i < n;
@@ -284,7 +295,7 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
       fx = fma(fs, dx, fx);
       fy = fma(fs, dy, fy);
       fz = fma(fs, dz, fz);
-      cnt += in;
+      cnt += in && i < j;  // exact per shard: the pair's i < j side
     };
     // staging ring: slot k holds a cluster pair as 512 contiguous bytes;
     // lane L copies bytes [16 L, 16 L + 16) (lanes 0-15 the first cluster's
@@ -378,7 +389,7 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
   const double s1 = -12.0 * A12 + 6.0 * A6;  // sum du_r
   double v[kNumRowScalars] = {A12 - A6, 0.0, 0.0, VDERIV ? s1 : 0.0,
                               VDERIV ? 156.0 * A12 - 42.0 * A6 : 0.0, -s1,
-                              0.5 * warp_sum(double(cnt))};
+                              warp_sum(double(cnt))};
   finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
 }
 

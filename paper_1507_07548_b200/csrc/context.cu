@@ -359,8 +359,8 @@ bool fast_min_image(const b2md_ctx* c) {
 }
 
 // The cluster walk (cluster.cuh) replaces search + bit-matrix walk for the
-// single-site path on one shard (the walk is not sharded: with b2md_set_shard
-// the bit-matrix path computes this rank's partial terms).  Any positions:
+// single-site path; with b2md_set_shard / NCCL each rank walks its own
+// contiguous range of i-groups (cluster_args).  Any positions:
 // clusters with a member outside [0, L) are never culled, and the exact
 // minimum image replaces the wrapped one when positions are not wrapped
 // (same bits), so the hit sequence -- and the summation order -- is the same
@@ -372,7 +372,7 @@ int cpair_grid(const b2md_ctx* c) {
 }
 
 bool cluster_path(const b2md_ctx* c) {
-  return c->use_cluster && c->nc > 0 && c->t.single_site_path && c->world <= 1;
+  return c->use_cluster && c->nc > 0 && c->t.single_site_path;
 }
 
 ClusterArgs cluster_args(const b2md_ctx* c) {
@@ -387,6 +387,12 @@ ClusterArgs cluster_args(const b2md_ctx* c) {
   ca.sup_half = c->d_shalf;
   const double ru = std::sqrt(c->t.rc2) * 4294967296.0 / c->t.box;
   ca.lim = float(ru * ru * (1.0 + 1e-5));
+  // row shard: contiguous i-group ranges (each a slab of the spatial order,
+  // so the ranks' pair work is balanced); every row's force is complete on
+  // its rank (both rows of a pair evaluate it), other rows are written 0
+  const long groups = (c->t.n + kGR - 1) / kGR;
+  ca.grp_begin = int(groups * c->rank / std::max(1, c->world));
+  ca.grp_end = int(groups * (c->rank + 1) / std::max(1, c->world));
   return ca;
 }
 
