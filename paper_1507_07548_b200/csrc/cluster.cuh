@@ -157,17 +157,18 @@ static __global__ void __launch_bounds__(kSC * kCS) k_step_drift_arcs(StepArgs s
   const int k = sc * kSC * kCS + threadIdx.x;  // slot
   const bool valid = k < a.n;
   const size_t p = size_t(r) * a.n + (valid ? k : sc * kSC * kCS);
-  uint4 u;
-  const int gid = r * a.n + sa.s.perm[p];  // loaded with the error flag
-  if (valid && *sa.error_mol == 0x7fffffff) {
-    bool ok = true;
+  uint4 u = a.fixpos[p];  // kept when frozen or failing
+  if (valid) {
+    const int gid = r * a.n + sa.s.perm[p];
+    bool frozen = false, ok = true;
     if constexpr (KICK_FIRST) {
-      ok = kick_one(sa, gid);
+      ok = kick_one(sa, gid, &frozen);
       if (!ok) atomicMin(sa.error_mol, gid);
+      if (ok && !frozen) u = kick_drift_one(sa, gid);
+    } else {
+      const uint4 f = kick_drift_one(sa, gid, &frozen);
+      if (!frozen) u = f;
     }
-    u = ok ? kick_drift_one(sa, gid) : a.fixpos[p];
-  } else {
-    u = a.fixpos[p];
   }
   cluster_arcs_block(a, r, sc, u, valid);
 }

@@ -1618,26 +1618,39 @@ static __global__ void k_stage_positions(const double* px, const double* py, con
 
 // engine.cpp:107-127 (+ build_scene offsets for the new orientation)
 // returns the new fixed-point position (zero without a.fixpos)
-__device__ __forceinline__ uint4 kick_drift_one(const StepArgs& a, int gid) {
+__device__ __forceinline__ uint4 kick_drift_one(const StepArgs& a, int gid, bool* frozen = nullptr) {
   const SysDev& s = a.s;
   const int r = gid / s.n, i = gid - r * s.n;
+  // every input first (independent loads in flight together -- after an L2
+  // flush each dependent round trip is a DRAM latency), then the error flag,
+  // then the stores
+  const int err = frozen ? *a.error_mol : 0x7fffffff;
   const DevSpecies& sp = s.tab->species[s.ns == 1 ? 0 : s.species_of[i]];
+  const double vx0 = a.st.vx[gid], vy0 = a.st.vy[gid], vz0 = a.st.vz[gid];
+  const double fx0 = a.st.fx[gid], fy0 = a.st.fy[gid], fz0 = a.st.fz[gid];
+  const double px0 = a.st.px[gid], py0 = a.st.py[gid], pz0 = a.st.pz[gid];
+  double q[4] = {a.st.qw[gid], a.st.qx[gid], a.st.qy[gid], a.st.qz[gid]};
+  const double tx0 = a.st.tx[gid], ty0 = a.st.ty[gid], tz0 = a.st.tz[gid];
+  const double w[3] = {a.st.wx[gid], a.st.wy[gid], a.st.wz[gid]};
+  const size_t slot = size_t(r) * s.n + s.slot_of[gid];
   const double dt = a.dt, half = mul(0.5, dt);
   const double c = __ddiv_rn(half, sp.total_mass);
-  const double vx = add(a.st.vx[gid], mul(a.st.fx[gid], c));
-  const double vy = add(a.st.vy[gid], mul(a.st.fy[gid], c));
-  const double vz = add(a.st.vz[gid], mul(a.st.fz[gid], c));
+  const double vx = add(vx0, mul(fx0, c));
+  const double vy = add(vy0, mul(fy0, c));
+  const double vz = add(vz0, mul(fz0, c));
+  double px = add(px0, mul(vx, dt));
+  double py = add(py0, mul(vy, dt));
+  double pz = add(pz0, mul(vz, dt));
+  if (frozen) {
+    *frozen = err != 0x7fffffff;  // state frozen after a failed step
+    if (*frozen) return make_uint4(0u, 0u, 0u, 0u);
+  }
   a.st.vx[gid] = vx;
   a.st.vy[gid] = vy;
   a.st.vz[gid] = vz;
-  double px = add(a.st.px[gid], mul(vx, dt));
-  double py = add(a.st.py[gid], mul(vy, dt));
-  double pz = add(a.st.pz[gid], mul(vz, dt));
-  double q[4] = {a.st.qw[gid], a.st.qx[gid], a.st.qy[gid], a.st.qz[gid]};
   if (sp.rotational_dof > 0) {
-    const D3 tb = rotate_inv_exact(q[0], q[1], q[2], q[3], {a.st.tx[gid], a.st.ty[gid], a.st.tz[gid]});
+    const D3 tb = rotate_inv_exact(q[0], q[1], q[2], q[3], {tx0, ty0, tz0});
     const double tbv[3] = {tb.x, tb.y, tb.z};
-    const double w[3] = {a.st.wx[gid], a.st.wy[gid], a.st.wz[gid]};
     double L[3];
     for (int k = 0; k < 3; ++k)
       L[k] = sp.inertia[k] > 0.0 ? add(mul(sp.inertia[k], w[k]), mul(half, tbv[k])) : 0.0;
@@ -1658,7 +1671,6 @@ __device__ __forceinline__ uint4 kick_drift_one(const StepArgs& a, int gid) {
   a.st.px[gid] = px;
   a.st.py[gid] = py;
   a.st.pz[gid] = pz;
-  const size_t slot = size_t(r) * s.n + s.slot_of[gid];
   a.st.pos4[slot] = pack_pos(px, py, pz, i);
   uint4 fix = make_uint4(0u, 0u, 0u, 0u);
   if (a.fixpos) {
@@ -1680,22 +1692,32 @@ __device__ __forceinline__ uint4 kick_drift_one(const StepArgs& a, int gid) {
 }
 
 // engine.cpp:131-142; returns check_finite (model.cpp:288-302)
-__device__ __forceinline__ bool kick_one(const StepArgs& a, int gid) {
+__device__ __forceinline__ bool kick_one(const StepArgs& a, int gid, bool* frozen = nullptr) {
   const SysDev& s = a.s;
   const int i = gid % s.n;
+  // inputs first, then the error flag, then the stores (kick_drift_one)
+  const int err = frozen ? *a.error_mol : 0x7fffffff;
   const DevSpecies& sp = s.tab->species[s.ns == 1 ? 0 : s.species_of[i]];
+  const double vx0 = a.st.vx[gid], vy0 = a.st.vy[gid], vz0 = a.st.vz[gid];
+  const double fx0 = a.st.fx[gid], fy0 = a.st.fy[gid], fz0 = a.st.fz[gid];
+  const double px = a.st.px[gid], py = a.st.py[gid], pz = a.st.pz[gid];
+  const double qw = a.st.qw[gid], qx = a.st.qx[gid], qy = a.st.qy[gid], qz = a.st.qz[gid];
+  const double tx = a.st.tx[gid], ty = a.st.ty[gid], tz = a.st.tz[gid];
+  double w0 = a.st.wx[gid], w1 = a.st.wy[gid], w2 = a.st.wz[gid];
   const double half = mul(0.5, a.dt);
   const double c = __ddiv_rn(half, sp.total_mass);
-  const double vx = add(a.st.vx[gid], mul(a.st.fx[gid], c));
-  const double vy = add(a.st.vy[gid], mul(a.st.fy[gid], c));
-  const double vz = add(a.st.vz[gid], mul(a.st.fz[gid], c));
+  const double vx = add(vx0, mul(fx0, c));
+  const double vy = add(vy0, mul(fy0, c));
+  const double vz = add(vz0, mul(fz0, c));
+  if (frozen) {
+    *frozen = err != 0x7fffffff;
+    if (*frozen) return true;
+  }
   a.st.vx[gid] = vx;
   a.st.vy[gid] = vy;
   a.st.vz[gid] = vz;
-  double w0 = a.st.wx[gid], w1 = a.st.wy[gid], w2 = a.st.wz[gid];
   if (sp.rotational_dof > 0) {
-    const D3 tb = rotate_inv_exact(a.st.qw[gid], a.st.qx[gid], a.st.qy[gid], a.st.qz[gid],
-                                   {a.st.tx[gid], a.st.ty[gid], a.st.tz[gid]});
+    const D3 tb = rotate_inv_exact(qw, qx, qy, qz, {tx, ty, tz});
     if (sp.inertia[0] > 0.0) w0 = add(w0, __ddiv_rn(mul(half, tb.x), sp.inertia[0]));
     if (sp.inertia[1] > 0.0) w1 = add(w1, __ddiv_rn(mul(half, tb.y), sp.inertia[1]));
     if (sp.inertia[2] > 0.0) w2 = add(w2, __ddiv_rn(mul(half, tb.z), sp.inertia[2]));
@@ -1703,9 +1725,8 @@ __device__ __forceinline__ bool kick_one(const StepArgs& a, int gid) {
     a.st.wy[gid] = w1;
     a.st.wz[gid] = w2;
   }
-  return isfinite(a.st.px[gid]) && isfinite(a.st.py[gid]) && isfinite(a.st.pz[gid]) &&
-         isfinite(vx) && isfinite(vy) && isfinite(vz) && isfinite(w0) && isfinite(w1) &&
-         isfinite(w2) && isfinite(a.st.qw[gid]);
+  return isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(vx) && isfinite(vy) &&
+         isfinite(vz) && isfinite(w0) && isfinite(w1) && isfinite(w2) && isfinite(qw);
 }
 
 // k_kick's work for one molecule inside a force kernel's row epilogue: its
@@ -1727,16 +1748,16 @@ __device__ __forceinline__ void fused_kick(const ForceArgs& f, size_t gid) {
 static __global__ void __launch_bounds__(256) k_kick_drift(StepArgs a) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= a.s.n * a.s.R) return;
-  if (*a.error_mol != 0x7fffffff) return;  // state frozen after a failed step
-  kick_drift_one(a, gid);
+  bool frozen;  // state frozen after a failed step
+  kick_drift_one(a, gid, &frozen);
 }
 
 // second half of a step: half kick + check_finite
 static __global__ void __launch_bounds__(256) k_kick(StepArgs a) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= a.s.n * a.s.R) return;
-  if (*a.error_mol != 0x7fffffff) return;
-  if (!kick_one(a, gid)) atomicMin(a.error_mol, gid);
+  bool frozen;
+  if (!kick_one(a, gid, &frozen)) atomicMin(a.error_mol, gid);
 }
 
 // end of step k fused with the start of step k+1 (one launch in the step loop).
@@ -1746,12 +1767,12 @@ static __global__ void __launch_bounds__(256) k_kick(StepArgs a) {
 static __global__ void __launch_bounds__(256) k_kick_kick_drift(StepArgs a) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= a.s.n * a.s.R) return;
-  if (*a.error_mol != 0x7fffffff) return;
-  if (!kick_one(a, gid)) {
+  bool frozen;
+  if (!kick_one(a, gid, &frozen)) {
     atomicMin(a.error_mol, gid);
     return;
   }
-  kick_drift_one(a, gid);
+  if (!frozen) kick_drift_one(a, gid);
 }
 
 // wrap (model.cpp:279-286) for set_state
