@@ -230,6 +230,33 @@ def test_cluster_walk_cfg3_void():
     check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
 
 
+@pytest.mark.parametrize("n", [1001, 2053])
+def test_cluster_walk_replicas(n):
+    """Single-site replicas through the cluster walk (rc < 0.3 L: re-sorted
+    every 20 steps): per-replica oracle forces, energies, pair lists and a
+    30-step trajectory.  n is not a multiple of the cluster size, so each
+    replica's last cluster is short and its staging reads into the next
+    replica (or the zeroed padding)."""
+    wls = [configs.lj_fluid_config(n, 0.8, 2.5, seed=11 + r) for r in range(3)]
+    comp, opts = wls[0].comp, wls[0].opts
+    states = [w.states[0] for w in wls]
+    dt, steps = 0.005, 30
+    eng = b2.Engine(comp, opts, dt, replicas=3)
+    eng.set_state(states)
+    first = eng.states()
+    eng.step(steps)
+    outs = eng.states()
+    o = pyoracle.OracleFF(comp, opts)
+    for r, st in enumerate(states):
+        ref0 = o.evaluate(st.pos, st.orient)
+        check_vec(first[r].force, ref0["force"], what=f"replica {r} force")
+        check_energy(first[r].energy, ref0["energy"], first[r].virial, ref0["virial"])
+        ref = o.run(dt, steps, st.pos, st.orient, st.vel, st.ang_vel)
+        compare_states(outs[r], ref, comp.box_length)
+        check_energy(outs[r].energy, ref["energy"])
+        assert np.array_equal(eng.pair_list(r), o.pair_list(ref["pos"]))
+
+
 def test_cluster_walk_unwrapped_positions(monkeypatch):
     """The cluster walk on positions outside [0, L) (ForceField::evaluate
     takes them as given): such clusters are never culled, the exact minimum
