@@ -494,30 +494,53 @@ EwaldArgs ewald_args(b2md_ctx* c) {
   return a;
 }
 
-int launch_ewald(b2md_ctx* c) {
-  if (!c->t.ewald || c->nq == 0) return B2MD_OK;
+// Ewald::evaluate (src/ewald.cpp:107-180): per-site phase tables, S(k) and
+// U_recip (first part, stream st), then the forces/torques added onto the
+// real-space ones (second part, after the real-space kernel on c->stream)
+int launch_ewald_sk(b2md_ctx* c, cudaStream_t st) {
   EwaldArgs a = ewald_args(c);
   const int nt = c->nq * c->R;
-  PROF(c, F_EWALD_TAB, (k_ewald_tables<<<(nt + 127) / 128, 128, 0, c->stream>>>(a)));
+  const bool prof = st == c->stream;  // profiling events live on c->stream
+  if (prof)
+    PROF(c, F_EWALD_TAB, (k_ewald_tables<<<(nt + 127) / 128, 128, 0, st>>>(a)));
+  else
+    k_ewald_tables<<<(nt + 127) / 128, 128, 0, st>>>(a);
+  CU(cudaGetLastError());
   if (a.nk > 0) {
-    PROF(c, F_EWALD_SK, (k_ewald_sk<<<dim3(a.nk, c->R), 256, 0, c->stream>>>(a)));
-    // k-split: P warps per molecule so that molecules x P reach ~16 warps per SM
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    int P = 1;
-    while (P < 8 && long(c->t.n) * c->R * P < long(sms) * 16) P *= 2;
-    if (const char* e = std::getenv("B2MD_EWALD_KPARTS")) P = std::max(1, std::min(8, std::atoi(e)));
-    while (8 % P) --P;
-    a.kparts = P;
-    const int mpc = 8 / P;
-    PROF(c, F_EWALD_F,
-         (k_ewald_force<<<dim3((c->t.n + mpc - 1) / mpc, c->R), 256, 0, c->stream>>>(a)));
+    if (prof)
+      PROF(c, F_EWALD_SK, (k_ewald_sk<<<dim3(a.nk, c->R), 256, 0, st>>>(a)));
+    else
+      k_ewald_sk<<<dim3(a.nk, c->R), 256, 0, st>>>(a);
+    CU(cudaGetLastError());
   } else {
     for (int r = 0; r < c->R; ++r)
       CU(cudaMemsetAsync(sums_ptr(c) + size_t(r) * kNumSums + kNumRowScalars, 0, sizeof(double),
-                         c->stream));
+                         st));
   }
   return B2MD_OK;
+}
+
+int launch_ewald_force(b2md_ctx* c) {
+  EwaldArgs a = ewald_args(c);
+  if (a.nk == 0) return B2MD_OK;
+  // k-split: P warps per molecule so that molecules x P reach ~16 warps per SM
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  int P = 1;
+  while (P < 8 && long(c->t.n) * c->R * P < long(sms) * 16) P *= 2;
+  if (const char* e = std::getenv("B2MD_EWALD_KPARTS")) P = std::max(1, std::min(8, std::atoi(e)));
+  while (8 % P) --P;
+  a.kparts = P;
+  const int mpc = 8 / P;
+  PROF(c, F_EWALD_F,
+       (k_ewald_force<<<dim3((c->t.n + mpc - 1) / mpc, c->R), 256, 0, c->stream>>>(a)));
+  return B2MD_OK;
+}
+
+int launch_ewald(b2md_ctx* c) {
+  if (!c->t.ewald || c->nq == 0) return B2MD_OK;
+  TRY(launch_ewald_sk(c, c->stream));
+  return launch_ewald_force(c);
 }
 
 int launch_allreduce(b2md_ctx* c) {
@@ -594,9 +617,25 @@ int enqueue_forces(b2md_ctx* c, bool offsets, bool kick) {
     CU(cudaGetLastError());
     TRY(launch_cluster_arcs(c));
   }
+  // the Ewald tables and S(k) only read positions: a parallel branch beside
+  // the search and the real-space kernel (which overwrites the forces the
+  // Ewald force kernel then adds to); serial while kernels are being timed
+  const bool ewald = c->t.ewald && c->nq > 0;
+  const bool fork = ewald && !c->profile && c->stream2;
+  if (fork) {
+    CU(cudaEventRecord(c->ev_fork, c->stream));
+    CU(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+    TRY(launch_ewald_sk(c, c->stream2));
+    CU(cudaEventRecord(c->ev_join, c->stream2));
+  }
   if (!cluster_path(c)) TRY(launch_search(c));
   TRY(launch_force(c, kick));
-  TRY(launch_ewald(c));
+  if (fork) {
+    CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    TRY(launch_ewald_force(c));
+  } else {
+    TRY(launch_ewald(c));
+  }
   TRY(launch_allreduce(c));
   return B2MD_OK;
 }
@@ -1004,6 +1043,9 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   if (device < 0 || device >= ndev) return set_err(B2MD_CUDA_ERROR, "b200md: no such CUDA device");
   CU(cudaSetDevice(device));
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   c->g = search_geometry(t.n);
   if (size_t(t.n) * size_t(t.n) > (size_t(1) << 32))
     return set_err(B2MD_CONFIG_ERROR, "b200md: too many molecules");
@@ -1251,6 +1293,9 @@ void free_ctx(b2md_ctx* c) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
 }
 

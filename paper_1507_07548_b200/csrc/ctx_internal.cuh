@@ -90,6 +90,10 @@ using namespace b2md;  // device types of the context (kernels.cuh, model.hpp)
 struct b2md_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // Ewald tables + S(k) run on stream2 beside the real-space kernel (fork /
+  // join events; captured into the step graphs as parallel branches)
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   ModelTables t;
   SearchGeometry g;
   int R = 1;
