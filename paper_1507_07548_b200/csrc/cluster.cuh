@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
       return norm2_exact(dx, dy, dz);
     };
     auto terms = [&](int j, bool in, double r2, double dx, double dy, double dz) {
-      const double inv_r2 = rcp_nr1(in ? r2 : 1.0);
+      const double inv_r2 = rcp_nr(in ? r2 : 1.0);
       const double t6 = inv_r2 * inv_r2 * inv_r2;
       const double ir6 = in ? t6 : 0.0;
       double fs;

@@ -647,15 +647,6 @@ __device__ __forceinline__ double erfcx_cheb(double x, const double* c, double t
   return fma(u, b1, c[0] - b2);
 }
 
-// 1/x from the hardware reciprocal seed (~2^-23 relative) refined by one
-// Newton step (~2^-46): force arithmetic, tolerance 1e-10
-__device__ __forceinline__ double rcp_nr1(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  const double e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-
 // 1/x to ~1 ulp without the IEEE-division slow path: hardware reciprocal
 // seed + two Newton steps (force arithmetic; tolerance 1e-10).
 __device__ __forceinline__ double rcp_nr(double x) {
