@@ -250,13 +250,19 @@ int launch_search(b2md_ctx* c) {
   }
   dim3 grid(c->n_super_tiles, c->R);
   const int st = c->g.st;
+  // generic path (mixtures, rmax >= L/2 (1 - 1e-3)) of small systems (few
+  // tiles): RS = 4 warps per tile row
 #define SEARCH_CASE(ST)                                                                  \
-  case ST:                                                                               \
+  case ST: {                                                                             \
+    constexpr int RS = ST <= 2 ? 4 : 1;                                                  \
     if (multi)                                                                           \
-      PROF(c, F_SEARCH, (k_search<ST, true><<<grid, ST * 32, 0, c->stream>>>(a)));       \
+      PROF(c, F_SEARCH, (k_search<ST, true, RS><<<grid, ST * 32 * RS, 0, c->stream>>>(a))); \
+    else if (!a.fix_ok)                                                                  \
+      PROF(c, F_SEARCH, (k_search<ST, false, RS><<<grid, ST * 32 * RS, 0, c->stream>>>(a))); \
     else                                                                                 \
       PROF(c, F_SEARCH, (k_search<ST, false><<<grid, ST * 32, 0, c->stream>>>(a)));      \
-    break;
+    break;                                                                               \
+  }
   switch (st) {
     SEARCH_CASE(1)
     SEARCH_CASE(2)

@@ -284,8 +284,11 @@ __device__ __forceinline__ bool tiles_apart(uint4 ca, uint4 ha, uint4 cb, uint4 
 // as whole 32-byte sectors of the row-major bit matrix M[r][row][word].
 // Certified fixed-point path for single-species, in-box tiles; the exact
 // generic fp64 path (any position, mixtures, rmax >= L/2) otherwise.
-template <int ST, bool MULTI>
-__global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArgs a) {
+template <int ST, bool MULTI, int RS = 1>
+__global__ void __launch_bounds__(ST * 32 * RS, (ST * RS >= 8 ? 4 : 8)) k_search(SearchArgs a) {
+  // RS > 1 (generic path only): RS warps share each tile row, 32 / RS rows
+  // each -- small systems have few tiles, and a lone warp per tile is
+  // latency-bound on the exact fp64 chain
   constexpr int T = ST * 32;
   __shared__ uint4 ui[T], uj[T];
   __shared__ int ispec[MULTI ? T : 1], jspec[MULTI ? T : 1];
@@ -306,8 +309,8 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
   const size_t roff = size_t(r) * n;
   const double4* __restrict__ gp = a.pos4 + roff;
 
-  bool inbox;
-  {
+  bool inbox = true;
+  if (tid < T) {
     const int i = ibase + tid, j = jbase + tid;
     // fixed-point positions + in-box flag, written by the integrator
     // (k_kick_drift) or k_fix_positions
@@ -331,10 +334,11 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
   }
   const bool boxed = __syncthreads_and(inbox);
 
-  const int I = warp;  // local tile row
+  const int I = warp % ST;  // local tile row
+  const int part = warp / ST;
   const int ib = I * 32;
   const int ilim = n - (ibase + ib);
-  if (boxed && a.fix_ok && !MULTI) {
+  if (RS == 1 && boxed && a.fix_ok && !MULTI) {
     const int jlim = n - jbase;
     const int neglo = -int(a.fix_lo);
     const int wd = int(a.fix_width);
@@ -442,7 +446,7 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
       const double xj = pj.x, yj = pj.y, zj = pj.z;
       const int sj = MULTI ? jspec[jl] : 0;
       const bool diag_tile = diag && c == I;
-      for (int ii = 0; ii < 32; ++ii) {
+      for (int ii = part * (32 / RS); ii < (part + 1) * (32 / RS); ++ii) {
         const int il = ib + ii;
         const int ig = ii < ilim ? ibase + il : 0;
         const double4 pi = gp[ig];
@@ -460,11 +464,20 @@ __global__ void __launch_bounds__(ST * 32, (ST >= 8 ? 4 : 8)) k_search(SearchArg
         const uint32_t b = __ballot_sync(0xffffffffu, pass);
         if (lane == 0) wu[(ib + ii) * ST + c] = b;
       }
-      __syncwarp();
-      wl[(c * 32 + lane) * ST + I] = warp_transpose32(wu[(ib + lane) * ST + c], lane);
+      if constexpr (RS == 1) {
+        __syncwarp();
+        wl[(c * 32 + lane) * ST + I] = warp_transpose32(wu[(ib + lane) * ST + c], lane);
+      }
+    }
+    if constexpr (RS > 1) {  // the tile's rows come from RS warps
+      __syncthreads();
+      if (part == 0)
+        for (int c = diag ? I : 0; c < ST; ++c)
+          wl[(c * 32 + lane) * ST + I] = warp_transpose32(wu[(ib + lane) * ST + c], lane);
     }
   }
   __syncthreads();
+  if (tid >= T) return;
 
   // store: rows of tile-row block SI get columns SJ*ST.. (wu); rows of block SJ
   // get columns SI*ST.. (wl).  Diagonal super-tiles merge both.
