@@ -204,6 +204,121 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// The cluster walk of one i-group (one warp; rows g0 + (lane & 3), this
+// lane's row i with position pi / fixed point fi, valid iv): the group's arc
+// against the super-cluster and cluster arcs, surviving clusters staged in
+// pairs, and for every pair step with some r2 < rc2 in the warp
+//   pair(ja, ina, ra, ax, ay, az, jb, inb, rb, bx, by, bz)
+// with each lane's partner slot j, in-cutoff flag, r2 and R = min_image(x_i -
+// x_j) on the reference's bits (potentials.cpp:156-161).
+template <bool WRAPPED, class Pair>
+__device__ __forceinline__ void cpair_walk(const ClusterArgs& ca, const double4* __restrict__ p4,
+                                           int r, int n, int i, bool iv, const double4& pi,
+                                           uint4 fi, double rc2, const MinImage mi, float thr,
+                                           int* __restrict__ wl, double4 (*stage)[2][kCS],
+                                           Pair&& pair) {
+  const int lane = threadIdx.x & 31, jl = lane >> 2;
+  const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+  const uint4* __restrict__ arcs = ca.arcs + size_t(r) * ca.nc;
+  const float4* __restrict__ half = ca.half + size_t(r) * ca.nc;
+  const uint4* __restrict__ sarcs = ca.sup_arcs + size_t(r) * ca.nsup;
+  const float4* __restrict__ shalf = ca.sup_half + size_t(r) * ca.nsup;
+  const float lim = ca.lim;
+  auto mimg = [&](double d) {
+    return WRAPPED ? min_image_wrapped(d, mi.negL, thr) : min_image(d, mi);
+  };
+  // the group's arc (offsets from lane 0's point; lanes repeat the 4 rows)
+  uint4 gc;
+  float4 gh;
+  {
+    const uint4 f0 = make_uint4(__shfl_sync(full, fi.x, 0), __shfl_sync(full, fi.y, 0),
+                                __shfl_sync(full, fi.z, 0), 0u);
+    const int ox = int(fi.x - f0.x), oy = int(fi.y - f0.y), oz = int(fi.z - f0.z);
+    const int mnx = __reduce_min_sync(full, ox), mxx = __reduce_max_sync(full, ox);
+    const int mny = __reduce_min_sync(full, oy), mxy = __reduce_max_sync(full, oy);
+    const int mnz = __reduce_min_sync(full, oz), mxz = __reduce_max_sync(full, oz);
+    const bool in = __all_sync(full, fi.w != 0u);
+    gc = make_uint4(arc_centre(f0.x, mnx, mxx), arc_centre(f0.y, mny, mxy),
+                    arc_centre(f0.z, mnz, mxz), 0u);
+    gh = in ? make_float4(arc_half(mnx, mxx), arc_half(mny, mxy), arc_half(mnz, mxz), 0.0f)
+            : make_float4(3e9f, 3e9f, 3e9f, 0.0f);
+  }
+  // one lane's pair: distance on the reference's bits
+  auto dist = [&](const double4& pj, double& dx, double& dy, double& dz) {
+    dx = mimg(sub(pi.x, pj.x));
+    dy = mimg(sub(pi.y, pj.y));
+    dz = mimg(sub(pi.z, pj.z));
+    return norm2_exact(dx, dy, dz);
+  };
+  // staging ring: slot k holds a cluster pair as 512 contiguous bytes;
+  // lane L copies bytes [16 L, 16 L + 16) (lanes 0-15 the first cluster's
+  // 8 double4, lanes 16-31 the second's)
+  const unsigned ring = smem_u32(&stage[0][0][0]) + 16u * lane;
+  const char* __restrict__ src0 = reinterpret_cast<const char*>(p4) + 16 * (lane & 15);
+  const int half_sel = lane >> 4;
+  const int ilim = iv ? n : 0;  // j < ilim: a real partner slot of a real row
+  // surviving clusters, in chunks of <= kGList: super-cluster batch sb
+  // (ballot sv), then each super-cluster's clusters (ballot, compacted)
+  int sb = 0;
+  unsigned sv = 0u;
+  for (;;) {
+    int nl = 0;
+    for (;;) {
+      if (sv == 0u) {
+        if (sb >= ca.nsup) break;
+        const bool near = sb + lane < ca.nsup && arcs_near(gc, gh, sarcs[sb + lane], shalf[sb + lane], lim);
+        sv = __ballot_sync(full, near);
+        sb += 32;
+        continue;
+      }
+      if (nl > kGList - 32) break;
+      const int sc = sb - 32 + __ffs(sv) - 1;
+      sv &= sv - 1u;
+      const int jc = sc * kSC + lane;
+      const bool keep = jc < ca.nc && arcs_near(gc, gh, arcs[jc], half[jc], lim);
+      const unsigned cv = __ballot_sync(full, keep);
+      if (keep) wl[nl + __popc(cv & lt)] = jc;
+      nl += __popc(cv);
+    }
+    if (nl == 0) break;
+    // odd tail: a cluster past the end (all j >= n; staged from pos4's
+    // zeroed padding or the next replica, so every lane's r2 is finite)
+    if (lane == 0) wl[nl] = ca.nc;
+    __syncwarp();
+    const int nsteps = (nl + 1) >> 1;
+    int next = 0;        // next pair to stage
+    unsigned wslot = 0;  // its ring slot (bytes)
+    auto issue = [&]() {
+      const int e = 2 * next + half_sel;
+      if (next < nsteps) cp_async16(ring + wslot, src0 + size_t(wl[e]) * (kCS * 32));
+      cp_async_commit();
+      ++next;
+      wslot = (wslot + 512u) & (512u * kGDepth - 1u);
+    };
+#pragma unroll
+    for (int k = 0; k < kGDepth - 1; ++k) issue();
+    const double4* rs = &stage[0][0][jl];
+    for (int st = 0; st < nsteps; ++st) {
+      issue();
+      cp_async_wait<kGDepth - 1>();
+      __syncwarp();
+      const int slot = st & (kGDepth - 1);
+      const int ja = wl[2 * st] * kCS + jl, jb = wl[2 * st + 1] * kCS + jl;
+      const bool va = ja < ilim && ja != i;
+      const bool vb = jb < ilim && jb != i;
+      double ax, ay, az, bx, by, bz;
+      const double ra = dist(rs[slot * 2 * kCS], ax, ay, az);
+      const double rb = dist(rs[slot * 2 * kCS + kCS], bx, by, bz);
+      __syncwarp();  // the slot's reads are consumed before it is refilled
+      const bool ina = va && ra < rc2, inb = vb && rb < rc2;  // potentials.cpp:161
+      if (__ballot_sync(full, ina || inb) == 0u) continue;
+      pair(ja, ina, ra, ax, ay, az, jb, inb, rb, bx, by, bz);
+    }
+    cp_async_wait<0>();
+    __syncwarp();  // wl and the ring are rewritten by the next chunk
+  }
+}
+
 template <bool MULTI_SPECIES, bool WRAPPED, bool VDERIV>
 __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, ClusterArgs ca) {
   __shared__ int clist[kGWarps][kGList + 1];
@@ -214,21 +329,9 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
   const size_t roff = size_t(r) * s.n;
   const double4* __restrict__ p4 = a.st.pos4 + roff;
   const uint4* __restrict__ fx4 = ca.fixpos + roff;
-  const uint4* __restrict__ arcs = ca.arcs + size_t(r) * ca.nc;
-  const float4* __restrict__ half = ca.half + size_t(r) * ca.nc;
-  const uint4* __restrict__ sarcs = ca.sup_arcs + size_t(r) * ca.nsup;
-  const float4* __restrict__ shalf = ca.sup_half + size_t(r) * ca.nsup;
-  const MinImage mi = s.mi;
-  const float thr = a.thr;
-  auto mimg = [&](double d) {
-    return WRAPPED ? min_image_wrapped(d, mi.negL, thr) : min_image(d, mi);
-  };
-  const double rc2 = a.rc2;
-  const float lim = ca.lim;
-  const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+  const unsigned full = 0xffffffffu;
   const int n = s.n;
   const int g0 = (blockIdx.x * kGWarps + warp) * kGR;  // the group's first slot
-  int* __restrict__ wl = clist[warp];
   // sums over all visits: single species B12 = sum ir6^2, B6 = sum ir6
   // (a12 = c12 B12, a6 = c6 B6); mixtures sum a12, a6 directly
   double B12 = 0, B6 = 0;
@@ -243,37 +346,12 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
       a.st.fz[e] = 0.0;
     }
   } else if (g0 < n) {  // warp-uniform
-    const int il = lane & (kGR - 1), jl = lane >> 2;
-    const int i = g0 + il;
+    const int i = g0 + (lane & (kGR - 1));
     const bool iv = i < n;
     const int ic = iv ? i : g0;  // clamped row
-    const uint4 fi = fx4[ic];
     const double4 pi = p4[ic];
     const int si = MULTI_SPECIES ? s.sp_slot[roff + ic] : 0;
-    // the group's arc (offsets from lane 0's point; lanes repeat the 4 rows)
-    uint4 gc;
-    float4 gh;
-    {
-      const uint4 f0 = make_uint4(__shfl_sync(full, fi.x, 0), __shfl_sync(full, fi.y, 0),
-                                  __shfl_sync(full, fi.z, 0), 0u);
-      const int ox = int(fi.x - f0.x), oy = int(fi.y - f0.y), oz = int(fi.z - f0.z);
-      const int mnx = __reduce_min_sync(full, ox), mxx = __reduce_max_sync(full, ox);
-      const int mny = __reduce_min_sync(full, oy), mxy = __reduce_max_sync(full, oy);
-      const int mnz = __reduce_min_sync(full, oz), mxz = __reduce_max_sync(full, oz);
-      const bool in = __all_sync(full, fi.w != 0u);
-      gc = make_uint4(arc_centre(f0.x, mnx, mxx), arc_centre(f0.y, mny, mxy),
-                      arc_centre(f0.z, mnz, mxz), 0u);
-      gh = in ? make_float4(arc_half(mnx, mxx), arc_half(mny, mxy), arc_half(mnz, mxz), 0.0f)
-              : make_float4(3e9f, 3e9f, 3e9f, 0.0f);
-    }
     double fx = 0, fy = 0, fz = 0;
-    // one lane's pair: distance on the reference's bits, then the terms
-    auto dist = [&](const double4& pj, double& dx, double& dy, double& dz) {
-      dx = mimg(sub(pi.x, pj.x));
-      dy = mimg(sub(pi.y, pj.y));
-      dz = mimg(sub(pi.z, pj.z));
-      return norm2_exact(dx, dy, dz);
-    };
     auto terms = [&](int j, bool in, double r2, double dx, double dy, double dz) {
       const double inv_r2 = rcp_nr(in ? r2 : 1.0);
       const double t6 = inv_r2 * inv_r2 * inv_r2;
@@ -298,74 +376,13 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
       fz = fma(fs, dz, fz);
       cnt += in && i < j;  // exact per shard: the pair's i < j side
     };
-    // staging ring: slot k holds a cluster pair as 512 contiguous bytes;
-    // lane L copies bytes [16 L, 16 L + 16) (lanes 0-15 the first cluster's
-    // 8 double4, lanes 16-31 the second's)
-    const unsigned ring = smem_u32(&stage[warp][0][0][0]) + 16u * lane;
-    const char* __restrict__ src0 = reinterpret_cast<const char*>(p4) + 16 * (lane & 15);
-    const int half_sel = lane >> 4;
-    const int ilim = iv ? n : 0;  // j < ilim: a real partner slot of a real row
-    // surviving clusters, in chunks of <= kGList: super-cluster batch sb
-    // (ballot sv), then each super-cluster's clusters (ballot, compacted)
-    int sb = 0;
-    unsigned sv = 0u;
-    for (;;) {
-      int nl = 0;
-      for (;;) {
-        if (sv == 0u) {
-          if (sb >= ca.nsup) break;
-          const bool near = sb + lane < ca.nsup && arcs_near(gc, gh, sarcs[sb + lane], shalf[sb + lane], lim);
-          sv = __ballot_sync(full, near);
-          sb += 32;
-          continue;
-        }
-        if (nl > kGList - 32) break;
-        const int sc = sb - 32 + __ffs(sv) - 1;
-        sv &= sv - 1u;
-        const int jc = sc * kSC + lane;
-        const bool keep = jc < ca.nc && arcs_near(gc, gh, arcs[jc], half[jc], lim);
-        const unsigned cv = __ballot_sync(full, keep);
-        if (keep) wl[nl + __popc(cv & lt)] = jc;
-        nl += __popc(cv);
-      }
-      if (nl == 0) break;
-      // odd tail: a cluster past the end (all j >= n; staged from pos4's
-      // zeroed padding or the next replica, so every lane's r2 is finite)
-      if (lane == 0) wl[nl] = ca.nc;
-      __syncwarp();
-      const int nsteps = (nl + 1) >> 1;
-      int next = 0;        // next pair to stage
-      unsigned wslot = 0;  // its ring slot (bytes)
-      auto issue = [&]() {
-        const int e = 2 * next + half_sel;
-        if (next < nsteps) cp_async16(ring + wslot, src0 + size_t(wl[e]) * (kCS * 32));
-        cp_async_commit();
-        ++next;
-        wslot = (wslot + 512u) & (512u * kGDepth - 1u);
-      };
-#pragma unroll
-      for (int k = 0; k < kGDepth - 1; ++k) issue();
-      const double4* rs = &stage[warp][0][0][jl];
-      for (int st = 0; st < nsteps; ++st) {
-        issue();
-        cp_async_wait<kGDepth - 1>();
-        __syncwarp();
-        const int slot = st & (kGDepth - 1);
-        const int ja = wl[2 * st] * kCS + jl, jb = wl[2 * st + 1] * kCS + jl;
-        const bool va = ja < ilim && ja != i;
-        const bool vb = jb < ilim && jb != i;
-        double ax, ay, az, bx, by, bz;
-        const double ra = dist(rs[slot * 2 * kCS], ax, ay, az);
-        const double rb = dist(rs[slot * 2 * kCS + kCS], bx, by, bz);
-        __syncwarp();  // the slot's reads are consumed before it is refilled
-        const bool ina = va && ra < rc2, inb = vb && rb < rc2;  // potentials.cpp:161
-        if (__ballot_sync(full, ina || inb) == 0u) continue;
-        terms(ja, ina, ra, ax, ay, az);
-        terms(jb, inb, rb, bx, by, bz);
-      }
-      cp_async_wait<0>();
-      __syncwarp();  // wl and the ring are rewritten by the next chunk
-    }
+    cpair_walk<WRAPPED>(ca, p4, r, n, i, iv, pi, fx4[ic], a.rc2, s.mi, a.thr, clist[warp],
+                        stage[warp],
+                        [&](int ja, bool ina, double ra, double ax, double ay, double az, int jb,
+                            bool inb, double rb, double bx, double by, double bz) {
+                          terms(ja, ina, ra, ax, ay, az);
+                          terms(jb, inb, rb, bx, by, bz);
+                        });
     // a row's 8 lanes (il fixed, jl = lane >> 2): fixed xor tree
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
@@ -392,6 +409,81 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
                               VDERIV ? 156.0 * A12 - 42.0 * A6 : 0.0, -s1,
                               warp_sum(double(cnt))};
   finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
+}
+
+// heat_flux (greenkubo.cpp:182-266) of a single-species, centred, LJ-only
+// system on the cluster walk (no partner search): the same row split as
+// k_heat_flux -- row i adds 0.5 (f_i . v_i) R_i over its partners (f_i the
+// pair's force on i, R_i = min_image(com_i - com_j)), 0.5 sum_p u_p v_i and,
+// where `kinetic` is set, (e_kin_i - h) v_i.  In-range lanes only carry
+// terms (ir6 = 0 elsewhere); per-row lane sums by a fixed xor tree.
+template <bool WRAPPED>
+__global__ void __launch_bounds__(kGWarps * 32, 8) k_heat_flux_cpair(FluxArgs fa, ClusterArgs ca) {
+  __shared__ int clist[kGWarps][kGList + 1];
+  __shared__ __align__(128) double4 stage[kGWarps][kGDepth][2][kCS];
+  const ForceArgs& a = fa.f;
+  const SysDev& s = a.s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.y;
+  const size_t roff = size_t(r) * s.n;
+  const double4* __restrict__ p4 = a.st.pos4 + roff;
+  const uint4* __restrict__ fx4 = ca.fixpos + roff;
+  const unsigned full = 0xffffffffu;
+  const int n = s.n;
+  const int grp = blockIdx.x * kGWarps + warp;
+  const int g0 = grp * kGR;  // the group's first slot
+  double jx = 0, jy = 0, jz = 0;
+  if (g0 < n && grp >= ca.grp_begin && grp < ca.grp_end) {  // warp-uniform
+    const int i = g0 + (lane & (kGR - 1));
+    const bool iv = i < n;
+    const int ic = iv ? i : g0;  // clamped row
+    const double4 pi = p4[ic];
+    const size_t ge = roff + ext_of(pi);
+    const double vix = a.st.vx[ge], viy = a.st.vy[ge], viz = a.st.vz[ge];
+    double tx = 0, ty = 0, tz = 0, up = 0;  // sum_p 0.5 (f.v_i) R_p, sum_p u_p
+    auto term = [&](bool in, double r2, double dx, double dy, double dz) {
+      const double inv_r2 = rcp_nr(in ? r2 : 1.0);
+      const double t6 = inv_r2 * inv_r2 * inv_r2;
+      const double ir6 = in ? t6 : 0.0;
+      const double a12 = a.c12 * ir6 * ir6, a6 = a.c6 * ir6;
+      const double fs = (12.0 * a12 - 6.0 * a6) * inv_r2;  // -du_r / r2
+      const double sp = 0.5 * fs * (dx * vix + dy * viy + dz * viz);
+      tx += sp * dx;
+      ty += sp * dy;
+      tz += sp * dz;
+      up += a12 - a6;
+    };
+    cpair_walk<WRAPPED>(ca, p4, r, n, i, iv, pi, fx4[ic], a.rc2, s.mi, a.thr, clist[warp],
+                        stage[warp],
+                        [&](int, bool ina, double ra, double ax, double ay, double az, int,
+                            bool inb, double rb, double bx, double by, double bz) {
+                          term(ina, ra, ax, ay, az);
+                          term(inb, rb, bx, by, bz);
+                        });
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      tx += __shfl_xor_sync(full, tx, o);
+      ty += __shfl_xor_sync(full, ty, o);
+      tz += __shfl_xor_sync(full, tz, o);
+      up += __shfl_xor_sync(full, up, o);
+    }
+    if (lane < kGR && iv) {
+      double e = 0.5 * up;
+      if (fa.kinetic) {
+        const DevSpecies& sp = s.tab->species[0];
+        const double wbx = a.st.wx[ge], wby = a.st.wy[ge], wbz = a.st.wz[ge];
+        const double ek = 0.5 * sp.total_mass * (vix * vix + viy * viy + viz * viz) +
+                          0.5 * (sp.inertia[0] * wbx * wbx + sp.inertia[1] * wby * wby +
+                                 sp.inertia[2] * wbz * wbz);
+        e += ek - fa.enthalpy[0];
+      }
+      jx = tx + e * vix;
+      jy = ty + e * viy;
+      jz = tz + e * viz;
+    }
+  }
+  double v[3] = {warp_sum(jx), warp_sum(jy), warp_sum(jz)};
+  finalize_scalars<3>(v, a.cta_part, a.ticket, fa.out, r, 0);
 }
 
 }  // namespace b2md

@@ -204,6 +204,9 @@ int launch_offsets(b2md_ctx* c);
 int launch_search(b2md_ctx* c);
 int ensure_mask(b2md_ctx* c);
 bool cluster_path(const b2md_ctx* c);
+int cpair_grid(const b2md_ctx* c);
+ClusterArgs cluster_args(const b2md_ctx* c);
+int launch_cluster_arcs(b2md_ctx* c);
 ForceArgs force_args(b2md_ctx* c);
 bool fast_min_image(const b2md_ctx* c);
 int resort(b2md_ctx* c);

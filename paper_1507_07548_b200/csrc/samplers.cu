@@ -11,6 +11,11 @@ namespace b2md_host {
 // heat_flux (src/greenkubo.cpp:182-266) over the current mask, site offsets
 // and packed positions (valid after set_state / step / evaluate), then the
 // cross-rank sum of the per-replica 3-vectors.
+// single species, centred LJ only: the cluster walk (no partner search)
+bool flux_cluster(const b2md_ctx* c) {
+  return cluster_path(c) && c->t.ns == 1 && c->t.qq[0].empty();
+}
+
 int launch_heat_flux(b2md_ctx* c, const double* enthalpy) {
   FluxArgs a;
   a.f = force_args(c);
@@ -18,6 +23,18 @@ int launch_heat_flux(b2md_ctx* c, const double* enthalpy) {
   a.out = c->d_flux;
   a.kinetic = c->rank == 0 ? 1 : 0;
   const bool w = fast_min_image(c);
+  if (flux_cluster(c)) {
+    const ClusterArgs ca = cluster_args(c);
+    dim3 pgrid(cpair_grid(c), c->R);
+    if (w)
+      PROF(c, F_HEAT_FLUX, (k_heat_flux_cpair<true><<<pgrid, kGWarps * 32, 0, c->stream>>>(a, ca)));
+    else
+      PROF(c, F_HEAT_FLUX, (k_heat_flux_cpair<false><<<pgrid, kGWarps * 32, 0, c->stream>>>(a, ca)));
+    if (c->world > 1 && c->comm)
+      NC(g_nccl.AllReduce(c->d_flux, c->d_flux, size_t(kNumSums) * c->R, ncclDouble, ncclSum,
+                          c->comm, c->stream));
+    return B2MD_OK;
+  }
   const bool offs = c->t.any_offsets;
   const bool one = c->t.ns == 1;
   dim3 grid(c->force_grid, c->R);
@@ -84,7 +101,7 @@ int b2md_heat_flux(b2md_ctx* c, const double* enthalpy, int n_enthalpy, double* 
   if (!c->state_valid)
     return set_err(B2MD_CONFIG_ERROR, "heat_flux: set_state must precede heat_flux");
   CU(cudaSetDevice(c->device));
-  TRY(ensure_mask(c));
+  if (!flux_cluster(c)) TRY(ensure_mask(c));  // (the cluster walk's arcs are current)
   TRY(launch_heat_flux(c, enthalpy));
   return download_flux(c, jq);
 }
@@ -111,8 +128,9 @@ int b2md_heat_flux_state(b2md_ctx* c, const double* pos, const double* orient, c
         c->st.px, c->st.py, c->st.pz, nt, c->t.n, c->d_slot_of, c->t.box,
         4294967296.0 / c->t.box, c->d_fixpos, c->st.pos4);
     CU(cudaGetLastError());
+    TRY(launch_cluster_arcs(c));
   }
-  TRY(launch_search(c));
+  if (!flux_cluster(c)) TRY(launch_search(c));
   TRY(launch_heat_flux(c, enthalpy));
   TRY(download_flux(c, jq));
   c->state_valid = false;  // forces not evaluated: not an engine state
