@@ -126,6 +126,30 @@ def test_baseline_100_step_trajectory(cfg):
     assert np.array_equal(eng.pair_list(), pyoracle.OracleFF(wl.comp, wl.opts).pair_list(ref["pos"]))
 
 
+def test_cfg3_100_step_trajectory_vs_reference():
+    """cfg3 (cluster walk, re-sorts every 20 steps) for 100 steps against the
+    unmodified reference engine's trajectory (tests/golden/traj_cfg3_100.npz,
+    make_cfg3_trajectory.py): every 8th molecule's position and velocity and
+    the energy at the north-star bar (1e-9)."""
+    g = np.load(GOLDEN / "traj_cfg3_100.npz")
+    wl = configs.make("cfg3")
+    st = wl.states[0]
+    eng = b2.Engine(wl.comp, wl.opts, wl.dt)
+    eng.set_state(st)
+    eng.step(int(g["steps"]))
+    out = eng.state()
+    k = int(g["stride"])
+    L = wl.comp.box_length
+    d = out.pos[::k] - g["pos"]
+    d -= L * np.round(d / L)
+    assert np.abs(d).max() / L <= T_TOL
+    assert np.abs(out.vel[::k] - g["vel"]).max() / np.abs(g["vel"]).max() <= T_TOL
+    e = out.energy
+    assert abs(e.total() - g["energy"][2]) <= T_TOL * abs(g["energy"][2])
+    assert abs(e.lj - g["energy"][0]) <= T_TOL * abs(g["energy"][0])
+    assert abs(out.virial - float(g["virial"])) <= T_TOL * abs(float(g["virial"]))
+
+
 def test_replica_batch_cfg4():
     wl = configs.make("cfg4", replicas=4, steps=20)
     eng = b2.Engine(wl.comp, wl.opts, wl.dt, replicas=4)
