@@ -312,7 +312,10 @@ int b2md_attach_nccl(b2md_ctx* ctx, const char id[128], int rank, int world);
  * of the decomposition on one device; b2md_attach_nccl is the production path. */
 int b2md_set_shard(b2md_ctx* ctx, int rank, int world);
 
-/* Opaque cudaStream_t of the context (for event timing by the caller). */
+/* Opaque cudaStream_t of the context (for event timing by the caller).  Every
+ * call's work is ordered on this stream; Ewald systems fork the tables and
+ * S(k) onto an internal second stream and join it back within the same call,
+ * so events recorded on this stream bracket the whole evaluation. */
 void* b2md_stream(b2md_ctx* ctx);
 
 /* Per-kernel CUDA-event timing of the device step (bench instrumentation).
