@@ -371,9 +371,12 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
         B12 = fma(ir6, ir6, B12);
         B6 += ir6;
       }
-      fx = fma(fs, dx, fx);
-      fy = fma(fs, dy, fy);
-      fz = fma(fs, dz, fz);
+      if (in) {  // (predicated: an excluded pair's R may be NaN -- a NaN position
+                 // fails the reference's r2 < rc2 test and touches nobody)
+        fx = fma(fs, dx, fx);
+        fy = fma(fs, dy, fy);
+        fz = fma(fs, dz, fz);
+      }
       cnt += in && i < j;  // exact per shard: the pair's i < j side
     };
     cpair_walk<WRAPPED>(ca, p4, r, n, i, iv, pi, fx4[ic], a.rc2, s.mi, a.thr, clist[warp],
@@ -447,10 +450,12 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_heat_flux_cpair(FluxArgs fa
       const double ir6 = in ? t6 : 0.0;
       const double a12 = a.c12 * ir6 * ir6, a6 = a.c6 * ir6;
       const double fs = (12.0 * a12 - 6.0 * a6) * inv_r2;  // -du_r / r2
-      const double sp = 0.5 * fs * (dx * vix + dy * viy + dz * viz);
-      tx += sp * dx;
-      ty += sp * dy;
-      tz += sp * dz;
+      if (in) {  // (an excluded pair's R may be NaN: see k_force_cpair)
+        const double sp = 0.5 * fs * (dx * vix + dy * viy + dz * viz);
+        tx += sp * dx;
+        ty += sp * dy;
+        tz += sp * dz;
+      }
       up += a12 - a6;
     };
     cpair_walk<WRAPPED>(ca, p4, r, n, i, iv, pi, fx4[ic], a.rc2, s.mi, a.thr, clist[warp],

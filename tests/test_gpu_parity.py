@@ -456,6 +456,23 @@ def test_nan_is_fatal():  # test_engine.cpp:232-245
         eng.step()
 
 
+def test_nan_is_fatal_cluster_walk():
+    """A NaN velocity on the cluster path (cfg3-like cutoff): the step fails
+    with the reference's message for the same molecule (check_finite's first
+    non-finite molecule after the NaN has reached its partners' forces)."""
+    wl = configs.lj_fluid_config(600, 0.7, 2.5, seed=9)
+    st = wl.states[0].copy()
+    st.vel[37] = (np.nan, 0.0, 0.0)
+    eng = b2.Engine(wl.comp, wl.opts, wl.dt)
+    eng.set_state(st)
+    with pytest.raises(b2.NumericalError) as got:
+        eng.step(3)
+    with pytest.raises(Exception) as ref:
+        pyoracle.OracleFF(wl.comp, wl.opts).run(wl.dt, 3, st.pos, st.orient, st.vel, st.ang_vel)
+    mol = lambda e: str(e.value).split("molecule")[1].split()[0]
+    assert mol(got) == mol(ref)
+
+
 @pytest.mark.parametrize("pinned", [True, False])
 def test_nan_deferred_to_get_state(pinned):
     """step_async defers the NumericalError to the next get_state (the flag
