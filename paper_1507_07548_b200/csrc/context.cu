@@ -1134,8 +1134,9 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     if (const char* e = std::getenv("B2MD_CLUSTER")) cl_mode = std::atoi(e);
     if (t.single_site_path && (cl_mode == 2 || (cl_mode == 1 && rmax < 0.3 * t.box))) {
       c->nc = (t.n + kCS - 1) / kCS;
-      if (rmax < 0.3 * t.box) c->sort_interval = 20;
+      if (rmax < 0.3 * t.box) c->sort_interval = 40;
     }
+    if (const char* e = std::getenv("B2MD_SORT_INTERVAL")) c->sort_interval = std::max(0, std::atoi(e));
     // tuning knobs (measurement only): warps per CTA, CTAs per replica
     if (const char* e = std::getenv("B2MD_FORCE_WARPS"))
       c->force_warps = std::max(1, std::min(kForceWarps, std::atoi(e)));

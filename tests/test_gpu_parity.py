@@ -127,7 +127,7 @@ def test_baseline_100_step_trajectory(cfg):
 
 
 def test_cfg3_100_step_trajectory_vs_reference():
-    """cfg3 (cluster walk, re-sorts every 20 steps) for 100 steps against the
+    """cfg3 (cluster walk, re-sorts every 40 steps) for 100 steps against the
     unmodified reference engine's trajectory (tests/golden/traj_cfg3_100.npz,
     make_cfg3_trajectory.py): every 8th molecule's position and velocity and
     the energy at the north-star bar (1e-9)."""
@@ -256,8 +256,8 @@ def test_cluster_walk_cfg3_void():
 
 @pytest.mark.parametrize("n", [1001, 2053])
 def test_cluster_walk_replicas(n):
-    """Single-site replicas through the cluster walk (rc < 0.3 L: re-sorted
-    every 20 steps): per-replica oracle forces, energies, pair lists and a
+    """Single-site replicas through the cluster walk (rc < 0.3 L, re-sorted
+    every 8 steps here): per-replica oracle forces, energies, pair lists and a
     30-step trajectory.  n is not a multiple of the cluster size, so each
     replica's last cluster is short and its staging reads into the next
     replica (or the zeroed padding)."""
@@ -266,6 +266,7 @@ def test_cluster_walk_replicas(n):
     states = [w.states[0] for w in wls]
     dt, steps = 0.005, 30
     eng = b2.Engine(comp, opts, dt, replicas=3)
+    eng.set_sort_interval(8)
     eng.set_state(states)
     first = eng.states()
     eng.step(steps)
@@ -300,13 +301,14 @@ def test_cluster_walk_unwrapped_positions(monkeypatch):
 
 
 def test_cfg3_trajectory_with_resorts():
-    """cfg3 (cluster walk, re-sorted every 20 steps) for 25 steps against the
-    oracle, and bit-identical when repeated (fixed summation order)."""
+    """cfg3 (cluster walk, re-sorted every 10 steps here) for 25 steps against
+    the oracle, and bit-identical when repeated (fixed summation order)."""
     wl = configs.make("cfg3")
     st = wl.states[0]
     outs = []
     for _ in range(2):
         eng = b2.Engine(wl.comp, wl.opts, wl.dt)
+        eng.set_sort_interval(10)
         eng.set_state(st)
         eng.step(25)
         outs.append(eng.state())
