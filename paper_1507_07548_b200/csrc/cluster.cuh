@@ -191,6 +191,10 @@ static __global__ void __launch_bounds__(kSC * kCS) k_step_drift_arcs(StepArgs s
 // taken on the i < j side (exact on every row shard).
 constexpr int kGR = 4;       // rows per i-group
 constexpr int kGWarps = 4;   // warps (i-groups) per CTA
+// 7 CTAs (28 warps) per SM: cfg3's 4096 groups still fit one wave, and the
+// 72 registers this allows beat 64 at 8 CTAs/SM (10.7k vs 9.5k steps/s; 6
+// CTAs / 80 registers: 10.5k)
+constexpr int kGMinBlocks = 7;
 constexpr int kGList = 256;  // per-warp chunk of surviving clusters (+1: odd-tail pad)
 constexpr int kGDepth = 4;   // staged cluster pairs in flight per warp (power of 2)
 
@@ -320,7 +324,7 @@ __device__ __forceinline__ void cpair_walk(const ClusterArgs& ca, const double4*
 }
 
 template <bool MULTI_SPECIES, bool WRAPPED, bool VDERIV>
-__global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, ClusterArgs ca) {
+__global__ void __launch_bounds__(kGWarps * 32, kGMinBlocks) k_force_cpair(ForceArgs a, ClusterArgs ca) {
   __shared__ int clist[kGWarps][kGList + 1];
   __shared__ __align__(128) double4 stage[kGWarps][kGDepth][2][kCS];
   const SysDev& s = a.s;
@@ -421,7 +425,7 @@ __global__ void __launch_bounds__(kGWarps * 32, 8) k_force_cpair(ForceArgs a, Cl
 // where `kinetic` is set, (e_kin_i - h) v_i.  In-range lanes only carry
 // terms (ir6 = 0 elsewhere); per-row lane sums by a fixed xor tree.
 template <bool WRAPPED>
-__global__ void __launch_bounds__(kGWarps * 32, 8) k_heat_flux_cpair(FluxArgs fa, ClusterArgs ca) {
+__global__ void __launch_bounds__(kGWarps * 32, kGMinBlocks) k_heat_flux_cpair(FluxArgs fa, ClusterArgs ca) {
   __shared__ int clist[kGWarps][kGList + 1];
   __shared__ __align__(128) double4 stage[kGWarps][kGDepth][2][kCS];
   const ForceArgs& a = fa.f;
