@@ -190,7 +190,11 @@ int b2md_sync(b2md_ctx* ctx);
 /* Raw upload of a complete dynamic state including the cached forces and
  * torques of that state — no wrap, no force evaluation (the data part of
  * tmd::Engine::restore_dynamic, src/engine.cpp:520-540).  NULL keeps the
- * device copy of that array. */
+ * device copy of that array.  The call is asynchronous on the context's
+ * stream: pinned (device-accessible) host buffers are read by the device
+ * AFTER it returns, so they must stay valid and unmodified until the next
+ * synchronising call on the context (b2md_sync, b2md_get_state, b2md_step).
+ * Pageable buffers are staged before it returns. */
 int b2md_upload_state(b2md_ctx* ctx, const double* pos, const double* orient, const double* vel,
                       const double* ang_vel, const double* force, const double* torque);
 

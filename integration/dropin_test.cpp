@@ -101,8 +101,17 @@ int main() {
     GpuEngine gpu(comp, opts, 0.002);
     ref.set_state(st);
     gpu.set_state(st);
-    for (int k = 0; k < 50; ++k) ref.step();
-    gpu.step(50);
+    // Massieu sampling every 5 steps into the reference's own accumulator:
+    // the CPU engine's energies vs the GPU engine's device-side scalars
+    DerivativeAccumulator mref(comp.temperature, comp.volume(), comp.molecule_count(), 2, 10);
+    DerivativeAccumulator mgpu(comp.temperature, comp.volume(), comp.molecule_count(), 2, 10);
+    for (int k = 0; k < 10; ++k) {
+      for (int q = 0; q < 5; ++q) ref.step();
+      gpu.step(5);
+      const EnergyBreakdown& e = ref.state().energy;
+      mref.add(e.total(), e.du_dv(), e.d2u_dv2());
+      gpu.sample_massieu(mgpu);
+    }
     const SystemState a = ref.state(), b = gpu.state();
     double dp = 0.0;
     for (int i = 0; i < comp.molecule_count(); ++i)
@@ -122,6 +131,13 @@ int main() {
     const double js = std::max({1.0, std::abs(jr.x), std::abs(jr.y), std::abs(jr.z)});
     const double dj = std::max({std::abs(jr.x - jg.x), std::abs(jr.y - jg.y), std::abs(jr.z - jg.z)}) / js;
     expect(dj <= 1e-9, "heat flux after 50 steps |dJq| / max |Jq|", dj);
+    // the reference's Massieu estimators from the two sample streams
+    const DerivativeReport ra = mref.finalize(), rg = mgpu.finalize();
+    double dm = 0.0;
+    for (std::size_t k = 0; k < ra.entries.size(); ++k)
+      dm = std::max(dm, std::abs(ra.entries[k].value - rg.entries[k].value) /
+                            std::max(1.0, std::abs(ra.entries[k].value)));
+    expect(mref.samples() == mgpu.samples() && dm <= 1e-8, "Massieu derivatives (GPU scalars)", dm);
 
     // RDF: GPU counts finalized by the reference's own RdfHistogram, on a
     // host state and on the GPU engine's resident state (b = its download)

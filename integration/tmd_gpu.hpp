@@ -17,6 +17,7 @@
 #include "b200md.h"
 #include "tmd/engine.hpp"
 #include "tmd/checkpoint.hpp"
+#include "tmd/massieu.hpp"
 #include "tmd/parallel.hpp"
 #include "tmd/structure.hpp"
 
@@ -197,6 +198,24 @@ class GpuEngine {
   }
 
   b2md_ctx* context() const { return ctx_.get(); }
+
+  // EnergyBreakdown of the resident state (no array download)
+  EnergyBreakdown energy() const {
+    b2md_energy e;
+    b2md_detail::check(b2md_get_state(ctx_.get(), nullptr, nullptr, nullptr, nullptr, nullptr,
+                                      nullptr, &e, nullptr));
+    EnergyBreakdown out;
+    b2md_detail::from_c(e, out);
+    return out;
+  }
+
+  // Engine::sample_extended_step's Massieu sample (engine.cpp:228-229): the
+  // device-side U, dU/dV and d2U/dV2 fed to the reference's OWN
+  // DerivativeAccumulator (massieu.cpp:53-70) -- the estimator stays host code
+  void sample_massieu(DerivativeAccumulator& acc) const {
+    const EnergyBreakdown e = energy();
+    acc.add(e.total(), e.du_dv(), e.d2u_dv2());
+  }
 
   // checkpoint state block (engine.cpp:432-441) of the device state, for
   // Engine::checkpoint_bytes; restore = restore_dynamic's state part + forces

@@ -16,10 +16,7 @@ from .forcefield import (
     nccl_unique_id,
     shard_plan,
 )
-from .checkpoint import BlockStat, ByteReader, ByteWriter, EngineCheckpoint
-from .sampling import DerivativeAccumulator, accumulate_scalars
-from .structure import (RdfHistogram, RdfTable, finalize_tables, first_minimum, rdf_site_types,
-                        serialize_counts, solvation_number)
+from .structure import RdfHistogram, rdf_site_types, serialize_counts
 from .model import (
     ElectrostaticsMethod,
     EnergyBreakdown,

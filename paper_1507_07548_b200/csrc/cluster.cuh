@@ -362,7 +362,9 @@ __global__ void __launch_bounds__(kGWarps * 32, kGMinBlocks) k_force_cpair(Force
       const double ir6 = in ? t6 : 0.0;
       double fs;
       if constexpr (MULTI_SPECIES) {
-        const int sj = s.sp_slot[roff + j];
+        // lanes past the last slot (partial / odd-tail pad cluster) have no
+        // species: their ir6 is 0, any valid species index keeps c12, c6 finite
+        const int sj = in ? s.sp_slot[roff + j] : si;
         const DevPairInfo& pinfo = s.tab->pair[(i < j) ? si * s.ns + sj : sj * s.ns + si];
         const double c12 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c12 : 0.0;
         const double c6 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c6 : 0.0;

@@ -802,6 +802,7 @@ int launch_prof_graph(b2md_ctx* c) {
 // bit matrix always matches the current slot order); that step is issued
 // eagerly, all others as graphs.
 int run_steps(b2md_ctx* c, int64_t nsteps) {
+  c->state_in_box = true;  // every step's drift wraps before anything reads the positions
   const bool graphs = c->use_graphs && !c->profile;
   if (nsteps == 1 && c->use_graphs && !sort_due(c)) {
     ++c->steps_since_sort;
@@ -1405,6 +1406,7 @@ int b2md_evaluate(b2md_ctx* c, const double* pos, const double* orient, double* 
     return set_err(B2MD_INVALID_ARGUMENT, "evaluate: orientations required for multi-site species");
   }
   set_wrapped(c, false);
+  c->state_in_box = false;
   if (c->sort_interval > 0) TRY(resort(c));
   TRY(enqueue_forces(c, true));
   if (force) TRY(download_aos(c, 4, force, 3, c->st.fx, c->st.fy, c->st.fz, nullptr));
@@ -1429,6 +1431,7 @@ int b2md_set_state(b2md_ctx* c, const double* pos, const double* orient, const d
   k_wrap<<<(3 * nt + 255) / 256, 256, 0, c->stream>>>(c->st.px, 3 * nt, c->t.box);
   CU(cudaGetLastError());
   set_wrapped(c, true);
+  c->state_in_box = true;
   const int big = INT_MAX;
   CU(cudaMemcpyAsync(c->d_error, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   if (c->sort_interval > 0) TRY(resort(c));
@@ -1479,8 +1482,12 @@ int b2md_upload_state(b2md_ctx* c, const double* pos, const double* orient, cons
   if (torque) spec[n++] = {torque, 3, {c->st.tx, c->st.ty, c->st.tz, nullptr}};
   TRY(upload_arrays(c, spec, n));
   if (pos) c->mask_valid = false;
-  // steps wrap before every evaluation, so step-time forces may use the fast path
+  // steps wrap before every evaluation, so step-time forces may use the fast
+  // path; the uploaded positions themselves are taken as given (no wrap), so
+  // consumers of the current state (heat flux) use the exact minimum image
+  // until a step has wrapped them
   set_wrapped(c, true);
+  if (pos) c->state_in_box = false;
   c->state_valid = true;
   return B2MD_OK;
 }

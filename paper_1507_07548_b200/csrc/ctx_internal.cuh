@@ -100,7 +100,9 @@ struct b2md_ctx {
   double dt = 0.0;
   bool engine = false;
   bool state_valid = false;
-  bool positions_wrapped = false;  // device positions lie in [0, L)
+  bool positions_wrapped = false;  // step-time positions lie in [0, L) (the drift wraps first)
+  bool state_in_box = false;       // the CURRENT device positions lie in [0, L)
+                                   // (false after a raw upload / restore until a step wraps)
   // device tables
   DevTables* d_tab = nullptr;
   int* d_species_of = nullptr;

@@ -21,8 +21,12 @@ int launch_heat_flux(b2md_ctx* c, const double* enthalpy) {
   a.f = force_args(c);
   for (int k = 0; k < kMaxSpecies; ++k) a.enthalpy[k] = k < c->t.ns ? enthalpy[k] : 0.0;
   a.out = c->d_flux;
-  a.kinetic = c->rank == 0 ? 1 : 0;
-  const bool w = fast_min_image(c);
+  // the generic walk visits every row on every rank: rank 0 adds the
+  // kinetic term; the cluster walk visits only this rank's rows (disjoint
+  // over ranks), so each rank adds it for its own rows
+  a.kinetic = (c->rank == 0 || flux_cluster(c)) ? 1 : 0;
+  // positions after a raw upload / restore may lie outside [0, L)
+  const bool w = fast_min_image(c) && c->state_in_box;
   if (flux_cluster(c)) {
     const ClusterArgs ca = cluster_args(c);
     dim3 pgrid(cpair_grid(c), c->R);
@@ -119,6 +123,7 @@ int b2md_heat_flux_state(b2md_ctx* c, const double* pos, const double* orient, c
   TRY(upload_aos(c, 2, vel, 3, c->st.vx, c->st.vy, c->st.vz, nullptr));
   TRY(upload_aos(c, 3, ang_vel, 3, c->st.wx, c->st.wy, c->st.wz, nullptr));
   set_wrapped(c, false);  // the reference takes the positions as given
+  c->state_in_box = false;
   if (c->sort_interval > 0)
     TRY(resort_and_stage(c));
   else {
@@ -296,6 +301,7 @@ int b2md_restore_state_block(b2md_ctx* c, int replica, const uint8_t* buf, size_
   TRY(enqueue_forces(c, true));
   CU(cudaStreamSynchronize(c->stream));
   set_wrapped(c, true);  // steps wrap before every later evaluation
+  c->state_in_box = false;  // restored as given (no wrap) until a step wraps
   c->state_valid = true;
   return B2MD_OK;
 }

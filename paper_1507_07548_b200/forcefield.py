@@ -347,25 +347,6 @@ class Engine:
         """restore_dynamic's state part + compute_forces (engine.cpp:479-491, 540)."""
         check(_abi.lib().b2md_restore_state_block(self._c.ctx, replica, block, len(block)))
 
-    def checkpoint_bytes(self, meta=None, replica: int = 0) -> bytes:
-        """Engine::checkpoint_bytes: `meta` (an EngineCheckpoint: header,
-        counters, RNG, statistics, sampler sections) with this engine's
-        device state; default: the metadata of a freshly constructed engine
-        with seed 0."""
-        from .checkpoint import EngineCheckpoint
-        meta = meta if meta is not None else EngineCheckpoint.fresh(0)
-        meta.set_state_block(self.state_block(replica))
-        return meta.to_bytes()
-
-    def restore_checkpoint(self, data: bytes, replica: int = 0):
-        """Parses a checkpoint (the container header, then restore_dynamic's
-        reads) and restores its state into `replica`; returns the
-        EngineCheckpoint with the host-side metadata."""
-        from .checkpoint import EngineCheckpoint
-        meta = EngineCheckpoint.from_bytes(data, self._c.n)
-        self.restore_state_block(meta.state_block(), replica)
-        return meta
-
     def heat_fluxes(self, h_per_species) -> np.ndarray:
         """(replicas, 3) J_q of the device-resident state (what Engine::run
         samples every n_ext steps, src/engine.cpp:235-238)."""

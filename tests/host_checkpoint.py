@@ -1,4 +1,6 @@
-"""Checkpoint / restart byte format of tmd::Engine (src/engine.cpp:420-541,
+"""TEST INFRASTRUCTURE (not the product): the checkpoint container of
+tmd::Engine restated to check the device state block inside the reference's
+full checkpoint bytes.  Checkpoint / restart byte format of tmd::Engine (src/engine.cpp:420-541,
 include/tmd/checkpoint.hpp:15-100, src/results.cpp:39-57).
 
 The container is host data except its state block (u32 n, f64 box, 13 x f64
@@ -16,8 +18,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .configs import Rng
-from .errors import IoError
+from paper_1507_07548_b200.configs import Rng
+from paper_1507_07548_b200.errors import IoError
 
 MAGIC = b"TMDCKPT1"
 VERSION = 1
@@ -299,3 +301,19 @@ class EngineCheckpoint:
         if r.bytes(4) != b"END!":
             raise IoError("checkpoint: missing end marker")
         return c
+
+
+def checkpoint_bytes(engine, meta=None, replica: int = 0) -> bytes:
+    """Engine::checkpoint_bytes: `meta` (header, counters, RNG, statistics,
+    sampler sections) around the engine's device-packed state block."""
+    meta = meta if meta is not None else EngineCheckpoint.fresh(0)
+    meta.set_state_block(engine.state_block(replica))
+    return meta.to_bytes()
+
+
+def restore_checkpoint(engine, data: bytes, replica: int = 0):
+    """Parses a checkpoint container and restores its state block into the
+    engine's `replica` on the device; returns the host-side metadata."""
+    meta = EngineCheckpoint.from_bytes(data, engine._c.n)
+    engine.restore_state_block(meta.state_block(), replica)
+    return meta

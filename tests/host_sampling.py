@@ -1,4 +1,6 @@
-"""Scalar sampling of tmd::Engine::run (src/engine.cpp:218-229) and the
+"""TEST INFRASTRUCTURE (not the product): the reference's host samplers
+restated to check the device scalars against the reference's bytes.
+Scalar sampling of tmd::Engine::run (src/engine.cpp:218-229) and the
 Massieu derivative accumulator it feeds (src/massieu.cpp:9-70, 148-190):
 host arithmetic on the few scalars a step produces on the device (kinetic
 energies, U, dU/dV, d2U/dV2, virial).  The reference's operation order is
@@ -9,8 +11,8 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
-from .checkpoint import BlockStat, ByteReader, ByteWriter
-from .errors import ConfigError, IoError, NumericalError
+from host_checkpoint import BlockStat, ByteReader, ByteWriter
+from paper_1507_07548_b200.errors import ConfigError, IoError, NumericalError
 
 
 def block_stat_add(b: BlockStat, x: float) -> None:

@@ -10,7 +10,8 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from paper_1507_07548_b200 import BlockStat, ByteReader, ByteWriter, EngineCheckpoint, IoError
+from host_checkpoint import BlockStat, ByteReader, ByteWriter, EngineCheckpoint
+from paper_1507_07548_b200 import IoError
 
 import golden_cases
 

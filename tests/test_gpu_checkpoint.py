@@ -18,6 +18,8 @@ import paper_1507_07548_b200 as b2
 from oracle import pyoracle
 from paper_1507_07548_b200 import configs
 
+from host_checkpoint import EngineCheckpoint, checkpoint_bytes, restore_checkpoint
+
 import golden_cases
 
 pytestmark = pytest.mark.gpu
@@ -32,22 +34,22 @@ def test_fresh_engine_checkpoint_equals_reference():
     comp, opts, st = golden_cases.eval_cases()["two_clj"]
     eng = b2.Engine(comp, opts, 0.002)
     eng.set_state(st)
-    meta = b2.EngineCheckpoint.fresh(int(G["fresh_seed"]), n_blocks=10, n_production=0)
-    assert eng.checkpoint_bytes(meta) == G["fresh_two_clj"].tobytes()
+    meta = EngineCheckpoint.fresh(int(G["fresh_seed"]), n_blocks=10, n_production=0)
+    assert checkpoint_bytes(eng, meta) == G["fresh_two_clj"].tobytes()
 
 
 def test_restore_reference_checkpoint():
     comp, opts, _ = golden_cases.eval_cases()["water_ions"]
     data = G["sampled_water"].tobytes()
     eng = b2.Engine(comp, opts, 0.0005)
-    meta = eng.restore_checkpoint(data)
+    meta = restore_checkpoint(eng, data)
     s = eng.state()
     assert np.array_equal(records(s), meta.state)  # restore does not wrap (engine.cpp:483-491)
     ref = pyoracle.OracleFF(comp, opts).evaluate(meta.state[:, 0:3], meta.state[:, 3:7])
     scale = max(1.0, np.abs(ref["force"]).max())
     assert np.abs(s.force - ref["force"]).max() <= 1e-10 * scale
     assert np.abs(s.torque - ref["torque"]).max() <= 1e-10 * max(1.0, np.abs(ref["torque"]).max())
-    assert eng.checkpoint_bytes(meta) == data
+    assert checkpoint_bytes(eng, meta) == data
 
 
 @pytest.mark.parametrize("cfg,sort", [("cfg1", 0), ("cfg3", 0), ("cfg3", 100)])
@@ -57,11 +59,11 @@ def test_restart_continues_the_trajectory(cfg, sort):
     a.set_sort_interval(sort)
     a.set_state(wl.states[0])
     a.step(7)
-    data = a.checkpoint_bytes()
+    data = checkpoint_bytes(a)
     a.step(9)
     b = b2.Engine(wl.comp, wl.opts, wl.dt)
     b.set_sort_interval(sort)
-    b.restore_checkpoint(data)
+    restore_checkpoint(b, data)
     b.step(9)
     ra, rb = records(a.state()), records(b.state())
     if sort == 0:
@@ -90,7 +92,7 @@ def test_restore_errors():
     eng = b2.Engine(comp, opts, 0.002)
     eng.set_state(st)
     with pytest.raises(b2.IoError, match="molecule count mismatch"):
-        eng.restore_checkpoint(G["sampled_water"].tobytes())
+        restore_checkpoint(eng, G["sampled_water"].tobytes())
     block = eng.state_block()
     with pytest.raises(b2.IoError, match=r"truncated or corrupted data \(need 8 bytes at offset 116\)"):
         eng.restore_state_block(block[:120])

@@ -16,11 +16,20 @@ import paper_1507_07548_b200 as b2
 from oracle import pyoracle
 from paper_1507_07548_b200 import configs
 
+import host_rdf
+
 import golden_cases
 from test_rdf_oracle import flatten, lj_fluid
 
 pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def finalize(h, replica=0):
+    """The device counts through the reference's finalize arithmetic
+    (structure.cpp:78-128; tests/host_rdf.py, pinned to the reference)."""
+    counts, snaps = h.counts(replica)
+    return host_rdf.finalize_tables(h.comp, h.types, h.bin_width, h.r_max, counts, snaps)
 
 
 def state_of(comp, pos, orient):
@@ -41,7 +50,7 @@ def test_golden_rdf(name):
     assert snaps == int(g["snapshots"])
     assert np.array_equal(counts, g["counts"])
     if int(g["counts"].size):
-        assert np.array_equal(flatten(h.finalize()), g["finalize"])
+        assert np.array_equal(flatten(finalize(h)), g["finalize"])
     assert h.serialize() == g["serialized"].tobytes()
 
 
@@ -127,7 +136,7 @@ def test_single_pair_bin():  # :10-32
     comp = lj_fluid(2, 10.0)
     h = b2.RdfHistogram(b2.ForceField(comp, b2.ForceFieldOptions(cutoff=2.5)), 0.05, 5.0)
     h.accumulate(state_of(comp, [[2.0, 2, 2], [2.0, 2, 3.234]], [[1.0, 0, 0, 0]] * 2))
-    t = h.finalize()[0]
+    t = finalize(h)[0]
     nz = [b for b, g in enumerate(t.g) if g > 0.0]
     assert nz == [int(1.234 / 0.05)]
     assert t.n_cum[-1] == pytest.approx(1.0)
@@ -142,7 +151,7 @@ def test_fcc_first_shell_twelve_neighbours():  # :51-76
     h = b2.RdfHistogram(b2.ForceField(comp, b2.ForceFieldOptions(cutoff=2.0)), 0.02,
                         0.5 * comp.box_length)
     h.accumulate(state_of(comp, pos, [[1.0, 0, 0, 0]] * len(pos)))
-    t = h.finalize()[0]
+    t = finalize(h)[0]
     first = next(b for b, g in enumerate(t.g) if g > 0.0)
     assert abs(first - int(a / math.sqrt(2.0) / 0.02)) <= 1
     assert t.n_cum[first] == pytest.approx(12.0, rel=1e-12)
@@ -158,7 +167,7 @@ def test_ideal_gas_and_counting_identities():  # :79-101, :147-217
     for _ in range(400):
         pos = rng.uniform(0, L, size=(n, 3))
         h.accumulate(state_of(comp, pos, np.tile([1.0, 0, 0, 0], (n, 1))))
-    t = h.finalize()[0]
+    t = finalize(h)[0]
     for r, g in zip(t.r_mid, t.g):
         if 0.2 * 0.5 * L <= r <= 0.5 * L:
             assert g == pytest.approx(1.0, rel=0.02)
@@ -175,8 +184,8 @@ def test_ideal_gas_and_counting_identities():  # :79-101, :147-217
         r = np.sqrt((d * d).sum(-1))
         direct += float(((r < 1.5) & (r > 0)).sum())
     direct /= 25 * n
-    t = h.finalize()[0]
-    assert b2.solvation_number(t, t.partner_density, 1.5) == pytest.approx(direct, rel=1e-10)
+    t = finalize(h)[0]
+    assert host_rdf.solvation_number(t, t.partner_density, 1.5) == pytest.approx(direct, rel=1e-10)
     assert t.n_cum[int(1.5 / 0.05) - 1] == pytest.approx(direct, rel=1e-10)
 
 
@@ -189,7 +198,7 @@ def test_dummy_and_charge_sites():  # :219-261
     rng = np.random.default_rng(6)
     q = rng.normal(size=(20, 4))
     h.accumulate(state_of(comp, rng.uniform(0, 6, size=(20, 3)), q / np.linalg.norm(q, axis=1)[:, None]))
-    assert len(h.finalize()) == 3
+    assert len(finalize(h)) == 3
     ion = b2.build_species("ion_pair", [b2.make_charge_site(0.2, 0, 0, 0.5, 1.0),
                                         b2.make_charge_site(-0.2, 0, 0, -0.5, 1.0),
                                         b2.make_lj_site(0, 0, 0, 1, 1, 1)])
@@ -205,4 +214,4 @@ def test_rdf_validation():  # :263-269
         with pytest.raises(b2.ConfigError):
             b2.RdfHistogram(ff, bw, rmax)
     with pytest.raises(b2.Error, match="no snapshots"):
-        b2.RdfHistogram(ff, 0.02, 3.0).finalize()
+        finalize(b2.RdfHistogram(ff, 0.02, 3.0))

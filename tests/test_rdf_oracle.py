@@ -20,14 +20,12 @@ from paper_1507_07548_b200 import (
     SystemComposition,
     build_species,
     configs,
-    finalize_tables,
-    first_minimum,
     make_charge_site,
     make_lj_site,
     rdf_site_types,
     serialize_counts,
-    solvation_number,
 )
+from host_rdf import finalize_tables, first_minimum, solvation_number
 
 import golden_cases
 
@@ -136,7 +134,7 @@ def test_first_minimum_and_solvation_closed_forms():  # test_structure.cpp:131-1
     g = [1.0 + 1.8 * math.exp(-30.0 * (x - 1.1) ** 2) - 0.6 * math.exp(-25.0 * (x - 1.6) ** 2) for x in r]
     assert first_minimum(r, g) == pytest.approx(1.6, rel=0.02 / 1.6 + 0.02)
     assert math.isnan(first_minimum(r, [1.0] * 150))
-    from paper_1507_07548_b200 import RdfTable
+    from host_rdf import RdfTable
     t = RdfTable(bin_width=0.05, g=[1.0] * 100)
     assert solvation_number(t, 0.7, 1.5) == pytest.approx(4.0 / 3.0 * math.pi * 0.7 * 1.5 ** 3, rel=1e-12)
     t.g = [0.0] * 100

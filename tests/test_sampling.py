@@ -13,7 +13,9 @@ import numpy as np
 import pytest
 
 from oracle import pyoracle
-from paper_1507_07548_b200 import BlockStat, ByteReader, ByteWriter, DerivativeAccumulator, configs
+from host_checkpoint import BlockStat, ByteReader, ByteWriter
+from host_sampling import DerivativeAccumulator
+from paper_1507_07548_b200 import configs
 
 G = np.load(Path(__file__).resolve().parent / "golden" / "sampling.npz")
 needs_ref = pytest.mark.skipif(not pyoracle.ref_available(), reason="oracle/_ref not built")
