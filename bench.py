@@ -50,6 +50,10 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-flush", action="store_true")
+    p.add_argument("--equil", type=int, default=-1,
+                   help="untimed equilibration steps before the timed region (-1: 1000 for cfg3, "
+                        "else 0); with a re-sort interval the count is padded so the first timed "
+                        "step re-sorts")
     p.add_argument("--op", default="step", choices=["step", "heat_flux", "rdf"],
                    help="step: Engine::step (the north_star path); heat_flux: tmd::heat_flux, "
                         "rdf: RdfHistogram::accumulate (SURVEY 8(f) rows 1-2) of the set state")
@@ -63,11 +67,47 @@ def dist_env():
     return rank, world, local
 
 
-def workload(name, rank, world):
+def workload(name, rank, world, species_builder=None):
     from paper_1507_07548_b200 import configs
     if name == "cfg4":  # replicas only: 8 independent replicas per rank
-        return configs.make("cfg4", replicas=8, first_seed=8 * rank)
-    return configs.make(name)
+        return configs.make("cfg4", replicas=8, first_seed=8 * rank, species_builder=species_builder)
+    return configs.make(name, species_builder=species_builder)
+
+
+def physical_cores():
+    """Physical cores of the host (W = all physical cores)."""
+    try:
+        import psutil
+        n = psutil.cpu_count(logical=False)
+        if n:
+            return int(n)
+    except Exception:
+        pass
+    cores = set()
+    try:
+        phys = core = None
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("physical id"):
+                phys = line.split(":")[1].strip()
+            elif line.startswith("core id"):
+                core = line.split(":")[1].strip()
+            elif not line.strip() and core is not None:
+                cores.add((phys, core))
+                phys = core = None
+    except OSError:
+        pass
+    return len(cores) or (os.cpu_count() or 1)
+
+
+def product_libs_loaded():
+    """The repo's own native libraries mapped into this process (the reference
+    arm must map none of them)."""
+    try:
+        maps = open("/proc/self/maps").read()
+    except OSError:
+        return []
+    return sorted({ln.split()[-1] for ln in maps.splitlines()
+                   if "libb200md" in ln or "paper_1507_07548_b200" in ln})
 
 
 def algorithmic(wl, pairs_in_cutoff):
@@ -126,7 +166,7 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
-def cpu_reference_run(wl, steps_wanted, budget_s, threads):
+def cpu_reference_run(wl, steps_wanted, budget_s, threads, min_steps=1):
     """The reference tmd::Engine (oracle/_ref, built from /root/reference) on the
     host cores: set_state then step() x k, bounded to ~budget_s seconds."""
     from oracle import pyoracle
@@ -141,7 +181,7 @@ def cpu_reference_run(wl, steps_wanted, budget_s, threads):
     t0 = time.perf_counter()
     eng.step(1)  # warm-up + per-step estimate
     est = time.perf_counter() - t0
-    k = max(1, min(steps_wanted, int(budget_s / max(est, 1e-6))))
+    k = max(min_steps, min(steps_wanted, int(budget_s / max(est, 1e-6))))
     t0 = time.perf_counter()
     eng.step(k)
     dt = time.perf_counter() - t0
@@ -153,13 +193,18 @@ def run_reference_arm(args):
     if rank != 0:
         return
     from oracle import pyoracle
-    wl = workload(args.config, 0, 1)
-    threads = os.cpu_count() or 1
     if not pyoracle.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtmdref.so not built"}))
         return
+    # the same seeded workload, its species built by the reference's own
+    # tmd::build_species: nothing of the product is loaded on this arm
+    wl = workload(args.config, 0, 1, species_builder=pyoracle.ref_species_builder)
+    threads = os.cpu_count() or 1
     # each of the K steps is one reference step; bound the whole run to ~3 min
     value, k, workers = cpu_reference_run(wl, args.steps, 150.0, threads)
+    loaded = product_libs_loaded()
+    if loaded:
+        raise SystemExit(f"reference arm loaded product code: {loaded}")
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -176,8 +221,11 @@ def run_reference_arm(args):
         "data": "synthetic (seeded generator, paper_1507_07548_b200/configs.py)",
         "config": {"workload": f"{args.config}: {describe(wl)}"},
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": workers, "kind": "reference",
-                         "sample": f"{k} tmd::Engine::step calls after set_state, W={workers} threads"},
+                         "physical_cores": physical_cores(),
+                         "sample": f"{k} tmd::Engine::step calls after set_state, W={workers} threads "
+                                   f"(all logical CPUs)"},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_libs_loaded": loaded,
     }
     print(json.dumps(line), flush=True)
 
@@ -248,9 +296,12 @@ def run_op_reference(args):
     if not pyoracle.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtmdref.so not built"}))
         return
-    wl = workload(args.config, 0, 1)
+    wl = workload(args.config, 0, 1, species_builder=pyoracle.ref_species_builder)
     spec = OPS[args.op]
     value, k = cpu_reference_op(args.op, wl, args.steps, 150.0)
+    loaded = product_libs_loaded()
+    if loaded:
+        raise SystemExit(f"reference arm loaded product code: {loaded}")
     line = {
         "impl": "reference", "op": args.op, "metric": spec["metric"], "value": value,
         "unit": spec["unit"], "n_gpus": args.gpus, "steps": k, "warmup": 1, "ms_per_step": 1e3 / value,
@@ -473,15 +524,34 @@ def main():
     stream = torch.cuda.ExternalStream(eng.stream(), device=local)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
-    # ---- warm-up (also instantiates the single-step graphs used below)
+    # ---- warm-up: W steps (single-step graphs instantiated) and one step at
+    # every profiling level the later passes use (their graphs instantiated)
+    done = 0
     for _ in range(max(3, args.warmup)):
         eng.step_async(1)
+        done += 1
     eng.sync()
-    for level in (2, 1):
+    for level in (3, 2, 1):
         eng.profile(True, level)
         eng.step_async(1)
         eng.sync()
         eng.profile(False)
+        done += 1
+    # ---- equilibration away from the lattice start (the cull is tightest on
+    # the ordered start), padded so that the FIRST timed step re-sorts: a
+    # K-step window then holds ceil(K / interval) re-sorts, never fewer than
+    # its share
+    interval, since = eng.sort_interval()
+    equil = args.equil if args.equil >= 0 else (1000 if args.config == "cfg3" else 0)
+    if interval > 0:
+        to_due = interval - since
+        extra = to_due + interval * max(0, -(-(equil - to_due) // interval))
+    else:
+        extra = equil
+    if extra > 0:
+        eng.step_async(extra)
+        eng.sync()
+        done += extra
 
     def timed_pass(steps, flush_between):
         """K single steps, each bracketed by CUDA events on the library's stream."""
@@ -515,18 +585,34 @@ def main():
     energies, stats = eng.energies()
 
     # ---- live kernel timing (CUDA events on the library stream, same step
-    # structure): (1) events around the partner search only, K steps — the
-    # roofline's launch time; (2) events around every kernel, a short pass —
-    # the per-kernel breakdown and launch counts.  Event-record nodes stall the
-    # graph pipeline, so they are kept out of the headline region.
+    # structure, L2 flushed between steps): (1) events around the partner
+    # search only; (2) events around the force kernel only, harvested after
+    # every step -- the roofline's launch time is the MEDIAN per launch; (3)
+    # events around every kernel, a short pass -- the per-kernel breakdown and
+    # launch counts.  Event-record nodes stall the graph pipeline, so they are
+    # kept out of the headline region.
     eng.profile(True, 2)
     timed_pass(args.steps, flush)
     kt_search = eng.kernel_times()
     eng.profile(False)
-    eng.profile(True, 3)
-    timed_pass(args.steps, flush)
-    kt_force = eng.kernel_times()
-    eng.profile(False)
+
+    def per_launch(level, family, steps):
+        eng.profile(True, level)
+        out, prev = [], (0.0, 0)
+        with torch.cuda.stream(stream):
+            for _ in range(steps):
+                eng.step_async(1)
+                ms, n_l = eng.kernel_times().get(family, (0.0, 0))  # harvest (syncs)
+                if n_l > prev[1]:
+                    out.append((ms - prev[0]) / (n_l - prev[1]))
+                prev = (ms, n_l)
+                if flush is not None:
+                    flush.zero_()
+        eng.sync()
+        eng.profile(False)
+        return out
+
+    force_samples = per_launch(3, "force", args.steps)
     n_all = min(args.steps, 50)
     eng.profile(True, 1)
     timed_pass(n_all, flush)
@@ -584,8 +670,7 @@ def main():
     # cutoff; multi-site: 86 per LJ term, counted as if every term of a passing
     # molecule pair were inside rc (an upper bound).
     peak = peak_gflops / 1e3
-    force_ms, force_launches = kt_force.get("force", (0.0, 0))
-    avg_force_s = force_ms * 1e-3 / max(1, force_launches)
+    avg_force_s = statistics.median(force_samples) * 1e-3 if force_samples else 0.0
     single_site = all(sp.n_sites == 1 for sp in wl.comp.species)
     cand = n * (n - 1) // 2 * R
     # cluster walk: no search launches -- the force kernel decides every
@@ -643,6 +728,10 @@ def main():
             "l2": "flushed between timed steps (256 MiB memset outside the per-step events)"
             if flush is not None else "not flushed",
             "timing": "per-step CUDA events on the library stream; max over ranks",
+            "pre_steps": done,
+            "sort": (f"re-sort every {interval} steps; the first timed step re-sorts "
+                     f"({-(-args.steps // interval)} re-sorts in the window)" if interval > 0
+                     else "fixed slot order"),
         },
         "pair_interactions_per_s": pairs_total * args.steps * (world if args.config == "cfg4" else 1)
         / (total_ms * 1e-3),
@@ -663,12 +752,16 @@ def main():
             "traffic": traffic,
             "peak_source": "DFMA microbenchmark measured in this run (MEASURED_PEAKS.json has no fp64 entry)",
             "launch_ms": avg_force_s * 1e3,
+            "launch_ms_stats": ({"median": statistics.median(force_samples), "min": min(force_samples),
+                                 "max": max(force_samples), "launches": len(force_samples)}
+                                if force_samples else None),
             "share_of_step": avg_force_s / max(1e-12, step_s),
             "fp64_pipe_pct_executed": executed,
             "executed_note": "ncu sm__pipe_fp64_cycles_active of the same kernel (profiles/): the fp64 "
                              "work actually issued, vs the algorithmic count above",
-            "launch_timing": "CUDA events around the force kernel only, in a second K-step pass "
-                             "(same graph step structure); ncu launch list in profiles/",
+            "launch_timing": "median of per-launch CUDA-event times around the force kernel only "
+                             "(a second K-step pass, same graph step structure, L2 flushed between "
+                             "steps, profiling graph warmed before); ncu launch list in profiles/",
         },
         "search": ({
             "launch_ms": None,
@@ -695,10 +788,18 @@ def main():
         try:
             from oracle import pyoracle
             if pyoracle.ref_available():
-                threads = os.cpu_count() or 1
-                v, k, w = cpu_reference_run(wl, 10 ** 6, args.cpu_seconds, threads)
-                line["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": w, "kind": "reference",
-                                        "sample": f"{k} tmd::Engine::step of {args.config} at W={w}"}
+                # the reference engine at W = all physical cores (the value) and
+                # at W = 1, on the same workload and starting state
+                phys = physical_cores()
+                v, k, w = cpu_reference_run(wl, 10 ** 6, 0.65 * args.cpu_seconds, phys, min_steps=2)
+                v1, k1, _ = cpu_reference_run(wl, 10 ** 6, 0.35 * args.cpu_seconds, 1, min_steps=1)
+                line["cpu_baseline"] = {
+                    "value": v, "unit": "steps/s", "cores": w, "kind": "reference",
+                    "sample": f"{k} tmd::Engine::step of {args.config} at W={w} (all physical cores) "
+                              f"after set_state of the same start state",
+                    "w1": {"value": v1, "unit": "steps/s", "cores": 1,
+                           "sample": f"{k1} tmd::Engine::step at W=1"},
+                    "logical_cpus": os.cpu_count()}
         except Exception as exc:  # the GPU number stands without it
             line["cpu_baseline"] = {"error": str(exc)}
     print(json.dumps(line), flush=True)

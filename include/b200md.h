@@ -224,6 +224,9 @@ int b2md_set_search_options(b2md_ctx* ctx, int fix_prefilter, int tile_cull);
  * (i, j) order.  Default: 100 for a single species with COM radius < 0.3 L
  * (where the tile cull can use it), else 0. */
 int b2md_set_sort_interval(b2md_ctx* ctx, int steps);
+/* The current interval and the steps taken since the last re-sort (a step
+ * re-sorts when steps_since_sort >= steps > 0). */
+int b2md_get_sort_interval(const b2md_ctx* ctx, int* steps, int* steps_since_sort);
 
 /* Step structure (same results bit for bit; for tests and measurement):
  * fused_kick = 1 runs the end-of-step half kick (engine.cpp:131-142) in the

@@ -136,6 +136,13 @@ def build_species_c(sites, which="oracle") -> _abi.b2md_species:
     return out
 
 
+def ref_species_builder(name, sites):
+    """configs.make(species_builder=...) hook: the reference's own
+    tmd::build_species (oracle/_ref), wrapped as a MoleculeSpecies."""
+    from paper_1507_07548_b200.model import MoleculeSpecies
+    return MoleculeSpecies(name, build_species_c(sites, "ref"))
+
+
 def ewald_tune(delta, cutoff, box, which="oracle"):
     lib = oracle_lib() if which == "oracle" else ref_lib()
     a, k = C.c_double(), C.c_int()

@@ -23,7 +23,7 @@ from .model import (
     Site,
     SystemComposition,
     SystemState,
-    build_species,
+    build_species as _build_species_native,
     kinetic_energy_rot,
     kinetic_energy_trans,
     make_lj_site,
@@ -32,6 +32,16 @@ from .model import (
 )
 
 _M64 = (1 << 64) - 1
+
+# Species builder of the generators: tmd::build_species (src/model.cpp:68-129).
+# Default: b2md_build_species (the native library's bit-exact restatement).
+# bench.py's reference arm swaps in the reference's OWN build_species
+# (oracle/_ref) through `species_builder`, so that arm loads no product code.
+_species_builder = None
+
+
+def build_species(name, sites):
+    return (_species_builder or _build_species_native)(name, sites)
 
 
 class Rng:
@@ -245,7 +255,16 @@ def replica_batch_config(replicas: int = 8, first_seed: int = 0, steps: int = 50
     return wl
 
 
-def make(name: str, **kw) -> Workload:
+def make(name: str, species_builder=None, **kw) -> Workload:
+    """One of the five BASELINE.json configs.  species_builder(name, sites) ->
+    MoleculeSpecies replaces the native build_species (same bits)."""
+    global _species_builder
+    if species_builder is not None:
+        prev, _species_builder = _species_builder, species_builder
+        try:
+            return make(name, **kw)
+        finally:
+            _species_builder = prev
     if name == "cfg0":
         return lj_fluid_config(1000, 0.8, None, seed=kw.get("seed", 0), dt=0.005, steps=100,
                                side=10, name="cfg0")

@@ -41,7 +41,7 @@ int nccl_load() {
 
 const char* kFamilyName[F_COUNT] = {"offsets",  "search", "force",   "ewald_tables", "ewald_sk",
                                     "ewald_force", "kick_kick_drift", "kick_drift", "kick", "allreduce",
-                                    "heat_flux", "rdf", "cluster"};
+                                    "heat_flux", "rdf", "cluster", "force_jsum"};
 
 // AoS <-> SoA staging kernels (host layout Vec3 / Quat of include/tmd/geom.hpp)
 static __global__ void k_aos_to_soa(const double* aos, int count, int width, double* d0, double* d1,
@@ -331,6 +331,7 @@ ForceArgs force_args(b2md_ctx* c) {
   const int hh = hi32(0.5 * c->t.box);
   std::memcpy(&a.thr, &hh, 4);
   a.kick_dt = 0.0;
+  a.rmax2 = c->t.rmax2.empty() ? c->t.rc2 : c->t.rmax2[0];
   a.error_mol = c->d_error;
   return a;
 }
@@ -353,6 +354,10 @@ int rigid_sites(const ModelTables& t) {
   for (int k = 0; full && k < ns * ns; ++k) full = t.lj[0][k].a == k / ns && t.lj[0][k].b == k % ns;
   return full && (ns == 2 || ns == 3) ? ns : 0;
 }
+
+// the once-per-pair block-pair tiles apply (k_force_rigid_tile): the rigid
+// species k_force_rigid handles, records allocated
+bool tile_path(const b2md_ctx* c) { return c->use_tile && c->d_trec && rigid_sites(c->t) > 0; }
 
 // positions known to lie in [0, L) (set_state / step wrap them) and every
 // listed pair's components far from L/2: the branch-free minimum image is exact
@@ -418,6 +423,55 @@ int launch_cluster_force(b2md_ctx* c, bool kick) {
   ForceArgs a = force_args(c);
   if (kick) a.kick_dt = c->dt;
   const bool w = fast_min_image(c), m = c->t.ns > 1, v = a.vderiv != 0;
+  if (c->use_newton) {
+    const size_t nc = size_t(c->nc);
+    PairBuf pb;
+    pb.rec = c->d_prec;
+    pb.irec = c->d_pirec;
+    pb.olist = c->d_polist;
+    pb.ilist = pb.olist + size_t(R) * nc * nc;
+    pb.inslot = pb.ilist + size_t(R) * nc * nc;
+    int* q = c->d_pint;
+    pb.ocnt = q, q += size_t(R) * nc;
+    pb.ustart = q, q += size_t(R) * nc;
+    pb.in_base = q, q += size_t(R) * nc;
+    pb.in_cnt = q, q += size_t(R) * nc;
+    pb.umap = q, q += size_t(R) * c->pb_max_units;
+    pb.units = q, q += R;
+    pb.in_total = q, q += R;
+    pb.next_unit = q, q += R;
+    pb.ticket = reinterpret_cast<unsigned*>(q);
+    pb.max_units = c->pb_max_units;
+    pb.cbeg = int(long(c->nc) * c->rank / std::max(1, c->world));
+    pb.cend = int(long(c->nc) * (c->rank + 1) / std::max(1, c->world));
+    ForceArgs aw = a;
+    aw.kick_dt = 0.0;  // the rows are complete only after k_cpair_jsum
+    PROF(c, F_CLUSTER, (k_cpair_build<<<dim3((c->nc + kBuildWarps - 1) / kBuildWarps, R),
+                                     kBuildWarps * 32, 0, c->stream>>>(a, ca, pb)));
+    // persistent warps taking work units: NW warps per CTA (B2MD_N3_WARPS)
+    const int nw = c->n3_warps;
+    const dim3 ngrid(c->n3_grid, R);
+#define N3_LAUNCH(NW, M, W, V)                                                                   \
+  if (nw == NW && m == M && w == W && v == V)                                                    \
+    PROF(c, F_FORCE, (k_force_cpair_n3<NW, M, W, V><<<ngrid, NW * 32, 0, c->stream>>>(aw, ca, pb)));
+#define N3_NW(NW)                    \
+  N3_LAUNCH(NW, false, true, false)  \
+  N3_LAUNCH(NW, false, true, true)   \
+  N3_LAUNCH(NW, false, false, false) \
+  N3_LAUNCH(NW, false, false, true)  \
+  N3_LAUNCH(NW, true, true, false)   \
+  N3_LAUNCH(NW, true, true, true)    \
+  N3_LAUNCH(NW, true, false, false)  \
+  N3_LAUNCH(NW, true, false, true)
+    N3_NW(2)
+    N3_NW(4)
+#undef N3_NW
+#undef N3_LAUNCH
+    PROF(c, F_JSUM, (k_cpair_jsum<<<dim3((c->nc + kJsumWarps - 1) / kJsumWarps, R),
+                                    kJsumWarps * 32, 0, c->stream>>>(a, ca, pb)));
+    c->mask_valid = false;
+    return B2MD_OK;
+  }
   dim3 pgrid(cpair_grid(c), R);
 #define CPAIR_LAUNCH(M, W, V) \
   if (m == M && w == W && v == V) \
@@ -435,8 +489,36 @@ int launch_cluster_force(b2md_ctx* c, bool kick) {
   return B2MD_OK;
 }
 
+int launch_tile_force(b2md_ctx* c, bool kick) {
+  ForceArgs a = force_args(c);
+  if (kick) a.kick_dt = c->dt;
+  TileArgs ta;
+  ta.rec = c->d_trec;
+  ta.nb = c->tile_nb;
+  ta.nbp = c->tile_nbp;
+  ta.bp_begin = int(long(c->tile_nbp) * c->rank / std::max(1, c->world));
+  ta.bp_end = int(long(c->tile_nbp) * (c->rank + 1) / std::max(1, c->world));
+  ForceArgs aw = a;
+  aw.kick_dt = 0.0;  // the molecules are complete only after k_rigid_reduce
+  const bool w = fast_min_image(c);
+  const dim3 grid((c->tile_nbp + kTileWarps - 1) / kTileWarps, c->R);
+  const int ns = rigid_sites(c->t);
+  if (ns == 2 && w)
+    PROF(c, F_FORCE, (k_force_rigid_tile<2, true><<<grid, kTileWarps * 32, 0, c->stream>>>(aw, ta)));
+  else if (ns == 2)
+    PROF(c, F_FORCE, (k_force_rigid_tile<2, false><<<grid, kTileWarps * 32, 0, c->stream>>>(aw, ta)));
+  else if (w)
+    PROF(c, F_FORCE, (k_force_rigid_tile<3, true><<<grid, kTileWarps * 32, 0, c->stream>>>(aw, ta)));
+  else
+    PROF(c, F_FORCE, (k_force_rigid_tile<3, false><<<grid, kTileWarps * 32, 0, c->stream>>>(aw, ta)));
+  PROF(c, F_JSUM, (k_rigid_reduce<<<dim3(c->tile_nb, c->R), 192, 0, c->stream>>>(a, ta)));
+  c->mask_valid = false;  // no partner search ran: the bit matrix is built on demand
+  return B2MD_OK;
+}
+
 int launch_force(b2md_ctx* c, bool kick) {
   if (cluster_path(c)) return launch_cluster_force(c, kick);
+  if (tile_path(c)) return launch_tile_force(c, kick);
   ForceArgs a = force_args(c);
   if (kick) a.kick_dt = c->dt;
   a.split = c->force_split;
@@ -565,6 +647,7 @@ int launch_allreduce(b2md_ctx* c) {
 // Results do not depend on the order beyond summation order (pair lists are
 // exported in the reference's (i, j) order).
 int resort(b2md_ctx* c) {
+  NvtxRange nvtx_("b2md_resort");
   const int nt = n_total(c), n = c->t.n;
   const int g = (nt + 255) / 256;
   // columns of cross-section c^2 = 32 / (rho L) (about one 32-slot block
@@ -634,7 +717,7 @@ int enqueue_forces(b2md_ctx* c, bool offsets, bool kick) {
     TRY(launch_ewald_sk(c, c->stream2));
     CU(cudaEventRecord(c->ev_join, c->stream2));
   }
-  if (!cluster_path(c)) TRY(launch_search(c));
+  if (!cluster_path(c) && !tile_path(c)) TRY(launch_search(c));
   TRY(launch_force(c, kick));
   if (fork) {
     CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
@@ -1151,14 +1234,78 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     if (c->nc > 0) c->use_fused_kick = true;
     if (const char* e = std::getenv("B2MD_FUSED_KICK")) c->use_fused_kick = std::atoi(e) != 0;
   }
-  TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars *
-                                 std::max(c->force_grid, c->nc > 0 ? cpair_grid(c) : 0)));
+  // per-CTA scalar partials of the widest force grid: the row walks, the
+  // both-rows cluster walk (kGWarps groups per CTA) and the once-per-pair
+  // walk (down to one cluster per CTA)
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars *
+                                   std::max({c->force_grid, c->nc > 0 ? cpair_grid(c) : 0,
+                                             c->nc > 0 ? sms * kNWarpsPerSM : 0,
+                                             (((c->t.n + 31) / 32) * ((c->t.n + 31) / 32 + 1) / 2 +
+                                              kTileWarps - 1) / kTileWarps})));
+  }
   if (c->nc > 0) {
     c->nsup = (c->nc + kSC - 1) / kSC;
     TRY(dalloc(&c->d_carc, size_t(R) * c->nc));
     TRY(dalloc(&c->d_chalf, size_t(R) * c->nc));
     TRY(dalloc(&c->d_sarc, size_t(R) * c->nsup));
     TRY(dalloc(&c->d_shalf, size_t(R) * c->nsup));
+    // once-per-pair walk: triangular record array (192 B per cluster pair) and
+    // the bitmap (zeroed here; k_cpair_jsum clears what it reads)
+    if (const char* e = std::getenv("B2MD_NEWTON")) c->use_newton = std::atoi(e) != 0;
+    if (const char* e = std::getenv("B2MD_N3_WARPS")) {
+      const int v = std::atoi(e);
+      c->n3_warps = v >= 4 ? 4 : 2;
+    }
+    const size_t pairs = size_t(c->nc) * (c->nc + 1) / 2;
+    if (c->use_newton && size_t(R) * pairs * kCS * 3 * sizeof(double) > (size_t(8) << 30))
+      c->use_newton = false;  // beyond 8 GB of records: the both-rows walk
+    if (c->use_newton) {
+      const size_t nc = size_t(c->nc);
+      // units <= owned pairs / kUnit + one partial unit per cluster
+      c->pb_max_units = int(pairs / kUnit + nc);
+      TRY(dalloc(&c->d_prec, size_t(R) * pairs * kCS * 3));
+      TRY(dalloc(&c->d_pirec, size_t(R) * c->pb_max_units * kCS * 3));
+      TRY(dalloc(&c->d_polist, size_t(R) * nc * nc * 3));  // olist | ilist | inslot
+      const size_t ints = size_t(R) * (5 * nc + c->pb_max_units + 4);
+      TRY(dalloc(&c->d_pint, ints));
+      CU(cudaMemset(c->d_pint, 0, sizeof(int) * ints));
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      c->n3_grid = sms * (kNWarpsPerSM / c->n3_warps);
+      // keep the contribution records (written by the walk, read right after
+      // by k_cpair_jsum) resident in L2: a persisting access-policy window
+      // over the front of the unit-major record array
+      int l2p = 0;  // measured: no gain (B2MD_L2_PERSIST=1 enables)
+      if (const char* e = std::getenv("B2MD_L2_PERSIST")) l2p = std::atoi(e);
+      int maxp = 0, maxw = 0;
+      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, c->device);
+      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
+      if (l2p && maxp > 0 && maxw > 0) {
+        const size_t rec_bytes = size_t(R) * pairs * kCS * 3 * sizeof(double);
+        const size_t want = std::min<size_t>(size_t(maxp), size_t(64) << 20);
+        const size_t win = std::min({rec_bytes, size_t(maxw), size_t(48) << 20});
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.base_ptr = c->d_prec;
+        v.accessPolicyWindow.num_bytes = win;
+        v.accessPolicyWindow.hitRatio = float(std::min(1.0, double(want) / double(win)));
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        if (cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess)
+          cudaGetLastError();  // optional: the records then take the default policy
+      }
+    }
+  }
+  if (rigid_sites(c->t) > 0) {
+    if (const char* e = std::getenv("B2MD_TILE")) c->use_tile = std::atoi(e) != 0;
+    if (c->use_tile) {
+      c->tile_nb = (c->t.n + 31) / 32;
+      c->tile_nbp = c->tile_nb * (c->tile_nb + 1) / 2;
+      TRY(dalloc(&c->d_trec, size_t(R) * c->tile_nbp * 2 * 32 * 6));
+    }
   }
   TRY(dalloc(&c->d_ticket, size_t(2) * R));
   TRY(dalloc(&c->d_flux, size_t(kNumSums) * R));
@@ -1297,7 +1444,8 @@ void free_ctx(b2md_ctx* c) {
                   c->d_uk,    c->d_flux,  c->d_perm, c->d_slot_of, c->d_sp_slot, c->d_sb_slot,
                   c->d_nsites_slot, c->d_scan, c->d_keys[0], c->d_keys[1], c->d_vals[0],
                   c->d_vals[1], c->d_cub, c->d_ke, c->d_thermo_err, c->d_carc,
-                  c->d_chalf, c->d_sarc, c->d_shalf};
+                  c->d_chalf, c->d_sarc, c->d_shalf, c->d_prec, c->d_pirec,
+                  c->d_polist, c->d_pint, c->d_trec};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1377,6 +1525,7 @@ int b2md_shard_plan(int n_molecules, int n_kvectors, int world, int rank, int* r
 
 int b2md_create(int device, const b2md_composition* comp, const b2md_ff_options* opts, double dt,
                 int n_replicas, b2md_ctx** out) {
+  NvtxRange nvtx_("b2md_create");
   if (!comp || !opts || !out) return set_err(B2MD_INVALID_ARGUMENT, "create: null pointer");
   *out = nullptr;
   b2md_ctx* c = new b2md_ctx();
@@ -1397,6 +1546,7 @@ const char* b2md_warning(const b2md_ctx* ctx) { return ctx ? ctx->warning.c_str(
 
 int b2md_evaluate(b2md_ctx* c, const double* pos, const double* orient, double* force,
                   double* torque, b2md_energy* energy, b2md_eval_stats* stats) {
+  NvtxRange nvtx_("b2md_evaluate");
   if (!c || !pos) return set_err(B2MD_INVALID_ARGUMENT, "evaluate: null pointer");
   CU(cudaSetDevice(c->device));
   TRY(upload_aos(c, 0, pos, 3, c->st.px, c->st.py, c->st.pz, nullptr));
@@ -1419,6 +1569,7 @@ int b2md_evaluate(b2md_ctx* c, const double* pos, const double* orient, double* 
 
 int b2md_set_state(b2md_ctx* c, const double* pos, const double* orient, const double* vel,
                    const double* ang_vel) {
+  NvtxRange nvtx_("b2md_set_state");
   if (!c || !pos || !orient || !vel || !ang_vel)
     return set_err(B2MD_INVALID_ARGUMENT, "set_state: null pointer");
   CU(cudaSetDevice(c->device));
@@ -1442,6 +1593,7 @@ int b2md_set_state(b2md_ctx* c, const double* pos, const double* orient, const d
 }
 
 int b2md_step(b2md_ctx* c, int64_t nsteps) {
+  NvtxRange nvtx_("b2md_step");
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "step: null context");
   if (!c->engine) return set_err(B2MD_CONFIG_ERROR, "engine: time step must be positive");
   if (!c->state_valid) return set_err(B2MD_CONFIG_ERROR, "engine: set_state must precede step");
@@ -1452,6 +1604,7 @@ int b2md_step(b2md_ctx* c, int64_t nsteps) {
 }
 
 int b2md_step_async(b2md_ctx* c, int64_t nsteps) {
+  NvtxRange nvtx_("b2md_step_async");
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "step: null context");
   if (!c->engine) return set_err(B2MD_CONFIG_ERROR, "engine: time step must be positive");
   if (!c->state_valid) return set_err(B2MD_CONFIG_ERROR, "engine: set_state must precede step");
@@ -1463,6 +1616,7 @@ int b2md_step_async(b2md_ctx* c, int64_t nsteps) {
 }
 
 int b2md_sync(b2md_ctx* c) {
+  NvtxRange nvtx_("b2md_sync");
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "sync: null context");
   CU(cudaSetDevice(c->device));
   return check_error_flag(c);
@@ -1470,6 +1624,7 @@ int b2md_sync(b2md_ctx* c) {
 
 int b2md_upload_state(b2md_ctx* c, const double* pos, const double* orient, const double* vel,
                       const double* ang_vel, const double* force, const double* torque) {
+  NvtxRange nvtx_("b2md_upload_state");
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "upload_state: null context");
   CU(cudaSetDevice(c->device));
   AosSpec spec[6];
@@ -1494,6 +1649,7 @@ int b2md_upload_state(b2md_ctx* c, const double* pos, const double* orient, cons
 
 int b2md_get_state(b2md_ctx* c, double* pos, double* orient, double* vel, double* ang_vel,
                    double* force, double* torque, b2md_energy* energy, b2md_eval_stats* stats) {
+  NvtxRange nvtx_("b2md_get_state");
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "get_state: null context");
   CU(cudaSetDevice(c->device));
   AosSpec spec[6];
@@ -1539,7 +1695,15 @@ int b2md_set_sort_interval(b2md_ctx* c, int steps) {
   return B2MD_OK;
 }
 
+int b2md_get_sort_interval(const b2md_ctx* c, int* steps, int* steps_since_sort) {
+  if (!c) return set_err(B2MD_INVALID_ARGUMENT, "get_sort_interval: null context");
+  if (steps) *steps = c->sort_interval;
+  if (steps_since_sort) *steps_since_sort = c->steps_since_sort;
+  return B2MD_OK;
+}
+
 int b2md_pair_list(b2md_ctx* c, int replica, int32_t* pairs, int64_t capacity, int64_t* n_pairs) {
+  NvtxRange nvtx_("b2md_pair_list");
   if (!c || !n_pairs) return set_err(B2MD_INVALID_ARGUMENT, "pair_list: null pointer");
   if (replica < 0 || replica >= c->R) return set_err(B2MD_INVALID_ARGUMENT, "pair_list: bad replica");
   CU(cudaSetDevice(c->device));

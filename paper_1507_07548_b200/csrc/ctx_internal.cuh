@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <dlfcn.h>
 #include <algorithm>
 #include <cub/cub.cuh>
@@ -23,6 +24,15 @@
 #include "cluster.cuh"
 #include "model.hpp"
 #include "search_geometry.hpp"
+
+// NVTX range over one C-ABI call (header-only NVTX3: free unless a tool such as
+// nsys / ncu --nvtx attaches): the tracing hook of SURVEY 5
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace b2md_host {
 using namespace b2md;
@@ -80,7 +90,7 @@ int dalloc(T** p, size_t count) {
 }
 
 enum Family { F_OFFSETS, F_SEARCH, F_FORCE, F_EWALD_TAB, F_EWALD_SK, F_EWALD_F, F_KICK_KICK_DRIFT,
-              F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_HEAT_FLUX, F_RDF, F_CLUSTER, F_COUNT };
+              F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_HEAT_FLUX, F_RDF, F_CLUSTER, F_JSUM, F_COUNT };
 extern const char* kFamilyName[F_COUNT];
 
 }  // namespace b2md_host
@@ -123,6 +133,21 @@ struct b2md_ctx {
   float4* d_chalf = nullptr;  // R * nc arc half extents
   uint4* d_sarc = nullptr;    // R * nsup
   float4* d_shalf = nullptr;  // R * nsup
+  // once-per-pair walk (k_force_cpair_n3 + k_cpair_jsum): contribution records
+  // and their bitmap (B2MD_NEWTON=0: the both-rows walk k_force_cpair)
+  bool use_newton = false;     // B2MD_NEWTON=1: measured slower on cfg3 (DESIGN 5)
+  double* d_prec = nullptr;    // R * nc (nc + 1) / 2 * 24 doubles
+  double* d_pirec = nullptr;   // R * pb_max_units * 24 doubles
+  int* d_polist = nullptr;     // R * nc * nc * 3: owned lists | owner lists | slot map
+  int* d_pint = nullptr;       // per-cluster counts / bases, unit map, counters
+  int pb_max_units = 0;
+  int n3_grid = 0;             // persistent CTAs per replica of k_force_cpair_n3
+  // rigid single-species LJ molecules: once-per-pair block-pair tiles
+  // (k_force_rigid_tile + k_rigid_reduce; B2MD_TILE=0: search + k_force_rigid)
+  bool use_tile = false;
+  double* d_trec = nullptr;    // R * nbp * 2 * 32 * 6
+  int tile_nb = 0, tile_nbp = 0;
+  int n3_warps = 4;            // warps per CTA of the persistent k_force_cpair_n3
   double* d_cta_part = nullptr;  // force-kernel per-CTA scalar partials
   unsigned* d_ticket = nullptr;   // 2 * R: force, ewald
   int force_grid = 1;

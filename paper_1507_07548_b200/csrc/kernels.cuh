@@ -752,6 +752,7 @@ struct ForceArgs {
   // fused end-of-step half kick (kick_one) in the row epilogue: dt > 0 when
   // the forces are complete after this kernel (no Ewald term, no all-reduce)
   double kick_dt;
+  double rmax2;  // single-species COM radius^2 (rc + 2 reach)^2 (potentials.cpp:211-212)
   int* error_mol;
   int split;  // warps per row (row-split kernels)
 };
@@ -1366,6 +1367,229 @@ __global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a
   double v[kNumRowScalars] = {warp_sum(ulj), 0.0, 0.0, warp_sum(s1),
                               warp_sum(s2),  warp_sum(vir), warp_sum(cnt)};
   finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
+}
+
+// ------------------------- rigid molecules, once per pair (Newton's third law)
+// evaluate_pair_range (potentials.cpp:204-242) for one species of NS LJ sites
+// (2CLJ: BASELINE cfg1, cfg4), every molecule pair evaluated ONCE -- the
+// reference's own scheme (F_i += f, F_j -= f) -- with the partner side
+// accumulated without atomics:
+// * one warp per 32 x 32 block pair (BI <= BJ) of slots; lane l owns
+//   molecule BI*32 + l (position and site offsets in registers, force and
+//   torque accumulated in registers); the J block's positions and offsets
+//   are staged in shared memory;
+// * step k pairs lane l with j = (l + k) & 31 (k = 0..31; 1..16 on the
+//   diagonal block, k = 16 on lanes < 16 only), so in every step the 32
+//   lanes touch 32 distinct partners: each lane adds the pair's partner-side
+//   force and torque into the partner's shared-memory accumulator without
+//   conflicts, in step order (deterministic);
+// * each pair is computed in the reference's orientation (the lower
+//   external index is i: R = min_image(com_i - com_j), site vectors
+//   (R + d_a) - d_b, exactly as k_force_rigid), so COM and site cutoffs are
+//   decided on the reference's bits; energy, virial, s1, s2 once per pair;
+// * the block pair writes two records (32 molecules x force, torque): the
+//   I side and the J side; k_rigid_reduce sums each block's records in a
+//   fixed order (block-pair order) -- the per-pair contribution buffer and
+//   segmented reduction of the north star, at block-pair granularity.
+constexpr int kTileWarps = 4;
+
+struct TileArgs {
+  double* rec;   // R * nbp * 2 records of 32 x 6 doubles: [bp][side][lane][fx fy fz tx ty tz]
+  int nb;        // 32-slot blocks per replica
+  int nbp;       // block pairs per replica nb (nb + 1) / 2
+  int bp_begin, bp_end;  // this rank's block pairs (row shard)
+};
+
+__device__ __forceinline__ void tile_of(int bp, int nb, int& bi, int& bj) {
+  // bp = bi nb - bi (bi - 1) / 2 + (bj - bi): invert over the rows
+  int lo = 0, hi = nb - 1;
+  while (lo < hi) {  // largest bi with start(bi) <= bp
+    const int mid = (lo + hi + 1) >> 1;
+    const int st = mid * nb - ((mid * (mid - 1)) >> 1);
+    if (st <= bp) lo = mid; else hi = mid - 1;
+  }
+  bi = lo;
+  bj = bi + (bp - (bi * nb - ((bi * (bi - 1)) >> 1)));
+}
+
+template <int NS, bool WRAPPED>
+__global__ void __launch_bounds__(kTileWarps * 32, 4) k_force_rigid_tile(ForceArgs a, TileArgs ta_) {
+  constexpr int kJW = 3 + 3 * NS;  // staged doubles per partner: com, site offsets
+  __shared__ double jdat[kTileWarps][kJW][33];   // [field][j] (+1 pad: no bank conflicts)
+  __shared__ double jacc[kTileWarps][6][33];     // partner force / torque accumulators
+  __shared__ int jext[kTileWarps][32];
+  __shared__ double cpar[2][NS][NS];             // c12, c6
+  const SysDev& s = a.s;
+  const DevTables* __restrict__ tab = s.tab;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.y;
+  const int n = s.n;
+  const size_t roff = size_t(r) * n;
+  const size_t soff = size_t(r) * s.total_sites;
+  const double4* __restrict__ p4 = a.st.pos4 + roff;
+  const double4* __restrict__ o4 = a.st.off + soff;
+  if (threadIdx.x < NS * NS) {
+    cpar[0][threadIdx.x / NS][threadIdx.x % NS] = tab->lj[threadIdx.x].c12;
+    cpar[1][threadIdx.x / NS][threadIdx.x % NS] = tab->lj[threadIdx.x].c6;
+  }
+  __syncthreads();
+  const MinImage mi = s.mi;
+  const float thr = a.thr;
+  auto mimg = [&](double d) {
+    return WRAPPED ? min_image_wrapped(d, mi.negL, thr) : min_image(d, mi);
+  };
+  const double rc2 = a.rc2, rmax2 = a.rmax2;
+  double ulj = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
+  const int bp = blockIdx.x * kTileWarps + warp;
+  if (bp < ta_.nbp) {  // warp-uniform
+    int bi, bj;
+    tile_of(bp, ta_.nb, bi, bj);
+    const bool diag = bi == bj;
+    const int i = bi * 32 + lane;
+    const bool iv = i < n;
+    const int ic = iv ? i : bi * 32;
+    const double4 pi = p4[ic];
+    const int ei = ext_of(pi);
+    double4 di[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) di[k] = o4[ic * NS + k];
+    double (*jd)[33] = jdat[warp];
+    double (*ja)[33] = jacc[warp];
+    {
+      const int j = bj * 32 + lane;
+      const int jc = j < n ? j : bj * 32;
+      const double4 pj = p4[jc];
+      jd[0][lane] = pj.x, jd[1][lane] = pj.y, jd[2][lane] = pj.z;
+      jext[warp][lane] = j < n ? ext_of(pj) : -1;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const double4 o = o4[jc * NS + k];
+        jd[3 + 3 * k][lane] = o.x, jd[4 + 3 * k][lane] = o.y, jd[5 + 3 * k][lane] = o.z;
+      }
+#pragma unroll
+      for (int c = 0; c < 6; ++c) ja[c][lane] = 0.0;
+    }
+    __syncwarp();
+    double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
+    const bool mine = bp >= ta_.bp_begin && bp < ta_.bp_end;
+    const int k0 = diag ? 1 : 0, k1 = diag ? 16 : 31;
+    if (mine)
+    for (int k = k0; k <= k1; ++k) {
+      const int jl = (lane + k) & 31;
+      const int ej = jext[warp][jl];
+      const bool valid = iv && ej >= 0 && !(diag && k == 16 && lane >= 16);
+      const bool lo = ei < ej;
+      const double Rx = mimg(sub(pi.x, jd[0][jl]));
+      const double Ry = mimg(sub(pi.y, jd[1][jl]));
+      const double Rz = mimg(sub(pi.z, jd[2][jl]));
+      const double R2 = norm2_exact(Rx, Ry, Rz);
+      const bool pass = valid && R2 < rmax2;  // potentials.cpp:212
+      double gfx = 0, gfy = 0, gfz = 0, gtx = 0, gty = 0, gtz = 0;  // partner side
+      if (pass) {
+        cnt += 1.0;
+        double s1p = 0.0, s2p = 0.0;
+#pragma unroll
+        for (int ta = 0; ta < NS; ++ta)
+#pragma unroll
+          for (int tb = 0; tb < NS; ++tb) {
+            // reference term (ta on the lower molecule, tb on the upper one)
+            const double4 dI = lo ? di[ta] : di[tb];
+            const int kj = lo ? tb : ta;
+            const double djx = jd[3 + 3 * kj][jl], djy = jd[4 + 3 * kj][jl], djz = jd[5 + 3 * kj][jl];
+            double rx, ry, rz;
+            if (lo) {
+              rx = sub(add(Rx, dI.x), djx);
+              ry = sub(add(Ry, dI.y), djy);
+              rz = sub(add(Rz, dI.z), djz);
+            } else {
+              rx = add(sub(Rx, djx), dI.x);
+              ry = add(sub(Ry, djy), dI.y);
+              rz = add(sub(Rz, djz), dI.z);
+            }
+            const double r2 = norm2_exact(rx, ry, rz);
+            if (r2 < rc2) {
+              const double inv_r2 = rcp_nr(r2);
+              const double ir6 = inv_r2 * inv_r2 * inv_r2;
+              const double a12 = cpar[0][ta][tb] * ir6 * ir6;
+              const double a6 = cpar[1][ta][tb] * ir6;
+              const double du_r = -12.0 * a12 + 6.0 * a6;
+              const double fs = -du_r * inv_r2;
+              const double gx = fs * rx, gy = fs * ry, gz = fs * rz;
+              fx += gx, fy += gy, fz += gz;
+              tx += dI.y * gz - dI.z * gy;
+              ty += dI.z * gx - dI.x * gz;
+              tz += dI.x * gy - dI.y * gx;
+              gfx -= gx, gfy -= gy, gfz -= gz;
+              gtx -= djy * gz - djz * gy;
+              gty -= djz * gx - djx * gz;
+              gtz -= djx * gy - djy * gx;
+              ulj += a12 - a6;
+              vir += Rx * gx + Ry * gy + Rz * gz;
+              if (a.vderiv) {
+                const double d2u_r2 = 156.0 * a12 - 42.0 * a6;
+                const double rvR = rx * Rx + ry * Ry + rz * Rz;
+                const double arr = rvR * inv_r2;
+                s1p += du_r * arr;
+                s2p += d2u_r2 * arr * arr + du_r * inv_r2 * (R2 - rvR * arr);
+              }
+            }
+          }
+        s1 += s1p;
+        s2 += s2p;
+      }
+      // partner accumulators: 32 distinct partners this step
+      ja[0][jl] += gfx, ja[1][jl] += gfy, ja[2][jl] += gfz;
+      ja[3][jl] += gtx, ja[4][jl] += gty, ja[5][jl] += gtz;
+      __syncwarp();
+    }
+    // records: [bp][0] = the I block's side, [bp][1] = the J block's (on the
+    // diagonal the J side is added to the I side: one record)
+    double* rec = ta_.rec + (size_t(r) * ta_.nbp + bp) * 2 * 32 * 6;
+    __syncwarp();
+    if (diag) {
+      fx += ja[0][lane], fy += ja[1][lane], fz += ja[2][lane];
+      tx += ja[3][lane], ty += ja[4][lane], tz += ja[5][lane];
+    } else {
+#pragma unroll
+      for (int c = 0; c < 6; ++c) rec[(32 + lane) * 6 + c] = ja[c][lane];
+    }
+    rec[lane * 6 + 0] = fx, rec[lane * 6 + 1] = fy, rec[lane * 6 + 2] = fz;
+    rec[lane * 6 + 3] = tx, rec[lane * 6 + 4] = ty, rec[lane * 6 + 5] = tz;
+  }
+  double v[kNumRowScalars] = {warp_sum(ulj), 0.0, 0.0, warp_sum(s1),
+                              warp_sum(s2),  warp_sum(vir), warp_sum(cnt)};
+  finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
+}
+
+// Block B's force and torque: its records in block-pair order (the I side of
+// (B, x) for x >= B, the J side of (x, B) for x < B), one thread per
+// (molecule, component); then the fused end-of-step kick.  Block pairs
+// outside this rank's range contribute nothing (their records are not read).
+static __global__ void __launch_bounds__(192) k_rigid_reduce(ForceArgs a, TileArgs ta_) {
+  const int b = blockIdx.x, r = blockIdx.y;
+  const int n = a.s.n;
+  const int t = threadIdx.x, m = t / 6, c = t - 6 * (t / 6);
+  const int slot = b * 32 + m;
+  const int nb = ta_.nb;
+  const double* rec = ta_.rec + size_t(r) * ta_.nbp * 2 * 32 * 6;
+  double acc = 0.0;
+  for (int x = 0; x < nb; ++x) {
+    const int lo = min(b, x), hi = max(b, x);
+    const int bp = lo * nb - ((lo * (lo - 1)) >> 1) + (hi - lo);
+    if (bp < ta_.bp_begin || bp >= ta_.bp_end) continue;
+    const int side = b <= x ? 0 : 1;
+    acc += rec[(size_t(bp) * 2 + side) * 32 * 6 + m * 6 + c];
+  }
+  const size_t roff = size_t(r) * n;
+  __shared__ int ext[32];
+  if (t < 32) ext[t] = b * 32 + t < n ? ext_of(a.st.pos4[roff + b * 32 + t]) : 0;
+  __syncthreads();
+  if (slot < n) {
+    double* f[6] = {a.st.fx, a.st.fy, a.st.fz, a.st.tx, a.st.ty, a.st.tz};
+    f[c][roff + ext[m]] = acc;
+  }
+  __syncthreads();
+  if (c == 0 && slot < n && a.kick_dt > 0.0) fused_kick(a, roff + ext[m]);
 }
 
 // ------------------------------------------------------------------- Ewald

@@ -100,6 +100,7 @@ int check_enthalpy(const b2md_ctx* c, const double* enthalpy, int n_enthalpy, co
 using namespace b2md_host;
 
 int b2md_heat_flux(b2md_ctx* c, const double* enthalpy, int n_enthalpy, double* jq) {
+  NvtxRange nvtx_("b2md_heat_flux");
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "heat_flux: null context");
   TRY(check_enthalpy(c, enthalpy, n_enthalpy, jq));
   if (!c->state_valid)
@@ -113,6 +114,7 @@ int b2md_heat_flux(b2md_ctx* c, const double* enthalpy, int n_enthalpy, double* 
 int b2md_heat_flux_state(b2md_ctx* c, const double* pos, const double* orient, const double* vel,
                          const double* ang_vel, const double* enthalpy, int n_enthalpy,
                          double* jq) {
+  NvtxRange nvtx_("b2md_heat_flux_state");
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "heat_flux: null context");
   if (!pos || !orient || !vel || !ang_vel)
     return set_err(B2MD_INVALID_ARGUMENT, "heat_flux: null pointer");
@@ -190,6 +192,7 @@ int check_thermostat(b2md_ctx* c) {
 }
 
 int b2md_kinetic_energy(b2md_ctx* c, double* ke_trans, double* ke_rot) {
+  NvtxRange nvtx_("b2md_kinetic_energy");
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "kinetic_energy: null context");
   CU(cudaSetDevice(c->device));
   TRY(launch_kinetic(c));
@@ -204,6 +207,7 @@ int b2md_kinetic_energy(b2md_ctx* c, double* ke_trans, double* ke_rot) {
 }
 
 int b2md_apply_thermostat(b2md_ctx* c) {
+  NvtxRange nvtx_("b2md_apply_thermostat");
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "apply_thermostat: null context");
   if (!c->state_valid) return set_err(B2MD_CONFIG_ERROR, "engine: set_state must precede step");
   CU(cudaSetDevice(c->device));
@@ -215,6 +219,7 @@ int b2md_apply_thermostat(b2md_ctx* c) {
 // done+1 .. done+nsteps of the current phase, the rescale after every step
 // whose number is a multiple of `interval` (<= 0: none).
 int b2md_step_thermostat(b2md_ctx* c, int64_t nsteps, int interval, int64_t done) {
+  NvtxRange nvtx_("b2md_step_thermostat");
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "step: null context");
   if (!c->engine) return set_err(B2MD_CONFIG_ERROR, "engine: time step must be positive");
   if (!c->state_valid) return set_err(B2MD_CONFIG_ERROR, "engine: set_state must precede step");
@@ -244,6 +249,7 @@ int b2md_step_thermostat(b2md_ctx* c, int64_t nsteps, int interval, int64_t done
 size_t b2md_state_block_size(const b2md_ctx* c) { return c ? 12 + size_t(104) * c->t.n : 0; }
 
 int b2md_save_state_block(b2md_ctx* c, int replica, uint8_t* buf, size_t cap) {
+  NvtxRange nvtx_("b2md_save_state_block");
   if (!c || !buf) return set_err(B2MD_INVALID_ARGUMENT, "save_state_block: null pointer");
   if (replica < 0 || replica >= c->R)
     return set_err(B2MD_INVALID_ARGUMENT, "save_state_block: bad replica");
@@ -264,6 +270,7 @@ int b2md_save_state_block(b2md_ctx* c, int replica, uint8_t* buf, size_t cap) {
 }
 
 int b2md_restore_state_block(b2md_ctx* c, int replica, const uint8_t* buf, size_t len) {
+  NvtxRange nvtx_("b2md_restore_state_block");
   if (!c || !buf) return set_err(B2MD_INVALID_ARGUMENT, "restore_state_block: null pointer");
   if (replica < 0 || replica >= c->R)
     return set_err(B2MD_INVALID_ARGUMENT, "restore_state_block: bad replica");
@@ -496,12 +503,14 @@ int b2md_rdf_types(const b2md_rdf* h, int* species, int* site) {
 }
 
 int b2md_rdf_accumulate(b2md_rdf* h) {
+  NvtxRange nvtx_("b2md_rdf_accumulate");
   if (!h) return set_err(B2MD_INVALID_ARGUMENT, "rdf: null handle");
   CU(cudaSetDevice(h->ctx->device));
   return rdf_launch(h);
 }
 
 int b2md_rdf_accumulate_state(b2md_rdf* h, const double* pos, const double* orient) {
+  NvtxRange nvtx_("b2md_rdf_accumulate_state");
   if (!h || !pos || !orient) return set_err(B2MD_INVALID_ARGUMENT, "rdf: null pointer");
   b2md_ctx* c = h->ctx;
   CU(cudaSetDevice(c->device));

@@ -306,6 +306,12 @@ class Engine:
         (0 keeps the input order; results differ only in summation order)."""
         check(_abi.lib().b2md_set_sort_interval(self._c.ctx, int(steps)))
 
+    def sort_interval(self) -> tuple[int, int]:
+        """(re-sort period, steps taken since the last re-sort)."""
+        a, b = C.c_int(), C.c_int()
+        check(_abi.lib().b2md_get_sort_interval(self._c.ctx, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def set_search_options(self, fix_prefilter: bool = True, tile_cull: bool = True) -> None:
         """b2md_set_search_options: partner-search strategy (same results)."""
         check(_abi.lib().b2md_set_search_options(self._c.ctx, int(fix_prefilter), int(tile_cull)))

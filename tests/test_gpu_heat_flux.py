@@ -119,13 +119,16 @@ def test_heat_flux_replicas_cfg4():
         check_flux(wl.comp, s, h, jq[r], ref, f"replica {r}")
 
 
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_heat_flux_shards_sum_to_full(world):
-    """Tile-row shards (no communicator): the partial fluxes sum to the whole
-    (pair parts split by tiles, the kinetic part on rank 0 only)."""
-    wl = configs.make("cfg2")
+def test_heat_flux_shards_sum_to_full(cfg, world):
+    """Row shards (no communicator): the partial fluxes sum to the whole.
+    cfg2 takes the bit-matrix walk (pair parts split by tiles, the kinetic
+    part on rank 0 only), cfg3 the cluster walk (each rank owns disjoint rows
+    and adds their kinetic terms)."""
+    wl = configs.make(cfg)
     st0 = wl.states[0]
-    vel, ang_vel, h = golden_cases.flux_inputs("cfg2", wl.comp)
+    vel, ang_vel, h = golden_cases.flux_inputs(cfg, wl.comp)
     st = state_of(wl.comp, st0.pos, st0.orient, vel, ang_vel)
     full = b2.ForceField(wl.comp, wl.opts).heat_flux(st, h)
     total = np.zeros(3)

@@ -168,6 +168,25 @@ def test_replica_batch_cfg4():
         assert np.array_equal(eng.pair_list(r), o.pair_list(ref["pos"]))
 
 
+def test_replica_batch_cfg4_full_shape():
+    """cfg4 at the shape bench.py runs per GPU: the 8-replica batch (seeds
+    0-7, T_r = 1.5 + 1.5 u) for 100 steps, EVERY replica against the oracle's
+    Engine::step (src/engine.cpp:102-143): pos / L, velocities, quaternions,
+    angular velocities and energy at 1e-9, pair lists bit-exact."""
+    R, steps = 8, 100
+    wl = configs.make("cfg4", replicas=R, steps=steps)
+    eng = b2.Engine(wl.comp, wl.opts, wl.dt, replicas=R)
+    eng.set_state(wl.states)
+    eng.step(steps)
+    outs = eng.states()
+    o = pyoracle.OracleFF(wl.comp, wl.opts)
+    for r, st in enumerate(wl.states):
+        ref = o.run(wl.dt, steps, st.pos, st.orient, st.vel, st.ang_vel)
+        compare_states(outs[r], ref, wl.comp.box_length)
+        check_energy(outs[r].energy, ref["energy"])
+        assert np.array_equal(eng.pair_list(r), o.pair_list(ref["pos"]))
+
+
 # --------------------------------------------------------------- edge cases
 @pytest.mark.parametrize("n", [1, 2, 3, 31, 33, 100, 513, 1537, 4100, 8200])
 def test_sizes_and_partial_tiles(n):
@@ -252,6 +271,39 @@ def test_cluster_walk_cfg3_void():
     assert np.array_equal(ff.pair_list(), o.pair_list(st.pos))
     check_vec(out.force, ref["force"])
     check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+    # the walk's OWN pair decisions (its in-cutoff count, potentials.cpp:156-161),
+    # not only the on-demand list of k_search
+    assert ff.last_stats.com_pairs == ref["com_pairs"]
+
+
+@pytest.mark.skipif(not pyoracle.ref_available(), reason="oracle/_ref not built")
+def test_cfg3_100_steps_full_state_vs_reference_engine():
+    """cfg3 (N = 16384) through the cluster walk for 100 steps against the
+    unmodified reference tmd::Engine run live on the host cores (all threads):
+    EVERY molecule's position / velocity / force, the energy parts and the
+    walk's own pair count at step 0 and after the 100 steps
+    (src/engine.cpp:102-143, src/potentials.cpp:156-181)."""
+    import copy
+    import os
+    wl = configs.make("cfg3", steps=100)
+    st = wl.states[0]
+    eng = b2.Engine(wl.comp, wl.opts, wl.dt)
+    eng.set_state(st)
+    _, stats0 = eng.energies()
+    opts = copy.copy(wl.opts)
+    opts.workers = max(1, os.cpu_count() or 1)
+    ref = pyoracle.RefEngine(wl.comp, opts, wl.dt)
+    ref.set_state(st.pos, st.orient, st.vel, st.ang_vel)
+    o = pyoracle.OracleFF(wl.comp, wl.opts)
+    assert stats0[0].com_pairs == o.evaluate(st.pos, st.orient)["com_pairs"]
+    eng.step(100)
+    ref.step(100)
+    out, r = eng.state(), ref.state()
+    compare_states(out, r, wl.comp.box_length)
+    check_vec(out.force, r["force"], what="force after 100 steps")
+    check_energy(out.energy, r["energy"], out.virial, r["virial"])
+    _, stats = eng.energies()
+    assert stats[0].com_pairs == o.evaluate(out.pos, out.orient)["com_pairs"]
 
 
 @pytest.mark.parametrize("n", [1001, 2053])
@@ -750,3 +802,87 @@ def test_pinned_and_pageable_transfers_agree(cfg):
             eng.get_state_raw(*bufs)
         outs.append(np.hstack([np.array(b) for b in bufs]))
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+# ------------------------------------------ once-per-pair cluster walk (Newton)
+# k_cpair_build + k_force_cpair_n3 + k_cpair_jsum (csrc/cluster.cuh): each pair
+# evaluated once, partner contributions through the per-pair record buffer and
+# a fixed-order reduction (B2MD_NEWTON=1; the both-rows walk is the default).
+@pytest.mark.parametrize("n", [1, 2, 7, 9, 100, 1537, 4100])
+def test_newton_walk_sizes(monkeypatch, n):
+    monkeypatch.setenv("B2MD_CLUSTER", "2")
+    monkeypatch.setenv("B2MD_NEWTON", "1")
+    box = (n / 0.7) ** (1.0 / 3.0) if n > 8 else 8.0
+    rc = min(2.5, 0.5 * box)
+    if n > 8:
+        wl = configs.lj_fluid_config(n, n / box ** 3, rc, seed=n + 3)
+        comp, opts, st = wl.comp, wl.opts, wl.states[0]
+    else:
+        comp, opts = systems.lj_fluid(n, box), systems.lj_opts(rc)
+        st = systems.random_state(comp, n, 0.9)
+    o = pyoracle.OracleFF(comp, opts)
+    ref = o.evaluate(st.pos, st.orient)
+    ff, out = gpu_eval(comp, opts, st.pos, st.orient)
+    check_vec(out.force, ref["force"])
+    check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+    assert ff.last_stats.com_pairs == ref["com_pairs"]
+
+
+@pytest.mark.parametrize("n", [300, 2053])
+def test_newton_walk_mixture_and_trajectory(monkeypatch, n):
+    """Two species (Lorentz-Berthelot terms) and a 25-step trajectory with
+    re-sorts on the once-per-pair walk; repeated runs are bit-identical."""
+    monkeypatch.setenv("B2MD_CLUSTER", "2")
+    monkeypatch.setenv("B2MD_NEWTON", "1")
+    na = n // 3
+    box = (n / 0.7) ** (1.0 / 3.0)
+    comp = b2.SystemComposition([b2.build_species("a", [b2.make_lj_site(0, 0, 0, 1.0, 1.0, 1.0)]),
+                                 b2.build_species("b", [b2.make_lj_site(0, 0, 0, 0.9, 1.3, 2.0)])],
+                                [na, n - na], box, 1.0)
+    opts = systems.lj_opts(min(2.5, 0.45 * box))
+    st = systems.random_state(comp, n, 0.8)
+    o = pyoracle.OracleFF(comp, opts)
+    ref = o.evaluate(st.pos, st.orient)
+    ff, out = gpu_eval(comp, opts, st.pos, st.orient)
+    check_vec(out.force, ref["force"])
+    check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+    dt, steps = 0.002, 25
+    runs = []
+    for _ in range(2):
+        eng = b2.Engine(comp, opts, dt)
+        eng.set_sort_interval(7)
+        eng.set_state(st)
+        eng.step(steps)
+        runs.append(eng.state())
+    tr = o.run(dt, steps, st.pos, st.orient, st.vel, st.ang_vel)
+    compare_states(runs[0], tr, box)
+    assert np.array_equal(runs[0].pos, runs[1].pos) and np.array_equal(runs[0].force, runs[1].force)
+
+
+def test_newton_walk_replicas_and_cfg3(monkeypatch):
+    """Replicas (short last clusters) and cfg3 itself on the once-per-pair
+    walk: per-replica oracle forces / energies / pair counts, then cfg3's
+    100-step trajectory against the reference engine's golden states."""
+    monkeypatch.setenv("B2MD_NEWTON", "1")
+    wls = [configs.lj_fluid_config(1001, 0.8, 2.5, seed=21 + r) for r in range(3)]
+    comp, opts = wls[0].comp, wls[0].opts
+    eng = b2.Engine(comp, opts, 0.005, replicas=3)
+    eng.set_state([w.states[0] for w in wls])
+    outs, stats = eng.states(), eng.energies()[1]
+    o = pyoracle.OracleFF(comp, opts)
+    for r, w in enumerate(wls):
+        ref = o.evaluate(w.states[0].pos, w.states[0].orient)
+        check_vec(outs[r].force, ref["force"], what=f"replica {r}")
+        check_energy(outs[r].energy, ref["energy"], outs[r].virial, ref["virial"])
+        assert stats[r].com_pairs == ref["com_pairs"]
+    g = np.load(GOLDEN / "traj_cfg3_100.npz")
+    wl = configs.make("cfg3")
+    e3 = b2.Engine(wl.comp, wl.opts, wl.dt)
+    e3.set_state(wl.states[0])
+    e3.step(int(g["steps"]))
+    out = e3.state()
+    k, L = int(g["stride"]), wl.comp.box_length
+    d = out.pos[::k] - g["pos"]
+    d -= L * np.round(d / L)
+    assert np.abs(d).max() / L <= T_TOL
+    assert abs(out.energy.total() - g["energy"][2]) <= T_TOL * abs(g["energy"][2])
