@@ -228,6 +228,17 @@ int b2md_set_sort_interval(b2md_ctx* ctx, int steps);
  * re-sorts when steps_since_sort >= steps > 0). */
 int b2md_get_sort_interval(const b2md_ctx* ctx, int* steps, int* steps_since_sort);
 
+/* The once-per-pair cluster-pair list of the single-site cluster path
+ * (no reference counterpart: diagnostics for tests and
+ * measurement).  info[0] = 1 when the list path is active (else all 0),
+ * info[1] = entries (owned cluster pairs) of `replica`, info[2] = incoming
+ * record slots, info[3] = 1 when the list is stale (a molecule moved more than
+ * skin / 2 since the build: the exact per-step walk runs until the next
+ * build), info[4] = evaluations since the context was created, info[5] = steps
+ * since the last build, info[6] = scheduled build interval, info[7] = the
+ * skin in units of 1e-6 length.  Synchronises the context's stream. */
+int b2md_nlist_info(b2md_ctx* ctx, int replica, int64_t info[8]);
+
 /* Step structure (same results bit for bit; for tests and measurement):
  * fused_kick = 1 runs the end-of-step half kick (engine.cpp:131-142) in the
  * force kernel's row epilogue whenever a molecule's force is final there (no

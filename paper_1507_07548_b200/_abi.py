@@ -138,6 +138,7 @@ SIGNATURES = {
     "b2md_set_search_options": (C.c_int, [_CTX, C.c_int, C.c_int]),
     "b2md_set_sort_interval": (C.c_int, [_CTX, C.c_int]),
     "b2md_get_sort_interval": (C.c_int, [_CTX, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "b2md_nlist_info": (C.c_int, [_CTX, C.c_int, C.POINTER(C.c_int64)]),
     "b2md_set_step_options": (C.c_int, [_CTX, C.c_int]),
     "b2md_heat_flux": (C.c_int, [_CTX, _D, C.c_int, _D]),
     "b2md_heat_flux_state": (C.c_int, [_CTX, _D, _D, _D, _D, _D, C.c_int, _D]),

@@ -17,6 +17,8 @@
 // deterministic; culls only ever keep extra candidates.
 #pragma once
 
+#include <cub/block/block_scan.cuh>
+
 #include "kernels.cuh"
 
 namespace b2md {
@@ -35,6 +37,10 @@ struct ClusterArgs {
   float4* sup_half;             // R * nsup
   float lim;                    // (rc 2^32 / L)^2 (1 + 1e-5): cull radius^2
   int grp_begin, grp_end;       // this rank's i-groups (row shard; all of them on one rank)
+  // once-per-pair list (k_force_nl): build positions and control words; the
+  // drift keeps the largest displacement^2 since the build (null: no list)
+  const uint4* fixref;
+  int* nl_ctl;
 };
 
 // Lower bound of the circle distance between two arcs (centres x, y, half
@@ -171,6 +177,27 @@ static __global__ void __launch_bounds__(kSC * kCS) k_step_drift_arcs(StepArgs s
     }
   }
   cluster_arcs_block(a, r, sc, u, valid);
+  if (a.nl_ctl) {
+    // the largest displacement^2 since the list build (fixed-point circle
+    // distance; float bits compare as integers, a NaN or out-of-box position
+    // above +inf): one atomicMax per CTA
+    __shared__ unsigned dmax[kSC * kCS / 32];
+    unsigned db = 0u;
+    if (valid) {
+      const uint4 f0 = a.fixref[p];
+      const float dx = float(int(u.x - f0.x)), dy = float(int(u.y - f0.y)),
+                  dz = float(int(u.z - f0.z));
+      db = u.w ? __float_as_uint(dx * dx + dy * dy + dz * dz) : 0x7fc00000u;
+    }
+    db = __reduce_max_sync(0xffffffffu, db);
+    if ((threadIdx.x & 31) == 0) dmax[threadIdx.x >> 5] = db;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned m = 0u;
+      for (int w = 0; w < kSC * kCS / 32; ++w) m = max(m, dmax[w]);
+      atomicMax(reinterpret_cast<unsigned*>(a.nl_ctl) + size_t(r) * 8 + 6, m);  // kNLD2
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -207,6 +234,33 @@ __device__ __forceinline__ void cp_async16(unsigned smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Bulk (TMA) copies global -> shared completing on an mbarrier (tx bytes)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 // The cluster walk of one i-group (one warp; rows g0 + (lane & 3), this
 // lane's row i with position pi / fixed point fi, valid iv): the group's arc
@@ -323,25 +377,26 @@ __device__ __forceinline__ void cpair_walk(const ClusterArgs& ca, const double4*
   }
 }
 
-template <bool MULTI_SPECIES, bool WRAPPED, bool VDERIV>
-__global__ void __launch_bounds__(kGWarps * 32, kGMinBlocks) k_force_cpair(ForceArgs a, ClusterArgs ca) {
-  __shared__ int clist[kGWarps][kGList + 1];
-  __shared__ __align__(128) double4 stage[kGWarps][kGDepth][2][kCS];
+// The both-rows walk of one i-group grp (one warp): forces of its 4 rows
+// written (with the fused end-of-step kick when a.kick_dt > 0), the LJ sums
+// of every visit into B12 / B6 (each pair is visited from both rows: the
+// caller halves them) and the pair count on the i < j side into cnt.
+// Another rank's groups (row shard) write zero forces into the all-reduce.
+template <bool MULTI_SPECIES, bool WRAPPED>
+__device__ __forceinline__ void cpair_group_forces(const ForceArgs& a, const ClusterArgs& ca, int r,
+                                                   int grp, int* __restrict__ clist,
+                                                   double4 (*stage)[2][kCS], double& B12,
+                                                   double& B6, int& cnt) {
   const SysDev& s = a.s;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = blockIdx.y;
+  const int lane = threadIdx.x & 31;
   const size_t roff = size_t(r) * s.n;
   const double4* __restrict__ p4 = a.st.pos4 + roff;
   const uint4* __restrict__ fx4 = ca.fixpos + roff;
   const unsigned full = 0xffffffffu;
   const int n = s.n;
-  const int g0 = (blockIdx.x * kGWarps + warp) * kGR;  // the group's first slot
-  // sums over all visits: single species B12 = sum ir6^2, B6 = sum ir6
-  // (a12 = c12 B12, a6 = c6 B6); mixtures sum a12, a6 directly
-  double B12 = 0, B6 = 0;
-  int cnt = 0;
-  const int grp = blockIdx.x * kGWarps + warp;
-  if (g0 < n && (grp < ca.grp_begin || grp >= ca.grp_end)) {
+  const int g0 = grp * kGR;  // the group's first slot
+  if (g0 >= n) return;       // warp-uniform
+  if (grp < ca.grp_begin || grp >= ca.grp_end) {
     // another rank's rows (row shard): zero forces into the all-reduce
     if (lane < kGR && g0 + lane < n) {
       const size_t e = roff + ext_of(p4[g0 + lane]);
@@ -349,64 +404,77 @@ __global__ void __launch_bounds__(kGWarps * 32, kGMinBlocks) k_force_cpair(Force
       a.st.fy[e] = 0.0;
       a.st.fz[e] = 0.0;
     }
-  } else if (g0 < n) {  // warp-uniform
-    const int i = g0 + (lane & (kGR - 1));
-    const bool iv = i < n;
-    const int ic = iv ? i : g0;  // clamped row
-    const double4 pi = p4[ic];
-    const int si = MULTI_SPECIES ? s.sp_slot[roff + ic] : 0;
-    double fx = 0, fy = 0, fz = 0;
-    auto terms = [&](int j, bool in, double r2, double dx, double dy, double dz) {
-      const double inv_r2 = rcp_nr(in ? r2 : 1.0);
-      const double t6 = inv_r2 * inv_r2 * inv_r2;
-      const double ir6 = in ? t6 : 0.0;
-      double fs;
-      if constexpr (MULTI_SPECIES) {
-        // lanes past the last slot (partial / odd-tail pad cluster) have no
-        // species: their ir6 is 0, any valid species index keeps c12, c6 finite
-        const int sj = in ? s.sp_slot[roff + j] : si;
-        const DevPairInfo& pinfo = s.tab->pair[(i < j) ? si * s.ns + sj : sj * s.ns + si];
-        const double c12 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c12 : 0.0;
-        const double c6 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c6 : 0.0;
-        const double a12 = c12 * ir6 * ir6, a6 = c6 * ir6;
-        fs = (12.0 * a12 - 6.0 * a6) * inv_r2;  // -du_r / r2
-        B12 += a12;
-        B6 += a6;
-      } else {
-        fs = fma(ir6, a.c12x12, -a.c6x6) * ir6 * inv_r2;
-        B12 = fma(ir6, ir6, B12);
-        B6 += ir6;
-      }
-      if (in) {  // (predicated: an excluded pair's R may be NaN -- a NaN position
-                 // fails the reference's r2 < rc2 test and touches nobody)
-        fx = fma(fs, dx, fx);
-        fy = fma(fs, dy, fy);
-        fz = fma(fs, dz, fz);
-      }
-      cnt += in && i < j;  // exact per shard: the pair's i < j side
-    };
-    cpair_walk<WRAPPED>(ca, p4, r, n, i, iv, pi, fx4[ic], a.rc2, s.mi, a.thr, clist[warp],
-                        stage[warp],
-                        [&](int ja, bool ina, double ra, double ax, double ay, double az, int jb,
-                            bool inb, double rb, double bx, double by, double bz) {
-                          terms(ja, ina, ra, ax, ay, az);
-                          terms(jb, inb, rb, bx, by, bz);
-                        });
-    // a row's 8 lanes (il fixed, jl = lane >> 2): fixed xor tree
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      fx += __shfl_xor_sync(full, fx, o);
-      fy += __shfl_xor_sync(full, fy, o);
-      fz += __shfl_xor_sync(full, fz, o);
-    }
-    if (lane < kGR && iv) {
-      const size_t e = roff + ext_of(pi);
-      a.st.fx[e] = fx;
-      a.st.fy[e] = fy;
-      a.st.fz[e] = fz;
-      if (a.kick_dt > 0.0) fused_kick(a, e);
-    }
+    return;
   }
+  const int i = g0 + (lane & (kGR - 1));
+  const bool iv = i < n;
+  const int ic = iv ? i : g0;  // clamped row
+  const double4 pi = p4[ic];
+  const int si = MULTI_SPECIES ? s.sp_slot[roff + ic] : 0;
+  double fx = 0, fy = 0, fz = 0;
+  auto terms = [&](int j, bool in, double r2, double dx, double dy, double dz) {
+    const double inv_r2 = rcp_nr(in ? r2 : 1.0);
+    const double t6 = inv_r2 * inv_r2 * inv_r2;
+    const double ir6 = in ? t6 : 0.0;
+    double fs;
+    if constexpr (MULTI_SPECIES) {
+      // lanes past the last slot (partial / odd-tail pad cluster) have no
+      // species: their ir6 is 0, any valid species index keeps c12, c6 finite
+      const int sj = in ? s.sp_slot[roff + j] : si;
+      const DevPairInfo& pinfo = s.tab->pair[(i < j) ? si * s.ns + sj : sj * s.ns + si];
+      const double c12 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c12 : 0.0;
+      const double c6 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c6 : 0.0;
+      const double a12 = c12 * ir6 * ir6, a6 = c6 * ir6;
+      fs = (12.0 * a12 - 6.0 * a6) * inv_r2;  // -du_r / r2
+      B12 += a12;
+      B6 += a6;
+    } else {
+      fs = fma(ir6, a.c12x12, -a.c6x6) * ir6 * inv_r2;
+      B12 = fma(ir6, ir6, B12);
+      B6 += ir6;
+    }
+    if (in) {  // (predicated: an excluded pair's R may be NaN -- a NaN position
+               // fails the reference's r2 < rc2 test and touches nobody)
+      fx = fma(fs, dx, fx);
+      fy = fma(fs, dy, fy);
+      fz = fma(fs, dz, fz);
+    }
+    cnt += in && i < j;  // exact per shard: the pair's i < j side
+  };
+  cpair_walk<WRAPPED>(ca, p4, r, n, i, iv, pi, fx4[ic], a.rc2, s.mi, a.thr, clist, stage,
+                      [&](int ja, bool ina, double ra, double ax, double ay, double az, int jb,
+                          bool inb, double rb, double bx, double by, double bz) {
+                        terms(ja, ina, ra, ax, ay, az);
+                        terms(jb, inb, rb, bx, by, bz);
+                      });
+  // a row's 8 lanes (il fixed, jl = lane >> 2): fixed xor tree
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    fx += __shfl_xor_sync(full, fx, o);
+    fy += __shfl_xor_sync(full, fy, o);
+    fz += __shfl_xor_sync(full, fz, o);
+  }
+  if (lane < kGR && iv) {
+    const size_t e = roff + ext_of(pi);
+    a.st.fx[e] = fx;
+    a.st.fy[e] = fy;
+    a.st.fz[e] = fz;
+    if (a.kick_dt > 0.0) fused_kick(a, e);
+  }
+}
+
+template <bool MULTI_SPECIES, bool WRAPPED, bool VDERIV>
+__global__ void __launch_bounds__(kGWarps * 32, kGMinBlocks) k_force_cpair(ForceArgs a, ClusterArgs ca) {
+  __shared__ int clist[kGWarps][kGList + 1];
+  __shared__ __align__(128) double4 stage[kGWarps][kGDepth][2][kCS];
+  const int warp = threadIdx.x >> 5;
+  const int r = blockIdx.y;
+  // sums over all visits: single species B12 = sum ir6^2, B6 = sum ir6
+  // (a12 = c12 B12, a6 = c6 B6); mixtures sum a12, a6 directly
+  double B12 = 0, B6 = 0;
+  int cnt = 0;
+  cpair_group_forces<MULTI_SPECIES, WRAPPED>(a, ca, r, blockIdx.x * kGWarps + warp, clist[warp],
+                                             stage[warp], B12, B6, cnt);
   // every pair was visited twice (bit-identical terms): halve the sums
   double A12 = 0.5 * warp_sum(B12), A6 = 0.5 * warp_sum(B6);
   if constexpr (!MULTI_SPECIES) {
@@ -421,104 +489,116 @@ __global__ void __launch_bounds__(kGWarps * 32, kGMinBlocks) k_force_cpair(Force
 }
 
 // ---------------------------------------------------------------------------
-// Once-per-pair cluster walk (Newton's third law), the north star's race-free
-// scheme: every molecule pair is evaluated ONCE, its force applied to both
-// partners, and the partner-side contributions go to a per-pair contribution
-// buffer that is reduced in a fixed order -- the GPU form of the reference's
-// per-worker buffers summed in worker order (src/potentials.cpp:166-170,
-// src/parallel.cpp:84-95).  No atomics on floating-point data: results are
-// bit-identical run to run.
+// Once-per-pair cluster-pair list (Newton's third law): the north star's
+// race-free scheme.  Every molecule pair is evaluated ONCE, its force applied
+// to both partners; the partner-side contributions go to a per-pair
+// contribution buffer that is summed in a fixed order -- the GPU form of the
+// reference's +-f per pair (src/potentials.cpp:166-170) and its per-worker
+// buffers summed in worker order (src/parallel.cpp:84-95).  No atomics on
+// floating-point data: results are bit-identical run to run.
 //
-// * k_cpair_build -- one warp per cluster c, one cull (c's arc against
-//   super-cluster and cluster arcs) for both of c's roles.  Cluster pair
-//   {ci, jc} belongs to ci iff ci == jc (pairs j > i inside the cluster) or
-//   (ci < jc) == (ci + jc even) -- the checker rule, so every cluster owns
-//   about half of its neighbours wherever it sits in the spatial order.
-//   As owner, c's owned list goes to global memory, cut into work units of
-//   <= kUnit j-clusters (a contiguous unit range).  As receiver, c's owners
-//   (found in increasing index) get a contiguous record range: owner x's
-//   j-side record for c goes to slot in_base[c] + rank(x), published in a
-//   dense [owner][receiver] slot map.
-// * k_force_cpair_n3 -- persistent warps take work units from a counter
-//   (which warp runs a unit does not change its result).  lane = (j-member
-//   jl = lane >> 2, il = lane & 3) owns rows ia = 8 ci + il and ib = ia + 4;
-//   one warp step takes a whole j-cluster (64 pairs).  A unit's i-side force
-//   is one record; the j-side force of each step (the 8 rows summed through
-//   shared memory in a fixed order) is one 192-byte record per owned cluster
-//   pair at the pair's triangular index.  Small dynamically assigned units
-//   keep a cluster with a large neighbourhood (one straddling two columns)
-//   from setting the kernel's length.
-// * k_cpair_jsum -- one warp per cluster: its unit records in unit order,
-//   then its receiver records in owner order -- two contiguous ranges, a
-//   fixed order -- force = i-side - j-side, the fused end-of-step kick.
-// Each pair's r2 and cutoff decision are the reference's bits (as in
-// k_force_cpair); energy, virial, s1, s2 and the pair count are taken once
-// per pair (no halving).
-constexpr int kUnit = 16;  // j-clusters per work unit
+// * The list (built after every re-sort / staging and every nl_interval
+//   steps): every cluster pair whose bounding arcs were within rc + skin,
+//   each owned by one of its clusters -- ci == cj (pairs j > i inside the
+//   cluster) or (ci < cj) == (ci + cj even), the checker rule, so every
+//   cluster owns about half of its neighbours wherever it sits in the spatial
+//   order.  An owner's entries {cj | shift codes, ci, record slot, build gap}
+//   are contiguous (increasing cj), padded to a multiple of kB with entries
+//   that never pass the cull, so a batch of kB entries has one owner; a
+//   receiver's incoming records are contiguous (receiver-major slots, owner
+//   order).  Built by k_nl_count, k_nl_scan, k_nl_fill, k_nl_inrec (no
+//   atomics: the layout is a pure function of the arcs).
+// * Periodic images per entry: where neither cluster's arc (widened by the
+//   skin) can reach the box boundary on an axis, every member pair's raw
+//   difference d = x_i - x_j lies in one interval for the list's lifetime;
+//   when that interval is inside (-L/2, L/2), (L/2, 3L/2) or (-3L/2, -L/2)
+//   with a 1e-5 margin, the reference's nearbyint(d / L) is 0, 1 or -1 for
+//   every pair and its d - L nearbyint(d / L) is d, d - L or d + L: one
+//   correctly rounded add per axis, the reference's bits
+//   (potentials.hpp:176-181).  An entry with an axis that cannot be decided
+//   (code 3) takes min_image_wrapped per pair.
+// * Exactness of the pair set: the drift keeps D^2, the largest squared
+//   displacement of any molecule since the build (fixed-point circle
+//   distance).  A pair within rc now was within rc + 2 D at the build, so an
+//   entry whose build gap is >= rc + 2 D is skipped this step (the skin costs
+//   list length, not pair work), and while D <= skin / 2 every pair within rc
+//   is listed.  Beyond that the list is stale and never used -- k_force_nl
+//   runs the exact per-step cull walk (both rows, cpair_group_forces) until
+//   the next build.
+// * k_force_nl: batches of kB entries (one owner ci) dealt round-robin to
+//   the warps; a batch's surviving entries and the owner's 8 positions are
+//   staged into shared memory by bulk (TMA) copies on the warp's mbarrier,
+//   one batch ahead of the compute (double buffer).  lane = (j-member jl =
+//   lane >> 2, il = lane & 3) owns rows ia = 8 ci + il and ib = ia + 4; a
+//   warp step takes a whole j-cluster (64 pairs).  Each pair's r2 and cutoff
+//   decision are the reference's bits (potentials.cpp:156-161).  An entry
+//   with a pair in cutoff writes its 256-byte j-side record -- lane (jl, c)
+//   component c of member jl's sum over the 4 row lanes (fixed order, through
+//   shared memory), lane (jl, 3) the evaluation's epoch stamp -- and a batch
+//   its i-side record in the same layout.
+// * k_nl_reduce: one warp per cluster: its batches' i-side records, then its
+//   stamped incoming records -- force = i-side - j-side, a fixed order -- and
+//   the fused end-of-step kick.
+constexpr int kNLBuildWarps = 4;  // warps (clusters) per CTA of the build / reduce kernels
+constexpr int kNLWarps = 4;       // warps per CTA of k_force_nl
+#ifndef B2MD_NL_MINBLOCKS
+#define B2MD_NL_MINBLOCKS 5
+#endif
+constexpr int kNLMinBlocks = B2MD_NL_MINBLOCKS;  // 20 warps per SM (<= 96 registers)
+constexpr int kB = 16;            // entries per batch (one owner)
+#ifndef B2MD_NL_TMA
+#define B2MD_NL_TMA 0             // stage by bulk (TMA) copies instead of per-lane cp.async
+#endif
+constexpr int kRecD = kCS * 4;    // doubles per record: 8 members x (x, y, z, epoch stamp)
+constexpr int kNLCtl = 8;         // control words per replica
+constexpr int kJcBits = 24;       // entry.x = cj | shift codes << 24 (2 bits per axis)
+constexpr int kJcMask = (1 << kJcBits) - 1;
+// ctl words: entries (padded), incoming slots, epoch, ticket, overflow, D^2 bits
+enum { kNLEntries = 0, kNLIncoming = 1, kNLEpoch = 2, kNLTicket = 3, kNLOverflow = 5, kNLD2 = 6 };
 
-struct PairBuf {
-  double* rec;      // R * nc (nc + 1) / 2 j-side records of 8 x 3 doubles (i-side sign),
-                    // receiver-major: cluster c's records are slots in_base[c] + rank(owner)
-  double* irec;     // R * max_units i-side records (8 x 3 doubles)
-  int* olist;       // R * nc * nc: owned listed j-clusters of each cluster
-  int* ilist;       // R * nc * nc: owners of each cluster (increasing), build scratch
-  int* inslot;      // R * nc * nc: [owner][receiver] -> record slot
-  int* ocnt;        // R * nc
-  int* ustart;      // R * nc: first unit of each cluster (its units are contiguous)
-  int* umap;        // R * max_units: unit -> cluster
-  int* in_base;     // R * nc: first record slot of each receiver
-  int* in_cnt;      // R * nc: owners of each receiver
-  int* units;       // R: units of this evaluation (reset by the walk's last CTA)
-  int* in_total;    // R: record slots of this evaluation (reset by the walk's last CTA)
-  int* next_unit;   // R: work counter (reset by the walk's last CTA)
-  unsigned* ticket; // R: the walk's last-CTA ticket
-  int max_units;
-  int cbeg, cend;   // this rank's owner clusters (row shard)
+struct NListArgs {
+  int* ocnt;       // R * nc: owned entries of each cluster, padded to kB (0 for another rank's)
+  int* icnt;       // R * nc: incoming slots (owners x of {x, c}, c itself included)
+  int* ebase;      // R * (nc + 1): first entry of each cluster (per-replica numbering)
+  int* ibase;      // R * (nc + 1): first incoming slot
+  int4* ent;       // R * max_ent: {cj | codes << 24, ci, record slot, build gap^2 bits}
+  int* in_src;     // R * max_ent: owner of each incoming slot (build scratch)
+  double* rec;     // R * max_ent * kRecD: j-side sums g = sum_i f_ij (force on j: -g),
+                   // receiver-major (cluster c's incoming slots ibase[c] .. ibase[c + 1])
+  double* irec;    // R * (max_ent / kB) * kRecD: i-side force of each batch
+  uint4* fixref;   // R * n: fixed-point positions at the build (slot order)
+  int* ctl;        // R * kNLCtl
+  float lim_build;  // ((rc + skin) 2^32 / L)^2 (1 + 1e-5)
+  float skin_half;  // skin / 2 in fixed-point units (+ margin): the displacement bound
+  float rc_fix;     // rc 2^32 / L
+  unsigned d2_stale;  // bits of ((skin / 2) 2^32 / L)^2 (1 - 1e-4): D^2 above is stale
+  int max_ent;
+  int cbeg, cend;  // this rank's owner clusters
+  int dbg;         // measurement only (B2MD_NL_DBG): 1 no LJ, 2 no j-side, 4 no record stores, 16 no pairs
 };
 
-// triangular index of the unordered cluster pair {a, b}, a <= b (32-bit: the
-// record array is capped at 8 GB, i.e. < 2^26 pairs)
-__device__ __forceinline__ int tri_index(int a, int b, int nc) {
-  return a * nc - ((a * (a - 1)) >> 1) + (b - a);
+// The list cannot be used this evaluation (overflow at the build, or a
+// molecule moved more than skin / 2 since): read by k_force_nl and k_nl_reduce
+__device__ __forceinline__ bool nl_stale(const NListArgs& nl, const int* ctl) {
+  return ctl[kNLOverflow] != 0 || unsigned(ctl[kNLD2]) > nl.d2_stale;
 }
 
-__device__ __forceinline__ bool owns_pair(int ci, int jc) {
-  return ci == jc || ((ci < jc) == (((ci ^ jc) & 1) == 0));
-}
-
-constexpr int kBuildWarps = 4;
-
-// 32-byte load through L2 (data another SM wrote during this launch)
-__device__ __forceinline__ double4 ldcg4(const double4* p) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-  const double2 a = __ldcg(q), b = __ldcg(q + 1);
-  return make_double4(a.x, a.y, b.x, b.y);
-}
-
-static __global__ void __launch_bounds__(kBuildWarps * 32)
-    k_cpair_build(ForceArgs a, ClusterArgs ca, PairBuf pb) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = blockIdx.y;
-  const int nc = ca.nc, n = a.s.n;
-  const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
-  const int c = blockIdx.x * kBuildWarps + warp;
-  if (c >= nc) return;
-  const bool mine = c >= pb.cbeg && c < pb.cend;  // this rank owns c's pairs
-  const uint4* __restrict__ arcs = ca.arcs + size_t(r) * nc;
-  const float4* __restrict__ half = ca.half + size_t(r) * nc;
+// c's neighbour clusters within the cull radius^2 lim (fixed-point units),
+// in increasing order: for every batch of 32 candidates (one surviving
+// super-cluster) visit(jc, near) runs on all lanes (warp-uniform call).  Up
+// to 4 surviving super-clusters have their arc loads in flight together.
+template <class Visit>
+__device__ __forceinline__ void nl_scan(const ClusterArgs& ca, int r, uint4 gc, float4 gh, float lim,
+                                        Visit&& visit) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const uint4* __restrict__ arcs = ca.arcs + size_t(r) * ca.nc;
+  const float4* __restrict__ half = ca.half + size_t(r) * ca.nc;
   const uint4* __restrict__ sarcs = ca.sup_arcs + size_t(r) * ca.nsup;
   const float4* __restrict__ shalf = ca.sup_half + size_t(r) * ca.nsup;
-  const uint4 gc = arcs[c];
-  const float4 gh = half[c];
-  int* __restrict__ out = pb.olist + (size_t(r) * nc + c) * nc;
-  int* __restrict__ inl = pb.ilist + (size_t(r) * nc + c) * nc;
-  int nl = 0, ni = 0;
   for (int sb = 0; sb < ca.nsup; sb += 32) {
-    const int sc0 = sb + lane;
-    unsigned sv =
-        __ballot_sync(full, sc0 < ca.nsup && arcs_near(gc, gh, sarcs[sc0], shalf[sc0], ca.lim));
-    // 4 surviving super-clusters per round (their arc loads in flight together),
-    // in increasing index: owners are found in increasing order
+    unsigned sv = __ballot_sync(
+        full, sb + lane < ca.nsup && arcs_near(gc, gh, sarcs[sb + lane], shalf[sb + lane], lim));
     while (sv) {
       int scs[4];
 #pragma unroll
@@ -530,252 +610,423 @@ static __global__ void __launch_bounds__(kBuildWarps * 32)
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int jc = scs[b] * kSC + lane;
-        near[b] = scs[b] >= 0 && jc < nc && arcs_near(gc, gh, arcs[jc], half[jc], ca.lim);
+        near[b] = scs[b] >= 0 && jc < ca.nc && arcs_near(gc, gh, arcs[jc], half[jc], lim);
       }
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int jc = scs[b] * kSC + lane;
-        const bool own = near[b] && owns_pair(c, jc);
-        const bool inc = near[b] && (jc == c || !own);
-        // owned pairs only on the rank that owns c; owners: those on their rank
-        const bool o = own && mine;
-        const bool x = inc && jc >= pb.cbeg && jc < pb.cend;
-        const unsigned ov = __ballot_sync(full, o), xv = __ballot_sync(full, x);
-        if (o) out[nl + __popc(ov & lt)] = jc;
-        if (x) inl[ni + __popc(xv & lt)] = jc;
-        nl += __popc(ov);
-        ni += __popc(xv);
-      }
+      for (int b = 0; b < 4; ++b)
+        if (scs[b] >= 0) visit(scs[b] * kSC + lane, near[b]);
     }
   }
-  if (!mine && lane < kCS && c * kCS + lane < n) {
-    // another rank's rows (row shard): written 0 here, overwritten by
-    // k_cpair_jsum when this rank has records for them
-    const size_t roff = size_t(r) * n;
-    const size_t e = roff + ext_of(a.st.pos4[roff + c * kCS + lane]);
-    a.st.fx[e] = 0.0;
-    a.st.fy[e] = 0.0;
-    a.st.fz[e] = 0.0;
-  }
-  const int nu = (nl + kUnit - 1) / kUnit;
-  int ubase = 0, ibase = 0;
+}
+
+__device__ __forceinline__ bool owns_pair(int ci, int jc) {
+  return ci == jc || ((ci < jc) == (((ci ^ jc) & 1) == 0));
+}
+
+// Squared gap between two arcs (fixed-point units, a lower bound: arcs_near's margins)
+__device__ __forceinline__ float arcs_gap2(uint4 ca, float4 ha, uint4 cb, float4 hb) {
+  const float gx = arc_gap(ca.x, cb.x, ha.x + hb.x + kArcMargin);
+  const float gy = arc_gap(ca.y, cb.y, ha.y + hb.y + kArcMargin);
+  const float gz = arc_gap(ca.z, cb.z, ha.z + hb.z + kArcMargin);
+  return gx * gx + gy * gy + gz * gz;
+}
+
+// Shift code of one axis for the member pairs of arcs (ca, ha) x (cb, hb)
+// over the list's lifetime (every member within w = skin / 2 + margin of its
+// build position): 0: d, 1: d - L, 2: d + L for every pair; 3: per pair.
+// Fixed-point units (L = 2^32); double arithmetic on integers < 2^34 is exact.
+__device__ __forceinline__ int shift_code(uint32_t ca, float ha, uint32_t cb, float hb, float w) {
+  const double H = 4294967296.0, half = 2147483648.0, tol = 2147483648.0 * 1e-5 + 4096.0;
+  const double a0 = double(ca) - (double(ha) + w), a1 = double(ca) + (double(ha) + w);
+  const double b0 = double(cb) - (double(hb) + w), b1 = double(cb) + (double(hb) + w);
+  if (a0 < 0.0 || a1 >= H || b0 < 0.0 || b1 >= H) return 3;  // an arc may cross the boundary
+  const double lo = a0 - b1, hi = a1 - b0;                    // every raw difference d
+  if (lo > -half + tol && hi < half - tol) return 0;
+  if (lo > half + tol && hi < 3.0 * half - tol) return 1;
+  if (lo > -3.0 * half + tol && hi < -half - tol) return 2;
+  return 3;
+}
+
+// pass 1: owned entries (padded to kB) and incoming slots of every cluster
+static __global__ void __launch_bounds__(kNLBuildWarps * 32)
+    k_nl_count(ClusterArgs ca, NListArgs nl) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.y, nc = ca.nc;
+  const int c = blockIdx.x * kNLBuildWarps + warp;
+  if (c >= nc) return;
+  const unsigned full = 0xffffffffu;
+  const uint4 gc = ca.arcs[size_t(r) * nc + c];
+  const float4 gh = ca.half[size_t(r) * nc + c];
+  int no = 0, ni = 0;
+  nl_scan(ca, r, gc, gh, nl.lim_build, [&](int jc, bool near) {
+    const bool own = near && owns_pair(c, jc);
+    no += __popc(__ballot_sync(full, own));
+    ni += __popc(__ballot_sync(full, near && (jc == c || !own)));
+  });
   if (lane == 0) {
-    if (nu) ubase = atomicAdd(&pb.units[r], nu);
-    if (ni) ibase = atomicAdd(&pb.in_total[r], ni);
-    pb.ocnt[size_t(r) * nc + c] = nl;
-    pb.ustart[size_t(r) * nc + c] = ubase;
-    pb.in_cnt[size_t(r) * nc + c] = ni;
-    pb.in_base[size_t(r) * nc + c] = ibase;
+    const bool mine = c >= nl.cbeg && c < nl.cend;
+    nl.ocnt[size_t(r) * nc + c] = mine ? (no + kB - 1) / kB * kB : 0;
+    nl.icnt[size_t(r) * nc + c] = ni;
   }
-  ubase = __shfl_sync(full, ubase, 0);
-  ibase = __shfl_sync(full, ibase, 0);
-  for (int k = lane; k < nu; k += 32) pb.umap[size_t(r) * pb.max_units + ubase + k] = c;
-  __syncwarp();
-  for (int t = lane; t < ni; t += 32)
-    pb.inslot[(size_t(r) * nc + inl[t]) * nc + c] = ibase + t;
 }
 
-// L2 cache-policy hints for the contribution records: stored evict_last
-// (read back by k_cpair_jsum right after the walk), loaded evict_first
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void st_hint(double* a, double v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ double4 ld4_hint(const double4* a, uint64_t pol) {
-  double4 v;
-  const double2* q = reinterpret_cast<const double2*>(a);
-  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-               : "=d"(v.x), "=d"(v.y) : "l"(q), "l"(pol));
-  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-               : "=d"(v.z), "=d"(v.w) : "l"(q + 1), "l"(pol));
-  return v;
+// pass 2: exclusive scans of entries and incoming slots (one CTA per
+// replica); totals, overflow check and a fresh displacement bound into ctl
+// (an overflowing list is never used: the exact per-step walk runs instead)
+constexpr int kNLScanThreads = 1024;
+static __global__ void __launch_bounds__(kNLScanThreads) k_nl_scan(NListArgs nl, int nc) {
+  using Scan = cub::BlockScan<int, kNLScanThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry[2];
+  const int r = blockIdx.x;
+  const int* oc = nl.ocnt + size_t(r) * nc;
+  const int* ic = nl.icnt + size_t(r) * nc;
+  int* eb = nl.ebase + size_t(r) * (nc + 1);
+  int* ib = nl.ibase + size_t(r) * (nc + 1);
+  if (threadIdx.x < 2) carry[threadIdx.x] = 0;
+  __syncthreads();
+  for (int b = 0; b < nc; b += kNLScanThreads) {
+    const int c = b + threadIdx.x;
+    int x0, x1, t0, t1;
+    Scan(tmp).ExclusiveSum(c < nc ? oc[c] : 0, x0, t0);
+    __syncthreads();
+    Scan(tmp).ExclusiveSum(c < nc ? ic[c] : 0, x1, t1);
+    if (c < nc) {
+      eb[c] = carry[0] + x0;
+      ib[c] = carry[1] + x1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry[0] += t0, carry[1] += t1;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    eb[nc] = carry[0];
+    ib[nc] = carry[1];
+    int* ctl = nl.ctl + size_t(r) * kNLCtl;
+    ctl[kNLEntries] = carry[0];
+    ctl[kNLIncoming] = carry[1];
+    ctl[kNLTicket] = 0;
+    ctl[kNLOverflow] = (carry[0] > nl.max_ent || carry[1] > nl.max_ent) ? 1 : 0;
+    ctl[kNLD2] = 0;
+  }
 }
 
-// 28 resident warps per SM (72 registers)
-constexpr int kNWarpsPerSM = 28;
-constexpr int kJStride = 20;    // doubles per jl row of the j-side transpose (bank-conflict free)
+// pass 3: entries (owned, increasing cj, shift codes, build gap; padding
+// entries that never pass the cull), incoming owners (increasing) and the
+// build positions of the displacement bound
+static __global__ void __launch_bounds__(kNLBuildWarps * 32)
+    k_nl_fill(ClusterArgs ca, NListArgs nl) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.y, nc = ca.nc, n = ca.n;
+  const int c = blockIdx.x * kNLBuildWarps + warp;
+  if (c >= nc) return;
+  if (lane < kCS && c * kCS + lane < n)
+    nl.fixref[size_t(r) * n + c * kCS + lane] = ca.fixpos[size_t(r) * n + c * kCS + lane];
+  if (nl.ctl[size_t(r) * kNLCtl + kNLOverflow]) return;  // never read
+  const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+  const uint4 gc = ca.arcs[size_t(r) * nc + c];
+  const float4 gh = ca.half[size_t(r) * nc + c];
+  const bool mine = c >= nl.cbeg && c < nl.cend;
+  const int eb = nl.ebase[size_t(r) * (nc + 1) + c], ee = nl.ebase[size_t(r) * (nc + 1) + c + 1];
+  const int ib = nl.ibase[size_t(r) * (nc + 1) + c];
+  int4* __restrict__ ent = nl.ent + size_t(r) * nl.max_ent;
+  int* __restrict__ src = nl.in_src + size_t(r) * nl.max_ent;
+  const uint4* __restrict__ arcs = ca.arcs + size_t(r) * nc;
+  const float4* __restrict__ half = ca.half + size_t(r) * nc;
+  int no = 0, ni = 0;
+  nl_scan(ca, r, gc, gh, nl.lim_build, [&](int jc, bool near) {
+    const bool own = near && owns_pair(c, jc);
+    const bool inc = near && (jc == c || !own);
+    const unsigned ov = __ballot_sync(full, own && mine), iv = __ballot_sync(full, inc);
+    if (own && mine) {
+      const uint4 cj = arcs[jc];
+      const float4 hj = half[jc];
+      const int code = shift_code(gc.x, gh.x, cj.x, hj.x, nl.skin_half) |
+                       shift_code(gc.y, gh.y, cj.y, hj.y, nl.skin_half) << 2 |
+                       shift_code(gc.z, gh.z, cj.z, hj.z, nl.skin_half) << 4;
+      const float g2 = jc == c ? 0.0f : arcs_gap2(gc, gh, cj, hj);
+      ent[eb + no + __popc(ov & lt)] = make_int4(jc | code << kJcBits, c, 0, __float_as_int(g2));
+    }
+    if (inc) src[ib + ni + __popc(iv & lt)] = jc;
+    no += __popc(ov);
+    ni += __popc(iv);
+  });
+  for (int e = eb + no + lane; e < ee; e += 32)  // padding: above every c, never culled in
+    ent[e] = make_int4(kJcMask, c, 0, 0x7f800000);
+}
 
-template <int NW, bool MULTI_SPECIES, bool WRAPPED, bool VDERIV>
-__global__ void __launch_bounds__(NW * 32, kNWarpsPerSM / NW)
-    k_force_cpair_n3(ForceArgs a, ClusterArgs ca, PairBuf pb) {
-  __shared__ int wl_s[NW][kUnit + 2];
-  __shared__ int wr_s[NW][kUnit + 2];
-  __shared__ __align__(128) double4 stage[NW][kGDepth][2][kCS];
-  __shared__ __align__(16) double jt[NW][kCS * kJStride];  // j-side transpose
+// pass 4: the record slot of every entry: receiver c's incoming slot t of
+// owner x, found in x's (sorted) entries by binary search (owners on another
+// rank have no entries here: the slot is never written)
+static __global__ void __launch_bounds__(kNLBuildWarps * 32) k_nl_inrec(NListArgs nl, int nc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.y;
+  const int c = blockIdx.x * kNLBuildWarps + warp;
+  if (c >= nc || nl.ctl[size_t(r) * kNLCtl + kNLOverflow]) return;
+  const int* eb = nl.ebase + size_t(r) * (nc + 1);
+  int4* ent = nl.ent + size_t(r) * nl.max_ent;
+  const int i0 = nl.ibase[size_t(r) * (nc + 1) + c], i1 = nl.ibase[size_t(r) * (nc + 1) + c + 1];
+  for (int t = i0 + lane; t < i1; t += 32) {
+    const int x = nl.in_src[size_t(r) * nl.max_ent + t];
+    int lo = eb[x], hi = eb[x + 1];
+    while (lo < hi) {  // first entry >= c
+      const int mid = (lo + hi) >> 1;
+      if ((ent[mid].x & kJcMask) < c) lo = mid + 1; else hi = mid;
+    }
+    if (lo < eb[x + 1] && (ent[lo].x & kJcMask) == c) ent[lo].z = t;
+  }
+}
+
+__device__ __forceinline__ double stamp_of(int epoch) { return __longlong_as_double((long long)epoch); }
+
+template <bool MULTI_SPECIES, bool WRAPPED, bool VDERIV>
+__global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
+    k_force_nl(ForceArgs a, ClusterArgs ca, NListArgs nl) {
   const SysDev& s = a.s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int jl = lane >> 2, il = lane & 3;
   const int r = blockIdx.y;
   const size_t roff = size_t(r) * s.n;
-  const double4* __restrict__ p4 = a.st.pos4 + roff;
   const unsigned full = 0xffffffffu;
-  const int n = s.n, nc = ca.nc;
-  const int* __restrict__ ustart = pb.ustart + size_t(r) * nc;
-  const int* __restrict__ umap = pb.umap + size_t(r) * pb.max_units;
-  const int* __restrict__ ocnt = pb.ocnt + size_t(r) * nc;
-  double* __restrict__ rec = pb.rec + size_t(r) * (size_t(nc) * (nc + 1) / 2) * (kCS * 3);
-  double* __restrict__ irec = pb.irec + size_t(r) * pb.max_units * (kCS * 3);
-  const int total = pb.units[r];
-  const uint64_t pol = l2_policy_evict_last();
-  int* wl = wl_s[warp];
-  int* wr = wr_s[warp];
-  double* jtw = jt[warp];
-  const unsigned ring = smem_u32(&stage[warp][0][0][0]) + 16u * lane;
-  const char* __restrict__ src0 = reinterpret_cast<const char*>(p4) + 16 * (lane & 15);
-  const int half_sel = lane >> 4;
-  const MinImage mi = s.mi;
-  const float thr = a.thr;
-  const double rc2 = a.rc2;
-  auto mimg = [&](double d) {
-    return WRAPPED ? min_image_wrapped(d, mi.negL, thr) : min_image(d, mi);
-  };
-  auto dist = [&](const double4& pi, const double4& pj, double& dx, double& dy, double& dz) {
-    dx = mimg(sub(pi.x, pj.x));
-    dy = mimg(sub(pi.y, pj.y));
-    dz = mimg(sub(pi.z, pj.z));
-    return norm2_exact(dx, dy, dz);
-  };
-  double B12 = 0, B6 = 0;
+  const int n = s.n;
+  int* ctl = nl.ctl + size_t(r) * kNLCtl;
+  double B12 = 0, B6 = 0;  // once per pair (no halving)
   int cnt = 0;
-  // LJ force scalar -du_r / r2 of one pair (0 when out of range; the
-  // in-range flag also keeps a NaN position's R out of every sum)
-  auto lj = [&](bool in, double r2, int si, int sj) {
-    const double inv_r2 = rcp_nr(in ? r2 : 1.0);
-    const double t6 = inv_r2 * inv_r2 * inv_r2;
-    const double ir6 = in ? t6 : 0.0;
-    double fs;
-    if constexpr (MULTI_SPECIES) {
-      // Lorentz-Berthelot terms are symmetric in the species pair
-      const DevPairInfo& pinfo = s.tab->pair[si * s.ns + sj];
-      const double c12 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c12 : 0.0;
-      const double c6 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c6 : 0.0;
-      const double a12 = c12 * ir6 * ir6, a6 = c6 * ir6;
-      fs = (12.0 * a12 - 6.0 * a6) * inv_r2;
-      B12 += a12;
-      B6 += a6;
-    } else {
-      fs = fma(ir6, a.c12x12, -a.c6x6) * ir6 * inv_r2;
-      B12 = fma(ir6, ir6, B12);
-      B6 += ir6;
-    }
-    return fs;
-  };
-  for (;;) {
-    int u = 0;
-    if (lane == 0) u = atomicAdd(&pb.next_unit[r], 1);
-    u = __shfl_sync(full, u, 0);
-    if (u >= total) break;  // warp-uniform
-    const int ci = umap[u];
-    const int k0 = (u - ustart[ci]) * kUnit;
-    const int len = min(kUnit, ocnt[ci] - k0);
-    if (lane < len) {
-      const int jc = pb.olist[(size_t(r) * nc + ci) * nc + k0 + lane];
-      wl[lane] = jc;
-      wr[lane] = pb.inslot[(size_t(r) * nc + ci) * nc + jc] * (kCS * 3);  // in jc's range
-    }
-    if (lane == 0 && (len & 1)) {  // odd tail: a pad cluster past the end (no valid j)
-      wl[len] = nc;
-      wr[len] = -1;
-    }
-    const int ia = ci * kCS + il, ib = ia + 4;
-    const bool iva = ia < n, ivb = ib < n;
-    const double4 pa = p4[iva ? ia : ci * kCS], pbp = p4[ivb ? ib : ci * kCS];
-    const int sia = MULTI_SPECIES ? s.sp_slot[roff + (iva ? ia : ci * kCS)] : 0;
-    const int sib = MULTI_SPECIES ? s.sp_slot[roff + (ivb ? ib : ci * kCS)] : 0;
-    double fax = 0, fay = 0, faz = 0, fbx = 0, fby = 0, fbz = 0;
-    __syncwarp();
-    const int nsteps = (len + 1) >> 1;
-    int next = 0;
-    unsigned wslot = 0;
-    auto issue = [&]() {
-      const int e = 2 * next + half_sel;
-      if (next < nsteps) cp_async16(ring + wslot, src0 + size_t(wl[e]) * (kCS * 32));
-      cp_async_commit();
-      ++next;
-      wslot = (wslot + 512u) & (512u * kGDepth - 1u);
-    };
-#pragma unroll
-    for (int k = 0; k < kGDepth - 1; ++k) issue();
-    for (int st = 0; st < nsteps; ++st) {
-      issue();
-      cp_async_wait<kGDepth - 1>();
-      __syncwarp();
-      const int slot = st & (kGDepth - 1);
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        const int jc = wl[2 * st + h];
-        const int ro = wr[2 * st + h];
-        const int j = jc * kCS + jl;
-        const double4 pj = stage[warp][slot][h][jl];
-        const bool vj = j < n;
-        const bool self = jc == ci;
-        const bool va = iva && vj && (!self || j > ia);
-        const bool vb = ivb && vj && (!self || j > ib);
-        double dxa, dya, dza, dxb, dyb, dzb;
-        const double r2a = dist(pa, pj, dxa, dya, dza);
-        const double r2b = dist(pbp, pj, dxb, dyb, dzb);
-        const bool ina = va && r2a < rc2, inb = vb && r2b < rc2;  // potentials.cpp:161
-        double* rj = rec + ro + jl * 3 + il;
-        if (__ballot_sync(full, ina || inb) == 0u) {
-          if (ro >= 0 && il < 3) st_hint(rj, 0.0, pol);  // listed: the record is read
-          continue;
-        }
-        const int sj = MULTI_SPECIES ? (vj ? s.sp_slot[roff + j] : sia) : 0;
-        const double fsa = lj(ina, r2a, sia, sj);
-        const double fsb = lj(inb, r2b, sib, sj);
-        double gx = 0, gy = 0, gz = 0;
-        if (ina) {
-          gx = fsa * dxa, gy = fsa * dya, gz = fsa * dza;
-          fax += gx, fay += gy, faz += gz;
-        }
-        if (inb) {
-          const double hx = fsb * dxb, hy = fsb * dyb, hz = fsb * dzb;
-          fbx += hx, fby += hy, fbz += hz;
-          gx += hx, gy += hy, gz += hz;
-        }
-        cnt += int(ina) + int(inb);
-        // j-side: the 4 il lanes of member jl summed through shared memory
-        // (lane (jl, c) adds component c of rows il = 0..3 in order)
-        double* t = jtw + jl * kJStride + il * 4;
-        *reinterpret_cast<double2*>(t) = make_double2(gx, gy);
-        t[2] = gz;
-        __syncwarp();
-        if (il < 3) {
-          const double* v = jtw + jl * kJStride + il;
-          st_hint(rj, ((v[0] + v[4]) + v[8]) + v[12], pol);
-        }
-        __syncwarp();  // jt is rewritten by the next step
+  const int epoch = ctl[kNLEpoch];
+  // shared memory: the exact walk's per-warp lists and staging ring, or the
+  // list walk's staged batches (2 buffers x (kB j-clusters + the owner) per warp)
+  constexpr int kSlots = kB + 1;
+  __shared__ __align__(128) unsigned char smem[kNLWarps * 2 * kSlots * kCS * sizeof(double4)];
+  static_assert(sizeof(smem) >= (kNLWarps * (kGList + 1) * sizeof(int) + 127) / 128 * 128 +
+                                    kNLWarps * kGDepth * 2 * kCS * sizeof(double4),
+                "exact walk scratch");
+  if (nl_stale(nl, ctl)) {
+    // stale list: the exact per-step cull walk (both rows) for every group
+    auto clist = reinterpret_cast<int (*)[kGList + 1]>(smem);
+    constexpr size_t off = (kNLWarps * (kGList + 1) * sizeof(int) + 127) / 128 * 128;
+    auto stage = reinterpret_cast<double4 (*)[kGDepth][2][kCS]>(smem + off);
+    double b12 = 0, b6 = 0;
+    ForceArgs af = a;
+    af.kick_dt = 0.0;  // k_nl_reduce kicks
+    for (int grp = blockIdx.x * kNLWarps + warp; grp * kGR < n; grp += gridDim.x * kNLWarps)
+      cpair_group_forces<MULTI_SPECIES, WRAPPED>(af, ca, r, grp, clist[warp], stage[warp], b12, b6,
+                                                 cnt);
+    B12 = 0.5 * b12;  // both visits
+    B6 = 0.5 * b6;
+  } else {
+    const int E = ctl[kNLEntries];  // a multiple of kB
+    const int nbt = E / kB;
+    const int nw = gridDim.x * kNLWarps;
+    const int gw = blockIdx.x * kNLWarps + warp;
+    const int4* __restrict__ ent = nl.ent + size_t(r) * nl.max_ent;
+    double* __restrict__ rec = nl.rec + size_t(r) * nl.max_ent * kRecD + lane;
+    const double4* __restrict__ p4 = a.st.pos4 + roff;
+    const double L = s.mi.L;
+    const double stamp = stamp_of(epoch);
+    // this evaluation's cull: build gap^2 < (rc + 2 D)^2 (fixed-point units)
+    const float dd = nl.rc_fix + 2.0f * sqrtf(__uint_as_float(unsigned(ctl[kNLD2])));
+    const float lim_now = dd * dd * (1.0f + 1e-5f);
+    // LJ force scalar -du_r / r2 of one pair (0 when out of range; the
+    // in-range flag also keeps a NaN position's R out of every sum)
+    auto lj = [&](bool in, double r2, int si, int sj) {
+      const double inv_r2 = rcp_nr(r2);
+      const double t6 = inv_r2 * inv_r2 * inv_r2;
+      const double ir6 = in ? t6 : 0.0;
+      double fs;
+      if constexpr (MULTI_SPECIES) {
+        // Lorentz-Berthelot terms are symmetric in the species pair
+        const DevPairInfo& pinfo = s.tab->pair[si * s.ns + sj];
+        const double c12 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c12 : 0.0;
+        const double c6 = pinfo.lj_count ? s.tab->lj[pinfo.lj_begin].c6 : 0.0;
+        const double a12 = c12 * ir6 * ir6, a6 = c6 * ir6;
+        fs = (12.0 * a12 - 6.0 * a6) * inv_r2;
+        B12 += a12;
+        B6 += a6;
+      } else {
+        fs = fma(ir6, a.c12x12, -a.c6x6) * ir6 * inv_r2;
+        B12 = fma(ir6, ir6, B12);
+        B6 += ir6;
       }
-      __syncwarp();  // the slot's reads are consumed before it is refilled
-    }
-    cp_async_wait<0>();
-    // rows ia / ib: their 8 jl lanes by a fixed xor tree
+      return fs;
+    };
+    // per-warp scratch: the staged batches' surviving entries {cj | codes,
+    // record slot}, their j-clusters and the owner's cluster (256 contiguous
+    // bytes of pos4 each, bulk copies completing on the buffer's mbarrier),
+    // and two buffers of the j-side transpose (lane (jl, il) -> lane (jl, c))
+    __shared__ int2 elist[kNLWarps][2][kB];
+    __shared__ double jt[kNLWarps][2][4 * kCS * 3];
+    __shared__ __align__(8) uint64_t mbar[kNLWarps][2];
+    double4 (*jst)[kSlots][kCS] = reinterpret_cast<double4 (*)[kSlots][kCS]>(smem) + warp * 2;
+    if (lane < 2) mbar_init(&mbar[warp][lane], 1);
+    __syncwarp();
+    unsigned phase = 0u;  // bit p: parity of buffer p's next completion
+    int par = 0;
+    const int cw = il < 3 ? il : 2;  // component read by this lane in the transpose
+    // batch bt's cull, compaction and copies into buffer p (the surviving
+    // j-clusters and the owner's cluster); returns the number of survivors
+    // (0: no copies, no mbarrier phase)
+    auto stage_batch = [&](int p, const int4& en) {
+      const bool near = lane < kB && __int_as_float(en.w) < lim_now;
+      const unsigned act = __ballot_sync(full, near);
+      const int na = __popc(act);
+      const int owner = __shfl_sync(full, en.y, 0);
+      if (na == 0) return 0;
+#if B2MD_NL_TMA
+      fence_proxy_async();  // earlier reads of this buffer precede the copies
+      if (lane == 0)
+        mbar_arrive_expect_tx(&mbar[warp][p], unsigned(na + 1) * kCS * sizeof(double4));
+      __syncwarp();
+      if (near) {
+        const int t = __popc(act & ((1u << lane) - 1u));
+        elist[warp][p][t] = make_int2(en.x, en.z);
+        bulk_g2s(jst[p][t], p4 + (en.x & kJcMask) * kCS, kCS * sizeof(double4), &mbar[warp][p]);
+      }
+      if (lane == 31) bulk_g2s(jst[p][kB], p4 + owner * kCS, kCS * sizeof(double4), &mbar[warp][p]);
+#else
+      // 16-byte cp.async per lane: chunk q of the (na + 1) x 256 contiguous bytes
+      // (survivors in order, then the owner), one commit group per batch
+      if (near) {
+        const int t = __popc(act & ((1u << lane) - 1u));
+        elist[warp][p][t] = make_int2(en.x, en.z);
+      }
+      __syncwarp();
+      const unsigned dst = smem_u32(jst[p]);
+      for (int q = lane; q < (na + 1) * 16; q += 32) {
+        const int t = q >> 4;
+        const int jc = t < na ? (elist[warp][p][t].x & kJcMask) : owner;
+        const char* src = reinterpret_cast<const char*>(p4 + size_t(jc) * kCS) + 16 * (q & 15);
+        cp_async16(dst + (t < na ? t : kB) * 256 + 16 * (q & 15), src);
+      }
+      cp_async_commit();
+#endif
+      return na;
+    };
+    auto load_batch = [&](int bt) {
+      return (bt < nbt && lane < kB) ? ent[bt * kB + lane] : make_int4(0, 0, 0, 0x7f800000);
+    };
+    int4 en = load_batch(gw);
+    int ci = en.y;  // (lane 0's owner: broadcast below)
+    int na = gw < nbt ? stage_batch(0, en) : 0;
+    ci = __shfl_sync(full, ci, 0);
+    en = load_batch(gw + nw);
+    int p = 0;
+    for (int bt = gw; bt < nbt; bt += nw, p ^= 1) {
+      // stage the next batch into the other buffer, load the one after
+      const int ci_next = __shfl_sync(full, en.y, 0);
+      const int na_next = bt + nw < nbt ? stage_batch(p ^ 1, en) : 0;
+      en = load_batch(bt + 2 * nw);
+      if (na) {
+#if B2MD_NL_TMA
+        mbar_wait(&mbar[warp][p], (phase >> p) & 1u);
+        phase ^= 1u << p;
+#else
+        if (na_next) cp_async_wait<1>(); else cp_async_wait<0>();
+#endif
+        __syncwarp();  // elist, staged data
+        const int ia = ci * kCS + il, ib = ia + 4;
+        const bool iva = ia < n, ivb = ib < n;
+        const double4 qa = jst[p][kB][il], qb = jst[p][kB][il + 4];
+        const double pax = qa.x, pay = qa.y, paz = qa.z, pbx = qb.x, pby = qb.y, pbz = qb.z;
+        int sia = 0, sib = 0;
+        if constexpr (MULTI_SPECIES) {
+          sia = s.sp_slot[roff + (iva ? ia : ci * kCS)];
+          sib = s.sp_slot[roff + (ivb ? ib : ci * kCS)];
+        }
+        double fax = 0, fay = 0, faz = 0, fbx = 0, fby = 0, fbz = 0;
+        bool dirty = false;
+        for (int t = 0; t < na; ++t) {  // warp-uniform
+          const int2 cur = elist[warp][p][t];
+          const double4 pj = jst[p][t][jl];
+          if (nl.dbg & 16) {
+            dirty = true;
+            fax += pj.x;
+            continue;
+          }
+          const int jc = cur.x & kJcMask, code = cur.x >> kJcBits;
+          const int j = jc * kCS + jl;
+          const bool vj = j < n;
+          const bool self = jc == ci;
+          const bool va = iva && vj && (!self || j > ia);
+          const bool vb = ivb && vj && (!self || j > ib);
+          double dxa = sub(pax, pj.x), dya = sub(pay, pj.y), dza = sub(paz, pj.z);
+          double dxb = sub(pbx, pj.x), dyb = sub(pby, pj.y), dzb = sub(pbz, pj.z);
+          if constexpr (WRAPPED) {
+            if (code) {  // warp-uniform
+              if (code & (code >> 1) & 0x15) {  // some axis per pair: the per-pair image on all
+                const float thr = a.thr;
+                const double negL = s.mi.negL;
+                dxa = min_image_wrapped(dxa, negL, thr), dya = min_image_wrapped(dya, negL, thr);
+                dza = min_image_wrapped(dza, negL, thr), dxb = min_image_wrapped(dxb, negL, thr);
+                dyb = min_image_wrapped(dyb, negL, thr), dzb = min_image_wrapped(dzb, negL, thr);
+              } else {  // uniform images: d -+ L (a 0.0 shift leaves d as it is)
+                const int cx = code & 3, cy = (code >> 2) & 3, cz = code >> 4;
+                const double sx = cx == 0 ? 0.0 : (cx == 1 ? -L : L);
+                const double sy = cy == 0 ? 0.0 : (cy == 1 ? -L : L);
+                const double sz = cz == 0 ? 0.0 : (cz == 1 ? -L : L);
+                dxa = add(dxa, sx), dya = add(dya, sy), dza = add(dza, sz);
+                dxb = add(dxb, sx), dyb = add(dyb, sy), dzb = add(dzb, sz);
+              }
+            }
+          } else {
+            const MinImage mi = s.mi;
+            dxa = min_image(dxa, mi), dya = min_image(dya, mi), dza = min_image(dza, mi);
+            dxb = min_image(dxb, mi), dyb = min_image(dyb, mi), dzb = min_image(dzb, mi);
+          }
+          const double r2a = norm2_exact(dxa, dya, dza), r2b = norm2_exact(dxb, dyb, dzb);
+          const bool ina = va && r2a < a.rc2, inb = vb && r2b < a.rc2;  // potentials.cpp:161
+          if (__ballot_sync(full, ina || inb) == 0u) continue;  // no record: its stamp stays old
+          const int sj = MULTI_SPECIES ? (vj ? s.sp_slot[roff + j] : sia) : 0;
+          // both rows' terms in one block (two independent dependency chains)
+          const double fsa = (nl.dbg & 1) ? 0.0 : lj(ina, r2a, sia, sj);
+          const double fsb = (nl.dbg & 1) ? 0.0 : lj(inb, r2b, sib, sj);
+          double gx = 0, gy = 0, gz = 0;
+          if (ina) {
+            gx = fsa * dxa, gy = fsa * dya, gz = fsa * dza;
+            fax += gx, fay += gy, faz += gz;
+          }
+          if (inb) {
+            const double hx = fsb * dxb, hy = fsb * dyb, hz = fsb * dzb;
+            fbx += hx, fby += hy, fbz += hz;
+            gx += hx, gy += hy, gz += hz;
+          }
+          dirty = true;
+          cnt += int(ina) + int(inb);
+          if (nl.dbg & 2) continue;
+          // j-side: member jl's 4 row lanes summed in row order through
+          // shared memory (lane (jl, c) adds component c), stamped record
+          double* jb = jt[warp][par];
+          par ^= 1;
+          jb[il * 24 + jl * 3] = gx;
+          jb[il * 24 + jl * 3 + 1] = gy;
+          jb[il * 24 + jl * 3 + 2] = gz;
+          __syncwarp();
+          const double* jr = jb + jl * 3 + cw;
+          const double res = ((jr[0] + jr[24]) + jr[48]) + jr[72];
+          if (nl.dbg & 4) continue;
+          rec[cur.y * kRecD] = il == 3 ? stamp : res;
+        }
+        if (dirty) {  // the batch's i-side record (rows ia / ib: 8 jl lanes, xor tree)
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      fax += __shfl_xor_sync(full, fax, o);
-      fay += __shfl_xor_sync(full, fay, o);
-      faz += __shfl_xor_sync(full, faz, o);
-      fbx += __shfl_xor_sync(full, fbx, o);
-      fby += __shfl_xor_sync(full, fby, o);
-      fbz += __shfl_xor_sync(full, fbz, o);
+          for (int o = 4; o < 32; o <<= 1) {
+            fax += __shfl_xor_sync(full, fax, o);
+            fay += __shfl_xor_sync(full, fay, o);
+            faz += __shfl_xor_sync(full, faz, o);
+            fbx += __shfl_xor_sync(full, fbx, o);
+            fby += __shfl_xor_sync(full, fby, o);
+            fbz += __shfl_xor_sync(full, fbz, o);
+          }
+          if (lane < 4) {  // members il and il + 4: (x, y, z, stamp)
+            double* q = nl.irec + (size_t(r) * (nl.max_ent / kB) + bt) * kRecD;
+            *reinterpret_cast<double4*>(q + 4 * il) = make_double4(fax, fay, faz, stamp);
+            *reinterpret_cast<double4*>(q + 4 * (il + 4)) = make_double4(fbx, fby, fbz, stamp);
+          }
+        }
+      }
+      __syncwarp();  // this buffer's reads are done before it is restaged
+      ci = ci_next;
+      na = na_next;
     }
-    if (lane < 4) {  // the unit's i-side record: member m, component c at 3 m + c
-      double* q = irec + size_t(u) * (kCS * 3);
-      q[3 * il] = fax, q[3 * il + 1] = fay, q[3 * il + 2] = faz;
-      q[3 * (il + 4)] = fbx, q[3 * (il + 4) + 1] = fby, q[3 * (il + 4) + 2] = fbz;
-    }
-    __syncwarp();  // wl / wr / the ring are rewritten by the next unit
   }
-  // once per pair: no halving
   double A12 = warp_sum(B12), A6 = warp_sum(B6);
   if constexpr (!MULTI_SPECIES) {
     A12 *= a.c12;
@@ -786,93 +1037,76 @@ __global__ void __launch_bounds__(NW * 32, kNWarpsPerSM / NW)
                               VDERIV ? 156.0 * A12 - 42.0 * A6 : 0.0, -s1,
                               warp_sum(double(cnt))};
   finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
-  // the last CTA re-arms the unit counters for the next evaluation
+  // the last CTA advances the epoch: k_nl_reduce reads the stamps of this one
   __shared__ bool lastcta;
-  __syncthreads();
-  if (threadIdx.x == 0) lastcta = atomicAdd(&pb.ticket[r], 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) lastcta = atomicAdd(ctl + kNLTicket, 1) == int(gridDim.x) - 1;
   __syncthreads();
   if (lastcta && threadIdx.x == 0) {
-    pb.units[r] = 0;
-    pb.in_total[r] = 0;
-    pb.next_unit[r] = 0;
-    pb.ticket[r] = 0u;
+    ctl[kNLEpoch] = epoch + 1;
+    ctl[kNLTicket] = 0;
   }
 }
 
-// The fixed-order reduction of the contribution buffers: one warp per
-// cluster c.  Its records are two contiguous ranges -- its unit records
-// (i-side, unit order) and its receiver records (j-side, increasing owner)
-// -- read 5 at a time as double4 (lane = (record q = lane / 6, quarter p =
-// lane % 6)), each lane summing its quarter over records q, q + 5, ... (8
-// loads in flight); the 5 partial sums are added in q order.  Force =
-// i-side - j-side, then the fused end-of-step kick.
-constexpr int kJsumWarps = 4;
-
-static __global__ void __launch_bounds__(kJsumWarps * 32) k_cpair_jsum(ForceArgs a, ClusterArgs ca,
-                                                                        PairBuf pb) {
+// The fixed-order reduction of the contribution records: one warp per
+// cluster c, lane = (record offset q = lane >> 3, member m = lane & 7).  Group
+// q = 0 first adds c's batches' i-side records; then c's incoming records --
+// a contiguous, receiver-major range in owner order -- are subtracted, record
+// t by group t % 4 (32 records' loads in flight per round); the 4 groups are
+// combined by a fixed xor tree.  Only records stamped by this evaluation
+// count (an entry without a pair in cutoff writes nothing).  Then the fused
+// end-of-step kick.  On a stale list the forces were written by the exact
+// walk: only the kick.
+static __global__ void __launch_bounds__(kNLBuildWarps * 32)
+    k_nl_reduce(ForceArgs a, ClusterArgs ca, NListArgs nl) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane >> 3, m = lane & 7;
   const int r = blockIdx.y;
   const int n = a.s.n, nc = ca.nc;
-  const int c = blockIdx.x * kJsumWarps + warp;
+  const int c = blockIdx.x * kNLBuildWarps + warp;
   if (c >= nc) return;
   const unsigned full = 0xffffffffu;
   const size_t roff = size_t(r) * n;
-  const int q = lane / 6, p = lane - 6 * (lane / 6);  // record in a group of 5, quarter
-  const int u0 = pb.ustart[size_t(r) * nc + c];
-  const int nu = (pb.ocnt[size_t(r) * nc + c] + kUnit - 1) / kUnit;
-  const int i0 = pb.in_base[size_t(r) * nc + c];
-  const int ni = pb.in_cnt[size_t(r) * nc + c];
-  const int slot = c * kCS + (lane & 7);
-  const int ext = slot < n ? ext_of(a.st.pos4[roff + slot]) : 0;
-  const uint64_t pol = l2_policy_evict_first();
-  auto sum_range = [&](const double4* __restrict__ base, int cnt) {
-    double4 acc = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (q < 5) {
-      int e = q;
-      for (; e + 35 < cnt; e += 40) {
-        double4 v[8];
-#pragma unroll
-        for (int b = 0; b < 8; ++b) v[b] = ld4_hint(base + size_t(e + 5 * b) * 6 + p, pol);
-#pragma unroll
-        for (int b = 0; b < 8; ++b) acc.x += v[b].x, acc.y += v[b].y, acc.z += v[b].z, acc.w += v[b].w;
+  const int slot = c * kCS + m;
+  const int* ctl = nl.ctl + size_t(r) * kNLCtl;
+  if (!nl_stale(nl, ctl)) {
+    const long long epoch = ctl[kNLEpoch] - 1;  // advanced by the force kernel's last CTA
+    const int* eb = nl.ebase + size_t(r) * (nc + 1);
+    const double* __restrict__ irec = nl.irec + size_t(r) * (nl.max_ent / kB) * kRecD + 4 * m;
+    const double* __restrict__ rec = nl.rec + size_t(r) * nl.max_ent * kRecD + 4 * m;
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    if (q == 0)
+      for (int b = eb[c] / kB; b < eb[c + 1] / kB; ++b) {
+        const double4 u = *reinterpret_cast<const double4*>(irec + size_t(b) * kRecD);
+        if (__double_as_longlong(u.w) == epoch) fx += u.x, fy += u.y, fz += u.z;
       }
-      for (; e < cnt; e += 5) {
-        const double4 v = ld4_hint(base + size_t(e) * 6 + p, pol);
-        acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+    const int i1 = nl.ibase[size_t(r) * (nc + 1) + c + 1];
+    for (int t0 = nl.ibase[size_t(r) * (nc + 1) + c]; t0 < i1; t0 += 32) {
+      double4 u[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int t = t0 + 4 * k + q;
+        u[k] = t < i1 ? *reinterpret_cast<const double4*>(rec + size_t(t) * kRecD)
+                      : make_double4(0.0, 0.0, 0.0, __longlong_as_double(-1ll));
       }
-    }
-    return acc;
-  };
-  double4 ai = sum_range(reinterpret_cast<const double4*>(pb.irec + size_t(r) * pb.max_units * (kCS * 3)) +
-                             size_t(u0) * 6, nu);
-  double4 aj = sum_range(reinterpret_cast<const double4*>(
-                             pb.rec + size_t(r) * (size_t(nc) * (nc + 1) / 2) * (kCS * 3)) +
-                             size_t(i0) * 6, ni);
 #pragma unroll
-  for (int g = 1; g < 5; ++g) {
-    const int src = g * 6 + p;
-    const double xi = __shfl_sync(full, ai.x, src), yi = __shfl_sync(full, ai.y, src);
-    const double zi = __shfl_sync(full, ai.z, src), wi = __shfl_sync(full, ai.w, src);
-    const double xj = __shfl_sync(full, aj.x, src), yj = __shfl_sync(full, aj.y, src);
-    const double zj = __shfl_sync(full, aj.z, src), wj = __shfl_sync(full, aj.w, src);
-    if (q == 0) {
-      ai.x += xi, ai.y += yi, ai.z += zi, ai.w += wi;
-      aj.x += xj, aj.y += yj, aj.z += zj, aj.w += wj;
+      for (int k = 0; k < 8; ++k)
+        if (__double_as_longlong(u[k].w) == epoch) fx -= u[k].x, fy -= u[k].y, fz -= u[k].z;
     }
-  }
-  // lane p < 6 holds doubles 4p .. 4p + 3 of the 24 (member d / 3, component d % 3)
-  const double v[4] = {ai.x - aj.x, ai.y - aj.y, ai.z - aj.z, ai.w - aj.w};
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int d = 4 * p + t, m = d / 3, cc = d - 3 * (d / 3);
-    const int e = __shfl_sync(full, ext, m);
-    if (q == 0 && c * kCS + m < n) {
-      double* f = cc == 0 ? a.st.fx : (cc == 1 ? a.st.fy : a.st.fz);
-      f[roff + e] = v[t];
+    for (int o = 8; o < 32; o <<= 1) {
+      fx += __shfl_xor_sync(full, fx, o);
+      fy += __shfl_xor_sync(full, fy, o);
+      fz += __shfl_xor_sync(full, fz, o);
+    }
+    if (q == 0 && slot < n) {
+      const size_t e = roff + ext_of(a.st.pos4[roff + slot]);
+      a.st.fx[e] = fx;
+      a.st.fy[e] = fy;
+      a.st.fz[e] = fz;
     }
   }
   __syncwarp();
-  if (lane < kCS && slot < n && a.kick_dt > 0.0) fused_kick(a, roff + ext);
+  if (q == 0 && slot < n && a.kick_dt > 0.0) fused_kick(a, roff + ext_of(a.st.pos4[roff + slot]));
 }
 
 // heat_flux (greenkubo.cpp:182-266) of a single-species, centred, LJ-only

@@ -41,7 +41,7 @@ int nccl_load() {
 
 const char* kFamilyName[F_COUNT] = {"offsets",  "search", "force",   "ewald_tables", "ewald_sk",
                                     "ewald_force", "kick_kick_drift", "kick_drift", "kick", "allreduce",
-                                    "heat_flux", "rdf", "cluster", "force_jsum"};
+                                    "heat_flux", "rdf", "cluster", "force_jsum", "nl_build"};
 
 // AoS <-> SoA staging kernels (host layout Vec3 / Quat of include/tmd/geom.hpp)
 static __global__ void k_aos_to_soa(const double* aos, int count, int width, double* d0, double* d1,
@@ -404,7 +404,39 @@ ClusterArgs cluster_args(const b2md_ctx* c) {
   const long groups = (c->t.n + kGR - 1) / kGR;
   ca.grp_begin = int(groups * c->rank / std::max(1, c->world));
   ca.grp_end = int(groups * (c->rank + 1) / std::max(1, c->world));
+  ca.fixref = c->nl.fixref;
+  ca.nl_ctl = c->nl.ctl;
   return ca;
+}
+
+bool nl_path(const b2md_ctx* c) { return cluster_path(c) && c->use_newton && c->nl.ctl; }
+
+NListArgs nl_args(const b2md_ctx* c) {
+  NListArgs nl = c->nl;
+  nl.cbeg = int(long(c->nc) * c->rank / std::max(1, c->world));
+  nl.cend = int(long(c->nc) * (c->rank + 1) / std::max(1, c->world));
+  return nl;
+}
+
+// The once-per-pair list from the current cluster arcs (cluster.cuh): after
+// every staging of positions (re-sort, evaluate, set_state, restore) and at
+// the scheduled interval, always between a drift and a force evaluation.
+int nl_build(b2md_ctx* c) {
+  if (!nl_path(c)) return B2MD_OK;
+  const ClusterArgs ca = cluster_args(c);
+  const NListArgs nl = nl_args(c);
+  const dim3 g((c->nc + kNLBuildWarps - 1) / kNLBuildWarps, c->R);
+  const int bs = kNLBuildWarps * 32;
+  PROF(c, F_NL_BUILD, (k_nl_count<<<g, bs, 0, c->stream>>>(ca, nl)));
+  PROF(c, F_NL_BUILD, (k_nl_scan<<<c->R, kNLScanThreads, 0, c->stream>>>(nl, c->nc)));
+  PROF(c, F_NL_BUILD, (k_nl_fill<<<g, bs, 0, c->stream>>>(ca, nl)));
+  PROF(c, F_NL_BUILD, (k_nl_inrec<<<g, bs, 0, c->stream>>>(nl, c->nc)));
+  c->steps_since_nl = 0;
+  return B2MD_OK;
+}
+
+bool nl_due(const b2md_ctx* c) {
+  return nl_path(c) && c->nl_interval > 0 && c->steps_since_nl >= c->nl_interval;
 }
 
 // Cluster arcs are derived wherever fixed-point positions are written: by
@@ -414,7 +446,7 @@ int launch_cluster_arcs(b2md_ctx* c) {
   if (!cluster_path(c)) return B2MD_OK;
   const ClusterArgs ca = cluster_args(c);
   PROF(c, F_CLUSTER, (k_cluster_arcs<<<c->R * c->nsup, kSC * kCS, 0, c->stream>>>(ca, c->R)));
-  return B2MD_OK;
+  return nl_build(c);
 }
 
 int launch_cluster_force(b2md_ctx* c, bool kick) {
@@ -423,52 +455,25 @@ int launch_cluster_force(b2md_ctx* c, bool kick) {
   ForceArgs a = force_args(c);
   if (kick) a.kick_dt = c->dt;
   const bool w = fast_min_image(c), m = c->t.ns > 1, v = a.vderiv != 0;
-  if (c->use_newton) {
-    const size_t nc = size_t(c->nc);
-    PairBuf pb;
-    pb.rec = c->d_prec;
-    pb.irec = c->d_pirec;
-    pb.olist = c->d_polist;
-    pb.ilist = pb.olist + size_t(R) * nc * nc;
-    pb.inslot = pb.ilist + size_t(R) * nc * nc;
-    int* q = c->d_pint;
-    pb.ocnt = q, q += size_t(R) * nc;
-    pb.ustart = q, q += size_t(R) * nc;
-    pb.in_base = q, q += size_t(R) * nc;
-    pb.in_cnt = q, q += size_t(R) * nc;
-    pb.umap = q, q += size_t(R) * c->pb_max_units;
-    pb.units = q, q += R;
-    pb.in_total = q, q += R;
-    pb.next_unit = q, q += R;
-    pb.ticket = reinterpret_cast<unsigned*>(q);
-    pb.max_units = c->pb_max_units;
-    pb.cbeg = int(long(c->nc) * c->rank / std::max(1, c->world));
-    pb.cend = int(long(c->nc) * (c->rank + 1) / std::max(1, c->world));
+  if (nl_path(c)) {
+    const NListArgs nl = nl_args(c);
     ForceArgs aw = a;
-    aw.kick_dt = 0.0;  // the rows are complete only after k_cpair_jsum
-    PROF(c, F_CLUSTER, (k_cpair_build<<<dim3((c->nc + kBuildWarps - 1) / kBuildWarps, R),
-                                     kBuildWarps * 32, 0, c->stream>>>(a, ca, pb)));
-    // persistent warps taking work units: NW warps per CTA (B2MD_N3_WARPS)
-    const int nw = c->n3_warps;
+    aw.kick_dt = 0.0;  // the rows are complete only after k_nl_reduce
     const dim3 ngrid(c->n3_grid, R);
-#define N3_LAUNCH(NW, M, W, V)                                                                   \
-  if (nw == NW && m == M && w == W && v == V)                                                    \
-    PROF(c, F_FORCE, (k_force_cpair_n3<NW, M, W, V><<<ngrid, NW * 32, 0, c->stream>>>(aw, ca, pb)));
-#define N3_NW(NW)                    \
-  N3_LAUNCH(NW, false, true, false)  \
-  N3_LAUNCH(NW, false, true, true)   \
-  N3_LAUNCH(NW, false, false, false) \
-  N3_LAUNCH(NW, false, false, true)  \
-  N3_LAUNCH(NW, true, true, false)   \
-  N3_LAUNCH(NW, true, true, true)    \
-  N3_LAUNCH(NW, true, false, false)  \
-  N3_LAUNCH(NW, true, false, true)
-    N3_NW(2)
-    N3_NW(4)
-#undef N3_NW
-#undef N3_LAUNCH
-    PROF(c, F_JSUM, (k_cpair_jsum<<<dim3((c->nc + kJsumWarps - 1) / kJsumWarps, R),
-                                    kJsumWarps * 32, 0, c->stream>>>(a, ca, pb)));
+#define NL_LAUNCH(M, W, V) \
+  if (m == M && w == W && v == V) \
+    PROF(c, F_FORCE, (k_force_nl<M, W, V><<<ngrid, kNLWarps * 32, 0, c->stream>>>(aw, ca, nl)));
+    NL_LAUNCH(false, true, false)
+    NL_LAUNCH(false, true, true)
+    NL_LAUNCH(false, false, false)
+    NL_LAUNCH(false, false, true)
+    NL_LAUNCH(true, true, false)
+    NL_LAUNCH(true, true, true)
+    NL_LAUNCH(true, false, false)
+    NL_LAUNCH(true, false, true)
+#undef NL_LAUNCH
+    PROF(c, F_JSUM, (k_nl_reduce<<<dim3((c->nc + kNLBuildWarps - 1) / kNLBuildWarps, R),
+                                   kNLBuildWarps * 32, 0, c->stream>>>(a, ca, nl)));
     c->mask_valid = false;
     return B2MD_OK;
   }
@@ -887,8 +892,9 @@ int launch_prof_graph(b2md_ctx* c) {
 int run_steps(b2md_ctx* c, int64_t nsteps) {
   c->state_in_box = true;  // every step's drift wraps before anything reads the positions
   const bool graphs = c->use_graphs && !c->profile;
-  if (nsteps == 1 && c->use_graphs && !sort_due(c)) {
+  if (nsteps == 1 && c->use_graphs && !sort_due(c) && !nl_due(c)) {
     ++c->steps_since_sort;
+    ++c->steps_since_nl;
     if (c->profile) return launch_prof_graph(c);
     TRY(build_single_step_graph(c));
     CU(cudaGraphLaunch(c->single_graph, c->stream));
@@ -897,15 +903,23 @@ int run_steps(b2md_ctx* c, int64_t nsteps) {
   if (graphs) TRY(build_step_graph(c));
   TRY(launch_step_kernel(c, F_KICK_DRIFT));
   for (int64_t k = 0; k + 1 < nsteps; ++k) {
-    if (sort_due(c)) TRY(resort_and_stage(c));
+    if (sort_due(c))
+      TRY(resort_and_stage(c));  // (rebuilds the list)
+    else if (nl_due(c))
+      TRY(nl_build(c));
     ++c->steps_since_sort;
+    ++c->steps_since_nl;
     if (graphs)
       CU(cudaGraphLaunch(c->step_graph, c->stream));
     else
       TRY(enqueue_loop_body(c));
   }
-  if (sort_due(c)) TRY(resort_and_stage(c));
+  if (sort_due(c))
+    TRY(resort_and_stage(c));
+  else if (nl_due(c))
+    TRY(nl_build(c));
   ++c->steps_since_sort;
+  ++c->steps_since_nl;
   TRY(enqueue_forces_and_kick(c));
   return B2MD_OK;
 }
@@ -1242,7 +1256,7 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars *
                                    std::max({c->force_grid, c->nc > 0 ? cpair_grid(c) : 0,
-                                             c->nc > 0 ? sms * kNWarpsPerSM : 0,
+                                             c->nc > 0 ? sms * kNLMinBlocks : 0,
                                              (((c->t.n + 31) / 32) * ((c->t.n + 31) / 32 + 1) / 2 +
                                               kTileWarps - 1) / kTileWarps})));
   }
@@ -1252,51 +1266,50 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     TRY(dalloc(&c->d_chalf, size_t(R) * c->nc));
     TRY(dalloc(&c->d_sarc, size_t(R) * c->nsup));
     TRY(dalloc(&c->d_shalf, size_t(R) * c->nsup));
-    // once-per-pair walk: triangular record array (192 B per cluster pair) and
-    // the bitmap (zeroed here; k_cpair_jsum clears what it reads)
+    // once-per-pair list: worst-case capacity (every cluster pair listed),
+    // 192 B of record per entry; beyond 8 GB the both-rows walk runs
     if (const char* e = std::getenv("B2MD_NEWTON")) c->use_newton = std::atoi(e) != 0;
-    if (const char* e = std::getenv("B2MD_N3_WARPS")) {
-      const int v = std::atoi(e);
-      c->n3_warps = v >= 4 ? 4 : 2;
-    }
-    const size_t pairs = size_t(c->nc) * (c->nc + 1) / 2;
-    if (c->use_newton && size_t(R) * pairs * kCS * 3 * sizeof(double) > (size_t(8) << 30))
-      c->use_newton = false;  // beyond 8 GB of records: the both-rows walk
+    const size_t nc = size_t(c->nc);
+    // every cluster pair once, plus < kB padding entries per owner
+    const size_t max_ent = (nc * (nc + 1) / 2 + nc * kB + kB - 1) / kB * kB;
+    if (size_t(R) * max_ent * kRecD * sizeof(double) > (size_t(8) << 30))
+      c->use_newton = false;
     if (c->use_newton) {
-      const size_t nc = size_t(c->nc);
-      // units <= owned pairs / kUnit + one partial unit per cluster
-      c->pb_max_units = int(pairs / kUnit + nc);
-      TRY(dalloc(&c->d_prec, size_t(R) * pairs * kCS * 3));
-      TRY(dalloc(&c->d_pirec, size_t(R) * c->pb_max_units * kCS * 3));
-      TRY(dalloc(&c->d_polist, size_t(R) * nc * nc * 3));  // olist | ilist | inslot
-      const size_t ints = size_t(R) * (5 * nc + c->pb_max_units + 4);
-      TRY(dalloc(&c->d_pint, ints));
-      CU(cudaMemset(c->d_pint, 0, sizeof(int) * ints));
+      NListArgs& nl = c->nl;
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-      c->n3_grid = sms * (kNWarpsPerSM / c->n3_warps);
-      // keep the contribution records (written by the walk, read right after
-      // by k_cpair_jsum) resident in L2: a persisting access-policy window
-      // over the front of the unit-major record array
-      int l2p = 0;  // measured: no gain (B2MD_L2_PERSIST=1 enables)
-      if (const char* e = std::getenv("B2MD_L2_PERSIST")) l2p = std::atoi(e);
-      int maxp = 0, maxw = 0;
-      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, c->device);
-      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
-      if (l2p && maxp > 0 && maxw > 0) {
-        const size_t rec_bytes = size_t(R) * pairs * kCS * 3 * sizeof(double);
-        const size_t want = std::min<size_t>(size_t(maxp), size_t(64) << 20);
-        const size_t win = std::min({rec_bytes, size_t(maxw), size_t(48) << 20});
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-        cudaStreamAttrValue v{};
-        v.accessPolicyWindow.base_ptr = c->d_prec;
-        v.accessPolicyWindow.num_bytes = win;
-        v.accessPolicyWindow.hitRatio = float(std::min(1.0, double(want) / double(win)));
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        if (cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess)
-          cudaGetLastError();  // optional: the records then take the default policy
+      c->n3_grid = sms * kNLMinBlocks;
+      nl.max_ent = int(max_ent);
+      TRY(dalloc(&nl.rec, size_t(R) * max_ent * kRecD));
+      TRY(dalloc(&nl.irec, size_t(R) * (max_ent / kB) * kRecD));
+      TRY(dalloc(&nl.ocnt, size_t(R) * nc));
+      TRY(dalloc(&nl.icnt, size_t(R) * nc));
+      TRY(dalloc(&nl.ebase, size_t(R) * (nc + 1)));
+      TRY(dalloc(&nl.ibase, size_t(R) * (nc + 1)));
+      TRY(dalloc(&nl.ent, size_t(R) * max_ent));
+      TRY(dalloc(&nl.in_src, size_t(R) * max_ent));
+      TRY(dalloc(&nl.fixref, size_t(R) * c->t.n));
+      TRY(dalloc(&nl.ctl, size_t(R) * kNLCtl));
+      // stale until the first build; epoch 1 (the stamps start at 0)
+      std::vector<int> ctl(size_t(R) * kNLCtl, 0);
+      for (int r = 0; r < R; ++r) {
+        ctl[size_t(r) * kNLCtl + kNLOverflow] = 1;
+        ctl[size_t(r) * kNLCtl + kNLEpoch] = 1;
       }
+      CU(cudaMemcpy(nl.ctl, ctl.data(), sizeof(int) * ctl.size(), cudaMemcpyHostToDevice));
+      // skin and scheduled rebuild interval (B2MD_NL_SKIN, B2MD_NL_INTERVAL)
+      c->nl_skin = 1.0;
+      c->nl_interval = 20;
+      if (const char* e = std::getenv("B2MD_NL_SKIN")) c->nl_skin = std::max(0.0, std::atof(e));
+      if (const char* e = std::getenv("B2MD_NL_INTERVAL")) c->nl_interval = std::max(0, std::atoi(e));
+      const double rs = (std::sqrt(c->t.rc2) + c->nl_skin) * 4294967296.0 / c->t.box;
+      nl.lim_build = float(rs * rs * (1.0 + 1e-5));
+      nl.skin_half = float(0.5 * c->nl_skin * 4294967296.0 / c->t.box + 64.0);
+      nl.rc_fix = float(std::sqrt(c->t.rc2) * 4294967296.0 / c->t.box);
+      const double du = 0.5 * c->nl_skin * 4294967296.0 / c->t.box;
+      const float d2s = float(du * du * (1.0 - 1e-4));
+      std::memcpy(&nl.d2_stale, &d2s, sizeof d2s);
+      if (const char* e = std::getenv("B2MD_NL_DBG")) nl.dbg = std::atoi(e);
     }
   }
   if (rigid_sites(c->t) > 0) {
@@ -1444,8 +1457,10 @@ void free_ctx(b2md_ctx* c) {
                   c->d_uk,    c->d_flux,  c->d_perm, c->d_slot_of, c->d_sp_slot, c->d_sb_slot,
                   c->d_nsites_slot, c->d_scan, c->d_keys[0], c->d_keys[1], c->d_vals[0],
                   c->d_vals[1], c->d_cub, c->d_ke, c->d_thermo_err, c->d_carc,
-                  c->d_chalf, c->d_sarc, c->d_shalf, c->d_prec, c->d_pirec,
-                  c->d_polist, c->d_pint, c->d_trec};
+                  c->d_chalf, c->d_sarc, c->d_shalf, c->d_trec, c->nl.rec, c->nl.irec,
+                  c->nl.ocnt, c->nl.icnt, c->nl.ebase, c->nl.ibase, c->nl.ent,
+                  c->nl.in_src, c->nl.fixref,
+                  c->nl.ctl};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1699,6 +1714,26 @@ int b2md_get_sort_interval(const b2md_ctx* c, int* steps, int* steps_since_sort)
   if (!c) return set_err(B2MD_INVALID_ARGUMENT, "get_sort_interval: null context");
   if (steps) *steps = c->sort_interval;
   if (steps_since_sort) *steps_since_sort = c->steps_since_sort;
+  return B2MD_OK;
+}
+
+int b2md_nlist_info(b2md_ctx* c, int replica, int64_t info[8]) {
+  if (!c || !info || replica < 0 || replica >= c->R)
+    return set_err(B2MD_INVALID_ARGUMENT, "nlist_info: bad argument");
+  for (int k = 0; k < 8; ++k) info[k] = 0;
+  if (!nl_path(c)) return B2MD_OK;
+  int ctl[kNLCtl];
+  CU(cudaMemcpyAsync(ctl, c->nl.ctl + size_t(replica) * kNLCtl, sizeof ctl, cudaMemcpyDeviceToHost,
+                     c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  info[0] = 1;
+  info[1] = ctl[kNLEntries];
+  info[2] = ctl[kNLIncoming];
+  info[3] = (ctl[kNLOverflow] != 0 || unsigned(ctl[kNLD2]) > c->nl.d2_stale) ? 1 : 0;
+  info[4] = ctl[kNLEpoch] - 1;
+  info[5] = c->steps_since_nl;
+  info[6] = c->nl_interval;
+  info[7] = int64_t(std::llround(c->nl_skin * 1e6));
   return B2MD_OK;
 }
 

@@ -90,7 +90,8 @@ int dalloc(T** p, size_t count) {
 }
 
 enum Family { F_OFFSETS, F_SEARCH, F_FORCE, F_EWALD_TAB, F_EWALD_SK, F_EWALD_F, F_KICK_KICK_DRIFT,
-              F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_HEAT_FLUX, F_RDF, F_CLUSTER, F_JSUM, F_COUNT };
+              F_KICK_DRIFT, F_KICK, F_ALLREDUCE, F_HEAT_FLUX, F_RDF, F_CLUSTER, F_JSUM, F_NL_BUILD,
+              F_COUNT };
 extern const char* kFamilyName[F_COUNT];
 
 }  // namespace b2md_host
@@ -133,21 +134,18 @@ struct b2md_ctx {
   float4* d_chalf = nullptr;  // R * nc arc half extents
   uint4* d_sarc = nullptr;    // R * nsup
   float4* d_shalf = nullptr;  // R * nsup
-  // once-per-pair walk (k_force_cpair_n3 + k_cpair_jsum): contribution records
-  // and their bitmap (B2MD_NEWTON=0: the both-rows walk k_force_cpair)
-  bool use_newton = false;     // B2MD_NEWTON=1: measured slower on cfg3 (DESIGN 5)
-  double* d_prec = nullptr;    // R * nc (nc + 1) / 2 * 24 doubles
-  double* d_pirec = nullptr;   // R * pb_max_units * 24 doubles
-  int* d_polist = nullptr;     // R * nc * nc * 3: owned lists | owner lists | slot map
-  int* d_pint = nullptr;       // per-cluster counts / bases, unit map, counters
-  int pb_max_units = 0;
-  int n3_grid = 0;             // persistent CTAs per replica of k_force_cpair_n3
+  // once-per-pair cluster-pair list (k_force_nl + k_nl_reduce, cluster.cuh)
+  bool use_newton = false;     // B2MD_NEWTON=1 (measured slower on cfg3 so far: DESIGN 5)
+  NListArgs nl{};              // device arrays of the list (null: not allocated)
+  double nl_skin = 0.0;        // list skin (length units)
+  int nl_interval = 0;         // steps between scheduled builds (0: only at staging / re-sort)
+  int64_t steps_since_nl = 0;
+  int n3_grid = 0;             // persistent CTAs per replica of k_force_nl
   // rigid single-species LJ molecules: once-per-pair block-pair tiles
   // (k_force_rigid_tile + k_rigid_reduce; B2MD_TILE=0: search + k_force_rigid)
   bool use_tile = false;
   double* d_trec = nullptr;    // R * nbp * 2 * 32 * 6
   int tile_nb = 0, tile_nbp = 0;
-  int n3_warps = 4;            // warps per CTA of the persistent k_force_cpair_n3
   double* d_cta_part = nullptr;  // force-kernel per-CTA scalar partials
   unsigned* d_ticket = nullptr;   // 2 * R: force, ewald
   int force_grid = 1;
@@ -234,6 +232,7 @@ bool cluster_path(const b2md_ctx* c);
 int cpair_grid(const b2md_ctx* c);
 ClusterArgs cluster_args(const b2md_ctx* c);
 int launch_cluster_arcs(b2md_ctx* c);
+int nl_build(b2md_ctx* c);
 ForceArgs force_args(b2md_ctx* c);
 bool fast_min_image(const b2md_ctx* c);
 int resort(b2md_ctx* c);

@@ -173,6 +173,14 @@ class ForceField:
         (0 keeps the input order; results differ only in summation order)."""
         check(_abi.lib().b2md_set_sort_interval(self._c.ctx, int(steps)))
 
+    def nlist_info(self, replica: int = 0) -> dict:
+        """b2md_nlist_info: the once-per-pair cluster-pair list (diagnostics)."""
+        buf = (C.c_int64 * 8)()
+        check(_abi.lib().b2md_nlist_info(self._c.ctx, int(replica), buf))
+        keys = ("active", "entries", "incoming", "stale", "evaluations", "steps_since_build",
+                "interval", "skin_e6")
+        return dict(zip(keys, [int(x) for x in buf]))
+
     def set_search_options(self, fix_prefilter: bool = True, tile_cull: bool = True) -> None:
         """b2md_set_search_options: partner-search strategy (same results)."""
         check(_abi.lib().b2md_set_search_options(self._c.ctx, int(fix_prefilter), int(tile_cull)))
@@ -305,6 +313,8 @@ class Engine:
         """b2md_set_sort_interval: re-sort period of the internal spatial order
         (0 keeps the input order; results differ only in summation order)."""
         check(_abi.lib().b2md_set_sort_interval(self._c.ctx, int(steps)))
+
+    nlist_info = ForceField.nlist_info
 
     def sort_interval(self) -> tuple[int, int]:
         """(re-sort period, steps taken since the last re-sort)."""

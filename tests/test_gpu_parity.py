@@ -805,9 +805,10 @@ def test_pinned_and_pageable_transfers_agree(cfg):
 
 
 # ------------------------------------------ once-per-pair cluster walk (Newton)
-# k_cpair_build + k_force_cpair_n3 + k_cpair_jsum (csrc/cluster.cuh): each pair
-# evaluated once, partner contributions through the per-pair record buffer and
-# a fixed-order reduction (B2MD_NEWTON=1; the both-rows walk is the default).
+# k_nl_count/scan/fill/inrec + k_force_nl + k_nl_reduce (csrc/cluster.cuh): each
+# pair evaluated once from a cluster-pair list with a skin, partner
+# contributions through the per-pair record buffer and a fixed-order
+# reduction (B2MD_NEWTON=1; the both-rows walk is the default).
 @pytest.mark.parametrize("n", [1, 2, 7, 9, 100, 1537, 4100])
 def test_newton_walk_sizes(monkeypatch, n):
     monkeypatch.setenv("B2MD_CLUSTER", "2")
@@ -886,3 +887,43 @@ def test_newton_walk_replicas_and_cfg3(monkeypatch):
     d -= L * np.round(d / L)
     assert np.abs(d).max() / L <= T_TOL
     assert abs(out.energy.total() - g["energy"][2]) <= T_TOL * abs(g["energy"][2])
+
+
+@pytest.mark.parametrize("mode", ["stale", "both_rows", "every_step", "wide_skin", "rebuild_each_step"])
+def test_cluster_walk_modes(monkeypatch, mode):
+    """The list's exactness guard and schedule: skin 0 makes every list stale
+    after the first drift (the exact per-step walk runs instead), the
+    both-rows walk, per-step drift checks with a thin skin and frequent
+    re-sorts, a wide skin (long lists: the per-step arc cull keeps the pair
+    work), and a rebuild at every step.  Each: forces, energies and the pair
+    count against the oracle, a 30-step trajectory with re-sorts against the
+    oracle's Engine::step (src/engine.cpp:102-143), bit-identical repeats."""
+    env = {"stale": {"B2MD_NEWTON": "1", "B2MD_NL_SKIN": "0"},
+           "both_rows": {"B2MD_NEWTON": "0"},
+           "every_step": {"B2MD_NEWTON": "1", "B2MD_NL_SKIN": "0.05", "B2MD_NL_INTERVAL": "0"},
+           "wide_skin": {"B2MD_NEWTON": "1", "B2MD_NL_SKIN": "2.5", "B2MD_NL_INTERVAL": "0"},
+           "rebuild_each_step": {"B2MD_NEWTON": "1", "B2MD_NL_INTERVAL": "1"}}[mode]
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    monkeypatch.setenv("B2MD_CLUSTER", "2")
+    wl = configs.lj_fluid_config(4100, 0.8, 2.5, seed=17, temperature=2.0)
+    st = wl.states[0]
+    o = pyoracle.OracleFF(wl.comp, wl.opts)
+    ref = o.evaluate(st.pos, st.orient)
+    ff, out = gpu_eval(wl.comp, wl.opts, st.pos, st.orient)
+    check_vec(out.force, ref["force"])
+    check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+    assert ff.last_stats.com_pairs == ref["com_pairs"]
+    runs = []
+    for _ in range(2):
+        eng = b2.Engine(wl.comp, wl.opts, 0.005)
+        eng.set_sort_interval(13)
+        eng.set_state(st)
+        eng.step(30)
+        runs.append((eng.state(), eng.energies()[1][0].com_pairs))
+    tr = o.run(0.005, 30, st.pos, st.orient, st.vel, st.ang_vel)
+    compare_states(runs[0][0], tr, wl.comp.box_length)
+    check_energy(runs[0][0].energy, tr["energy"], runs[0][0].virial, tr["virial"])
+    assert runs[0][1] == o.evaluate(runs[0][0].pos, runs[0][0].orient)["com_pairs"]
+    assert np.array_equal(runs[0][0].pos, runs[1][0].pos)
+    assert np.array_equal(runs[0][0].force, runs[1][0].force)

@@ -46,16 +46,28 @@ def check(name, wl, steps=3):
 
 
 def main():
-    only = sys.argv[1:] or ["cluster", "bitmatrix", "rigid", "ewald", "replicas"]
+    only = sys.argv[1:] or ["cluster", "newton", "bitmatrix", "rigid", "tile", "ewald", "replicas"]
     if "cluster" in only:
         os.environ["B2MD_CLUSTER"] = "2"
         check("cluster walk (single-site, rc < 0.3 L)", configs.lj_fluid_config(1200, 0.8, 2.5, seed=5,
                                                                                name="san-cluster"))
         os.environ.pop("B2MD_CLUSTER")
+    if "newton" in only:
+        os.environ["B2MD_CLUSTER"] = "2"
+        os.environ["B2MD_NEWTON"] = "1"
+        check("once-per-pair cluster walk", configs.lj_fluid_config(1200, 0.8, 2.5, seed=5,
+                                                                   name="san-newton"))
+        os.environ.pop("B2MD_CLUSTER")
+        os.environ.pop("B2MD_NEWTON")
     if "bitmatrix" in only:
         check("search + bit-matrix walk", configs.lj_fluid_config(300, 0.8, None, seed=3, name="san-lj"))
     if "rigid" in only:
         check("rigid 2CLJ", configs.two_clj_config(200, 0.3, 5, 2.0, 0.002, 3, "san-2clj"))
+    if "tile" in only:
+        os.environ["B2MD_TILE"] = "1"
+        check("rigid 2CLJ block-pair tiles", configs.two_clj_config(200, 0.3, 5, 2.0, 0.002, 3,
+                                                                    "san-2clj-tile"))
+        os.environ.pop("B2MD_TILE")
     if "ewald" in only:
         wl = configs.make("cfg2")
         check("water + ions, Ewald (cfg2)", wl, steps=1)
