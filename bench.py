@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-flush", action="store_true")
+    p.add_argument("--group", action="store_true",
+                   help="one process for all --gpus devices (b2md_create_group); the default "
+                        "when --gpus N > 1 is given without torchrun")
     p.add_argument("--equil", type=int, default=-1,
                    help="untimed equilibration steps before the timed region (-1: 1000 for cfg3, "
                         "else 0); with a re-sort interval the count is padded so the first timed "
@@ -493,6 +496,141 @@ def describe(wl):
             f"rc={wl.opts.cutoff:.6f}, dt={wl.dt}, method={int(wl.opts.method)}")
 
 
+def run_group(args):
+    """--gpus N > 1 in ONE process (no torchrun): b2md_create_group -- one
+    context per device, ncclCommInitAll, the row-sharded step with its packed
+    all-reduce, every device's calls on its own worker thread -- or, for the
+    cfg4 replica batch, N independent engines (8 replicas each, no traffic).
+    Per-step CUDA events on every device's stream, L2 flushed on every device
+    between steps, the step time is the max over devices."""
+    import torch
+    import paper_1507_07548_b200 as b2
+    N = args.gpus
+    if torch.cuda.device_count() < N:
+        raise SystemExit(f"--gpus {N}: only {torch.cuda.device_count()} CUDA device(s) visible")
+    devs = list(range(N))
+    if args.config == "cfg4":
+        wls = [workload("cfg4", k, N) for k in devs]
+        engines = [b2.Engine(w.comp, w.opts, w.dt, device=k, replicas=w.replicas) for k, w in zip(devs, wls)]
+        for e, w in zip(engines, wls):
+            e.set_state(w.states)
+        wl = wls[0]
+        group = None
+
+        def step_all(k):
+            for e in engines:
+                e.step_async(k)
+
+        def sync_all():
+            for e in engines:
+                e.sync()
+    else:
+        wl = workload(args.config, 0, 1)
+        group = b2.EngineGroup(wl.comp, wl.opts, wl.dt, devices=devs, replicas=wl.replicas)
+        group.set_state(wl.states)
+        engines = group.engines
+        step_all, sync_all = group.step_async, group.sync
+    R, n = wl.replicas, wl.comp.molecule_count()
+    streams = [torch.cuda.ExternalStream(e.stream(), device=k) for k, e in zip(devs, engines)]
+    flushes = [None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{k}")
+               for k in devs]
+    for _ in range(max(3, args.warmup)):
+        step_all(1)
+    sync_all()
+    interval, since = engines[0].sort_interval()
+    equil = args.equil if args.equil >= 0 else (1000 if args.config == "cfg3" else 0)
+    extra = (interval - since + interval * max(0, -(-(equil - (interval - since)) // interval))
+             if interval > 0 else equil)
+    if extra > 0:
+        step_all(extra)
+        sync_all()
+
+    def timed_pass(steps):
+        ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)] for _ in devs]
+        for k in range(steps):
+            for d in devs:
+                ev[d][k][0].record(streams[d])
+            step_all(1)
+            for d in devs:
+                ev[d][k][1].record(streams[d])
+                if flushes[d] is not None:
+                    with torch.cuda.stream(streams[d]):
+                        flushes[d].zero_()
+        sync_all()
+        for d in devs:
+            torch.cuda.synchronize(d)
+        return max(float(sum(a.elapsed_time(b) for a, b in ev[d])) for d in devs)
+
+    clocks = ClockSampler(0)
+    clocks.start()
+    total_ms = timed_pass(args.steps)
+    clk = clocks.stop()
+    for e in engines:
+        e.profile(True, 1)
+    n_all = min(args.steps, 50)
+    timed_pass(n_all)
+    kts = [e.kernel_times() for e in engines]
+    for e in engines:
+        e.profile(False)
+    kt = kts[0]
+    launches = sum(c for kt_ in kts for name, (ms, c) in kt_.items()) / max(1, n_all)
+    _, stats = engines[0].energies()
+    pairs_total = int(sum(s.com_pairs for s in stats))
+    # end to end: host state to every device, the step, rank 0's state back
+    nt = n * R
+    pinned = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    bufs = [[pinned((nt, 3)), pinned((nt, 4)), pinned((nt, 3)), pinned((nt, 3)), pinned((nt, 3)),
+             pinned((nt, 3))] for _ in (devs if group is None else devs[:1])]
+    for e, b in zip(engines, bufs):
+        e.get_state_raw(*b)
+    point = all(sp.rotational_dof == 0 for sp in wl.comp.species)
+    sel = (lambda b: (b[0], None, b[2], None, b[4], None)) if point else (lambda b: tuple(b))
+    per_dev = 8 * nt * ((3 + 3 + 3) if point else (3 + 4 + 3 + 3 + 3 + 3))
+    e2e_steps = max(1, args.e2e_steps)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        if group is None:
+            for e, b in zip(engines, bufs):
+                e.upload_state_raw(*sel(b))
+                e.step_async(1)
+            for e, b in zip(engines, bufs):
+                e.get_state_raw(*sel(b))
+        else:
+            for e in engines:
+                e.upload_state_raw(*sel(bufs[0]))
+            group.step_async(1)
+            group.sync()
+            engines[0].get_state_raw(*sel(bufs[0]))
+    e2e_s = time.perf_counter() - t0
+    mult = R * N if args.config == "cfg4" else 1
+    line = {
+        "metric": METRIC, "value": args.steps * mult / (total_ms * 1e-3), "unit": "steps/s",
+        "n_gpus": N, "steps": args.steps, "warmup": max(3, args.warmup),
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak" if args.config == "cfg4" else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded xoshiro256++ generator, paper_1507_07548_b200/configs.py)",
+        "config": {
+            "workload": f"{args.config}: {describe(wl)}",
+            "parallelism": (f"replicas x{N} (one process, N engines)" if group is None else
+                            f"row-sharded x{N} + NCCL all-reduce (one process: b2md_create_group)"),
+            "l2": "flushed between timed steps on every device" if flushes[0] is not None else "not flushed",
+            "timing": "per-step CUDA events on every device's library stream; max over devices",
+        },
+        "pair_interactions_per_s": pairs_total * args.steps * (N if args.config == "cfg4" else 1)
+        / (total_ms * 1e-3),
+        "e2e": {"value": e2e_steps * mult / e2e_s, "unit": "steps/s",
+                "h2d_bytes_per_step": per_dev * N, "d2h_bytes_per_step": per_dev * (N if group is None else 1),
+                "path": "b2md_upload_state on every device + step + b2md_get_state (pinned host buffers)"},
+        "kernel_ms_per_launch": {k: v[0] / max(1, v[1]) for k, v in kt.items()},
+        "gpu_launches": int(round(launches * args.steps)),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if group is not None:
+        group.close()
+
+
 def main():
     args = parse()
     if args.op != "step":
@@ -500,6 +638,9 @@ def main():
         return
     if args.impl == "reference":
         run_reference_arm(args)
+        return
+    if args.group or (args.gpus > 1 and "WORLD_SIZE" not in os.environ):
+        run_group(args)
         return
     rank, world, local = dist_env()
     import torch

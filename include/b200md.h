@@ -324,6 +324,35 @@ int b2md_rdf_set_counts(b2md_rdf* rdf, int replica, const uint64_t* counts, int6
 int b2md_nccl_unique_id(char id[128]);
 int b2md_attach_nccl(b2md_ctx* ctx, const char id[128], int rank, int world);
 
+/* One process driving `ndev` GPUs: the single-process
+ * counterpart of one rank per GPU, for a caller shaped like the reference's
+ * Engine, which owns the whole computation in one process
+ * (src/engine.cpp:100-143) and splits it only over in-process workers
+ * (src/parallel.cpp:84-95).  One context per device (b2md_create on
+ * devices[k], or device k when devices is NULL), one NCCL communicator per
+ * device from ncclCommInitAll; context k is rank k of an ndev-way row shard
+ * (as after b2md_attach_nccl).  Group calls run the per-context call on one
+ * worker thread per device, so every device's collectives are in flight
+ * together, and return the first failure.  Every context holds the whole
+ * replicated state; b2md_group_get_state reads rank 0's.  b2md_group_context
+ * gives a rank's context for per-device calls (streams, profiling); do not
+ * step a group's contexts one by one from a single thread (the all-reduce of
+ * one device would wait for the others). */
+typedef struct b2md_group b2md_group;
+int b2md_create_group(int ndev, const int* devices, const b2md_composition* comp,
+                      const b2md_ff_options* opts, double dt, int n_replicas, b2md_group** out);
+void b2md_destroy_group(b2md_group* group);
+int b2md_group_size(const b2md_group* group);
+b2md_ctx* b2md_group_context(b2md_group* group, int rank);
+int b2md_group_set_state(b2md_group* group, const double* pos, const double* orient,
+                         const double* vel, const double* ang_vel);
+int b2md_group_step(b2md_group* group, int64_t nsteps);
+int b2md_group_step_async(b2md_group* group, int64_t nsteps);
+int b2md_group_sync(b2md_group* group);
+int b2md_group_get_state(b2md_group* group, double* pos, double* orient, double* vel,
+                         double* ang_vel, double* force, double* torque, b2md_energy* energy,
+                         b2md_eval_stats* stats);
+
 /* Restrict the context to rank `rank`'s shard of a `world`-way split
  * WITHOUT a communicator: evaluations then return that rank's partial forces,
  * torques and sums (what each rank holds before the all-reduce).  For tests

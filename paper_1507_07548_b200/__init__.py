@@ -5,6 +5,7 @@ include/tmd/engine.hpp) and the C ABI in include/b200md.h."""
 from .errors import ConfigError, CudaError, Error, IoError, ModelError, NumericalError
 from .forcefield import (
     Engine,
+    EngineGroup,
     EvalStats,
     EwaldParams,
     ForceField,

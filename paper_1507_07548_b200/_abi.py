@@ -158,6 +158,22 @@ SIGNATURES = {
     "b2md_rdf_set_counts": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.c_int64]),
     "b2md_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "b2md_attach_nccl": (C.c_int, [_CTX, C.c_char_p, C.c_int, C.c_int]),
+    "b2md_create_group": (
+        C.c_int,
+        [C.c_int, C.POINTER(C.c_int), C.POINTER(b2md_composition), C.POINTER(b2md_ff_options),
+         C.c_double, C.c_int, C.POINTER(_CTX)],
+    ),
+    "b2md_destroy_group": (None, [_CTX]),
+    "b2md_group_size": (C.c_int, [_CTX]),
+    "b2md_group_context": (_CTX, [_CTX, C.c_int]),
+    "b2md_group_set_state": (C.c_int, [_CTX, _D, _D, _D, _D]),
+    "b2md_group_step": (C.c_int, [_CTX, C.c_int64]),
+    "b2md_group_step_async": (C.c_int, [_CTX, C.c_int64]),
+    "b2md_group_sync": (C.c_int, [_CTX]),
+    "b2md_group_get_state": (
+        C.c_int,
+        [_CTX, _D, _D, _D, _D, _D, _D, C.POINTER(b2md_energy), C.POINTER(b2md_eval_stats)],
+    ),
     "b2md_set_shard": (C.c_int, [_CTX, C.c_int, C.c_int]),
     "b2md_stream": (C.c_void_p, [_CTX]),
     "b2md_profile_enable": (C.c_int, [_CTX, C.c_int]),

@@ -32,8 +32,11 @@ int nccl_load() {
   g_nccl.AllReduce = reinterpret_cast<decltype(g_nccl.AllReduce)>(sym("ncclAllReduce"));
   g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(sym("ncclCommDestroy"));
   g_nccl.GetErrorString = reinterpret_cast<decltype(g_nccl.GetErrorString)>(sym("ncclGetErrorString"));
+  g_nccl.CommInitAll = reinterpret_cast<decltype(g_nccl.CommInitAll)>(sym("ncclCommInitAll"));
+  g_nccl.GroupStart = reinterpret_cast<decltype(g_nccl.GroupStart)>(sym("ncclGroupStart"));
+  g_nccl.GroupEnd = reinterpret_cast<decltype(g_nccl.GroupEnd)>(sym("ncclGroupEnd"));
   if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy ||
-      !g_nccl.GetErrorString)
+      !g_nccl.GetErrorString || !g_nccl.GroupStart || !g_nccl.GroupEnd)
     return set_err(B2MD_CUDA_ERROR, "NCCL: missing symbols");
   g_nccl.loaded = true;
   return B2MD_OK;
@@ -638,9 +641,18 @@ int launch_ewald(b2md_ctx* c) {
 
 int launch_allreduce(b2md_ctx* c) {
   if (c->world <= 1 || !c->comm) return B2MD_OK;
-  const size_t count = size_t(6) * n_total(c) + size_t(kNumSums) * c->R;
   TRY(prof_begin(c, F_ALLREDUCE));
-  NC(g_nccl.AllReduce(c->d_fbuf, c->d_fbuf, count, ncclDouble, ncclSum, c->comm, c->stream));
+  const size_t nt = size_t(n_total(c));
+  if (c->t.any_offsets) {  // forces, torques and sums: one contiguous unit
+    NC(g_nccl.AllReduce(c->d_fbuf, c->d_fbuf, 6 * nt + size_t(kNumSums) * c->R, ncclDouble, ncclSum,
+                        c->comm, c->stream));
+  } else {  // centred sites only: no torques (zero on every rank), forces + sums
+    NC(g_nccl.GroupStart());
+    NC(g_nccl.AllReduce(c->d_fbuf, c->d_fbuf, 3 * nt, ncclDouble, ncclSum, c->comm, c->stream));
+    NC(g_nccl.AllReduce(c->d_fbuf + 6 * nt, c->d_fbuf + 6 * nt, size_t(kNumSums) * c->R, ncclDouble,
+                        ncclSum, c->comm, c->stream));
+    NC(g_nccl.GroupEnd());
+  }
   TRY(prof_end(c));
   return B2MD_OK;
 }

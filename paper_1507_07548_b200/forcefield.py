@@ -414,6 +414,106 @@ def heat_flux(ff: ForceField, state: SystemState, h_per_species) -> np.ndarray:
     return ff.heat_flux(state, h_per_species)
 
 
+class _ContextView(_Context):
+    """A context owned by a b2md_group (not destroyed here)."""
+
+    def __init__(self, comp, opts, replicas, device, ctx):
+        self.comp = comp
+        self.opts = opts
+        self.n = comp.molecule_count()
+        self.replicas = int(replicas)
+        self.device = int(device)
+        self.ctx = C.c_void_p(ctx)
+
+    def close(self) -> None:
+        self.ctx = None
+
+
+class EngineGroup:
+    """b2md_create_group: one process driving several GPUs -- the single-process
+    caller shape of tmd::Engine (src/engine.cpp:100-143) over a row-sharded
+    system (src/parallel.cpp:84-95's split, one packed NCCL all-reduce per
+    evaluation).  `engines[k]` is rank k's context (streams, profiling,
+    energies); stepping goes through the group (all devices together)."""
+
+    def __init__(self, comp: SystemComposition, ff_opts: ForceFieldOptions, dt: float,
+                 devices=None, replicas: int = 1):
+        devs = list(range(_device_count())) if devices is None else [int(d) for d in devices]
+        if not devs:
+            from .errors import CudaError
+            raise CudaError("create_group: no CUDA device")
+        self.comp, self.dt, self.replicas = comp, float(dt), int(replicas)
+        cc, self._keep = comp.to_c()
+        oc = ff_opts.to_c()
+        arr = (C.c_int * len(devs))(*devs)
+        g = C.c_void_p()
+        check(_abi.lib().b2md_create_group(len(devs), arr, C.byref(cc), C.byref(oc), float(dt),
+                                           self.replicas, C.byref(g)))
+        self._g = g
+        self.devices = devs
+        self.engines = []
+        for k, d in enumerate(devs):
+            e = Engine.__new__(Engine)
+            e._c = _ContextView(comp, ff_opts, self.replicas, d,
+                                _abi.lib().b2md_group_context(g, k))
+            e.dt, e.replicas = self.dt, self.replicas
+            self.engines.append(e)
+
+    def size(self) -> int:
+        return int(_abi.lib().b2md_group_size(self._g))
+
+    def set_state(self, states) -> None:
+        if isinstance(states, SystemState):
+            states = [states]
+        n = self.comp.molecule_count()
+        cat = lambda k, w: np.ascontiguousarray(
+            np.concatenate([_f64(getattr(s, k), (n, w)) for s in states]), dtype=np.float64)
+        check(_abi.lib().b2md_group_set_state(self._g, _abi.dptr(cat("pos", 3)),
+                                              _abi.dptr(cat("orient", 4)), _abi.dptr(cat("vel", 3)),
+                                              _abi.dptr(cat("ang_vel", 3))))
+
+    def step(self, nsteps: int = 1) -> None:
+        check(_abi.lib().b2md_group_step(self._g, int(nsteps)))
+
+    def step_async(self, nsteps: int = 1) -> None:
+        check(_abi.lib().b2md_group_step_async(self._g, int(nsteps)))
+
+    def sync(self) -> None:
+        check(_abi.lib().b2md_group_sync(self._g))
+
+    def states(self) -> list[SystemState]:
+        """rank 0's copy (every rank holds the whole replicated state)."""
+        self.sync()
+        return self.engines[0].states()
+
+    def state(self) -> SystemState:
+        return self.states()[0]
+
+    def close(self) -> None:
+        if getattr(self, "_g", None) is not None and self._g.value:
+            for e in self.engines:
+                e._c.close()
+            _abi.lib().b2md_destroy_group(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _device_count() -> int:
+    n = C.c_int(0)
+    try:
+        cudart = C.CDLL("libcudart.so")
+    except OSError:
+        import torch
+        return torch.cuda.device_count()
+    cudart.cudaGetDeviceCount(C.byref(n))
+    return int(n.value)
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(_abi.lib().b2md_nccl_unique_id(buf))
