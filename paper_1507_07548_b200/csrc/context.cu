@@ -1480,6 +1480,7 @@ void free_ctx(b2md_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
+  cudaGetLastError();  // (a context that failed to create leaves no error behind)
 }
 
 int check_error_flag(b2md_ctx* c) {

@@ -39,12 +39,16 @@ using namespace b2md;
 
 int set_err(int code, const std::string& msg);
 
+// (a failed call's error is consumed here, so a non-sticky error -- e.g. an
+// invalid device number -- is not reported again by a later launch check)
 #define CU(expr)                                                                          \
   do {                                                                                    \
     cudaError_t e_ = (expr);                                                              \
-    if (e_ != cudaSuccess)                                                                \
+    if (e_ != cudaSuccess) {                                                              \
+      cudaGetLastError();                                                                 \
       return set_err(B2MD_CUDA_ERROR, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
                                           " at " #expr);                                  \
+    }                                                                                     \
   } while (0)
 
 // NCCL is resolved at first multi-GPU use (dlopen), not linked: a process
