@@ -509,7 +509,7 @@ int launch_tile_force(b2md_ctx* c, bool kick) {
   ForceArgs aw = a;
   aw.kick_dt = 0.0;  // the molecules are complete only after k_rigid_reduce
   const bool w = fast_min_image(c);
-  const dim3 grid((c->tile_nbp + kTileWarps - 1) / kTileWarps, c->R);
+  const dim3 grid((c->tile_nbp * kTileSplit + kTileWarps - 1) / kTileWarps, c->R);
   const int ns = rigid_sites(c->t);
   if (ns == 2 && w)
     PROF(c, F_FORCE, (k_force_rigid_tile<2, true><<<grid, kTileWarps * 32, 0, c->stream>>>(aw, ta)));
@@ -1158,6 +1158,7 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
   CU(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return set_err(B2MD_CUDA_ERROR, "b200md: no such CUDA device");
   CU(cudaSetDevice(device));
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
   CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
@@ -1269,8 +1270,8 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars *
                                    std::max({c->force_grid, c->nc > 0 ? cpair_grid(c) : 0,
                                              c->nc > 0 ? sms * kNLMinBlocks : 0,
-                                             (((c->t.n + 31) / 32) * ((c->t.n + 31) / 32 + 1) / 2 +
-                                              kTileWarps - 1) / kTileWarps})));
+                                             (((c->t.n + 31) / 32) * ((c->t.n + 31) / 32 + 1) / 2 *
+                                                  kTileSplit + kTileWarps - 1) / kTileWarps})));
   }
   if (c->nc > 0) {
     c->nsup = (c->nc + kSC - 1) / kSC;
@@ -1329,7 +1330,7 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     if (c->use_tile) {
       c->tile_nb = (c->t.n + 31) / 32;
       c->tile_nbp = c->tile_nb * (c->tile_nb + 1) / 2;
-      TRY(dalloc(&c->d_trec, size_t(R) * c->tile_nbp * 2 * 32 * 6));
+      TRY(dalloc(&c->d_trec, size_t(R) * c->tile_nbp * kTileSplit * 2 * 32 * 6));
     }
   }
   TRY(dalloc(&c->d_ticket, size_t(2) * R));

@@ -107,6 +107,7 @@ using namespace b2md;  // device types of the context (kernels.cuh, model.hpp)
 
 struct b2md_ctx {
   int device = 0;
+  int sms = 148;  // streaming multiprocessors of the device
   cudaStream_t stream = nullptr;
   // Ewald tables + S(k) run on stream2 beside the real-space kernel (fork /
   // join events; captured into the step graphs as parallel branches)
@@ -151,7 +152,7 @@ struct b2md_ctx {
   // rigid single-species LJ molecules: once-per-pair block-pair tiles
   // (k_force_rigid_tile + k_rigid_reduce; B2MD_TILE=0: search + k_force_rigid)
   bool use_tile = false;
-  double* d_trec = nullptr;    // R * nbp * 2 * 32 * 6
+  double* d_trec = nullptr;    // R * nbp * kTileSplit * 2 * 32 * 6
   int tile_nb = 0, tile_nbp = 0;
   double* d_cta_part = nullptr;  // force-kernel per-CTA scalar partials
   unsigned* d_ticket = nullptr;   // 2 * R: force, ewald

@@ -1306,13 +1306,18 @@ __global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a
             rz = add(sub(Rz, dJ.z), dI.z);
           }
           const double r2 = norm2_exact(rx, ry, rz);
-          if (r2 < rc2) {
-            const double inv_r2 = rcp_nr(r2);
-            const double ir6 = inv_r2 * inv_r2 * inv_r2;
-            const double a12 = c12[ta][tb] * ir6 * ir6;
-            const double a6 = c6[ta][tb] * ir6;
-            const double du_r = -12.0 * a12 + 6.0 * a6;
-            const double fs = -du_r * inv_r2;
+          // branch-free (the NS^2 terms are independent dependency chains the
+          // compiler interleaves): out-of-range terms take r2 = 1 and ir6 = 0,
+          // and their R (NaN for a NaN position) reaches no sum
+          const bool in = r2 < rc2;
+          const double inv_r2 = rcp_nr(in ? r2 : 1.0);
+          const double t6 = inv_r2 * inv_r2 * inv_r2;
+          const double ir6 = in ? t6 : 0.0;
+          const double a12 = c12[ta][tb] * ir6 * ir6;
+          const double a6 = c6[ta][tb] * ir6;
+          const double du_r = -12.0 * a12 + 6.0 * a6;
+          const double fs = -du_r * inv_r2;
+          if (in) {
             const double gx = fs * rx, gy = fs * ry, gz = fs * rz;
             fx += gx;
             fy += gy;
@@ -1392,9 +1397,15 @@ __global__ void __launch_bounds__(kForceWarps * 32, 2) k_force_rigid(ForceArgs a
 //   fixed order (block-pair order) -- the per-pair contribution buffer and
 //   segmented reduction of the north star, at block-pair granularity.
 constexpr int kTileWarps = 4;
+#ifndef B2MD_TILE_MINBLOCKS
+#define B2MD_TILE_MINBLOCKS 5
+#endif
+constexpr int kTileMinBlocks = B2MD_TILE_MINBLOCKS;  // 20 warps per SM (<= 96 registers)
+constexpr int kTileSplit = 2;      // work items per block pair (parts of its 32 steps)
 
 struct TileArgs {
-  double* rec;   // R * nbp * 2 records of 32 x 6 doubles: [bp][side][lane][fx fy fz tx ty tz]
+  double* rec;   // R * nbp * kTileSplit * 2 records of 32 x 6 doubles:
+                 // [bp][part][side][lane][fx fy fz tx ty tz]
   int nb;        // 32-slot blocks per replica
   int nbp;       // block pairs per replica nb (nb + 1) / 2
   int bp_begin, bp_end;  // this rank's block pairs (row shard)
@@ -1413,17 +1424,17 @@ __device__ __forceinline__ void tile_of(int bp, int nb, int& bi, int& bj) {
 }
 
 template <int NS, bool WRAPPED>
-__global__ void __launch_bounds__(kTileWarps * 32, 4) k_force_rigid_tile(ForceArgs a, TileArgs ta_) {
+__global__ void __launch_bounds__(kTileWarps * 32, kTileMinBlocks) k_force_rigid_tile(ForceArgs a, TileArgs ta_) {
   constexpr int kJW = 3 + 3 * NS;  // staged doubles per partner: com, site offsets
-  __shared__ double jdat[kTileWarps][kJW][33];   // [field][j] (+1 pad: no bank conflicts)
-  __shared__ double jacc[kTileWarps][6][33];     // partner force / torque accumulators
+  __shared__ double jdat[kTileWarps][kJW][33];  // [field][j] (+1 pad: no bank conflicts)
   __shared__ int jext[kTileWarps][32];
-  __shared__ double cpar[2][NS][NS];             // c12, c6
+  __shared__ double cpar[2][NS][NS];            // c12, c6
   const SysDev& s = a.s;
   const DevTables* __restrict__ tab = s.tab;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.y;
   const int n = s.n;
+  const unsigned full = 0xffffffffu;
   const size_t roff = size_t(r) * n;
   const size_t soff = size_t(r) * s.total_sites;
   const double4* __restrict__ p4 = a.st.pos4 + roff;
@@ -1440,21 +1451,31 @@ __global__ void __launch_bounds__(kTileWarps * 32, 4) k_force_rigid_tile(ForceAr
   };
   const double rc2 = a.rc2, rmax2 = a.rmax2;
   double ulj = 0, vir = 0, s1 = 0, s2 = 0, cnt = 0;
-  const int bp = blockIdx.x * kTileWarps + warp;
-  if (bp < ta_.nbp) {  // warp-uniform
+  double (*jd)[33] = jdat[warp];
+  const int items = ta_.nbp * kTileSplit;
+  // one work item (block pair, part of its steps) per warp: a fixed
+  // assignment, so every scalar sum is taken in the same order every run
+  for (int it = blockIdx.x * kTileWarps + warp; it < items; it += gridDim.x * kTileWarps) {
+    const int bp = it / kTileSplit, part = it - bp * kTileSplit;
     int bi, bj;
     tile_of(bp, ta_.nb, bi, bj);
     const bool diag = bi == bj;
+    // steps of this part: k0 .. k1 (the diagonal block pair has steps 1 .. 16,
+    // step 16 on lanes < 16 only)
+    const int span = diag ? 16 : 32;
+    const int k0 = (diag ? 1 : 0) + part * span / kTileSplit;
+    const int k1 = (diag ? 1 : 0) + (part + 1) * span / kTileSplit - 1;
     const int i = bi * 32 + lane;
     const bool iv = i < n;
     const int ic = iv ? i : bi * 32;
     const double4 pi = p4[ic];
     const int ei = ext_of(pi);
-    double4 di[NS];
+    double dix[NS], diy[NS], diz[NS];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) di[k] = o4[ic * NS + k];
-    double (*jd)[33] = jdat[warp];
-    double (*ja)[33] = jacc[warp];
+    for (int k = 0; k < NS; ++k) {
+      const double4 o = o4[ic * NS + k];
+      dix[k] = o.x, diy[k] = o.y, diz[k] = o.z;
+    }
     {
       const int j = bj * 32 + lane;
       const int jc = j < n ? j : bj * 32;
@@ -1466,119 +1487,132 @@ __global__ void __launch_bounds__(kTileWarps * 32, 4) k_force_rigid_tile(ForceAr
         const double4 o = o4[jc * NS + k];
         jd[3 + 3 * k][lane] = o.x, jd[4 + 3 * k][lane] = o.y, jd[5 + 3 * k][lane] = o.z;
       }
-#pragma unroll
-      for (int c = 0; c < 6; ++c) ja[c][lane] = 0.0;
     }
     __syncwarp();
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
+    // the partner side travels with its partner: at step k lane l holds the
+    // accumulators of partner (l + k) & 31 and passes them to lane l - 1
+    double gfx = 0, gfy = 0, gfz = 0, gtx = 0, gty = 0, gtz = 0;
     const bool mine = bp >= ta_.bp_begin && bp < ta_.bp_end;
-    const int k0 = diag ? 1 : 0, k1 = diag ? 16 : 31;
+    const int src = (lane + 1) & 31;
     if (mine)
-    for (int k = k0; k <= k1; ++k) {
-      const int jl = (lane + k) & 31;
-      const int ej = jext[warp][jl];
-      const bool valid = iv && ej >= 0 && !(diag && k == 16 && lane >= 16);
-      const bool lo = ei < ej;
-      const double Rx = mimg(sub(pi.x, jd[0][jl]));
-      const double Ry = mimg(sub(pi.y, jd[1][jl]));
-      const double Rz = mimg(sub(pi.z, jd[2][jl]));
-      const double R2 = norm2_exact(Rx, Ry, Rz);
-      const bool pass = valid && R2 < rmax2;  // potentials.cpp:212
-      double gfx = 0, gfy = 0, gfz = 0, gtx = 0, gty = 0, gtz = 0;  // partner side
-      if (pass) {
-        cnt += 1.0;
-        double s1p = 0.0, s2p = 0.0;
+      for (int k = k0; k <= k1; ++k) {
+        const int jl = (lane + k) & 31;
+        const int ej = jext[warp][jl];
+        const bool valid = iv && ej >= 0 && !(diag && k == 16 && lane >= 16);
+        const bool lo = ei < ej;
+        const double Rx = mimg(sub(pi.x, jd[0][jl]));
+        const double Ry = mimg(sub(pi.y, jd[1][jl]));
+        const double Rz = mimg(sub(pi.z, jd[2][jl]));
+        const double R2 = norm2_exact(Rx, Ry, Rz);
+        const bool pass = valid && R2 < rmax2;  // potentials.cpp:212
+        if (__ballot_sync(full, pass)) {
+          cnt += pass ? 1.0 : 0.0;
+          double s1p = 0.0, s2p = 0.0;
 #pragma unroll
-        for (int ta = 0; ta < NS; ++ta)
+          for (int ta = 0; ta < NS; ++ta)
 #pragma unroll
-          for (int tb = 0; tb < NS; ++tb) {
-            // reference term (ta on the lower molecule, tb on the upper one)
-            const double4 dI = lo ? di[ta] : di[tb];
-            const int kj = lo ? tb : ta;
-            const double djx = jd[3 + 3 * kj][jl], djy = jd[4 + 3 * kj][jl], djz = jd[5 + 3 * kj][jl];
-            double rx, ry, rz;
-            if (lo) {
-              rx = sub(add(Rx, dI.x), djx);
-              ry = sub(add(Ry, dI.y), djy);
-              rz = sub(add(Rz, dI.z), djz);
-            } else {
-              rx = add(sub(Rx, djx), dI.x);
-              ry = add(sub(Ry, djy), dI.y);
-              rz = add(sub(Rz, djz), dI.z);
-            }
-            const double r2 = norm2_exact(rx, ry, rz);
-            if (r2 < rc2) {
-              const double inv_r2 = rcp_nr(r2);
-              const double ir6 = inv_r2 * inv_r2 * inv_r2;
+            for (int tb = 0; tb < NS; ++tb) {
+              // reference term: ta on the lower molecule, tb on the upper one
+              const int ka = lo ? ta : tb, kb = lo ? tb : ta;  // this lane's site, partner's site
+              const double ax = NS == 2 ? (ka ? dix[1] : dix[0]) : dix[ka];
+              const double ay = NS == 2 ? (ka ? diy[1] : diy[0]) : diy[ka];
+              const double az = NS == 2 ? (ka ? diz[1] : diz[0]) : diz[ka];
+              const double bx = jd[3 + 3 * kb][jl], by = jd[4 + 3 * kb][jl], bz = jd[5 + 3 * kb][jl];
+              double rx, ry, rz;
+              if (lo) {
+                rx = sub(add(Rx, ax), bx);
+                ry = sub(add(Ry, ay), by);
+                rz = sub(add(Rz, az), bz);
+              } else {
+                rx = add(sub(Rx, bx), ax);
+                ry = add(sub(Ry, by), ay);
+                rz = add(sub(Rz, bz), az);
+              }
+              const double r2 = norm2_exact(rx, ry, rz);
+              const bool in = pass && r2 < rc2;
+              const double inv_r2 = rcp_nr(in ? r2 : 1.0);
+              const double t6 = inv_r2 * inv_r2 * inv_r2;
+              const double ir6 = in ? t6 : 0.0;
               const double a12 = cpar[0][ta][tb] * ir6 * ir6;
               const double a6 = cpar[1][ta][tb] * ir6;
               const double du_r = -12.0 * a12 + 6.0 * a6;
               const double fs = -du_r * inv_r2;
-              const double gx = fs * rx, gy = fs * ry, gz = fs * rz;
-              fx += gx, fy += gy, fz += gz;
-              tx += dI.y * gz - dI.z * gy;
-              ty += dI.z * gx - dI.x * gz;
-              tz += dI.x * gy - dI.y * gx;
-              gfx -= gx, gfy -= gy, gfz -= gz;
-              gtx -= djy * gz - djz * gy;
-              gty -= djz * gx - djx * gz;
-              gtz -= djx * gy - djy * gx;
-              ulj += a12 - a6;
-              vir += Rx * gx + Ry * gy + Rz * gz;
-              if (a.vderiv) {
-                const double d2u_r2 = 156.0 * a12 - 42.0 * a6;
-                const double rvR = rx * Rx + ry * Ry + rz * Rz;
-                const double arr = rvR * inv_r2;
-                s1p += du_r * arr;
-                s2p += d2u_r2 * arr * arr + du_r * inv_r2 * (R2 - rvR * arr);
+              if (in) {  // an excluded pair's R may be NaN: it reaches no sum
+                const double gx = fs * rx, gy = fs * ry, gz = fs * rz;
+                fx += gx, fy += gy, fz += gz;
+                tx += ay * gz - az * gy;
+                ty += az * gx - ax * gz;
+                tz += ax * gy - ay * gx;
+                gfx -= gx, gfy -= gy, gfz -= gz;
+                gtx -= by * gz - bz * gy;
+                gty -= bz * gx - bx * gz;
+                gtz -= bx * gy - by * gx;
+                ulj += a12 - a6;
+                vir += Rx * gx + Ry * gy + Rz * gz;
+                if (a.vderiv) {
+                  const double d2u_r2 = 156.0 * a12 - 42.0 * a6;
+                  const double rvR = rx * Rx + ry * Ry + rz * Rz;
+                  const double arr = rvR * inv_r2;
+                  s1p += du_r * arr;
+                  s2p += d2u_r2 * arr * arr + du_r * inv_r2 * (R2 - rvR * arr);
+                }
               }
             }
-          }
-        s1 += s1p;
-        s2 += s2p;
+          s1 += s1p;
+          s2 += s2p;
+        }
+        gfx = __shfl_sync(full, gfx, src), gfy = __shfl_sync(full, gfy, src);
+        gfz = __shfl_sync(full, gfz, src), gtx = __shfl_sync(full, gtx, src);
+        gty = __shfl_sync(full, gty, src), gtz = __shfl_sync(full, gtz, src);
       }
-      // partner accumulators: 32 distinct partners this step
-      ja[0][jl] += gfx, ja[1][jl] += gfy, ja[2][jl] += gfz;
-      ja[3][jl] += gtx, ja[4][jl] += gty, ja[5][jl] += gtz;
-      __syncwarp();
-    }
-    // records: [bp][0] = the I block's side, [bp][1] = the J block's (on the
-    // diagonal the J side is added to the I side: one record)
-    double* rec = ta_.rec + (size_t(r) * ta_.nbp + bp) * 2 * 32 * 6;
-    __syncwarp();
-    if (diag) {
-      fx += ja[0][lane], fy += ja[1][lane], fz += ja[2][lane];
-      tx += ja[3][lane], ty += ja[4][lane], tz += ja[5][lane];
-    } else {
-#pragma unroll
-      for (int c = 0; c < 6; ++c) rec[(32 + lane) * 6 + c] = ja[c][lane];
-    }
+    // records of the item: side 0 = the I block (lane l: molecule l), side 1
+    // = the J block (lane l holds partner (l + k1 + 1) & 31 after the last pass)
+    double* rec = ta_.rec + ((size_t(r) * ta_.nbp + bp) * kTileSplit + part) * 2 * 32 * 6;
+    const int jp = (lane + k1 + 1) & 31;
     rec[lane * 6 + 0] = fx, rec[lane * 6 + 1] = fy, rec[lane * 6 + 2] = fz;
     rec[lane * 6 + 3] = tx, rec[lane * 6 + 4] = ty, rec[lane * 6 + 5] = tz;
+    double* rj = rec + (32 + jp) * 6;
+    rj[0] = gfx, rj[1] = gfy, rj[2] = gfz, rj[3] = gtx, rj[4] = gty, rj[5] = gtz;
+    __syncwarp();  // jd / jext are restaged by the next item
   }
   double v[kNumRowScalars] = {warp_sum(ulj), 0.0, 0.0, warp_sum(s1),
                               warp_sum(s2),  warp_sum(vir), warp_sum(cnt)};
   finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
 }
 
-// Block B's force and torque: its records in block-pair order (the I side of
-// (B, x) for x >= B, the J side of (x, B) for x < B), one thread per
-// (molecule, component); then the fused end-of-step kick.  Block pairs
-// outside this rank's range contribute nothing (their records are not read).
+// Block B's force and torque: the records of every item touching B in
+// (block pair, part) order -- the I side of (B, x) for x >= B, the J side of
+// (x, B) for x <= B, both for the diagonal block pair -- thread (m, c) sums
+// component c of molecule m, 8 loads in flight.  Block pairs outside this
+// rank's range contribute nothing (not read).
 static __global__ void __launch_bounds__(192) k_rigid_reduce(ForceArgs a, TileArgs ta_) {
   const int b = blockIdx.x, r = blockIdx.y;
   const int n = a.s.n;
   const int t = threadIdx.x, m = t / 6, c = t - 6 * (t / 6);
   const int slot = b * 32 + m;
   const int nb = ta_.nb;
-  const double* rec = ta_.rec + size_t(r) * ta_.nbp * 2 * 32 * 6;
-  double acc = 0.0;
-  for (int x = 0; x < nb; ++x) {
+  const double* rec = ta_.rec + size_t(r) * ta_.nbp * kTileSplit * 2 * 32 * 6 + m * 6 + c;
+  auto rec_of = [&](int x, int side, int part) -> long {  // record offset, or -1
     const int lo = min(b, x), hi = max(b, x);
     const int bp = lo * nb - ((lo * (lo - 1)) >> 1) + (hi - lo);
-    if (bp < ta_.bp_begin || bp >= ta_.bp_end) continue;
-    const int side = b <= x ? 0 : 1;
-    acc += rec[(size_t(bp) * 2 + side) * 32 * 6 + m * 6 + c];
+    if (bp < ta_.bp_begin || bp >= ta_.bp_end) return -1;
+    return ((long(bp) * kTileSplit + part) * 2 + side) * 32 * 6;
+  };
+  const int total = (nb + 1) * kTileSplit;  // x = nb: the diagonal's J side
+  double acc = 0.0;
+  for (int u0 = 0; u0 < total; u0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int uu = u0 + u, x = uu / kTileSplit, part = uu - x * kTileSplit;
+      long o = -1;
+      if (x < nb) o = rec_of(x, b <= x ? 0 : 1, part);
+      else if (x == nb) o = rec_of(b, 1, part);
+      v[u] = o >= 0 ? rec[o] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
   }
   const size_t roff = size_t(r) * n;
   __shared__ int ext[32];
