@@ -590,6 +590,14 @@ EwaldArgs ewald_args(b2md_ctx* c) {
   return a;
 }
 
+EwaldTiled ewald_tiled(b2md_ctx* c) {
+  EwaldTiled et;
+  et.Sp = c->d_ewSp;
+  et.fq = c->d_ewfq;
+  et.nchunks = (c->nq + kEwSkQ - 1) / kEwSkQ;
+  return et;
+}
+
 // Ewald::evaluate (src/ewald.cpp:107-180): per-site phase tables, S(k) and
 // U_recip (first part, stream st), then the forces/torques added onto the
 // real-space ones (second part, after the real-space kernel on c->stream)
@@ -602,7 +610,19 @@ int launch_ewald_sk(b2md_ctx* c, cudaStream_t st) {
   else
     k_ewald_tables<<<(nt + 127) / 128, 128, 0, st>>>(a);
   CU(cudaGetLastError());
-  if (a.nk > 0) {
+  if (a.nk > 0 && c->ew_tiled) {
+    const EwaldTiled et = ewald_tiled(c);
+    const dim3 g(et.nchunks, c->R);
+    const dim3 g2((a.nk + kEwSumK - 1) / kEwSumK, c->R);
+    if (prof) {
+      PROF(c, F_EWALD_SK, (k_ewald_sk_tiled<<<g, 256, 0, st>>>(a, et)));
+      PROF(c, F_EWALD_SK, (k_ewald_sk_sum<<<g2, kEwSumK * 8, 0, st>>>(a, et)));
+    } else {
+      k_ewald_sk_tiled<<<g, 256, 0, st>>>(a, et);
+      k_ewald_sk_sum<<<g2, kEwSumK * 8, 0, st>>>(a, et);
+    }
+    CU(cudaGetLastError());
+  } else if (a.nk > 0) {
     if (prof)
       PROF(c, F_EWALD_SK, (k_ewald_sk<<<dim3(a.nk, c->R), 256, 0, st>>>(a)));
     else
@@ -619,6 +639,14 @@ int launch_ewald_sk(b2md_ctx* c, cudaStream_t st) {
 int launch_ewald_force(b2md_ctx* c) {
   EwaldArgs a = ewald_args(c);
   if (a.nk == 0) return B2MD_OK;
+  if (c->ew_tiled) {
+    const EwaldTiled et = ewald_tiled(c);
+    PROF(c, F_EWALD_F, (k_ewald_force_tiled<<<dim3((c->nq + kEwFQ - 1) / kEwFQ, c->R),
+                                              kEwFQ * kEwFParts, 0, c->stream>>>(a, et)));
+    PROF(c, F_EWALD_F,
+         (k_ewald_apply<<<dim3((c->t.n + 255) / 256, c->R), 256, 0, c->stream>>>(a, et)));
+    return B2MD_OK;
+  }
   // k-split: P warps per molecule so that molecules x P reach ~16 warps per SM
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -1444,6 +1472,16 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     TRY(dalloc(&c->d_etab, size_t(R) * 3 * (t.kmax + 1) * std::max(c->nq, 1)));
     TRY(dalloc(&c->d_S, size_t(R) * std::max<size_t>(kv.size(), 1)));
     TRY(dalloc(&c->d_uk, size_t(R) * std::max<size_t>(kv.size(), 1)));
+    // tiled S(k) / forces (kernels.cuh): chunk partials and per-charge forces
+    // (measured on cfg2: equal to the gather form -- 6.33k vs 6.38k steps/s --
+    // so the gather form stays the default; B2MD_EWALD_TILED=1 selects it)
+    c->ew_tiled = false;
+    if (const char* e = std::getenv("B2MD_EWALD_TILED")) c->ew_tiled = t.kmax + 1 <= kEwMaxK && std::atoi(e) != 0;
+    if (c->ew_tiled) {
+      const size_t nch = (size_t(std::max(c->nq, 1)) + kEwSkQ - 1) / kEwSkQ;
+      TRY(dalloc(&c->d_ewSp, size_t(R) * nch * std::max<size_t>(kv.size(), 1)));
+      TRY(dalloc(&c->d_ewfq, size_t(R) * std::max(c->nq, 1) * 3));
+    }
   }
   c->rank = 0;
   c->world = 1;
@@ -1470,7 +1508,7 @@ void free_ctx(b2md_ctx* c) {
                   c->d_uk,    c->d_flux,  c->d_perm, c->d_slot_of, c->d_sp_slot, c->d_sb_slot,
                   c->d_nsites_slot, c->d_scan, c->d_keys[0], c->d_keys[1], c->d_vals[0],
                   c->d_vals[1], c->d_cub, c->d_ke, c->d_thermo_err, c->d_carc,
-                  c->d_chalf, c->d_sarc, c->d_shalf, c->d_trec, c->nl.rec, c->nl.irec,
+                  c->d_chalf, c->d_sarc, c->d_shalf, c->d_trec, c->d_ewSp, c->d_ewfq, c->nl.rec, c->nl.irec,
                   c->nl.ocnt, c->nl.icnt, c->nl.ebase, c->nl.ibase, c->nl.ent,
                   c->nl.in_src, c->nl.fixref,
                   c->nl.ctl};

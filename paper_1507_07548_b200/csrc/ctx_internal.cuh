@@ -174,6 +174,9 @@ struct b2md_ctx {
   double2* d_etab = nullptr;
   double2* d_S = nullptr;
   double* d_uk = nullptr;
+  bool ew_tiled = false;        // tiled S(k) / force kernels (B2MD_EWALD_TILED=0: gather form)
+  double2* d_ewSp = nullptr;    // R * chunks * nk: S(k) partials
+  double* d_ewfq = nullptr;     // R * nq * 3: reciprocal force per charge
   double* d_flux = nullptr;  // R * kNumSums: heat flux totals
   double2* d_ke = nullptr;    // R: (kinetic_energy_trans, kinetic_energy_rot)
   int* d_thermo_err = nullptr;  // R: thermostat failure code (0 ok)

@@ -1786,6 +1786,176 @@ static __global__ void __launch_bounds__(256) k_ewald_force(EwaldArgs a) {
   }
 }
 
+// ------------------------------------------------- Ewald, tiled (default)
+// S(k) and the reciprocal forces with the per-charge phase tables staged in
+// shared memory instead of gathered per (k, charge) from L2 (which read the
+// 3 x 16-byte table entries of every charge for every k-vector: ~100 MB per
+// evaluation on cfg2).  Same arithmetic as k_ewald_sk / k_ewald_force
+// (ewald.cpp:156-178); the summation orders are fixed (deterministic).
+constexpr int kEwSkQ = 32;    // charges per CTA of k_ewald_sk_tiled (tables in shared memory)
+constexpr int kEwFQ = 32;     // charges per CTA of k_ewald_force_tiled
+constexpr int kEwFParts = 16; // k-ranges per CTA (one warp each) of k_ewald_force_tiled
+constexpr int kEwMaxK = 12;   // kmax + 1 <= kEwMaxK for the tiled kernels (else the gather form)
+
+struct EwaldTiled {
+  double2* Sp;  // R * nchunks * nk: S(k) partials of each charge chunk
+  double* fq;   // R * nq * 3: reciprocal force of every charge
+  int nchunks;
+};
+
+// staged tables of charges [q0, q0 + cnt): t[(axis * K + n) * (Q + 1) + ql]
+// (rows padded by one entry: different rows of one column fall in different banks)
+template <int Q>
+__device__ __forceinline__ void ewald_stage(const EwaldArgs& a, int r, int q0, int cnt,
+                                            double2* __restrict__ t) {
+  const int K = a.kmax + 1;
+  const double2* base = a.tab + size_t(r) * 3 * K * a.nq;
+  for (int e = threadIdx.x; e < 3 * K * Q; e += blockDim.x) {
+    const int row = e / Q, ql = e - row * Q;
+    t[row * (Q + 1) + ql] = ql < cnt ? base[size_t(row) * a.nq + q0 + ql] : make_double2(0.0, 0.0);
+  }
+}
+
+template <int Q>
+__device__ __forceinline__ double2 ewald_phase_s(const double2* __restrict__ t, int K, int ql,
+                                                 const DevKVec& k) {
+  double2 e = t[k.nx * (Q + 1) + ql];
+  double2 vy = t[(K + abs(k.ny)) * (Q + 1) + ql];
+  if (k.ny < 0) vy.y = -vy.y;
+  e = cmul(e, vy);
+  double2 vz = t[(2 * K + abs(k.nz)) * (Q + 1) + ql];
+  if (k.nz < 0) vz.y = -vz.y;
+  return cmul(e, vz);
+}
+
+// S(k) partials: one CTA per chunk of kEwSkQ charges, thread per k-vector
+// (strided): every charge's tables are read once per evaluation
+static __global__ void __launch_bounds__(256) k_ewald_sk_tiled(EwaldArgs a, EwaldTiled et) {
+  __shared__ double2 t[3 * kEwMaxK * (kEwSkQ + 1)];
+  const int chunk = blockIdx.x, r = blockIdx.y;
+  const int q0 = chunk * kEwSkQ, cnt = min(kEwSkQ, a.nq - q0);
+  const int K = a.kmax + 1;
+  ewald_stage<kEwSkQ>(a, r, q0, cnt, t);
+  __shared__ double qs[kEwSkQ];
+  if (threadIdx.x < kEwSkQ) qs[threadIdx.x] = threadIdx.x < cnt ? a.q_val[q0 + threadIdx.x] : 0.0;
+  __syncthreads();
+  double2* Sp = et.Sp + (size_t(r) * et.nchunks + chunk) * a.nk;
+  for (int kl = threadIdx.x; kl < a.nk; kl += blockDim.x) {
+    const DevKVec k = a.kv[a.k_begin + kl];
+    // four independent accumulators (charges ql = 4 i + c), summed in order
+    double sre[4] = {0.0, 0.0, 0.0, 0.0}, sim[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q4 = 0; q4 < kEwSkQ; q4 += 4) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double2 e = ewald_phase_s<kEwSkQ>(t, K, q4 + c, k);  // (zero past cnt)
+        sre[c] = fma(e.x, qs[q4 + c], sre[c]);
+        sim[c] = fma(e.y, qs[q4 + c], sim[c]);
+      }
+    }
+    Sp[kl] = make_double2((sre[0] + sre[1]) + (sre[2] + sre[3]), (sim[0] + sim[1]) + (sim[2] + sim[3]));
+  }
+}
+
+// S(k) = the chunks' partials in chunk order (lanes q of a k split the chunks,
+// fixed xor tree), U_recip = sum_k 0.5 coeff |S|^2 by per-CTA partials totalled
+// in order by the last CTA (ewald.cpp:163-169)
+constexpr int kEwSumK = 32;  // k-vectors per CTA of k_ewald_sk_sum (8 lanes each)
+static __global__ void __launch_bounds__(kEwSumK * 8) k_ewald_sk_sum(EwaldArgs a, EwaldTiled et) {
+  const int r = blockIdx.y;
+  const int kl = blockIdx.x * kEwSumK + (threadIdx.x >> 3), sub8 = threadIdx.x & 7;
+  const double2* P = et.Sp + size_t(r) * et.nchunks * a.nk;
+  double sre = 0.0, sim = 0.0;
+  if (kl < a.nk) {
+#pragma unroll 4
+    for (int c = sub8; c < et.nchunks; c += 8) {
+      const double2 v = P[size_t(c) * a.nk + kl];
+      sre += v.x;
+      sim += v.y;
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    sre += __shfl_xor_sync(0xffffffffu, sre, o);
+    sim += __shfl_xor_sync(0xffffffffu, sim, o);
+  }
+  double u = 0.0;
+  if (kl < a.nk && sub8 == 0) {
+    a.S[size_t(r) * a.nk_total + a.k_begin + kl] = make_double2(sre, sim);
+    u = 0.5 * a.kv[a.k_begin + kl].coeff * (sre * sre + sim * sim);
+  }
+  const double v[1] = {warp_sum(u)};
+  finalize_scalars<1>(v, a.uk, a.ticket, a.sums, r, kNumRowScalars);
+}
+
+// Reciprocal force of every charge: one CTA per kEwFQ charges (lane = charge),
+// warp p takes the p-th of kEwFParts contiguous k-ranges; the parts are
+// summed in part order through shared memory (ewald.cpp:171-178)
+static __global__ void __launch_bounds__(kEwFQ * kEwFParts) k_ewald_force_tiled(EwaldArgs a, EwaldTiled et) {
+  __shared__ double2 t[3 * kEwMaxK * (kEwFQ + 1)];
+  __shared__ double part[kEwFParts][3][kEwFQ];
+  const int r = blockIdx.y;
+  const int q0 = blockIdx.x * kEwFQ, cnt = min(kEwFQ, a.nq - q0);
+  const int K = a.kmax + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  ewald_stage<kEwFQ>(a, r, q0, cnt, t);
+  __syncthreads();
+  const int per = (a.nk + kEwFParts - 1) / kEwFParts;
+  const int k0 = warp * per, k1 = min(a.nk, k0 + per);
+  const double2* S = a.S + size_t(r) * a.nk_total + a.k_begin;
+  // two independent accumulator sets (even / odd k of the range), summed in order
+  double fx[2] = {0.0, 0.0}, fy[2] = {0.0, 0.0}, fz[2] = {0.0, 0.0};
+#pragma unroll 2
+  for (int kl = k0; kl < k1; ++kl) {
+    const DevKVec k = a.kv[a.k_begin + kl];  // (warp-uniform: broadcast loads)
+    const double2 Sk = S[kl];
+    const double2 e = ewald_phase_s<kEwFQ>(t, K, lane, k);
+    const double im = e.y * Sk.x - e.x * Sk.y;
+    const double c = k.coeff * im;
+    const int h = (kl - k0) & 1;
+    fx[h] = fma(c, k.kx, fx[h]);
+    fy[h] = fma(c, k.ky, fy[h]);
+    fz[h] = fma(c, k.kz, fz[h]);
+  }
+  part[warp][0][lane] = fx[0] + fx[1];
+  part[warp][1][lane] = fy[0] + fy[1];
+  part[warp][2][lane] = fz[0] + fz[1];
+  __syncthreads();
+  if (threadIdx.x < 3 * kEwFQ) {
+    const int comp = threadIdx.x / kEwFQ, ql = threadIdx.x - comp * kEwFQ;
+    if (ql < cnt) {
+      double v = 0.0;
+      for (int p = 0; p < kEwFParts; ++p) v += part[p][comp][ql];
+      et.fq[(size_t(r) * a.nq + q0 + ql) * 3 + comp] = a.q_val[q0 + ql] * v;
+    }
+  }
+}
+
+// Per molecule: its charges' reciprocal forces (in charge order) and their
+// torques off x F, added to the real-space totals
+static __global__ void __launch_bounds__(256) k_ewald_apply(EwaldArgs a, EwaldTiled et) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+  if (m >= a.s.n) return;
+  const int q0 = a.mol_qbegin[m], q1 = a.mol_qbegin[m + 1];
+  if (q0 == q1) return;
+  const size_t soff = size_t(r) * a.s.total_sites;
+  double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
+  for (int q = q0; q < q1; ++q) {
+    const double* f = et.fq + (size_t(r) * a.nq + q) * 3;
+    const double4 o = a.st.off[soff + site_slot(a.s, r, m, a.q_site[q])];
+    fx += f[0], fy += f[1], fz += f[2];
+    tx += o.y * f[2] - o.z * f[1];
+    ty += o.z * f[0] - o.x * f[2];
+    tz += o.x * f[1] - o.y * f[0];
+  }
+  const size_t e = size_t(r) * a.s.n + m;
+  a.st.fx[e] += fx;
+  a.st.fy[e] += fy;
+  a.st.fz[e] += fz;
+  a.st.tx[e] += tx;
+  a.st.ty[e] += ty;
+  a.st.tz[e] += tz;
+}
+
 // ------------------------------------------------------------- integrator
 // engine.cpp:13-19
 __device__ __forceinline__ void permute4(int axis, const double q[4], double o[4]) {

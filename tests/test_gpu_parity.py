@@ -927,3 +927,21 @@ def test_cluster_walk_modes(monkeypatch, mode):
     assert runs[0][1] == o.evaluate(runs[0][0].pos, runs[0][0].orient)["com_pairs"]
     assert np.array_equal(runs[0][0].pos, runs[1][0].pos)
     assert np.array_equal(runs[0][0].force, runs[1][0].force)
+
+
+@pytest.mark.parametrize("tiled", ["0", "1"])
+def test_ewald_forms_cfg2(monkeypatch, tiled):
+    """Both reciprocal-space forms (per-(k, charge) table gathers, and the
+    shared-memory tiled S(k) / force kernels of B2MD_EWALD_TILED=1) against the
+    oracle on cfg2 (ewald.cpp:107-180): forces, torques, energies; repeated
+    evaluations bit-identical."""
+    monkeypatch.setenv("B2MD_EWALD_TILED", tiled)
+    wl = configs.make("cfg2")
+    st = wl.states[0]
+    ref = pyoracle.OracleFF(wl.comp, wl.opts).evaluate(st.pos, st.orient)
+    outs = [gpu_eval(wl.comp, wl.opts, st.pos, st.orient)[1] for _ in range(2)]
+    check_vec(outs[0].force, ref["force"])
+    check_vec(outs[0].torque, ref["torque"])
+    check_energy(outs[0].energy, ref["energy"], outs[0].virial, ref["virial"])
+    assert np.array_equal(outs[0].force, outs[1].force)
+    assert outs[0].energy.total() == outs[1].energy.total()
