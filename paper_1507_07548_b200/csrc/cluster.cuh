@@ -574,7 +574,6 @@ struct NListArgs {
   unsigned d2_stale;  // bits of ((skin / 2) 2^32 / L)^2 (1 - 1e-4): D^2 above is stale
   int max_ent;
   int cbeg, cend;  // this rank's owner clusters
-  int dbg;         // measurement only (B2MD_NL_DBG): 1 no LJ, 2 no j-side, 4 no record stores, 16 no pairs
 };
 
 // The list cannot be used this evaluation (overflow at the build, or a
@@ -937,11 +936,6 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
         for (int t = 0; t < na; ++t) {  // warp-uniform
           const int2 cur = elist[warp][p][t];
           const double4 pj = jst[p][t][jl];
-          if (nl.dbg & 16) {
-            dirty = true;
-            fax += pj.x;
-            continue;
-          }
           const int jc = cur.x & kJcMask, code = cur.x >> kJcBits;
           const int j = jc * kCS + jl;
           const bool vj = j < n;
@@ -977,8 +971,8 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
           if (__ballot_sync(full, ina || inb) == 0u) continue;  // no record: its stamp stays old
           const int sj = MULTI_SPECIES ? (vj ? s.sp_slot[roff + j] : sia) : 0;
           // both rows' terms in one block (two independent dependency chains)
-          const double fsa = (nl.dbg & 1) ? 0.0 : lj(ina, r2a, sia, sj);
-          const double fsb = (nl.dbg & 1) ? 0.0 : lj(inb, r2b, sib, sj);
+          const double fsa = lj(ina, r2a, sia, sj);
+          const double fsb = lj(inb, r2b, sib, sj);
           double gx = 0, gy = 0, gz = 0;
           if (ina) {
             gx = fsa * dxa, gy = fsa * dya, gz = fsa * dza;
@@ -991,7 +985,6 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
           }
           dirty = true;
           cnt += int(ina) + int(inb);
-          if (nl.dbg & 2) continue;
           // j-side: member jl's 4 row lanes summed in row order through
           // shared memory (lane (jl, c) adds component c), stamped record
           double* jb = jt[warp][par];
@@ -1002,7 +995,6 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
           __syncwarp();
           const double* jr = jb + jl * 3 + cw;
           const double res = ((jr[0] + jr[24]) + jr[48]) + jr[72];
-          if (nl.dbg & 4) continue;
           rec[cur.y * kRecD] = il == 3 ? stamp : res;
         }
         if (dirty) {  // the batch's i-side record (rows ia / ib: 8 jl lanes, xor tree)

@@ -1350,7 +1350,6 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
       const double du = 0.5 * c->nl_skin * 4294967296.0 / c->t.box;
       const float d2s = float(du * du * (1.0 - 1e-4));
       std::memcpy(&nl.d2_stale, &d2s, sizeof d2s);
-      if (const char* e = std::getenv("B2MD_NL_DBG")) nl.dbg = std::atoi(e);
     }
   }
   if (rigid_sites(c->t) > 0) {
