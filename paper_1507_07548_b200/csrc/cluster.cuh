@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(kGWarps * 32, kGMinBlocks) k_force_cpair(Force
 //   are contiguous (increasing cj), padded to a multiple of kB with entries
 //   that never pass the cull, so a batch of kB entries has one owner; a
 //   receiver's incoming records are contiguous (receiver-major slots, owner
-//   order).  Built by k_nl_count, k_nl_scan, k_nl_fill, k_nl_inrec (no
+//   order).  Built by k_nl_count, k_nl_scan, k_nl_fill, k_nl_zfill (no
 //   atomics: the layout is a pure function of the arcs).
 // * Periodic images per entry: where neither cluster's arc (widened by the
 //   skin) can reach the box boundary on an axis, every member pair's raw
@@ -540,6 +540,7 @@ __global__ void __launch_bounds__(kGWarps * 32, kGMinBlocks) k_force_cpair(Force
 //   stamped incoming records -- force = i-side - j-side, a fixed order -- and
 //   the fused end-of-step kick.
 constexpr int kNLBuildWarps = 4;  // warps (clusters) per CTA of the build / reduce kernels
+constexpr int kNLParts = 4;       // build warps per cluster (contiguous super-cluster ranges)
 constexpr int kNLWarps = 4;       // warps per CTA of k_force_nl
 #ifndef B2MD_NL_MINBLOCKS
 #define B2MD_NL_MINBLOCKS 5
@@ -549,7 +550,8 @@ constexpr int kB = 16;            // entries per batch (one owner)
 #ifndef B2MD_NL_TMA
 #define B2MD_NL_TMA 0             // stage by bulk (TMA) copies instead of per-lane cp.async
 #endif
-constexpr int kRecD = kCS * 4;    // doubles per record: 8 members x (x, y, z, epoch stamp)
+constexpr int kRecD = kCS * 4;    // doubles per i-side record: 8 members x (x, y, z, epoch stamp)
+constexpr int kRecP = kCS * 3;    // doubles per j-side record: 8 members x (x, y, z); stamp apart
 constexpr int kNLCtl = 8;         // control words per replica
 constexpr int kJcBits = 24;       // entry.x = cj | shift codes << 24 (2 bits per axis)
 constexpr int kJcMask = (1 << kJcBits) - 1;
@@ -558,13 +560,18 @@ enum { kNLEntries = 0, kNLIncoming = 1, kNLEpoch = 2, kNLTicket = 3, kNLOverflow
 
 struct NListArgs {
   int* ocnt;       // R * nc: owned entries of each cluster, padded to kB (0 for another rank's)
+  int* ocp;        // R * nc * kNLParts: owned entries found by each build part (unpadded)
+  int* icp;        // R * nc * kNLParts: incoming slots found by each build part
   int* icnt;       // R * nc: incoming slots (owners x of {x, c}, c itself included)
   int* ebase;      // R * (nc + 1): first entry of each cluster (per-replica numbering)
   int* ibase;      // R * (nc + 1): first incoming slot
   int4* ent;       // R * max_ent: {cj | codes << 24, ci, record slot, build gap^2 bits}
   int* in_src;     // R * max_ent: owner of each incoming slot (build scratch)
-  double* rec;     // R * max_ent * kRecD: j-side sums g = sum_i f_ij (force on j: -g),
+  int* smap;       // R * nc * nc: [owner][receiver] -> incoming slot (build scratch; null when
+                   // too large: k_nl_inrec's binary searches instead)
+  double* rec;     // R * max_ent * kRecP: j-side sums g = sum_i f_ij (force on j: -g),
                    // receiver-major (cluster c's incoming slots ibase[c] .. ibase[c + 1])
+  int* rstamp;     // R * max_ent: epoch of the evaluation that wrote each j-side record
   double* irec;    // R * (max_ent / kB) * kRecD: i-side force of each batch
   uint4* fixref;   // R * n: fixed-point positions at the build (slot order)
   int* ctl;        // R * kNLCtl
@@ -582,22 +589,23 @@ __device__ __forceinline__ bool nl_stale(const NListArgs& nl, const int* ctl) {
   return ctl[kNLOverflow] != 0 || unsigned(ctl[kNLD2]) > nl.d2_stale;
 }
 
-// c's neighbour clusters within the cull radius^2 lim (fixed-point units),
-// in increasing order: for every batch of 32 candidates (one surviving
+// c's neighbour clusters within the cull radius^2 lim (fixed-point units)
+// among super-clusters [sb0, sb1), in increasing order: for every batch of 32
+// candidates (one surviving
 // super-cluster) visit(jc, near) runs on all lanes (warp-uniform call).  Up
 // to 4 surviving super-clusters have their arc loads in flight together.
 template <class Visit>
 __device__ __forceinline__ void nl_scan(const ClusterArgs& ca, int r, uint4 gc, float4 gh, float lim,
-                                        Visit&& visit) {
+                                        int sb0, int sb1, Visit&& visit) {
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
   const uint4* __restrict__ arcs = ca.arcs + size_t(r) * ca.nc;
   const float4* __restrict__ half = ca.half + size_t(r) * ca.nc;
   const uint4* __restrict__ sarcs = ca.sup_arcs + size_t(r) * ca.nsup;
   const float4* __restrict__ shalf = ca.sup_half + size_t(r) * ca.nsup;
-  for (int sb = 0; sb < ca.nsup; sb += 32) {
+  for (int sb = sb0; sb < sb1; sb += 32) {
     unsigned sv = __ballot_sync(
-        full, sb + lane < ca.nsup && arcs_near(gc, gh, sarcs[sb + lane], shalf[sb + lane], lim));
+        full, sb + lane < sb1 && arcs_near(gc, gh, sarcs[sb + lane], shalf[sb + lane], lim));
     while (sv) {
       int scs[4];
 #pragma unroll
@@ -646,26 +654,28 @@ __device__ __forceinline__ int shift_code(uint32_t ca, float ha, uint32_t cb, fl
   return 3;
 }
 
-// pass 1: owned entries (padded to kB) and incoming slots of every cluster
+// pass 1: owned entries and incoming slots of every cluster, kNLParts warps
+// per cluster (part p: super-clusters [p nsup / P, (p+1) nsup / P))
 static __global__ void __launch_bounds__(kNLBuildWarps * 32)
     k_nl_count(ClusterArgs ca, NListArgs nl) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.y, nc = ca.nc;
-  const int c = blockIdx.x * kNLBuildWarps + warp;
+  const int w = blockIdx.x * kNLBuildWarps + warp, c = w / kNLParts, part = w - c * kNLParts;
   if (c >= nc) return;
   const unsigned full = 0xffffffffu;
   const uint4 gc = ca.arcs[size_t(r) * nc + c];
   const float4 gh = ca.half[size_t(r) * nc + c];
+  const int sb0 = part * ca.nsup / kNLParts, sb1 = (part + 1) * ca.nsup / kNLParts;
   int no = 0, ni = 0;
-  nl_scan(ca, r, gc, gh, nl.lim_build, [&](int jc, bool near) {
+  nl_scan(ca, r, gc, gh, nl.lim_build, sb0, sb1, [&](int jc, bool near) {
     const bool own = near && owns_pair(c, jc);
     no += __popc(__ballot_sync(full, own));
     ni += __popc(__ballot_sync(full, near && (jc == c || !own)));
   });
   if (lane == 0) {
     const bool mine = c >= nl.cbeg && c < nl.cend;
-    nl.ocnt[size_t(r) * nc + c] = mine ? (no + kB - 1) / kB * kB : 0;
-    nl.icnt[size_t(r) * nc + c] = ni;
+    nl.ocp[size_t(r) * nc * kNLParts + w] = mine ? no : 0;
+    nl.icp[size_t(r) * nc * kNLParts + w] = ni;
   }
 }
 
@@ -678,18 +688,27 @@ static __global__ void __launch_bounds__(kNLScanThreads) k_nl_scan(NListArgs nl,
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry[2];
   const int r = blockIdx.x;
-  const int* oc = nl.ocnt + size_t(r) * nc;
-  const int* ic = nl.icnt + size_t(r) * nc;
   int* eb = nl.ebase + size_t(r) * (nc + 1);
   int* ib = nl.ibase + size_t(r) * (nc + 1);
   if (threadIdx.x < 2) carry[threadIdx.x] = 0;
   __syncthreads();
   for (int b = 0; b < nc; b += kNLScanThreads) {
     const int c = b + threadIdx.x;
+    int ov = 0, iv = 0;
+    if (c < nc) {
+#pragma unroll
+      for (int q = 0; q < kNLParts; ++q) {
+        ov += nl.ocp[(size_t(r) * nc + c) * kNLParts + q];
+        iv += nl.icp[(size_t(r) * nc + c) * kNLParts + q];
+      }
+      ov = (ov + kB - 1) / kB * kB;  // padded to whole batches
+      nl.ocnt[size_t(r) * nc + c] = ov;
+      nl.icnt[size_t(r) * nc + c] = iv;
+    }
     int x0, x1, t0, t1;
-    Scan(tmp).ExclusiveSum(c < nc ? oc[c] : 0, x0, t0);
+    Scan(tmp).ExclusiveSum(ov, x0, t0);
     __syncthreads();
-    Scan(tmp).ExclusiveSum(c < nc ? ic[c] : 0, x1, t1);
+    Scan(tmp).ExclusiveSum(iv, x1, t1);
     if (c < nc) {
       eb[c] = carry[0] + x0;
       ib[c] = carry[1] + x1;
@@ -717,23 +736,29 @@ static __global__ void __launch_bounds__(kNLBuildWarps * 32)
     k_nl_fill(ClusterArgs ca, NListArgs nl) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.y, nc = ca.nc, n = ca.n;
-  const int c = blockIdx.x * kNLBuildWarps + warp;
+  const int w = blockIdx.x * kNLBuildWarps + warp, c = w / kNLParts, part = w - c * kNLParts;
   if (c >= nc) return;
-  if (lane < kCS && c * kCS + lane < n)
+  if (part == 0 && lane < kCS && c * kCS + lane < n)
     nl.fixref[size_t(r) * n + c * kCS + lane] = ca.fixpos[size_t(r) * n + c * kCS + lane];
   if (nl.ctl[size_t(r) * kNLCtl + kNLOverflow]) return;  // never read
   const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
   const uint4 gc = ca.arcs[size_t(r) * nc + c];
   const float4 gh = ca.half[size_t(r) * nc + c];
   const bool mine = c >= nl.cbeg && c < nl.cend;
-  const int eb = nl.ebase[size_t(r) * (nc + 1) + c], ee = nl.ebase[size_t(r) * (nc + 1) + c + 1];
-  const int ib = nl.ibase[size_t(r) * (nc + 1) + c];
+  // this part's offsets: the earlier parts' counts
+  int eb = nl.ebase[size_t(r) * (nc + 1) + c], ib = nl.ibase[size_t(r) * (nc + 1) + c];
+  const int ee = nl.ebase[size_t(r) * (nc + 1) + c + 1];
+  for (int q = 0; q < part; ++q) {
+    eb += nl.ocp[(size_t(r) * nc + c) * kNLParts + q];
+    ib += nl.icp[(size_t(r) * nc + c) * kNLParts + q];
+  }
+  const int sb0 = part * ca.nsup / kNLParts, sb1 = (part + 1) * ca.nsup / kNLParts;
   int4* __restrict__ ent = nl.ent + size_t(r) * nl.max_ent;
   int* __restrict__ src = nl.in_src + size_t(r) * nl.max_ent;
   const uint4* __restrict__ arcs = ca.arcs + size_t(r) * nc;
   const float4* __restrict__ half = ca.half + size_t(r) * nc;
   int no = 0, ni = 0;
-  nl_scan(ca, r, gc, gh, nl.lim_build, [&](int jc, bool near) {
+  nl_scan(ca, r, gc, gh, nl.lim_build, sb0, sb1, [&](int jc, bool near) {
     const bool own = near && owns_pair(c, jc);
     const bool inc = near && (jc == c || !own);
     const unsigned ov = __ballot_sync(full, own && mine), iv = __ballot_sync(full, inc);
@@ -746,12 +771,16 @@ static __global__ void __launch_bounds__(kNLBuildWarps * 32)
       const float g2 = jc == c ? 0.0f : arcs_gap2(gc, gh, cj, hj);
       ent[eb + no + __popc(ov & lt)] = make_int4(jc | code << kJcBits, c, 0, __float_as_int(g2));
     }
-    if (inc) src[ib + ni + __popc(iv & lt)] = jc;
+    if (inc) {
+      src[ib + ni + __popc(iv & lt)] = jc;
+      if (nl.smap) nl.smap[(size_t(r) * nc + jc) * nc + c] = ib + ni + __popc(iv & lt);
+    }
     no += __popc(ov);
     ni += __popc(iv);
   });
-  for (int e = eb + no + lane; e < ee; e += 32)  // padding: above every c, never culled in
-    ent[e] = make_int4(kJcMask, c, 0, 0x7f800000);
+  if (part == kNLParts - 1)
+    for (int e = eb + no + lane; e < ee; e += 32)  // padding: above every c, never culled in
+      ent[e] = make_int4(kJcMask, c, 0, 0x7f800000);
 }
 
 // pass 4: the record slot of every entry: receiver c's incoming slot t of
@@ -773,6 +802,22 @@ static __global__ void __launch_bounds__(kNLBuildWarps * 32) k_nl_inrec(NListArg
       if ((ent[mid].x & kJcMask) < c) lo = mid + 1; else hi = mid;
     }
     if (lo < eb[x + 1] && (ent[lo].x & kJcMask) == c) ent[lo].z = t;
+  }
+}
+
+// pass 4 with the dense [owner][receiver] slot map: every entry's record
+// slot in one gather (one warp per owner)
+static __global__ void __launch_bounds__(kNLBuildWarps * 32) k_nl_zfill(NListArgs nl, int nc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.y;
+  const int x = blockIdx.x * kNLBuildWarps + warp;
+  if (x >= nc || nl.ctl[size_t(r) * kNLCtl + kNLOverflow]) return;
+  const int* eb = nl.ebase + size_t(r) * (nc + 1);
+  int4* ent = nl.ent + size_t(r) * nl.max_ent;
+  const int* sm = nl.smap + (size_t(r) * nc + x) * nc;
+  for (int e = eb[x] + lane; e < eb[x + 1]; e += 32) {
+    const int jc = ent[e].x & kJcMask;
+    if (jc != kJcMask) ent[e].z = sm[jc];
   }
 }
 
@@ -818,7 +863,8 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
     const int nw = gridDim.x * kNLWarps;
     const int gw = blockIdx.x * kNLWarps + warp;
     const int4* __restrict__ ent = nl.ent + size_t(r) * nl.max_ent;
-    double* __restrict__ rec = nl.rec + size_t(r) * nl.max_ent * kRecD + lane;
+    double* __restrict__ rec = nl.rec + size_t(r) * nl.max_ent * kRecP + 3 * jl + (il < 3 ? il : 2);
+    int* __restrict__ rstamp = nl.rstamp + size_t(r) * nl.max_ent;
     const double4* __restrict__ p4 = a.st.pos4 + roff;
     const double L = s.mi.L;
     const double stamp = stamp_of(epoch);
@@ -995,7 +1041,8 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
           __syncwarp();
           const double* jr = jb + jl * 3 + cw;
           const double res = ((jr[0] + jr[24]) + jr[48]) + jr[72];
-          rec[cur.y * kRecD] = il == 3 ? stamp : res;
+          if (il < 3) rec[size_t(cur.y) * kRecP] = res;
+          if (lane == 0) rstamp[cur.y] = epoch;
         }
         if (dirty) {  // the batch's i-side record (rows ia / ib: 8 jl lanes, xor tree)
 #pragma unroll
@@ -1064,25 +1111,62 @@ static __global__ void __launch_bounds__(kNLBuildWarps * 32)
     const long long epoch = ctl[kNLEpoch] - 1;  // advanced by the force kernel's last CTA
     const int* eb = nl.ebase + size_t(r) * (nc + 1);
     const double* __restrict__ irec = nl.irec + size_t(r) * (nl.max_ent / kB) * kRecD + 4 * m;
-    const double* __restrict__ rec = nl.rec + size_t(r) * nl.max_ent * kRecD + 4 * m;
+    const double* __restrict__ rec = nl.rec + size_t(r) * nl.max_ent * kRecP + 3 * m;
+    const int* __restrict__ rstamp = nl.rstamp + size_t(r) * nl.max_ent;
     double fx = 0.0, fy = 0.0, fz = 0.0;
-    if (q == 0)
-      for (int b = eb[c] / kB; b < eb[c + 1] / kB; ++b) {
-        const double4 u = *reinterpret_cast<const double4*>(irec + size_t(b) * kRecD);
-        if (__double_as_longlong(u.w) == epoch) fx += u.x, fy += u.y, fz += u.z;
+    {  // the batches' i-side records: batch b by group (b - first) % 4, 8 in flight
+      const int b0 = eb[c] / kB, b1 = eb[c + 1] / kB;
+      for (int bb = b0; bb < b1; bb += 8) {
+        double4 u[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int b = bb + 4 * h + q;
+          u[h] = b < b1 ? *reinterpret_cast<const double4*>(irec + size_t(b) * kRecD)
+                        : make_double4(0.0, 0.0, 0.0, __longlong_as_double(-1ll));
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (__double_as_longlong(u[h].w) == epoch) fx += u[h].x, fy += u[h].y, fz += u[h].z;
       }
+    }
     const int i1 = nl.ibase[size_t(r) * (nc + 1) + c + 1];
-    for (int t0 = nl.ibase[size_t(r) * (nc + 1) + c]; t0 < i1; t0 += 32) {
-      double4 u[8];
+    // the stamps of up to 256 slots at once (one round trip) compacted into
+    // the warp's list of stamped slots (slot order), then only the stamped
+    // payloads: the k-th listed slot by group k % 4, 16 payloads in flight
+    constexpr int kSpan = 256;
+    __shared__ int slist[kNLBuildWarps][kSpan];
+    int* sl = slist[warp];
+    for (int s0 = nl.ibase[size_t(r) * (nc + 1) + c]; s0 < i1; s0 += kSpan) {
+      int st[kSpan / 32];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int t = t0 + 4 * k + q;
-        u[k] = t < i1 ? *reinterpret_cast<const double4*>(rec + size_t(t) * kRecD)
-                      : make_double4(0.0, 0.0, 0.0, __longlong_as_double(-1ll));
+      for (int j = 0; j < kSpan / 32; ++j) {
+        const int t = s0 + 32 * j + lane;
+        st[j] = t < i1 ? rstamp[t] : -1;
       }
+      int cnt = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (__double_as_longlong(u[k].w) == epoch) fx -= u[k].x, fy -= u[k].y, fz -= u[k].z;
+      for (int j = 0; j < kSpan / 32; ++j) {
+        const bool okl = st[j] == int(epoch);
+        const unsigned ok = __ballot_sync(full, okl);
+        if (okl) sl[cnt + __popc(ok & ((1u << lane) - 1u))] = s0 + 32 * j + lane;
+        cnt += __popc(ok);
+      }
+      __syncwarp();
+      for (int k0 = 0; k0 < cnt; k0 += 32) {
+        double px[8], py[8], pz[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const int k = k0 + 4 * h + q;
+          px[h] = py[h] = pz[h] = 0.0;
+          if (k < cnt) {
+            const double* pr = rec + size_t(sl[k]) * kRecP;
+            px[h] = __ldg(pr), py[h] = __ldg(pr + 1), pz[h] = __ldg(pr + 2);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) fx -= px[h], fy -= py[h], fz -= pz[h];
+      }
+      __syncwarp();  // the list is rewritten by the next span
     }
 #pragma unroll
     for (int o = 8; o < 32; o <<= 1) {

@@ -429,11 +429,15 @@ int nl_build(b2md_ctx* c) {
   const ClusterArgs ca = cluster_args(c);
   const NListArgs nl = nl_args(c);
   const dim3 g((c->nc + kNLBuildWarps - 1) / kNLBuildWarps, c->R);
+  const dim3 gp((c->nc * kNLParts + kNLBuildWarps - 1) / kNLBuildWarps, c->R);
   const int bs = kNLBuildWarps * 32;
-  PROF(c, F_NL_BUILD, (k_nl_count<<<g, bs, 0, c->stream>>>(ca, nl)));
+  PROF(c, F_NL_BUILD, (k_nl_count<<<gp, bs, 0, c->stream>>>(ca, nl)));
   PROF(c, F_NL_BUILD, (k_nl_scan<<<c->R, kNLScanThreads, 0, c->stream>>>(nl, c->nc)));
-  PROF(c, F_NL_BUILD, (k_nl_fill<<<g, bs, 0, c->stream>>>(ca, nl)));
-  PROF(c, F_NL_BUILD, (k_nl_inrec<<<g, bs, 0, c->stream>>>(nl, c->nc)));
+  PROF(c, F_NL_BUILD, (k_nl_fill<<<gp, bs, 0, c->stream>>>(ca, nl)));
+  if (nl.smap)
+    PROF(c, F_NL_BUILD, (k_nl_zfill<<<g, bs, 0, c->stream>>>(nl, c->nc)));
+  else
+    PROF(c, F_NL_BUILD, (k_nl_inrec<<<g, bs, 0, c->stream>>>(nl, c->nc)));
   c->steps_since_nl = 0;
   return B2MD_OK;
 }
@@ -1313,22 +1317,31 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     const size_t nc = size_t(c->nc);
     // every cluster pair once, plus < kB padding entries per owner
     const size_t max_ent = (nc * (nc + 1) / 2 + nc * kB + kB - 1) / kB * kB;
-    if (size_t(R) * max_ent * kRecD * sizeof(double) > (size_t(8) << 30))
+    if (size_t(R) * max_ent * kRecP * sizeof(double) > (size_t(8) << 30))
       c->use_newton = false;
     if (c->use_newton) {
+      // the end-of-step kick rides with the next step's drift
+      // (k_step_drift_arcs<true>): the reduce then only writes forces
+      c->use_fused_kick = false;
+      if (const char* e = std::getenv("B2MD_FUSED_KICK")) c->use_fused_kick = std::atoi(e) != 0;
       NListArgs& nl = c->nl;
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
       c->n3_grid = sms * kNLMinBlocks;
       nl.max_ent = int(max_ent);
-      TRY(dalloc(&nl.rec, size_t(R) * max_ent * kRecD));
+      TRY(dalloc(&nl.rec, size_t(R) * max_ent * kRecP));
+      TRY(dalloc(&nl.rstamp, size_t(R) * max_ent));
       TRY(dalloc(&nl.irec, size_t(R) * (max_ent / kB) * kRecD));
       TRY(dalloc(&nl.ocnt, size_t(R) * nc));
+      TRY(dalloc(&nl.ocp, size_t(R) * nc * kNLParts));
+      TRY(dalloc(&nl.icp, size_t(R) * nc * kNLParts));
       TRY(dalloc(&nl.icnt, size_t(R) * nc));
       TRY(dalloc(&nl.ebase, size_t(R) * (nc + 1)));
       TRY(dalloc(&nl.ibase, size_t(R) * (nc + 1)));
       TRY(dalloc(&nl.ent, size_t(R) * max_ent));
       TRY(dalloc(&nl.in_src, size_t(R) * max_ent));
+      // dense [owner][receiver] slot map up to 256 MB (nc <= 8k clusters on one replica)
+      if (size_t(R) * nc * nc * sizeof(int) <= (size_t(256) << 20)) TRY(dalloc(&nl.smap, size_t(R) * nc * nc));
       TRY(dalloc(&nl.fixref, size_t(R) * c->t.n));
       TRY(dalloc(&nl.ctl, size_t(R) * kNLCtl));
       // stale until the first build; epoch 1 (the stamps start at 0)
@@ -1509,7 +1522,7 @@ void free_ctx(b2md_ctx* c) {
                   c->d_vals[1], c->d_cub, c->d_ke, c->d_thermo_err, c->d_carc,
                   c->d_chalf, c->d_sarc, c->d_shalf, c->d_trec, c->d_ewSp, c->d_ewfq, c->nl.rec, c->nl.irec,
                   c->nl.ocnt, c->nl.icnt, c->nl.ebase, c->nl.ibase, c->nl.ent,
-                  c->nl.in_src, c->nl.fixref,
+                  c->nl.in_src, c->nl.fixref, c->nl.rstamp, c->nl.smap, c->nl.ocp, c->nl.icp,
                   c->nl.ctl};
   for (void* p : ptrs)
     if (p) cudaFree(p);
