@@ -231,6 +231,16 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 __device__ __forceinline__ void cp_async16(unsigned smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
 }
+template <int OFF>
+__device__ __forceinline__ void sts_f64(unsigned addr, double v) {
+  asm volatile("st.shared.f64 [%0+%2], %1;" ::"r"(addr), "d"(v), "n"(OFF) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(addr), "n"(OFF) : "memory");
+  return v;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -821,6 +831,69 @@ static __global__ void __launch_bounds__(kNLBuildWarps * 32) k_nl_zfill(NListArg
   }
 }
 
+// pass 5: every entry's build gap tightened from the arcs' bound to the
+// smallest member-pair distance at the build.  One warp per batch (one owner:
+// its 8 members in registers), two lanes per entry (4 j-members each against
+// the 8 i-members).  Integer arithmetic on the wrapping fixed-point
+// differences (the minimum image), truncated to 16 bits per axis: each
+// component is off by < 1 unit of 2^16, the distance by < sqrt(3) units; 2
+// units are taken off (the rest covers the coordinates' own rounding) and
+// 1e-6 relative for the float conversion, square root and square -- a lower
+// bound, so `gap >= rc + 2 D` still proves that no member pair is within rc.
+// Entries whose members are all beyond rc + skin get a gap the per-step cull
+// never passes while the list is valid.  A member outside [0, L) keeps the
+// arcs' bound (0: whole-circle arcs).
+static __global__ void __launch_bounds__(kNLBuildWarps * 32) k_nl_gaps(ClusterArgs ca, NListArgs nl) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.y, n = ca.n;
+  const int* ctl = nl.ctl + size_t(r) * kNLCtl;
+  if (ctl[kNLOverflow]) return;
+  const int nbt = ctl[kNLEntries] / kB;
+  int4* __restrict__ ent = nl.ent + size_t(r) * nl.max_ent;
+  const uint4* __restrict__ fix = ca.fixpos + size_t(r) * n;
+  static_assert(kB * 2 == 32 && kCS == 8, "two lanes per entry");
+  for (int bt = blockIdx.x * kNLBuildWarps + warp; bt < nbt; bt += gridDim.x * kNLBuildWarps) {
+    const int e = bt * kB + (lane >> 1);
+    const int4 en = ent[e];
+    const int ci = en.y;
+    // padding entries never pass the cull and a cluster's own entry has gap 0
+    const bool live = (en.x & kJcMask) != kJcMask && (en.x & kJcMask) != ci;
+    const int jc = live ? (en.x & kJcMask) : ci;
+    bool inbox = true;
+    int ix[kCS], iy[kCS], iz[kCS];
+    bool iv[kCS];
+#pragma unroll
+    for (int m = 0; m < kCS; ++m) {
+      iv[m] = ci * kCS + m < n;
+      const uint4 u = fix[iv[m] ? ci * kCS + m : ci * kCS];
+      ix[m] = int(u.x), iy[m] = int(u.y), iz[m] = int(u.z);
+      inbox = inbox && u.w != 0u;
+    }
+    unsigned best = 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < kCS / 2; ++k) {
+      const int j = jc * kCS + (lane & 1) * (kCS / 2) + k;
+      const bool vj = j < n;
+      const uint4 u = fix[vj ? j : jc * kCS];
+      inbox = inbox && u.w != 0u;
+#pragma unroll
+      for (int m = 0; m < kCS; ++m) {
+        const int dx = (ix[m] - int(u.x)) >> 16, dy = (iy[m] - int(u.y)) >> 16,
+                  dz = (iz[m] - int(u.z)) >> 16;
+        const unsigned d2 = unsigned(dx * dx) + unsigned(dy * dy) + unsigned(dz * dz);
+        if (vj && iv[m]) best = min(best, d2);
+      }
+    }
+    best = min(best, __shfl_xor_sync(0xffffffffu, best, 1));
+    inbox = __shfl_xor_sync(0xffffffffu, int(inbox), 1) != 0 && inbox;
+    if ((lane & 1) == 0 && inbox && live) {
+      const float g = fmaxf(sqrtf(float(best)) - 2.0f, 0.0f) * (65536.0f * (1.0f - 1e-6f));
+      const float g2 = fmaxf(g * g, __int_as_float(en.w));
+      ent[e].w = __float_as_int(g2);
+    }
+  }
+}
+
 __device__ __forceinline__ double stamp_of(int epoch) { return __longlong_as_double((long long)epoch); }
 
 template <bool MULTI_SPECIES, bool WRAPPED, bool VDERIV>
@@ -905,8 +978,19 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
     if (lane < 2) mbar_init(&mbar[warp][lane], 1);
     __syncwarp();
     unsigned phase = 0u;  // bit p: parity of buffer p's next completion
-    int par = 0;
     const int cw = il < 3 ? il : 2;  // component read by this lane in the transpose
+    // the entry loop's per-lane addresses, kept in registers (opaque to the
+    // compiler, which otherwise re-derives them from the kernel arguments in
+    // every entry): the transpose's write / read slots (buffer 0; buffer 1 is
+    // jt_flip bytes on) and this lane's word of record 0
+    unsigned jt_wr = smem_u32(&jt[warp][0][il * 24 + jl * 3]);
+    unsigned jt_rd = smem_u32(&jt[warp][0][jl * 3 + cw]);
+    unsigned jt_par = 0u;
+    constexpr unsigned jt_flip = 4 * kCS * 3 * sizeof(double);
+    asm volatile("" : "+r"(jt_wr), "+r"(jt_rd));
+    asm volatile("" : "+l"(rec), "+l"(rstamp));
+    // only the partial last cluster has members that do not exist
+    const int last_c = (n & (kCS - 1)) ? n / kCS : -1;
     // batch bt's cull, compaction and copies into buffer p (the surviving
     // j-clusters and the owner's cluster); returns the number of survivors
     // (0: no copies, no mbarrier phase)
@@ -984,10 +1068,12 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
           const double4 pj = jst[p][t][jl];
           const int jc = cur.x & kJcMask, code = cur.x >> kJcBits;
           const int j = jc * kCS + jl;
-          const bool vj = j < n;
-          const bool self = jc == ci;
-          const bool va = iva && vj && (!self || j > ia);
-          const bool vb = ivb && vj && (!self || j > ib);
+          bool va = true, vb = true;
+          if (jc == ci || jc == last_c || ci == last_c) {  // warp-uniform, rare
+            const bool vj = j < n, self = jc == ci;
+            va = iva && vj && (!self || j > ia);
+            vb = ivb && vj && (!self || j > ib);
+          }
           double dxa = sub(pax, pj.x), dya = sub(pay, pj.y), dza = sub(paz, pj.z);
           double dxb = sub(pbx, pj.x), dyb = sub(pby, pj.y), dzb = sub(pbz, pj.z);
           if constexpr (WRAPPED) {
@@ -1015,7 +1101,7 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
           const double r2a = norm2_exact(dxa, dya, dza), r2b = norm2_exact(dxb, dyb, dzb);
           const bool ina = va && r2a < a.rc2, inb = vb && r2b < a.rc2;  // potentials.cpp:161
           if (__ballot_sync(full, ina || inb) == 0u) continue;  // no record: its stamp stays old
-          const int sj = MULTI_SPECIES ? (vj ? s.sp_slot[roff + j] : sia) : 0;
+          const int sj = MULTI_SPECIES ? (j < n ? s.sp_slot[roff + j] : sia) : 0;
           // both rows' terms in one block (two independent dependency chains)
           const double fsa = lj(ina, r2a, sia, sj);
           const double fsb = lj(inb, r2b, sib, sj);
@@ -1033,16 +1119,17 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
           cnt += int(ina) + int(inb);
           // j-side: member jl's 4 row lanes summed in row order through
           // shared memory (lane (jl, c) adds component c), stamped record
-          double* jb = jt[warp][par];
-          par ^= 1;
-          jb[il * 24 + jl * 3] = gx;
-          jb[il * 24 + jl * 3 + 1] = gy;
-          jb[il * 24 + jl * 3 + 2] = gz;
+          sts_f64<0>(jt_wr + jt_par, gx);
+          sts_f64<8>(jt_wr + jt_par, gy);
+          sts_f64<16>(jt_wr + jt_par, gz);
           __syncwarp();
-          const double* jr = jb + jl * 3 + cw;
-          const double res = ((jr[0] + jr[24]) + jr[48]) + jr[72];
-          if (il < 3) rec[size_t(cur.y) * kRecP] = res;
-          if (lane == 0) rstamp[cur.y] = epoch;
+          const unsigned jr = jt_rd + jt_par;
+          jt_par ^= jt_flip;
+          const double res = ((lds_f64<0>(jr) + lds_f64<192>(jr)) + lds_f64<384>(jr)) + lds_f64<576>(jr);
+          if (il < 3)
+            asm volatile("st.global.f64 [%0], %1;" ::"l"(rec + size_t(cur.y) * kRecP), "d"(res) : "memory");
+          if (lane == 0)
+            asm volatile("st.global.u32 [%0], %1;" ::"l"(rstamp + cur.y), "r"(epoch) : "memory");
         }
         if (dirty) {  // the batch's i-side record (rows ia / ib: 8 jl lanes, xor tree)
 #pragma unroll

@@ -438,6 +438,8 @@ int nl_build(b2md_ctx* c) {
     PROF(c, F_NL_BUILD, (k_nl_zfill<<<g, bs, 0, c->stream>>>(nl, c->nc)));
   else
     PROF(c, F_NL_BUILD, (k_nl_inrec<<<g, bs, 0, c->stream>>>(nl, c->nc)));
+  if (c->nl_member_gaps)
+    PROF(c, F_NL_BUILD, (k_nl_gaps<<<dim3(c->n3_grid * 2, c->R), bs, 0, c->stream>>>(ca, nl)));
   c->steps_since_nl = 0;
   return B2MD_OK;
 }
@@ -1356,6 +1358,8 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
       c->nl_interval = 20;
       if (const char* e = std::getenv("B2MD_NL_SKIN")) c->nl_skin = std::max(0.0, std::atof(e));
       if (const char* e = std::getenv("B2MD_NL_INTERVAL")) c->nl_interval = std::max(0, std::atoi(e));
+      // member-pair build gaps (k_nl_gaps); 0: the arcs' bound only (measurement)
+      if (const char* e = std::getenv("B2MD_NL_GAPS")) c->nl_member_gaps = std::atoi(e) != 0;
       const double rs = (std::sqrt(c->t.rc2) + c->nl_skin) * 4294967296.0 / c->t.box;
       nl.lim_build = float(rs * rs * (1.0 + 1e-5));
       nl.skin_half = float(0.5 * c->nl_skin * 4294967296.0 / c->t.box + 64.0);
