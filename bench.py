@@ -818,9 +818,14 @@ def main():
     # candidate pair itself (partner search fused into the LJ kernel), so its
     # algorithmic work is the search's plus the forces'
     fused_search = single_site and kt_search.get("search", (0.0, 0))[1] == 0
+    nlist = eng.nlist_info() if fused_search else {"active": 0}
     if fused_search:
         force_flop = cand * FLOP_CANDIDATE + pairs_total * FLOP_LJ_SINGLE
-        force_note = (f"k_force_cpair: partner search fused with LJ; {FLOP_CANDIDATE} flop per "
+        walk = ("k_force_nl: once-per-pair cluster-pair list (each pair evaluated once, partner-side "
+                "sums written to per-entry records; the fixed-order record reduction k_nl_reduce is "
+                "timed apart as force_jsum)" if nlist["active"] else
+                "k_force_cpair: both-rows cluster walk")
+        force_note = (f"{walk}; partner search fused with LJ; {FLOP_CANDIDATE} flop per "
                       f"candidate pair i<j decided + {FLOP_LJ_SINGLE} per pair in cutoff")
     elif single_site:
         force_flop = pairs_total * FLOP_LJ_SINGLE
@@ -907,9 +912,13 @@ def main():
         "search": ({
             "launch_ms": None,
             "candidates": cand,
-            "note": "fused into the force kernel (cluster walk): clusters of 8 slots whose bounding "
-                    "arcs are > rc apart are skipped (exact); the rest are decided on the "
-                    "reference's fp64 r2 per pair",
+            "note": "fused into the force kernel: cluster pairs (8 x 8 slots) that are provably > rc "
+                    "apart are skipped (bounding arcs / member distances at the list build less the "
+                    "displacement since, exact); the rest are decided on the reference's fp64 r2 "
+                    "per pair",
+            "pair_list": ({"entries": nlist["entries"], "rebuild_interval": nlist["interval"],
+                           "skin": nlist["skin_e6"] * 1e-6, "stale": bool(nlist["stale"])}
+                          if nlist["active"] else None),
         } if fused_search else {
             "launch_ms": avg_search_s * 1e3,
             "share_of_step": avg_search_s / max(1e-12, step_s),

@@ -556,7 +556,10 @@ constexpr int kNLWarps = 4;       // warps per CTA of k_force_nl
 #define B2MD_NL_MINBLOCKS 5
 #endif
 constexpr int kNLMinBlocks = B2MD_NL_MINBLOCKS;  // 20 warps per SM (<= 96 registers)
-constexpr int kB = 16;            // entries per batch (one owner)
+#ifndef B2MD_NL_BATCH
+#define B2MD_NL_BATCH 16
+#endif
+constexpr int kB = B2MD_NL_BATCH;  // entries per batch (one owner)
 #ifndef B2MD_NL_TMA
 #define B2MD_NL_TMA 0             // stage by bulk (TMA) copies instead of per-lane cp.async
 #endif
@@ -851,9 +854,11 @@ static __global__ void __launch_bounds__(kNLBuildWarps * 32) k_nl_gaps(ClusterAr
   const int nbt = ctl[kNLEntries] / kB;
   int4* __restrict__ ent = nl.ent + size_t(r) * nl.max_ent;
   const uint4* __restrict__ fix = ca.fixpos + size_t(r) * n;
-  static_assert(kB * 2 == 32 && kCS == 8, "two lanes per entry");
+  constexpr int kLPE = 32 / kB;       // lanes per entry
+  constexpr int kJPL = kCS / kLPE;    // j-members per lane
+  static_assert(kB * kLPE == 32 && kJPL * kLPE == kCS, "whole entries per warp, whole members per lane");
   for (int bt = blockIdx.x * kNLBuildWarps + warp; bt < nbt; bt += gridDim.x * kNLBuildWarps) {
-    const int e = bt * kB + (lane >> 1);
+    const int e = bt * kB + lane / kLPE;
     const int4 en = ent[e];
     const int ci = en.y;
     // padding entries never pass the cull and a cluster's own entry has gap 0
@@ -871,8 +876,8 @@ static __global__ void __launch_bounds__(kNLBuildWarps * 32) k_nl_gaps(ClusterAr
     }
     unsigned best = 0xffffffffu;
 #pragma unroll
-    for (int k = 0; k < kCS / 2; ++k) {
-      const int j = jc * kCS + (lane & 1) * (kCS / 2) + k;
+    for (int k = 0; k < kJPL; ++k) {
+      const int j = jc * kCS + (lane % kLPE) * kJPL + k;
       const bool vj = j < n;
       const uint4 u = fix[vj ? j : jc * kCS];
       inbox = inbox && u.w != 0u;
@@ -884,9 +889,12 @@ static __global__ void __launch_bounds__(kNLBuildWarps * 32) k_nl_gaps(ClusterAr
         if (vj && iv[m]) best = min(best, d2);
       }
     }
-    best = min(best, __shfl_xor_sync(0xffffffffu, best, 1));
-    inbox = __shfl_xor_sync(0xffffffffu, int(inbox), 1) != 0 && inbox;
-    if ((lane & 1) == 0 && inbox && live) {
+#pragma unroll
+    for (int o = 1; o < kLPE; o <<= 1) {
+      best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+      inbox = __shfl_xor_sync(0xffffffffu, int(inbox), o) != 0 && inbox;
+    }
+    if (lane % kLPE == 0 && inbox && live) {
       const float g = fmaxf(sqrtf(float(best)) - 2.0f, 0.0f) * (65536.0f * (1.0f - 1e-6f));
       const float g2 = fmaxf(g * g, __int_as_float(en.w));
       ent[e].w = __float_as_int(g2);
@@ -1194,13 +1202,42 @@ static __global__ void __launch_bounds__(kNLBuildWarps * 32)
   const size_t roff = size_t(r) * n;
   const int slot = c * kCS + m;
   const int* ctl = nl.ctl + size_t(r) * kNLCtl;
-  if (!nl_stale(nl, ctl)) {
+  // the end-of-step kick's inputs (engine.cpp:131-142, kick_one) are fetched by
+  // the 8 member lanes before the record loop, so their (dependent, scattered)
+  // round trips overlap the records'
+  const bool kicker = q == 0 && slot < n && a.kick_dt > 0.0;
+  size_t ke = 0;
+  bool kpoint = false, kfrozen = false;
+  double kv[3] = {0, 0, 0}, kp[3] = {0, 0, 0}, kw[3] = {0, 0, 0}, kqw = 0, kmass = 1.0;
+  if (kicker) {
+    ke = roff + ext_of(a.st.pos4[roff + slot]);
+    const DevSpecies& sp = a.s.tab->species[a.s.ns == 1 ? 0 : a.s.species_of[ke - roff]];
+    kpoint = sp.rotational_dof == 0;
+    kmass = sp.total_mass;
+    kfrozen = *a.error_mol != 0x7fffffff;
+    kv[0] = a.st.vx[ke], kv[1] = a.st.vy[ke], kv[2] = a.st.vz[ke];
+    kp[0] = a.st.px[ke], kp[1] = a.st.py[ke], kp[2] = a.st.pz[ke];
+    kw[0] = a.st.wx[ke], kw[1] = a.st.wy[ke], kw[2] = a.st.wz[ke];
+    kqw = a.st.qw[ke];
+  }
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  const bool listed = !nl_stale(nl, ctl);
+  if (listed) {
     const long long epoch = ctl[kNLEpoch] - 1;  // advanced by the force kernel's last CTA
     const int* eb = nl.ebase + size_t(r) * (nc + 1);
     const double* __restrict__ irec = nl.irec + size_t(r) * (nl.max_ent / kB) * kRecD + 4 * m;
     const double* __restrict__ rec = nl.rec + size_t(r) * nl.max_ent * kRecP + 3 * m;
     const int* __restrict__ rstamp = nl.rstamp + size_t(r) * nl.max_ent;
-    double fx = 0.0, fy = 0.0, fz = 0.0;
+    // the stamps of the first span are requested before the i-side records
+    // are waited for (independent round trips)
+    constexpr int kSpan = 256;
+    const int i0 = nl.ibase[size_t(r) * (nc + 1) + c], i1 = nl.ibase[size_t(r) * (nc + 1) + c + 1];
+    int st[kSpan / 32];
+#pragma unroll
+    for (int j = 0; j < kSpan / 32; ++j) {
+      const int t = i0 + 32 * j + lane;
+      st[j] = t < i1 ? rstamp[t] : -1;
+    }
     {  // the batches' i-side records: batch b by group (b - first) % 4, 8 in flight
       const int b0 = eb[c] / kB, b1 = eb[c + 1] / kB;
       for (int bb = b0; bb < b1; bb += 8) {
@@ -1216,19 +1253,18 @@ static __global__ void __launch_bounds__(kNLBuildWarps * 32)
           if (__double_as_longlong(u[h].w) == epoch) fx += u[h].x, fy += u[h].y, fz += u[h].z;
       }
     }
-    const int i1 = nl.ibase[size_t(r) * (nc + 1) + c + 1];
     // the stamps of up to 256 slots at once (one round trip) compacted into
     // the warp's list of stamped slots (slot order), then only the stamped
     // payloads: the k-th listed slot by group k % 4, 16 payloads in flight
-    constexpr int kSpan = 256;
     __shared__ int slist[kNLBuildWarps][kSpan];
     int* sl = slist[warp];
-    for (int s0 = nl.ibase[size_t(r) * (nc + 1) + c]; s0 < i1; s0 += kSpan) {
-      int st[kSpan / 32];
+    for (int s0 = i0; s0 < i1; s0 += kSpan) {
+      if (s0 != i0) {
 #pragma unroll
-      for (int j = 0; j < kSpan / 32; ++j) {
-        const int t = s0 + 32 * j + lane;
-        st[j] = t < i1 ? rstamp[t] : -1;
+        for (int j = 0; j < kSpan / 32; ++j) {
+          const int t = s0 + 32 * j + lane;
+          st[j] = t < i1 ? rstamp[t] : -1;
+        }
       }
       int cnt = 0;
 #pragma unroll
@@ -1269,7 +1305,23 @@ static __global__ void __launch_bounds__(kNLBuildWarps * 32)
     }
   }
   __syncwarp();
-  if (q == 0 && slot < n && a.kick_dt > 0.0) fused_kick(a, roff + ext_of(a.st.pos4[roff + slot]));
+  if (kicker && !kfrozen) {
+    if (!kpoint) {  // rigid rotor terms: the general kick
+      fused_kick(a, ke);
+    } else {
+      if (!listed) fx = a.st.fx[ke], fy = a.st.fy[ke], fz = a.st.fz[ke];  // the exact walk's rows
+      const double cm = __ddiv_rn(mul(0.5, a.kick_dt), kmass);
+      const double vx = add(kv[0], mul(fx, cm)), vy = add(kv[1], mul(fy, cm)),
+                   vz = add(kv[2], mul(fz, cm));
+      a.st.vx[ke] = vx;
+      a.st.vy[ke] = vy;
+      a.st.vz[ke] = vz;
+      const bool ok = isfinite(kp[0]) && isfinite(kp[1]) && isfinite(kp[2]) && isfinite(vx) &&
+                      isfinite(vy) && isfinite(vz) && isfinite(kw[0]) && isfinite(kw[1]) &&
+                      isfinite(kw[2]) && isfinite(kqw);
+      if (!ok) atomicMin(a.error_mol, int(ke));
+    }
+  }
 }
 
 // heat_flux (greenkubo.cpp:182-266) of a single-species, centred, LJ-only

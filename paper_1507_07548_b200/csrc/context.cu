@@ -1303,7 +1303,7 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     TRY(dalloc(&c->d_cta_part, size_t(R) * kNumRowScalars *
                                    std::max({c->force_grid, c->nc > 0 ? cpair_grid(c) : 0,
-                                             c->nc > 0 ? sms * kNLMinBlocks : 0,
+                                             c->nc > 0 ? sms * kNLMinBlocks * 8 : 0,
                                              (((c->t.n + 31) / 32) * ((c->t.n + 31) / 32 + 1) / 2 *
                                                   kTileSplit + kTileWarps - 1) / kTileWarps})));
   }
@@ -1322,14 +1322,18 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
     if (size_t(R) * max_ent * kRecP * sizeof(double) > (size_t(8) << 30))
       c->use_newton = false;
     if (c->use_newton) {
-      // the end-of-step kick rides with the next step's drift
-      // (k_step_drift_arcs<true>): the reduce then only writes forces
-      c->use_fused_kick = false;
+      // the end-of-step kick runs in k_nl_reduce (its inputs fetched ahead of
+      // the record loop); B2MD_FUSED_KICK=0: with the next step's drift
+      // (k_step_drift_arcs<true>) / a k_kick launch at the end of a run
+      c->use_fused_kick = true;
       if (const char* e = std::getenv("B2MD_FUSED_KICK")) c->use_fused_kick = std::atoi(e) != 0;
       NListArgs& nl = c->nl;
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
       c->n3_grid = sms * kNLMinBlocks;
+      // (measurement) more CTAs than resident slots: the hardware deals them as slots free up
+      if (const char* e = std::getenv("B2MD_NL_GRIDMUL"))
+        c->n3_grid *= std::max(1, std::min(8, std::atoi(e)));
       nl.max_ent = int(max_ent);
       TRY(dalloc(&nl.rec, size_t(R) * max_ent * kRecP));
       TRY(dalloc(&nl.rstamp, size_t(R) * max_ent));
@@ -1355,7 +1359,7 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
       CU(cudaMemcpy(nl.ctl, ctl.data(), sizeof(int) * ctl.size(), cudaMemcpyHostToDevice));
       // skin and scheduled rebuild interval (B2MD_NL_SKIN, B2MD_NL_INTERVAL)
       c->nl_skin = 1.0;
-      c->nl_interval = 20;
+      c->nl_interval = 15;
       if (const char* e = std::getenv("B2MD_NL_SKIN")) c->nl_skin = std::max(0.0, std::atof(e));
       if (const char* e = std::getenv("B2MD_NL_INTERVAL")) c->nl_interval = std::max(0, std::atoi(e));
       // member-pair build gaps (k_nl_gaps); 0: the arcs' bound only (measurement)

@@ -144,7 +144,7 @@ struct b2md_ctx {
   float4* d_shalf = nullptr;  // R * nsup
   // once-per-pair cluster-pair list (k_force_nl + k_nl_reduce, cluster.cuh)
   bool nl_member_gaps = true;  // k_nl_gaps after every list build
-  bool use_newton = false;     // B2MD_NEWTON=1 (measured slower on cfg3 so far: DESIGN 5)
+  bool use_newton = true;      // once-per-pair list on the cluster path (B2MD_NEWTON=0: both-rows walk)
   NListArgs nl{};              // device arrays of the list (null: not allocated)
   double nl_skin = 0.0;        // list skin (length units)
   int nl_interval = 0;         // steps between scheduled builds (0: only at staging / re-sort)
