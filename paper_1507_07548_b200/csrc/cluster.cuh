@@ -1027,12 +1027,13 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
         elist[warp][p][t] = make_int2(en.x, en.z);
       }
       __syncwarp();
-      const unsigned dst = smem_u32(jst[p]);
-      for (int q = lane; q < (na + 1) * 16; q += 32) {
-        const int t = q >> 4;
+      // lane = (half h = lane >> 4, 16-byte chunk k = lane & 15): survivor t's 256 bytes
+      // by the 16 lanes of half t & 1, the owner's by half na & 1
+      const unsigned dst = smem_u32(jst[p]) + 16 * (lane & 15);
+      const char* src = reinterpret_cast<const char*>(p4) + 16 * (lane & 15);
+      for (int t = lane >> 4; t <= na; t += 2) {
         const int jc = t < na ? (elist[warp][p][t].x & kJcMask) : owner;
-        const char* src = reinterpret_cast<const char*>(p4 + size_t(jc) * kCS) + 16 * (q & 15);
-        cp_async16(dst + (t < na ? t : kB) * 256 + 16 * (q & 15), src);
+        cp_async16(dst + (t < na ? t : kB) * 256, src + size_t(jc) * (kCS * sizeof(double4)));
       }
       cp_async_commit();
 #endif
@@ -1085,21 +1086,20 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
           double dxa = sub(pax, pj.x), dya = sub(pay, pj.y), dza = sub(paz, pj.z);
           double dxb = sub(pbx, pj.x), dyb = sub(pby, pj.y), dzb = sub(pbz, pj.z);
           if constexpr (WRAPPED) {
-            if (code) {  // warp-uniform
-              if (code & (code >> 1) & 0x15) {  // some axis per pair: the per-pair image on all
-                const float thr = a.thr;
-                const double negL = s.mi.negL;
-                dxa = min_image_wrapped(dxa, negL, thr), dya = min_image_wrapped(dya, negL, thr);
-                dza = min_image_wrapped(dza, negL, thr), dxb = min_image_wrapped(dxb, negL, thr);
-                dyb = min_image_wrapped(dyb, negL, thr), dzb = min_image_wrapped(dzb, negL, thr);
-              } else {  // uniform images: d -+ L (a 0.0 shift leaves d as it is)
-                const int cx = code & 3, cy = (code >> 2) & 3, cz = code >> 4;
-                const double sx = cx == 0 ? 0.0 : (cx == 1 ? -L : L);
-                const double sy = cy == 0 ? 0.0 : (cy == 1 ? -L : L);
-                const double sz = cz == 0 ? 0.0 : (cz == 1 ? -L : L);
-                dxa = add(dxa, sx), dya = add(dya, sy), dza = add(dza, sz);
-                dxb = add(dxb, sx), dyb = add(dyb, sy), dzb = add(dzb, sz);
-              }
+            if (code) {  // warp-uniform; per axis: 3 the per-pair image, 1 / 2 one add of -+L
+              const float thr = a.thr;
+              const double negL = s.mi.negL;
+              auto image = [&](int c, double& da, double& db) {
+                if (c == 3) {
+                  da = min_image_wrapped(da, negL, thr), db = min_image_wrapped(db, negL, thr);
+                } else if (c) {
+                  const double sh = c == 1 ? negL : L;
+                  da = add(da, sh), db = add(db, sh);
+                }
+              };
+              image(code & 3, dxa, dxb);
+              image((code >> 2) & 3, dya, dyb);
+              image(code >> 4, dza, dzb);
             }
           } else {
             const MinImage mi = s.mi;
