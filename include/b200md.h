@@ -229,8 +229,8 @@ int b2md_set_sort_interval(b2md_ctx* ctx, int steps);
 int b2md_get_sort_interval(const b2md_ctx* ctx, int* steps, int* steps_since_sort);
 
 /* The once-per-pair cluster-pair list of the single-site cluster path
- * (no reference counterpart: diagnostics for tests and
- * measurement).  info[0] = 1 when the list path is active (else all 0),
+ * (the default walk of single-site systems with rc < 0.3 L;
+ * no reference counterpart: diagnostics for tests and measurement).  info[0] = 1 when the list path is active (else all 0),
  * info[1] = entries (owned cluster pairs) of `replica`, info[2] = incoming
  * record slots, info[3] = 1 when the list is stale (a molecule moved more than
  * skin / 2 since the build: the exact per-step walk runs until the next

@@ -5,8 +5,10 @@ written by the unmodified reference (tests/golden/ckpt.npz) and the oracle.
 * a GPU engine after set_state writes the reference's bytes exactly;
 * a restored reference checkpoint gives the file's state bit for bit, forces
   equal to the oracle's on it, and re-emits the same bytes;
-* restart is bit-exact (the summation order is fixed when the spatial order
-  is; with periodic re-sorting it agrees to rounding)."""
+* restart is bit-exact where the summation order is a function of the state
+  alone (fixed spatial order, row / both-rows walks); with periodic re-sorting
+  or the once-per-pair list (rebuilt from the restored positions) it agrees to
+  rounding."""
 from __future__ import annotations
 
 from pathlib import Path

@@ -808,7 +808,7 @@ def test_pinned_and_pageable_transfers_agree(cfg):
 # k_nl_count/scan/fill/inrec + k_force_nl + k_nl_reduce (csrc/cluster.cuh): each
 # pair evaluated once from a cluster-pair list with a skin, partner
 # contributions through the per-pair record buffer and a fixed-order
-# reduction (B2MD_NEWTON=1; the both-rows walk is the default).
+# reduction (B2MD_NEWTON=1, the default; the env pins it for these cases).
 @pytest.mark.parametrize("n", [1, 2, 7, 9, 100, 1537, 4100])
 def test_newton_walk_sizes(monkeypatch, n):
     monkeypatch.setenv("B2MD_CLUSTER", "2")
