@@ -995,7 +995,8 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
     unsigned jt_rd = smem_u32(&jt[warp][0][jl * 3 + cw]);
     unsigned jt_par = 0u;
     constexpr unsigned jt_flip = 4 * kCS * 3 * sizeof(double);
-    asm volatile("" : "+r"(jt_wr), "+r"(jt_rd));
+    unsigned jt_wr0 = smem_u32(&jt[warp][0][0]);
+    asm volatile("" : "+r"(jt_wr), "+r"(jt_rd), "+r"(jt_wr0));
     asm volatile("" : "+l"(rec), "+l"(rstamp));
     // only the partial last cluster has members that do not exist
     const int last_c = (n & (kCS - 1)) ? n / kCS : -1;
@@ -1139,20 +1140,35 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
           if (lane == 0)
             asm volatile("st.global.u32 [%0], %1;" ::"l"(rstamp + cur.y), "r"(epoch) : "memory");
         }
-        if (dirty) {  // the batch's i-side record (rows ia / ib: 8 jl lanes, xor tree)
-#pragma unroll
-          for (int o = 4; o < 32; o <<= 1) {
-            fax += __shfl_xor_sync(full, fax, o);
-            fay += __shfl_xor_sync(full, fay, o);
-            faz += __shfl_xor_sync(full, faz, o);
-            fbx += __shfl_xor_sync(full, fbx, o);
-            fby += __shfl_xor_sync(full, fby, o);
-            fbz += __shfl_xor_sync(full, fbz, o);
-          }
-          if (lane < 4) {  // members il and il + 4: (x, y, z, stamp)
-            double* q = nl.irec + (size_t(r) * (nl.max_ent / kB) + bt) * kRecD;
-            *reinterpret_cast<double4*>(q + 4 * il) = make_double4(fax, fay, faz, stamp);
-            *reinterpret_cast<double4*>(q + 4 * (il + 4)) = make_double4(fbx, fby, fbz, stamp);
+        if (dirty) {
+          // the batch's i-side record: rows ia / ib summed over their 8 jl lanes
+          // in jl order through the (idle) transpose buffers, laid out
+          // [component][lane]; lane (member m, component c) adds and stores
+          // one word, lanes 24..31 the members' stamps
+          static_assert(2 * 4 * kCS * 3 >= 6 * 32, "transpose buffers hold 6 words per lane");
+          __syncwarp();  // the last entry's transpose reads are complete
+          sts_f64<0>(jt_wr0 + 8 * lane, fax);
+          sts_f64<256>(jt_wr0 + 8 * lane, fay);
+          sts_f64<512>(jt_wr0 + 8 * lane, faz);
+          sts_f64<768>(jt_wr0 + 8 * lane, fbx);
+          sts_f64<1024>(jt_wr0 + 8 * lane, fby);
+          sts_f64<1280>(jt_wr0 + 8 * lane, fbz);
+          __syncwarp();
+          double* q = nl.irec + (size_t(r) * (nl.max_ent / kB) + bt) * kRecD;
+          if (lane < 24) {
+            const int m = lane / 3, c = lane - 3 * m;
+            const unsigned src = jt_wr0 + 256 * ((m >> 2) * 3 + c) + 8 * (m & 3);
+            double sum = lds_f64<0>(src);
+            sum += lds_f64<32>(src);
+            sum += lds_f64<64>(src);
+            sum += lds_f64<96>(src);
+            sum += lds_f64<128>(src);
+            sum += lds_f64<160>(src);
+            sum += lds_f64<192>(src);
+            sum += lds_f64<224>(src);
+            q[4 * m + c] = sum;
+          } else {
+            q[4 * (lane - 24) + 3] = stamp;
           }
         }
       }
