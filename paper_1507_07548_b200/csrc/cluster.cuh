@@ -1186,15 +1186,10 @@ __global__ void __launch_bounds__(kNLWarps * 32, kNLMinBlocks)
   double v[kNumRowScalars] = {A12 - A6, 0.0, 0.0, VDERIV ? s1 : 0.0,
                               VDERIV ? 156.0 * A12 - 42.0 * A6 : 0.0, -s1,
                               warp_sum(double(cnt))};
-  finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0);
-  // the last CTA advances the epoch: k_nl_reduce reads the stamps of this one
-  __shared__ bool lastcta;
-  if (threadIdx.x == 0) lastcta = atomicAdd(ctl + kNLTicket, 1) == int(gridDim.x) - 1;
-  __syncthreads();
-  if (lastcta && threadIdx.x == 0) {
+  // the last CTA (the scalars' ticket) advances the epoch: k_nl_reduce reads
+  // the stamps of this one
+  if (finalize_scalars<kNumRowScalars>(v, a.cta_part, a.ticket, a.sums, r, 0) && threadIdx.x == 0)
     ctl[kNLEpoch] = epoch + 1;
-    ctl[kNLTicket] = 0;
-  }
 }
 
 // The fixed-order reduction of the contribution records: one warp per

@@ -673,8 +673,9 @@ __device__ __forceinline__ double rcp_nr(double x) {
 
 // Per-CTA scalar partials -> one fixed-order total per replica, done by the
 // last CTA to finish (integer ticket; no floating-point atomics).
+// Returns true on the last CTA (all its threads), false elsewhere.
 template <int NS>
-__device__ void finalize_scalars(const double* v /* NS values, valid on lane 0 of each warp */,
+__device__ bool finalize_scalars(const double* v /* NS values, valid on lane 0 of each warp */,
                                  double* cta_part, unsigned* ticket, double* sums, int r,
                                  int sum_offset) {
   __shared__ double red[kForceWarps][NS];
@@ -689,12 +690,15 @@ __device__ void finalize_scalars(const double* v /* NS values, valid on lane 0 o
     double t = 0.0;
     for (int w = 0; w < nw; ++w) t += red[w][threadIdx.x];
     cta_part[(size_t(r) * NS + threadIdx.x) * nblk + blockIdx.x] = t;
+    // release: the writers' stores precede the ticket (only they fence: a
+    // fence also waits for the thread's other outstanding stores -- the
+    // walks' record / force stores -- which the kernel boundary orders)
+    __threadfence();
   }
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(&ticket[r], 1u) == unsigned(nblk - 1);
   __syncthreads();
-  if (!last) return;
+  if (!last) return false;
   __threadfence();
   // fixed-order totals: every thread sums its strided slice of all NS
   // columns at once (__ldcg: L2, not a possibly stale L1; all loads in
@@ -721,6 +725,7 @@ __device__ void finalize_scalars(const double* v /* NS values, valid on lane 0 o
     sums[size_t(r) * kNumSums + sum_offset + threadIdx.x] = tt;
   }
   if (threadIdx.x == 0) ticket[r] = 0u;  // re-armed for the next launch / graph replay
+  return true;
 }
 
 // ------------------------------------------------------- single-site forces
