@@ -593,6 +593,7 @@ EwaldArgs ewald_args(b2md_ctx* c) {
   a.sums = sums_ptr(c);
   a.nk_total = int(c->t.kv.size());
   a.two_pi_over_L = 2.0 * 3.14159265358979323846 / c->t.box;
+  a.frec = nullptr;
   return a;
 }
 
@@ -642,7 +643,10 @@ int launch_ewald_sk(b2md_ctx* c, cudaStream_t st) {
   return B2MD_OK;
 }
 
-int launch_ewald_force(b2md_ctx* c) {
+// side == false: after the real-space kernel on c->stream, added to its
+// totals; side == true: on the Ewald branch stream beside it, written to
+// d_frec (ewald_overlap: the end-of-step kick adds the two)
+int launch_ewald_force(b2md_ctx* c, bool side) {
   EwaldArgs a = ewald_args(c);
   if (a.nk == 0) return B2MD_OK;
   if (c->ew_tiled) {
@@ -662,6 +666,12 @@ int launch_ewald_force(b2md_ctx* c) {
   while (8 % P) --P;
   a.kparts = P;
   const int mpc = 8 / P;
+  if (side) {
+    a.frec = c->d_frec;
+    k_ewald_force<<<dim3((c->t.n + mpc - 1) / mpc, c->R), 256, 0, c->stream2>>>(a);
+    CU(cudaGetLastError());
+    return B2MD_OK;
+  }
   PROF(c, F_EWALD_F,
        (k_ewald_force<<<dim3((c->t.n + mpc - 1) / mpc, c->R), 256, 0, c->stream>>>(a)));
   return B2MD_OK;
@@ -670,7 +680,16 @@ int launch_ewald_force(b2md_ctx* c) {
 int launch_ewald(b2md_ctx* c) {
   if (!c->t.ewald || c->nq == 0) return B2MD_OK;
   TRY(launch_ewald_sk(c, c->stream));
-  return launch_ewald_force(c);
+  return launch_ewald_force(c, false);
+}
+
+// The reciprocal forces can be computed beside the real-space kernel (they
+// read S(k) and the phase tables only) when an end-of-step kick follows that
+// adds them: step paths, one rank (the all-reduce unit is the force array),
+// the gather form of the kernel, not while kernels are being timed.
+bool ewald_overlap(const b2md_ctx* c) {
+  return c->engine && c->t.ewald && c->nq > 0 && c->k_end > c->k_begin && !c->profile && c->stream2 &&
+         c->d_frec && c->ew_overlap && !c->ew_tiled && !(c->world > 1 && c->comm);
 }
 
 int launch_allreduce(b2md_ctx* c) {
@@ -747,7 +766,7 @@ bool sort_due(const b2md_ctx* c) {
 }
 
 // ForceField::evaluate (src/parallel.cpp:79-122) on the device state.
-int enqueue_forces(b2md_ctx* c, bool offsets, bool kick) {
+int enqueue_forces(b2md_ctx* c, bool offsets, bool kick, bool recip_beside) {
   if (offsets) {  // evaluate / set_state path: the integrator did not refresh these
     TRY(launch_offsets(c));
     const int nt = n_total(c);
@@ -766,13 +785,14 @@ int enqueue_forces(b2md_ctx* c, bool offsets, bool kick) {
     CU(cudaEventRecord(c->ev_fork, c->stream));
     CU(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
     TRY(launch_ewald_sk(c, c->stream2));
+    if (recip_beside) TRY(launch_ewald_force(c, true));
     CU(cudaEventRecord(c->ev_join, c->stream2));
   }
   if (!cluster_path(c) && !tile_path(c)) TRY(launch_search(c));
   TRY(launch_force(c, kick));
   if (fork) {
     CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-    TRY(launch_ewald_force(c));
+    if (!recip_beside) TRY(launch_ewald_force(c, false));
   } else {
     TRY(launch_ewald(c));
   }
@@ -798,8 +818,9 @@ StepArgs step_args(b2md_ctx* c) {
 // first of step s+1 share one launch), or, when the kick fuses into the force
 // kernel (kick_fusable),
 //   kick_drift, [forces+kick, kick_drift] x (k-1), forces+kick.
-int launch_step_kernel(b2md_ctx* c, int fam) {
+int launch_step_kernel(b2md_ctx* c, int fam, bool add_recip = false) {
   StepArgs a = step_args(c);
+  if (add_recip) a.frec = c->d_frec;  // (F_KICK, F_KICK_KICK_DRIFT: the end-of-step kick)
   const int nt = n_total(c);
   // small CTAs: 16k molecules must still spread over all 148 SMs
   const int bs = 64, g = (nt + bs - 1) / bs;
@@ -822,16 +843,18 @@ int launch_step_kernel(b2md_ctx* c, int fam) {
 
 int enqueue_loop_body(b2md_ctx* c) {
   const bool fused = kick_fusable(c);
-  TRY(enqueue_forces(c, false, fused));
-  TRY(launch_step_kernel(c, fused ? F_KICK_DRIFT : F_KICK_KICK_DRIFT));
+  const bool beside = !fused && ewald_overlap(c);
+  TRY(enqueue_forces(c, false, fused, beside));
+  TRY(launch_step_kernel(c, fused ? F_KICK_DRIFT : F_KICK_KICK_DRIFT, beside));
   return B2MD_OK;
 }
 
 // forces + the end-of-step half kick
 int enqueue_forces_and_kick(b2md_ctx* c) {
   const bool fused = kick_fusable(c);
-  TRY(enqueue_forces(c, false, fused));
-  if (!fused) TRY(launch_step_kernel(c, F_KICK));
+  const bool beside = !fused && ewald_overlap(c);
+  TRY(enqueue_forces(c, false, fused, beside));
+  if (!fused) TRY(launch_step_kernel(c, F_KICK, beside));
   return B2MD_OK;
 }
 
@@ -1502,6 +1525,10 @@ int create_impl(int device, const b2md_composition* comp, const b2md_ff_options*
       TRY(dalloc(&c->d_ewSp, size_t(R) * nch * std::max<size_t>(kv.size(), 1)));
       TRY(dalloc(&c->d_ewfq, size_t(R) * std::max(c->nq, 1) * 3));
     }
+    // reciprocal forces / torques written beside the real-space kernel in the
+    // step paths (ewald_overlap; B2MD_EWALD_OVERLAP=0: after it, added in place)
+    if (c->nq > 0) TRY(dalloc(&c->d_frec, size_t(6) * R * t.n));
+    if (const char* e = std::getenv("B2MD_EWALD_OVERLAP")) c->ew_overlap = std::atoi(e) != 0;
   }
   c->rank = 0;
   c->world = 1;
@@ -1528,7 +1555,7 @@ void free_ctx(b2md_ctx* c) {
                   c->d_uk,    c->d_flux,  c->d_perm, c->d_slot_of, c->d_sp_slot, c->d_sb_slot,
                   c->d_nsites_slot, c->d_scan, c->d_keys[0], c->d_keys[1], c->d_vals[0],
                   c->d_vals[1], c->d_cub, c->d_ke, c->d_thermo_err, c->d_carc,
-                  c->d_chalf, c->d_sarc, c->d_shalf, c->d_trec, c->d_ewSp, c->d_ewfq, c->nl.rec, c->nl.irec,
+                  c->d_chalf, c->d_sarc, c->d_shalf, c->d_trec, c->d_ewSp, c->d_ewfq, c->d_frec, c->nl.rec, c->nl.irec,
                   c->nl.ocnt, c->nl.icnt, c->nl.ebase, c->nl.ibase, c->nl.ent,
                   c->nl.in_src, c->nl.fixref, c->nl.rstamp, c->nl.smap, c->nl.ocp, c->nl.icp,
                   c->nl.ctl};

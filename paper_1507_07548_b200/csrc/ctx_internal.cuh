@@ -178,6 +178,8 @@ struct b2md_ctx {
   bool ew_tiled = false;        // tiled S(k) / force kernels (B2MD_EWALD_TILED=0: gather form)
   double2* d_ewSp = nullptr;    // R * chunks * nk: S(k) partials
   double* d_ewfq = nullptr;     // R * nq * 3: reciprocal force per charge
+  double* d_frec = nullptr;     // 6 * R * n: reciprocal forces / torques (ewald_overlap)
+  bool ew_overlap = true;       // k_ewald_force beside the real-space kernel in step paths
   double* d_flux = nullptr;  // R * kNumSums: heat flux totals
   double2* d_ke = nullptr;    // R: (kinetic_energy_trans, kinetic_energy_rot)
   int* d_thermo_err = nullptr;  // R: thermostat failure code (0 ok)
@@ -249,7 +251,7 @@ ForceArgs force_args(b2md_ctx* c);
 bool fast_min_image(const b2md_ctx* c);
 int resort(b2md_ctx* c);
 int resort_and_stage(b2md_ctx* c);
-int enqueue_forces(b2md_ctx* c, bool offsets, bool kick = false);
+int enqueue_forces(b2md_ctx* c, bool offsets, bool kick = false, bool recip_beside = false);
 int run_steps(b2md_ctx* c, int64_t nsteps);
 int upload_aos(b2md_ctx* c, int slot, const double* host, int width, double* d0, double* d1,
                double* d2, double* d3);

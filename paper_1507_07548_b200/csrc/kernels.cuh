@@ -1654,6 +1654,10 @@ struct EwaldArgs {
   int nk_total;
   int kparts;           // warps per molecule in k_ewald_force (1, 2, 4, 8)
   double two_pi_over_L;
+  // k_ewald_force's output: null: added to the (complete) real-space totals;
+  // else written (=) to frec[6][R n] -- the kernel then runs beside the
+  // real-space kernel and the end-of-step kick adds the two (StepArgs::frec)
+  double* frec;
 };
 
 static __global__ void k_ewald_tables(EwaldArgs a) {
@@ -1780,14 +1784,20 @@ static __global__ void __launch_bounds__(256) k_ewald_force(EwaldArgs a) {
   double v[6] = {warp_sum(fx), warp_sum(fy), warp_sum(fz), warp_sum(tx), warp_sum(ty), warp_sum(tz)};
   bool own = lane == 0;
   if (P > 1) own = combine_parts<6>(v, slab, warp, lane, P);
-  if (own && in && q0 != q1) {
+  if (own && in) {
     const size_t roff = size_t(r) * a.s.n;
-    a.st.fx[roff + m] += v[0];
-    a.st.fy[roff + m] += v[1];
-    a.st.fz[roff + m] += v[2];
-    a.st.tx[roff + m] += v[3];
-    a.st.ty[roff + m] += v[4];
-    a.st.tz[roff + m] += v[5];
+    if (a.frec) {  // every molecule (zeros without charges)
+      const size_t nt = size_t(a.s.R) * a.s.n;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) a.frec[k * nt + roff + m] = v[k];
+    } else if (q0 != q1) {
+      a.st.fx[roff + m] += v[0];
+      a.st.fy[roff + m] += v[1];
+      a.st.fz[roff + m] += v[2];
+      a.st.tx[roff + m] += v[3];
+      a.st.ty[roff + m] += v[4];
+      a.st.tz[roff + m] += v[5];
+    }
   }
 }
 
@@ -2022,6 +2032,10 @@ struct StepArgs {
   int write_offsets;
   uint4* fixpos;     // fixed-point positions for the search (may be null)
   double fix_scale;  // 2^32 / L
+  // end-of-step kick after an Ewald evaluation whose reciprocal forces were
+  // computed beside the real-space kernel: frec[6][R n] is added to the
+  // forces / torques first (ewald.cpp:171-178's +=) and the totals stored
+  const double* frec = nullptr;
 };
 
 __device__ __forceinline__ double wrap1(double x, double L) {
@@ -2136,11 +2150,16 @@ __device__ __forceinline__ bool kick_one(const StepArgs& a, int gid, bool* froze
   const int err = frozen ? *a.error_mol : 0x7fffffff;
   const DevSpecies& sp = s.tab->species[s.ns == 1 ? 0 : s.species_of[i]];
   const double vx0 = a.st.vx[gid], vy0 = a.st.vy[gid], vz0 = a.st.vz[gid];
-  const double fx0 = a.st.fx[gid], fy0 = a.st.fy[gid], fz0 = a.st.fz[gid];
+  double fx0 = a.st.fx[gid], fy0 = a.st.fy[gid], fz0 = a.st.fz[gid];
   const double px = a.st.px[gid], py = a.st.py[gid], pz = a.st.pz[gid];
   const double qw = a.st.qw[gid], qx = a.st.qx[gid], qy = a.st.qy[gid], qz = a.st.qz[gid];
-  const double tx = a.st.tx[gid], ty = a.st.ty[gid], tz = a.st.tz[gid];
+  double tx = a.st.tx[gid], ty = a.st.ty[gid], tz = a.st.tz[gid];
   double w0 = a.st.wx[gid], w1 = a.st.wy[gid], w2 = a.st.wz[gid];
+  if (a.frec) {
+    const size_t nt = size_t(s.R) * s.n;
+    fx0 = add(fx0, a.frec[gid]), fy0 = add(fy0, a.frec[nt + gid]), fz0 = add(fz0, a.frec[2 * nt + gid]);
+    tx = add(tx, a.frec[3 * nt + gid]), ty = add(ty, a.frec[4 * nt + gid]), tz = add(tz, a.frec[5 * nt + gid]);
+  }
   const double half = mul(0.5, a.dt);
   const double c = __ddiv_rn(half, sp.total_mass);
   const double vx = add(vx0, mul(fx0, c));
@@ -2153,6 +2172,10 @@ __device__ __forceinline__ bool kick_one(const StepArgs& a, int gid, bool* froze
   a.st.vx[gid] = vx;
   a.st.vy[gid] = vy;
   a.st.vz[gid] = vz;
+  if (a.frec) {  // the totals (Engine::state's forces, the next step's first kick)
+    a.st.fx[gid] = fx0, a.st.fy[gid] = fy0, a.st.fz[gid] = fz0;
+    a.st.tx[gid] = tx, a.st.ty[gid] = ty, a.st.tz[gid] = tz;
+  }
   if (sp.rotational_dof > 0) {
     const D3 tb = rotate_inv_exact(qw, qx, qy, qz, {tx, ty, tz});
     if (sp.inertia[0] > 0.0) w0 = add(w0, __ddiv_rn(mul(half, tb.x), sp.inertia[0]));

@@ -945,3 +945,34 @@ def test_ewald_forms_cfg2(monkeypatch, tiled):
     check_energy(outs[0].energy, ref["energy"], outs[0].virial, ref["virial"])
     assert np.array_equal(outs[0].force, outs[1].force)
     assert outs[0].energy.total() == outs[1].energy.total()
+
+
+def test_ewald_steps_cfg2(monkeypatch):
+    """Engine::step with an Ewald term (src/engine.cpp:102-143 over
+    src/ewald.cpp:107-180): in the step paths the reciprocal forces are computed
+    beside the real-space kernel and added by the end-of-step kick
+    (B2MD_EWALD_OVERLAP, the default); =0 adds them in place after it.  Both:
+    single-step and multi-step calls against the oracle's trajectory, forces /
+    torques / energies of the final state against the oracle's evaluation of it;
+    and the two forms bit-identical (the same single addition per component)."""
+    wl = configs.make("cfg2")
+    st = wl.states[0]
+    o = pyoracle.OracleFF(wl.comp, wl.opts)
+    calls = (1, 1, 4, 3)
+    tr = o.run(wl.dt, sum(calls), st.pos, st.orient, st.vel, st.ang_vel)
+    outs = []
+    for overlap in ("1", "0"):
+        monkeypatch.setenv("B2MD_EWALD_OVERLAP", overlap)
+        eng = b2.Engine(wl.comp, wl.opts, wl.dt)
+        eng.set_state(st)
+        for k in calls:
+            eng.step(k)
+        out = eng.state()
+        compare_states(out, tr, wl.comp.box_length)
+        ref = o.evaluate(out.pos, out.orient)
+        check_vec(out.force, ref["force"], what="force")
+        check_vec(out.torque, ref["torque"], what="torque")
+        check_energy(out.energy, ref["energy"], out.virial, ref["virial"])
+        outs.append(np.hstack([out.pos, out.orient, out.vel, out.ang_vel, out.force, out.torque]))
+    assert np.array_equal(outs[0], outs[1])
+
