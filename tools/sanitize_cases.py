@@ -49,9 +49,11 @@ def main():
     only = sys.argv[1:] or ["cluster", "newton", "bitmatrix", "rigid", "tile", "ewald", "replicas"]
     if "cluster" in only:
         os.environ["B2MD_CLUSTER"] = "2"
+        os.environ["B2MD_NEWTON"] = "0"  # the both-rows walk (the list is the default)
         check("cluster walk (single-site, rc < 0.3 L)", configs.lj_fluid_config(1200, 0.8, 2.5, seed=5,
                                                                                name="san-cluster"))
         os.environ.pop("B2MD_CLUSTER")
+        os.environ.pop("B2MD_NEWTON")
     if "newton" in only:
         os.environ["B2MD_CLUSTER"] = "2"
         os.environ["B2MD_NEWTON"] = "1"
