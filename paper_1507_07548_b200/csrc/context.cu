@@ -329,6 +329,7 @@ ForceArgs force_args(b2md_ctx* c) {
       a.erfcx_c[j] = (j == 0 ? 1.0 : 2.0) * sum / N;
     }
     a.erfcx_tlo = t_lo;
+    a.erfcx_uscale = 2.0 / (1.0 - t_lo);
   }
   a.vderiv = c->t.vderiv ? 1 : 0;
   const int hh = hi32(0.5 * c->t.box);

@@ -645,11 +645,13 @@ __device__ __forceinline__ bool combine_parts(double (&v)[NV], double (*slab)[NV
   return owner;
 }
 
+__device__ __forceinline__ double rcp_nr(double x);
 // erfcx(x) for 0 <= x < kErfcxMax: Clenshaw sum of the Chebyshev series in
-// u = 2 (t - t_lo) / (1 - t_lo) - 1, t = 1 / (1 + x/2)
-__device__ __forceinline__ double erfcx_cheb(double x, const double* c, double t_lo) {
-  const double t = 1.0 / (1.0 + 0.5 * x);
-  const double u = 2.0 * (t - t_lo) / (1.0 - t_lo) - 1.0;
+// u = 2 (t - t_lo) / (1 - t_lo) - 1, t = 1 / (1 + x/2); u_scale = 2 / (1 - t_lo)
+// from the host and the reciprocal by rcp_nr (no IEEE-division slow paths)
+__device__ __forceinline__ double erfcx_cheb(double x, const double* c, double t_lo, double u_scale) {
+  const double t = rcp_nr(fma(0.5, x, 1.0));
+  const double u = fma(t - t_lo, u_scale, -1.0);
   double b1 = 0.0, b2 = 0.0;
 #pragma unroll
   for (int j = kErfcxDeg; j >= 1; --j) {
@@ -751,7 +753,7 @@ struct ForceArgs {
   // t = 1 / (1 + x/2) (host-interpolated, ~1e-14 relative): the Ewald
   // real-space term then shares exp(-x^2) with its force factor
   double erfcx_c[19];
-  double erfcx_tlo;
+  double erfcx_tlo, erfcx_uscale;  // t_lo = 1 / (1 + kErfcxMax / 2), 2 / (1 - t_lo)
   int vderiv;
   float thr;  // hi32(L/2) as float (min_image_wrapped)
   // fused end-of-step half kick (kick_one) in the row epilogue: dt > 0 when
@@ -971,13 +973,15 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
             // qq 2 alpha/sqrt(pi) exp(-alpha^2 r^2), one exponential for both
             const double x = a.alpha * rr;
             const double ex = exp(-x * x);
-            const double ec = x < kErfcxMax ? ex * erfcx_cheb(x, a.erfcx_c, a.erfcx_tlo) : erfc(x);
-            const double e = ec * t.qq / rr;
+            const double ec = x < kErfcxMax
+                                  ? ex * erfcx_cheb(x, a.erfcx_c, a.erfcx_tlo, a.erfcx_uscale)
+                                  : erfc(x);
+            const double e = ec * t.qq * (rr * inv_r2);  // 1 / r = r / r^2
             const double g = t.qq * a.two_alpha_over_sqrt_pi * ex;
             uu = e;
             du_r = -(e + g);
           } else {
-            uu = t.qq / rr;
+            uu = t.qq * (rr * inv_r2);  // 1 / r = r / r^2
             du_r = -uu;
             d2u_r2 = 2.0 * uu;
             const double rf = t.qq * a.rf_r3inv * r2;

@@ -16,4 +16,7 @@ ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip
   -o $out/force -f python bench.py --config $cfg --steps 20 --warmup 3 --equil 200 --no-cpu-baseline \
   > $out/ncu_full.log 2>&1
 python tools/ncu_to_json.py $out/force.ncu-rep "$k" $cfg $out/ncu_force.json > /dev/null || true
+python tools/ncu_summary.py $out/force.ncu-rep > $out/ncu_force_summary.txt 2>/dev/null || true
+# gpurun brings back at most 64 MiB: keep the report only when asked to (KEEP_REP=1)
+[ "${KEEP_REP:-0}" = 1 ] || rm -f $out/force.ncu-rep
 echo done
