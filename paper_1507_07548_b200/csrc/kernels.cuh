@@ -673,6 +673,15 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(r, fma(e, e, e), r);
 }
 
+// 1/sqrt(x) to ~1 ulp: hardware seed (relative error ~2^-20) + one third-order
+// step y (1 + e/2 + 3 e^2/8), e = 1 - x y^2 (charge terms: r = x y, 1/r^2 = y^2).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y * y, 1.0);
+  return fma(y, e * fma(0.375, e, 0.5), y);
+}
+
 // Per-CTA scalar partials -> one fixed-order total per replica, done by the
 // last CTA to finish (integer ticket; no floating-point atomics).
 // Returns true on the last CTA (all its threads), false elsewhere.
@@ -965,8 +974,8 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
           double rx, ry, rz, dix, diy, diz;
           const double r2 = site_term(t.a, t.b, rx, ry, rz, dix, diy, diz);
           if (r2 >= rc2) continue;
-          const double inv_r2 = rcp_nr(r2);
-          const double rr = sqrt(r2);
+          const double inv_rr = rsqrt_nr(r2);
+          const double inv_r2 = inv_rr * inv_rr, rr = r2 * inv_rr;
           double uu, du_r, d2u_r2 = 0.0, rfu = 0.0;
           if constexpr (METHOD == 2) {
             // potentials.cpp:252-258: erfc(alpha r) qq / r and the force factor
@@ -976,12 +985,12 @@ __global__ void __launch_bounds__(kForceWarps * 32) k_force_multi(ForceArgs a) {
             const double ec = x < kErfcxMax
                                   ? ex * erfcx_cheb(x, a.erfcx_c, a.erfcx_tlo, a.erfcx_uscale)
                                   : erfc(x);
-            const double e = ec * t.qq * (rr * inv_r2);  // 1 / r = r / r^2
+            const double e = ec * t.qq * inv_rr;
             const double g = t.qq * a.two_alpha_over_sqrt_pi * ex;
             uu = e;
             du_r = -(e + g);
           } else {
-            uu = t.qq * (rr * inv_r2);  // 1 / r = r / r^2
+            uu = t.qq * inv_rr;
             du_r = -uu;
             d2u_r2 = 2.0 * uu;
             const double rf = t.qq * a.rf_r3inv * r2;

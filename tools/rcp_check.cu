@@ -1,4 +1,5 @@
-// Accuracy of the force kernels' reciprocal (csrc/kernels.cuh rcp_nr) against IEEE division:
+// Accuracy of the force kernels' reciprocal and reciprocal square root (csrc/kernels.cuh rcp_nr,
+// rsqrt_nr) against IEEE division / square root:
 // max relative error over 2^24 inputs spread over [2^-4, 2^8) (r^2 of pairs inside a cutoff).
 // nvcc -gencode arch=compute_100a,code=sm_100a -o rcp_check tools/rcp_check.cu && ./rcp_check
 #include <cstdio>
@@ -8,6 +9,12 @@ __device__ __forceinline__ double rcp3(double x) {
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
   const double e = fma(-x, r, 1.0);
   return fma(r, fma(e, e, e), r);
+}
+__device__ __forceinline__ double rsq3(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y * y, 1.0);
+  return fma(y, e * fma(0.375, e, 0.5), y);
 }
 __device__ __forceinline__ double seed(double x) {
   double r;
@@ -19,7 +26,8 @@ __global__ void k(double* out) {
   // log-uniform over 12 octaves, 2^24 samples, irrational stride inside the octave
   const double x = exp2(-4.0 + 12.0 * (double(t) + 0.5) / 16777216.0) * (1.0 + 1e-9 * double(t % 977));
   const double ref = 1.0 / x;
-  const double e3 = fabs(rcp3(x) - ref) / ref, es = fabs(seed(x) - ref) / ref;
+  const double rs = 1.0 / sqrt(x);
+  const double e3 = fabs(rcp3(x) - ref) / ref, es = fabs(rsq3(x) - rs) / rs;
   __shared__ double m3[256], ms[256];
   m3[threadIdx.x] = e3;
   ms[threadIdx.x] = es;
@@ -42,6 +50,7 @@ int main() {
   cudaMemcpy(h, d, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost);
   double a = 0, b = 0;
   for (int i = 0; i < nb; ++i) a = fmax(a, h[2 * i]), b = fmax(b, h[2 * i + 1]);
-  printf("max rel error: third-order step %.3e (%.2f ulp), seed %.3e (2^%.1f)\n", a, a / 1.11e-16, b, log2(b));
+  printf("max rel error: rcp third-order step %.3e (%.2f ulp), rsqrt third-order step %.3e (%.2f ulp)\n", a,
+         a / 1.11e-16, b, b / 1.11e-16);
   return cudaGetLastError() != cudaSuccess;
 }
