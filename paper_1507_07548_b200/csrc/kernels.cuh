@@ -646,20 +646,17 @@ __device__ __forceinline__ bool combine_parts(double (&v)[NV], double (*slab)[NV
 }
 
 __device__ __forceinline__ double rcp_nr(double x);
-// erfcx(x) for 0 <= x < kErfcxMax: Clenshaw sum of the Chebyshev series in
-// u = 2 (t - t_lo) / (1 - t_lo) - 1, t = 1 / (1 + x/2); u_scale = 2 / (1 - t_lo)
-// from the host and the reciprocal by rcp_nr (no IEEE-division slow paths)
+// erfcx(x) for 0 <= x < kErfcxMax: the degree-kErfcxDeg interpolant in
+// u = 2 (t - t_lo) / (1 - t_lo) - 1, t = 1 / (1 + x/2), by Horner's rule on its
+// monomial coefficients c (from the Chebyshev series, on the host);
+// u_scale = 2 / (1 - t_lo), the reciprocal by rcp_nr (no IEEE-division slow paths)
 __device__ __forceinline__ double erfcx_cheb(double x, const double* c, double t_lo, double u_scale) {
   const double t = rcp_nr(fma(0.5, x, 1.0));
   const double u = fma(t - t_lo, u_scale, -1.0);
-  double b1 = 0.0, b2 = 0.0;
+  double p = c[kErfcxDeg];
 #pragma unroll
-  for (int j = kErfcxDeg; j >= 1; --j) {
-    const double b0 = fma(2.0 * u, b1, c[j] - b2);
-    b2 = b1;
-    b1 = b0;
-  }
-  return fma(u, b1, c[0] - b2);
+  for (int j = kErfcxDeg - 1; j >= 0; --j) p = fma(p, u, c[j]);
+  return p;
 }
 
 // 1/x to ~1 ulp without the IEEE-division slow path: hardware reciprocal
@@ -758,7 +755,7 @@ struct ForceArgs {
   double rc2;
   double alpha, two_alpha_over_sqrt_pi;
   double rf_r3inv, rf_shift;
-  // erfcx(x) = erfc(x) exp(x^2) on [0, kErfcxMax] as a Chebyshev series in
+  // erfcx(x) = erfc(x) exp(x^2) on [0, kErfcxMax] as a polynomial (monomial form) in
   // t = 1 / (1 + x/2) (host-interpolated, ~1e-14 relative): the Ewald
   // real-space term then shares exp(-x^2) with its force factor
   double erfcx_c[19];
