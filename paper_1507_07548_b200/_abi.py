@@ -231,8 +231,22 @@ def lib():
     return _lib
 
 
+# ndarray -> double* conversions cost ~3 us each in ctypes; a caller that steps
+# through the same (pinned) buffers pays it once per buffer.  The cache keeps
+# the array alive, so its id and data pointer cannot be reused while cached.
+_PTR_CACHE: dict[int, tuple[np.ndarray, object]] = {}
+_PTR_CACHE_MAX = 64
+
+
 def dptr(a: np.ndarray | None):
     if a is None:
         return None
+    hit = _PTR_CACHE.get(id(a))
+    if hit is not None and hit[0] is a:
+        return hit[1]
     assert a.dtype == np.float64 and a.flags.c_contiguous
-    return a.ctypes.data_as(_D)
+    p = a.ctypes.data_as(_D)
+    if len(_PTR_CACHE) >= _PTR_CACHE_MAX:
+        _PTR_CACHE.clear()
+    _PTR_CACHE[id(a)] = (a, p)
+    return p

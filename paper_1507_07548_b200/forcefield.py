@@ -115,7 +115,7 @@ class _Context:
         return _abi.lib().b2md_warning(self.ctx).decode()
 
     def energies(self, e_arr, s_arr):
-        es = [EnergyBreakdown.from_c(e_arr[r]) for r in range(self.replicas)]
+        es = EnergyBreakdown.list_from_c(e_arr, self.replicas)
         ss = [EvalStats(s_arr[r].virial, s_arr[r].s1, s_arr[r].s2, s_arr[r].com_pairs)
               for r in range(self.replicas)]
         return es, ss

@@ -177,6 +177,13 @@ class EnergyBreakdown:  # energy.hpp:9-25
     def from_c(cls, e: _abi.b2md_energy) -> "EnergyBreakdown":
         return cls(**{f: getattr(e, f) for f in _ENERGY_FIELDS})
 
+    @classmethod
+    def list_from_c(cls, e_arr, count: int) -> list["EnergyBreakdown"]:
+        """`count` b2md_energy structs (all doubles, in field order) in one pass."""
+        nf = len(_ENERGY_FIELDS)
+        vals = np.frombuffer(e_arr, dtype=np.float64, count=count * nf).tolist()
+        return [cls(*vals[r * nf:(r + 1) * nf]) for r in range(count)]
+
 
 class SystemState:
     """model.hpp:75-92 with numpy arrays."""
