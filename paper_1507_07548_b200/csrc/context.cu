@@ -748,11 +748,14 @@ int resort(b2md_ctx* c) {
   const double side = c->use_cluster && c->nc > 0 ? std::cbrt(double(kCS) / rho)
                                                   : std::sqrt(32.0 / (rho * L));
   const int G = std::max(1, std::min(1024, int(L / side)));
-  k_sort_keys<<<g, 256, 0, c->stream>>>(c->st.px, c->st.py, c->st.pz, nt, n, L, G,
+  int cbits = 1;  // bits of the column index (< G^2)
+  while ((1 << cbits) < G * G) ++cbits;
+  k_sort_keys<<<g, 256, 0, c->stream>>>(c->st.px, c->st.py, c->st.pz, nt, n, L, G, cbits,
                                         c->d_keys[0], c->d_vals[0]);
   CU(cudaGetLastError());
-  int end_bit = 40;
-  while ((1 << (end_bit - 40)) < c->R) ++end_bit;
+  // (cfg3: 8 + 14 bits, three 8-bit radix passes instead of the five of a fixed 40-bit key)
+  int end_bit = cbits + kSortXBits;
+  while ((1 << (end_bit - cbits - kSortXBits)) < c->R) ++end_bit;
   size_t bytes = c->cub_bytes;
   CU(cub::DeviceRadixSort::SortPairs(c->d_cub, bytes, c->d_keys[0], c->d_keys[1], c->d_vals[0],
                                      c->d_vals[1], nt, 0, end_bit, c->stream));

@@ -2417,8 +2417,10 @@ static __global__ void k_unpack_state(StateDev st, int n, int r, const double* i
 // words.  Key = (replica, column, x on 2^20 bins); values are global
 // molecule indices; the stable radix sort makes the order a deterministic
 // function of the positions.
+// key = replica | column (cbits) | x (kSortXBits): as few radix digits as the grid needs
+constexpr int kSortXBits = 14;
 static __global__ void k_sort_keys(const double* px, const double* py, const double* pz, int count,
-                            int n, double L, int G, unsigned long long* keys, int* vals) {
+                            int n, double L, int G, int cbits, unsigned long long* keys, int* vals) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= count) return;
   auto bin = [L](double x, int nb) {
@@ -2428,8 +2430,8 @@ static __global__ void k_sort_keys(const double* px, const double* py, const dou
     return unsigned(c < 0 ? 0 : (c >= nb ? nb - 1 : c));
   };
   const unsigned long long col = bin(pz[gid], G) * unsigned(G) + bin(py[gid], G);
-  keys[gid] = (static_cast<unsigned long long>(gid / n) << 40) | (col << 20) |
-              bin(px[gid], 1 << 20);
+  keys[gid] = (static_cast<unsigned long long>(gid / n) << (cbits + kSortXBits)) | (col << kSortXBits) |
+              bin(px[gid], 1 << kSortXBits);
   vals[gid] = gid;
 }
 
